@@ -1,0 +1,367 @@
+"""Pins of the fp64 oracle against what the paper and the mathematics fix.
+
+None of these re-types the oracle's formula: each is a worked example printed in
+SPEC.md / PAPER.md (tests/golden/spec_examples.json), a closed form, a special
+case that reduces to a library routine, an invariant, or brute force on a tiny
+input.  Together they are chosen so that a plausible slip in oracle.c (a dropped
+term, a wrong sign, scale or index, a transposed operand, an off-by-one mask)
+fails at least one of them.  CPU only.
+"""
+import itertools
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))
+
+
+def rng(seed):
+    return np.random.default_rng(seed)
+
+
+def tiny_model(L=2, H=16, h=4, F=64, V=32, max_seq=16, seed=3, bf16=False):
+    layers, emb = synth.model_host(L, H, F, V, max_seq, seed, bf16)
+    return oracle.make_cfg(L, H, h, F), layers, emb
+
+
+# ----------------------------------------------------------------------------- index maps (P1-P3)
+@pytest.mark.parametrize("ex", GOLD["index_maps"])
+def test_index_maps_spec_examples(ex):
+    off, pack, pos, unpack = oracle.index_maps(ex["lens"], ex["S"])
+    assert list(off) == ex["offsets"] and off[-1] == ex["T"]
+    assert list(pack) == ex["pack_idx"]
+    assert list(unpack) == ex["unpack_idx"]
+
+
+def test_index_maps_exhaustive_small():
+    """Brute force over every lens vector with B<=3, S<=4."""
+    for S in range(1, 5):
+        for B in range(1, 4):
+            for lens in itertools.product(range(1, S + 1), repeat=B):
+                off, pack, pos, unpack = oracle.index_maps(lens, S)
+                T = sum(lens)
+                assert off[-1] == T and len(pack) == T
+                # enumerate the valid (b, s) cells in row-major order: that *is* packing
+                cells = [b * S + s for b in range(B) for s in range(S) if s < lens[b]]
+                assert list(pack) == cells
+                assert list(pos) == [c % S for c in cells]
+                inv = [-1] * (B * S)
+                for t, c in enumerate(cells):
+                    inv[c] = t
+                assert list(unpack) == inv
+                assert all(off[b + 1] - off[b] == lens[b] for b in range(B))
+
+
+def test_index_maps_full_lengths_identity():
+    off, pack, pos, unpack = oracle.index_maps([7, 7, 7], 7)
+    assert np.array_equal(pack, np.arange(21)) and np.array_equal(unpack, np.arange(21))
+
+
+@pytest.mark.parametrize("ex", GOLD["drce_savings"])
+def test_drce_savings(ex):
+    off, *_ = oracle.index_maps(ex["lens"], ex["S"])
+    assert off[-1] / (len(ex["lens"]) * ex["S"]) == ex["ratio"]
+
+
+def test_pack_unpack_roundtrip():
+    """P2: unpack(pack(x)) = x on valid rows, 0 elsewhere, bit-exact."""
+    lens, S, H = [3, 1, 5], 6, 4
+    x = rng(0).standard_normal((len(lens), S, H))
+    off, pack, pos, unpack = oracle.index_maps(lens, S)
+    packed = x.reshape(-1, H)[pack]
+    back = np.where(unpack[:, None] >= 0, packed[np.maximum(unpack, 0)], 0.0).reshape(x.shape)
+    for b, n in enumerate(lens):
+        assert np.array_equal(back[b, :n], x[b, :n]) and not back[b, n:].any()
+
+
+# ----------------------------------------------------------------------------- primitives
+@pytest.mark.parametrize("ex", GOLD["matmul"])
+def test_matmul_spec(ex):
+    assert np.array_equal(oracle.matmul(ex["a"], ex["b"]), np.array(ex["c"], float))
+
+
+def test_matmul_vs_library():
+    a, b = rng(42).standard_normal((7, 5)), rng(43).standard_normal((5, 3))
+    np.testing.assert_allclose(oracle.matmul(a, b), a @ b, rtol=0, atol=1e-13)
+
+
+def test_layernorm_spec_example():
+    ex = GOLD["layer_norm"][0]
+    y = oracle.layernorm([ex["x"]], [1, 1], [0, 0], eps=ex["eps"])
+    assert np.array_equal(y[0], ex["y"])
+
+
+def test_layernorm_eps_and_affine():
+    # biased variance of [1,3] is 1: (x-mu)/sqrt(1+eps) closed form; gamma scales, beta shifts
+    y = oracle.layernorm([[1.0, 3.0]], [2.0, 2.0], [1.0, 1.0], eps=1e-5)
+    z = 1.0 / math.sqrt(1.0 + 1e-5)
+    np.testing.assert_allclose(y[0], [1 - 2 * z, 1 + 2 * z], rtol=0, atol=1e-15)
+    assert abs(z - 0.999995000037) < 1e-12
+    # constant row -> beta (zero variance numerator)
+    assert np.array_equal(oracle.layernorm([[5.0] * 8], [3.0] * 8, [0.25] * 8)[0], [0.25] * 8)
+
+
+def test_layernorm_statistics():
+    """random rows -> mean |mu| < 1e-12, var = v/(v+eps) (eps accounted)."""
+    x = rng(7).standard_normal((4, 8))
+    y = oracle.layernorm(x, np.ones(8), np.zeros(8), eps=1e-5)
+    v = x.var(axis=1)
+    assert np.abs(y.mean(axis=1)).max() < 1e-12
+    np.testing.assert_allclose(y.var(axis=1), v / (v + 1e-5), rtol=0, atol=1e-9)
+
+
+@pytest.mark.parametrize("ex", GOLD["gelu"])
+def test_gelu_values(ex):
+    assert abs(oracle.gelu(ex["x"]) - ex["y"]) <= ex["tol"]
+
+
+def test_gelu_odd_part():
+    """For any odd inner function, gelu(x) - gelu(-x) = x exactly (pins the 0.5 factor)."""
+    for x in [0.3, 1.7, -2.2, 4.0]:
+        assert abs(oracle.gelu(x) - oracle.gelu(-x) - x) < 1e-15
+
+
+# ----------------------------------------------------------------------------- attention (P5, P6)
+def test_attention_uniform_noncausal_is_mean():
+    """Zero scores (q = 0): every allowed key has weight 1/n -> mean of V rows."""
+    B, S, H = 2, 4, 6
+    V = rng(1).standard_normal((B, S, H))
+    Q = np.zeros_like(V)
+    K = rng(2).standard_normal((B, S, H))
+    C = oracle.attention(Q, K, V, h=2, lens=[4, 2], causal=0)
+    np.testing.assert_allclose(C[0], np.broadcast_to(V[0].mean(0), (S, H)), atol=1e-15)
+    np.testing.assert_allclose(C[1, :2], np.broadcast_to(V[1, :2].mean(0), (2, H)), atol=1e-15)
+
+
+def test_attention_causal_mean_and_row0():
+    """Causal: row 0 sees only key 0 -> exactly V[0]; row s -> mean of V[0..s]."""
+    B, S, H = 1, 5, 4
+    V = rng(3).standard_normal((B, S, H))
+    C = oracle.attention(np.zeros_like(V), V, V, h=1, lens=[5], causal=1)
+    assert np.array_equal(C[0, 0], V[0, 0])
+    for s in range(S):
+        np.testing.assert_allclose(C[0, s], V[0, :s + 1].mean(0), atol=1e-15)
+
+
+def test_attention_length_mask_ignores_pad_keys():
+    """lens=[2], S=4: pad keys have probability exactly 0, so their values never matter."""
+    B, S, H = 1, 4, 4
+    Q, K, V = (rng(i).standard_normal((B, S, H)) for i in (4, 5, 6))
+    C1 = oracle.attention(Q, K, V, h=2, lens=[2], causal=0)
+    K2, V2 = K.copy(), V.copy()
+    K2[0, 2:] = 1e3
+    V2[0, 2:] = np.nan
+    C2 = oracle.attention(Q, K2, V2, h=2, lens=[2], causal=0)
+    assert np.array_equal(C1[0, :2], C2[0, :2])
+
+
+def test_attention_two_key_closed_form():
+    """Two allowed keys: p1 = sigmoid((q.k1 - q.k0)/sqrt(d)) -- pins the 1/sqrt(d) scale and the sign."""
+    d = 4
+    q = np.array([0.5, -1.0, 2.0, 0.25])
+    k0 = np.array([1.0, 0.0, 0.5, -1.0])
+    k1 = np.array([-0.5, 1.5, 1.0, 2.0])
+    v0, v1 = np.array([1.0, 2.0, 3.0, 4.0]), np.array([-4.0, 0.0, 1.0, 8.0])
+    Q = np.stack([q, q])[None]
+    K = np.stack([k0, k1])[None]
+    V = np.stack([v0, v1])[None]
+    C = oracle.attention(Q, K, V, h=1, lens=[2], causal=1)
+    p1 = 1.0 / (1.0 + math.exp(-(q @ k1 - q @ k0) / math.sqrt(d)))
+    np.testing.assert_allclose(C[0, 1], (1 - p1) * v0 + p1 * v1, rtol=0, atol=1e-14)
+    assert np.array_equal(C[0, 0], v0)
+
+
+def test_attention_heads_are_independent():
+    """Head i reads and writes only columns [i d, (i+1) d)."""
+    B, S, H, h = 1, 3, 8, 2
+    Q, K, V = (rng(i).standard_normal((B, S, H)) for i in (7, 8, 9))
+    C1 = oracle.attention(Q, K, V, h=h, lens=[3], causal=1)
+    Q2, K2, V2 = Q.copy(), K.copy(), V.copy()
+    for A in (Q2, K2, V2):
+        A[..., 4:] = rng(10).standard_normal((B, S, 4))
+    C2 = oracle.attention(Q2, K2, V2, h=h, lens=[3], causal=1)
+    assert np.array_equal(C1[..., :4], C2[..., :4]) and not np.array_equal(C1[..., 4:], C2[..., 4:])
+
+
+def test_attention_bruteforce_tiny():
+    """SPEC.md:83 B=2,S=4,H=8,h=2: brute-force enumeration of every (b, head, s) softmax."""
+    B, S, H, h = 2, 4, 8, 2
+    d = H // h
+    Q, K, V = (rng(i).standard_normal((B, S, H)) for i in (11, 12, 13))
+    lens = [4, 3]
+    C = oracle.attention(Q, K, V, h=h, lens=lens, causal=1)
+    for b in range(B):
+        for i in range(h):
+            cols = slice(i * d, (i + 1) * d)
+            for s in range(lens[b]):
+                keys = [t for t in range(lens[b]) if t <= s]
+                logits = np.array([Q[b, s, cols] @ K[b, t, cols] for t in keys]) / math.sqrt(d)
+                w = np.exp(logits - logits.max())
+                w /= w.sum()
+                ref = sum(wt * V[b, t, cols] for wt, t in zip(w, keys))
+                np.testing.assert_allclose(C[b, s, cols], ref, rtol=0, atol=1e-13)
+
+
+# ----------------------------------------------------------------------------- layer (P7, P8)
+def zero_layer(H, F):
+    shapes = synth.layer_shapes(H, F)
+    return {n: np.zeros(s) for n, s in shapes.items()} | {"ln1_g": np.ones(H), "ln2_g": np.ones(H)}
+
+
+def test_layer_zero_weights_is_identity():
+    """all weights and biases 0 -> output = input (residuals only)."""
+    H, F = 8, 32
+    X = rng(14).standard_normal((2, 3, H))
+    cfg = oracle.make_cfg(1, H, 2, F)
+    assert np.array_equal(oracle.layer_padded(cfg, zero_layer(H, F), X, [3, 2]), X)
+
+
+def test_layer_biases_only():
+    """Weights 0: attention branch = bo, MLP branch = gelu(b1)·0 + b2 -> X + bo + b2."""
+    H, F = 8, 32
+    X = rng(15).standard_normal((1, 2, H))
+    w = zero_layer(H, F)
+    w["bo"] = rng(16).standard_normal(H)
+    w["b1"] = rng(17).standard_normal(F)
+    w["b2"] = rng(18).standard_normal(H)
+    cfg = oracle.make_cfg(1, H, 2, F)
+    np.testing.assert_allclose(oracle.layer_padded(cfg, w, X, [2]), X + w["bo"] + w["b2"], rtol=0, atol=1e-15)
+
+
+def test_layer_single_token_reduces_to_matmuls():
+    """S=1: the attention weight is exactly 1, so the layer is a chain of library matmuls."""
+    H, F, h = 8, 32, 2
+    cfg = oracle.make_cfg(1, H, h, F)
+    w = {n: rng(20 + i).standard_normal(s) * 0.3 for i, (n, s) in enumerate(synth.layer_shapes(H, F).items())}
+    X = rng(19).standard_normal((1, 1, H))
+    Y = oracle.layer_padded(cfg, w, X, [1])
+
+    def ln(x, g, b):
+        mu = x.mean()
+        return (x - mu) / np.sqrt(((x - mu) ** 2).mean() + 1e-5) * g + b
+
+    x = X[0, 0]
+    a = ln(x, w["ln1_g"], w["ln1_b"])
+    x1 = x + (a @ w["wv"] + w["bv"]) @ w["wo"] + w["bo"]
+    u = ln(x1, w["ln2_g"], w["ln2_b"]) @ w["w1"] + w["b1"]
+    g = np.array([oracle.gelu(t) for t in u])
+    x2 = x1 + g @ w["w2"] + w["b2"]
+    np.testing.assert_allclose(Y[0, 0], x2, rtol=0, atol=1e-12)
+
+
+def test_param_count_gpt3_layer():
+    """P14 / PAPER.md:397: one GPT-3 layer = 12H^2+13H = 1.812e9 parameters, 3.375 GiB in FP16."""
+    g = GOLD["gpt3_layer_params"]
+    H = g["H"]
+    n = sum(int(np.prod(s)) for s in synth.layer_shapes(H, 4 * H).values())
+    assert n == g["params"]
+    assert abs(n * 2 / 2 ** 30 - g["fp16_gib"]) < 1e-3
+
+
+def test_embed_gathers_token_and_position_rows():
+    H, V, S = 4, 6, 3
+    cfg = oracle.make_cfg(0, H, 1, 16)
+    emb = {"tok_emb": np.arange(V * H, dtype=float).reshape(V, H), "pos_emb": 1000.0 * np.arange(S * H).reshape(S, H)}
+    tok = np.array([[5, 2, 0]])
+    X = oracle.embed(cfg, emb, tok)
+    assert np.array_equal(X[0, 1], emb["tok_emb"][2] + emb["pos_emb"][1])
+    assert np.array_equal(X[0, 2], emb["tok_emb"][0] + emb["pos_emb"][2])
+
+
+# ----------------------------------------------------------------------------- stack properties
+def batch(B, S, V, seed, lens=None):
+    lens = lens or synth.random_lengths(B, S, seed)
+    return synth.tokens(B, S, V, lens, seed), lens
+
+
+def test_stack_no_layers_is_final_ln_of_embedding():
+    """SPEC.md:163 serial_forward L=0 -> final_norm(embedding lookup)."""
+    cfg, _, emb = tiny_model(L=0)
+    tok, lens = batch(2, 5, 32, 1)
+    Y = oracle.forward_padded(cfg, [], emb, tok, lens)
+    np.testing.assert_allclose(Y, oracle.layernorm(oracle.embed(cfg, emb, tok), emb["lnf_g"], emb["lnf_b"]),
+                               rtol=0, atol=0)
+
+
+@pytest.mark.parametrize("causal", [1, 0])
+def test_drce_equals_padded_bitexact(causal):
+    """P10 / SPEC.md:478-479: DRCE = padded at valid positions (bit-exact in fp64), pad rows exactly 0."""
+    cfg, layers, emb = tiny_model()
+    cfg.causal = causal
+    tok, lens = batch(3, 7, 32, 2)
+    Yp = oracle.forward_padded(cfg, layers, emb, tok, lens)
+    Yd = oracle.forward_drce(cfg, layers, emb, tok, lens)
+    for b, n in enumerate(lens):
+        assert np.array_equal(Yp[b, :n], Yd[b, :n])
+        assert not Yd[b, n:].any()
+
+
+def test_drce_full_lengths_identical_everywhere():
+    cfg, layers, emb = tiny_model()
+    tok, lens = batch(2, 5, 32, 3, lens=[5, 5])
+    assert np.array_equal(oracle.forward_padded(cfg, layers, emb, tok, lens),
+                          oracle.forward_drce(cfg, layers, emb, tok, lens))
+
+
+def test_tp_equals_serial():
+    """P9 / SPEC.md:306-317: k=1 bit-exact; k=2,4 within 1e-9; exactly 2L reductions."""
+    cfg, layers, emb = tiny_model(L=2, H=16, h=4, F=64)
+    tok, lens = batch(2, 6, 32, 4)
+    Y = oracle.forward_padded(cfg, layers, emb, tok, lens)
+    Y1, n1 = oracle.forward_tp(cfg, 1, layers, emb, tok, lens)
+    assert np.array_equal(Y1, Y) and n1 == 2 * cfg.L
+    Y2, n2 = oracle.forward_tp(cfg, 2, layers, emb, tok, lens)
+    Y4, n4 = oracle.forward_tp(cfg, 4, layers, emb, tok, lens)
+    assert n2 == n4 == 2 * cfg.L
+    for b, n in enumerate(lens):
+        assert np.abs(Y2[b, :n] - Y[b, :n]).max() < 1e-9
+        assert np.abs(Y4[b, :n] - Y2[b, :n]).max() < 1e-9
+
+
+def test_pad_content_independence():
+    """P11 / SPEC.md:155: batches differing only in pad tokens -> identical valid outputs."""
+    cfg, layers, emb = tiny_model()
+    tok, lens = batch(2, 6, 32, 5, lens=[3, 6])
+    tok2 = tok.copy()
+    tok2[0, 3:] = [7, 9, 11]
+    Y1 = oracle.forward_padded(cfg, layers, emb, tok, lens)
+    Y2 = oracle.forward_padded(cfg, layers, emb, tok2, lens)
+    assert np.array_equal(Y1[0, :3], Y2[0, :3]) and np.array_equal(Y1[1], Y2[1])
+
+
+def test_sequence_independence():
+    """P12: the output of sequence b depends only on sequence b (licenses sampled-sequence parity)."""
+    cfg, layers, emb = tiny_model()
+    tok, lens = batch(4, 6, 32, 6)
+    Y = oracle.forward_padded(cfg, layers, emb, tok, lens)
+    sel = [3, 1]
+    Ys = oracle.forward_padded(cfg, layers, emb, tok[sel], [lens[i] for i in sel])
+    for j, b in enumerate(sel):
+        assert np.array_equal(Ys[j, :lens[b]], Y[b, :lens[b]])
+
+
+def test_causal_prefix_invariance():
+    """P13: extending a sequence leaves the outputs at earlier positions unchanged (causal)."""
+    cfg, layers, emb = tiny_model()
+    tok, _ = batch(1, 6, 32, 7, lens=[6])
+    Y6 = oracle.forward_padded(cfg, layers, emb, tok, [6])
+    Y4 = oracle.forward_padded(cfg, layers, emb, tok, [4])
+    assert np.array_equal(Y6[0, :4], Y4[0, :4])
+
+
+def test_layers_compose():
+    """layers_padded(0,L) = L applications of layer_padded (teacher-forced parity entry)."""
+    cfg, layers, emb = tiny_model(L=3)
+    tok, lens = batch(2, 5, 32, 8)
+    X = oracle.embed(cfg, emb, tok)
+    Xa = oracle.layers_padded(cfg, layers, 0, 3, X, lens)
+    Xb = X
+    for l in range(3):
+        Xb = oracle.layer_padded(cfg, layers[l], Xb, lens)
+    assert np.array_equal(Xa, Xb)
