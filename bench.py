@@ -1,0 +1,371 @@
+"""bench.py -- valid tokens/s and batch latency of the DRCE tensor-parallel GPT layer stack on B200.
+
+Metric (BASELINE.json): "valid tokens/sec & batch latency, GPT-3-13B-shape stack, TP 1/2/4/8 B200".
+One step = one forward pass of the whole hot path (index maps, embed+pack,
+40 x (LN, QKV GEMM, unpack, attention, repack, out-proj GEMM, [allreduce], residual+LN, up GEMM,
+down GEMM, [allreduce], residual+LN), final LN + unpack) over one synthetic batch of the GPT-3-13B
+shape (B=16, max_len=512, exact padding ratio 0.5 -> T=4096 valid tokens), bf16, random-init weights.
+
+  python bench.py [--gpus N --steps K --warmup W]       energon arm (N>1: under torchrun, TP=N)
+  python bench.py --impl reference ...                  the fp64 CPU oracle arm (rank 0 only)
+
+Timing: W untimed warm-up steps, then K steps bracketed by barrier + cuda.synchronize, CUDA events
+on the forward stream, max over ranks.  value = valid tokens per step * K / time (TP: every rank
+works on the same batch, so the job's units are the batch's T valid tokens -> "scaling": "strong").
+The per-step working set (25 GB of bf16 weights at TP=1) is far larger than the 126 MB L2, so no
+explicit flush is needed between steps.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "valid tokens/sec & batch latency, GPT-3-13B-shape stack, TP 1/2/4/8 B200"
+UNIT = "tokens/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="energon", choices=["energon", "reference"])
+    ap.add_argument("--config", default="gpt3_13b")
+    ap.add_argument("--p", type=float, default=None, help="padding ratio (exact-p configs)")
+    ap.add_argument("--regime", default=None, choices=[None, "exact_p", "paper", "random"])
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--drce", type=int, default=1)
+    ap.add_argument("--layers", type=int, default=None, help="override the layer count (debug only)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-tokens", type=int, default=192)
+    return ap.parse_args()
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(path))
+        return {"hbm_gbs": d["hbm_gbs"], "bf16_tflops": d["bf16_tflops"],
+                "bf16_tflops_sustained": d.get("bf16_tflops_sustained", d["bf16_tflops"]), "source": "measured"}
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "source": "fallback"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+    FIELDS = "clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown," \
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap"
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        sm, smax, reasons = [], None, set()
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = float(parts[1])
+            except ValueError:
+                continue
+            for name, v in zip(self.NAMES, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ============================================================================= oracle (CPU) arm
+def oracle_sample(args, shape, lens, tok, sample_tokens):
+    """Bounded sample of the workload for the fp64 oracle: layer 0 of the stack over the first
+    `sample_tokens` tokens of the longest sequence (an exact sub-problem: causal prefix, P13 and
+    sequence independence, P12).  Returns (fn, tokens_per_call, layers_extrapolated)."""
+    import numpy as np
+
+    import oracle
+    import synth
+    b = int(np.argmax(lens))
+    n = min(sample_tokens, lens[b])
+    layers, emb = synth.model_host(1, shape["H"], shape["F"], shape["V"], shape["max_seq"], args.seed, True,
+                                   layer_ids=[0])
+    cfg = oracle.make_cfg(1, shape["H"], shape["h"], shape["F"])
+    X = oracle.embed(cfg, emb, tok[b:b + 1, :n])
+
+    def run():
+        oracle.layers_padded(cfg, layers, 0, 1, X, [n])
+
+    return run, n, shape["L"]
+
+
+def reference_arm(args, world, rank):
+    if rank != 0:
+        return  # rank 0 alone runs the oracle arm
+    import oracle
+    import synth
+    shape = dict(synth.SHAPES[args.config])
+    if args.layers:
+        shape["L"] = args.layers
+    bcfg = synth.BATCHES[args.config]
+    lens = synth.batch_lengths(args.config, args.seed, p=args.p, regime=args.regime)
+    tok = synth.tokens(bcfg["B"], bcfg["S"], shape["V"], lens, args.seed)
+    ntok = max(8, args.cpu_sample_tokens // 6)
+    run, n, L = oracle_sample(args, shape, lens, tok, ntok)
+    for _ in range(args.warmup):
+        run()
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        run()
+        times.append(time.perf_counter() - t0)
+    tot = sum(times)
+    value = n * args.steps / (tot * L)
+    cores = oracle.num_threads()
+    sample = (f"oracle fp64: layer 0 of {L} over the first {n} tokens of the longest sequence per step, "
+              f"tokens/s extrapolated by the layer count ({L}x)")
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic", "config": workload_config(args, shape, bcfg, lens, world),
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def workload_config(args, shape, bcfg, lens, world):
+    T = sum(lens)
+    B, S = bcfg["B"], bcfg["S"]
+    return {"workload": f"{args.config}: {shape['L']} layers, H={shape['H']}, {shape['h']} heads, B={B}, "
+                        f"max_len={S}, padding {1 - T / (B * S):.3f} (T={T}), bf16, TP={world}",
+            "layers": shape["L"], "hidden": shape["H"], "heads": shape["h"], "batch": B, "max_len": S,
+            "padding_ratio": round(1 - T / (B * S), 4), "valid_tokens_per_step": T, "tp": world,
+            "parallelism": f"tp{world}", "drce": bool(args.drce),
+            "l2": "no flush: per-step working set (weights) > 126 MB L2"}
+
+
+# ============================================================================= energon (GPU) arm
+def energon_arm(args, world, rank, local):
+    import numpy as np
+    import torch
+
+    import synth
+    from paper_2209_02341_b200 import energon
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    energon.load_library()
+    shape = dict(synth.SHAPES[args.config])
+    if args.layers:
+        shape["L"] = args.layers
+    bcfg = synth.BATCHES[args.config]
+    B, S = bcfg["B"], bcfg["S"]
+    lens = synth.batch_lengths(args.config, args.seed, p=args.p, regime=args.regime)
+    T = sum(lens)
+    tok_np = synth.tokens(B, S, shape["V"], lens, args.seed)
+    H = shape["H"]
+
+    cfg = energon.make_config(shape["L"], H, shape["h"], shape["F"], shape["V"], shape["max_seq"], B * S,
+                              dtype="bf16", drce=args.drce, tp_size=world, tp_rank=rank, device=local)
+    uid = None
+    if world > 1:
+        buf = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            buf.copy_(torch.frombuffer(bytearray(energon.energon_get_unique_id()), dtype=torch.uint8))
+        dist.broadcast(buf, 0)
+        uid = bytes(buf.cpu().numpy().tobytes())
+    ctx = energon.energon_init(cfg, uid)
+
+    # weights: generated on the device by the seeded counter-based generator, loaded unsharded
+    emb = {n: synth.emb_tensor_device(n, H, shape["V"], shape["max_seq"], args.seed, True, torch.bfloat16)
+           for n in synth.EMB_TENSORS}
+    energon.energon_load_embeddings(ctx, emb["tok_emb"], emb["pos_emb"], emb["lnf_g"], emb["lnf_b"])
+    del emb
+    for l in range(shape["L"]):
+        w = {n: synth.layer_tensor_device(n, l, H, shape["F"], args.seed, True, torch.bfloat16)
+             for n in synth.LAYER_TENSORS}
+        energon.energon_load_layer_weights(ctx, l, w)
+        del w
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+
+    stream = torch.cuda.current_stream()
+    tok = torch.from_numpy(tok_np).cuda()
+    out = torch.empty(B, S, H, dtype=torch.bfloat16, device="cuda")
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        energon.energon_forward(ctx, tok, lens, out, stream)
+    energon.energon_sync(ctx)
+
+    # ---------------- device-timed region: inputs resident in HBM
+    launches0 = energon.energon_get_stats(ctx)["kernel_launches"]
+    energon.energon_set_profiling(ctx, True)
+    clocks = ClockSampler(local)
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    evs[0].record(stream)
+    for i in range(args.steps):
+        energon.energon_forward(ctx, tok, lens, out, stream)
+        evs[i + 1].record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    energon.energon_sync(ctx)
+    step_ms = [evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)]
+    total_ms = max_over_ranks(evs[0].elapsed_time(evs[-1]))
+    launches = energon.energon_get_stats(ctx)["kernel_launches"] - launches0
+    prof = energon.energon_get_profile(ctx)
+    energon.energon_set_profiling(ctx, False)
+    value = T * args.steps / (total_ms * 1e-3)
+
+    # ---------------- end-to-end: host tokens -> device, forward, result -> host, every step
+    e2e = None
+    if not args.no_e2e:
+        tok_h = torch.from_numpy(tok_np).pin_memory()
+        out_h = torch.empty(B, S, H, dtype=torch.bfloat16).pin_memory()
+        tok_d = torch.empty_like(tok)
+
+        def e2e_step():
+            tok_d.copy_(tok_h, non_blocking=True)
+            energon.energon_forward(ctx, tok_d, lens, out, stream)
+            out_h.copy_(out, non_blocking=True)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        e2e_ms = max_over_ranks(e0.elapsed_time(e1))
+        e2e = {"value": T * args.steps / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": tok_h.numel() * 4,
+               "d2h_bytes_per_step": out_h.numel() * 2, "ms_per_step": e2e_ms / args.steps}
+    energon.energon_sync(ctx)
+
+    pk = peaks()
+    gemm_ms_avg = prof["gemm_ms"] / max(prof["gemm_launches"], 1)
+    achieved = prof["gemm_flops"] / (prof["gemm_ms"] * 1e-3) / 1e12 if prof["gemm_ms"] > 0 else None
+    traffic = None
+    try:
+        tr = json.load(open(os.path.join(ROOT, "profiles", "gemm_traffic.json")))
+        traffic = tr.get(args.config, {}).get(f"tp{world}")
+    except Exception:
+        pass
+    roofline = {"bound": "tensor", "kernel": "gemm_tc_kernel (a4/a8/a10/a11, tcgen05 bf16)",
+                "achieved": achieved, "peak": pk["bf16_tflops_sustained"], "unit": "TFLOP/s",
+                "frac": (achieved / pk["bf16_tflops_sustained"]) if achieved else None, "traffic": traffic,
+                "peak_source": f"{pk['source']} bf16_tflops_sustained (kernel timed inside a long step)",
+                "frac_of_burst": (achieved / pk["bf16_tflops"]) if achieved else None,
+                "frac_of_2250_nominal": (achieved / 2250.0) if achieved else None,
+                "avg_launch_ms": gemm_ms_avg, "flops_per_step": prof["gemm_flops"] / args.steps}
+    phases = {
+        "gemm": {"ms_per_step": prof["gemm_ms"] / args.steps, "launches": prof["gemm_launches"] // args.steps,
+                 "tflops": achieved},
+        "attention": {"ms_per_step": prof["attn_ms"] / args.steps,
+                      "tflops": prof["attn_flops"] / (prof["attn_ms"] * 1e-3) / 1e12 if prof["attn_ms"] else None},
+        "memory_bound": {"ms_per_step": prof["mem_ms"] / args.steps,
+                         "gbs": prof["mem_bytes"] / (prof["mem_ms"] * 1e-3) / 1e9 if prof["mem_ms"] else None,
+                         "frac_of_hbm": (prof["mem_bytes"] / (prof["mem_ms"] * 1e-3) / 1e9 / pk["hbm_gbs"])
+                         if prof["mem_ms"] else None},
+        "allreduce": {"ms_per_step": prof["comm_ms"] / args.steps, "calls": prof["comm_calls"] // args.steps,
+                      "bus_gbs": (prof["comm_bytes"] * 2 * (world - 1) / world / (prof["comm_ms"] * 1e-3) / 1e9)
+                      if prof["comm_ms"] else None},
+    }
+    result = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+              "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+              "latency_ms_p50": statistics.median(step_ms), "latency_ms_p95": sorted(step_ms)[
+                  min(len(step_ms) - 1, int(round(0.95 * (len(step_ms) - 1))))],
+              "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+              "data": "synthetic (seeded counter-based generator; random-init weights of the GPT-3-13B shape)",
+              "config": workload_config(args, shape, bcfg, lens, world), "clocks": clk, "e2e": e2e,
+              "gpu_launches": int(launches), "roofline": roofline, "phases": phases}
+
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import oracle
+        run, n, L = oracle_sample(args, shape, lens, tok_np, args.cpu_sample_tokens)
+        t0 = time.perf_counter()
+        run()
+        dt = time.perf_counter() - t0
+        result["cpu_baseline"] = {"value": n / (dt * L), "unit": UNIT, "cores": oracle.num_threads(),
+                                  "kind": "oracle",
+                                  "sample": f"fp64 oracle, layer 0 of {L} over the first {n} tokens of the longest "
+                                            f"sequence ({dt:.1f} s), tokens/s extrapolated by the layer count"}
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    energon.energon_destroy(ctx)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world == 1 and args.gpus > 1:
+        print(json.dumps({"error": "--gpus > 1 must be launched under torchrun"}))
+        sys.exit(2)
+    if args.impl == "reference":
+        reference_arm(args, world, rank)
+    else:
+        energon_arm(args, world, rank, local)
+
+
+if __name__ == "__main__":
+    main()

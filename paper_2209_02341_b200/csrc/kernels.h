@@ -1,0 +1,79 @@
+// kernels.h -- host-side launchers of the energon CUDA kernels (internal; not part of the C ABI).
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define ENERGON_MAX_B 1024
+
+namespace energon {
+
+typedef __nv_bfloat16 bf16;
+
+// seq_lens passed by value as a kernel parameter (4 KB): no host->device copy, no sync.
+struct LensParam {
+  int lens[ENERGON_MAX_B];
+};
+
+struct PtrList {
+  void* p[8];
+};
+
+// a1
+void launch_index_maps(const LensParam& lp, int B, int S, int* offsets, int* pack_idx, int* pos, int* unpack_idx,
+                       cudaStream_t st);
+// a2 + a3
+template <typename Act>
+void launch_embed_ln(const int* tok, const int* pack_idx, int rows, int S, int V, int H, const Act* tok_emb,
+                     const Act* pos_emb, const float* g, const float* b, float eps, float* X, Act* A, int* err,
+                     cudaStream_t st);
+template <typename Act>
+void launch_gather_ln(const float* x, const int* pack_idx, int rows, int H, const float* g, const float* b, float eps,
+                      float* X, Act* A, cudaStream_t st);
+// a9 / a12
+template <typename Act>
+void launch_residual_ln(float* X, const Act* P, const float* bias, int rows, int H, const float* g, const float* b,
+                        float eps, Act* A, cudaStream_t st);
+// a13
+template <typename Out>
+void launch_final_ln_unpack(const float* X, const int* unpack_idx, int rows_are_cells, int cells, int H, const float* g,
+                            const float* b, float eps, int apply_ln, Out* out, cudaStream_t st);
+// a5 / a7
+template <typename Act>
+void launch_unpack_qkv(const Act* QKV, const int* pack_idx, int T, int S, int hk, int d, Act* Q, Act* K, Act* V,
+                       cudaStream_t st);
+template <typename Act>
+void launch_repack(const Act* O, const int* pack_idx, const int* unpack_idx, int T, int S, int hk, int d, Act* C,
+                   cudaStream_t st);
+template <typename Act>
+void launch_local_allreduce(const PtrList& parts, int k, int64_t n, cudaStream_t st);
+// load-time relayout
+template <typename Src, typename Dst>
+void launch_relayout(const Src* src, int64_t ld, int64_t row0, int64_t col0, int N, int K, Dst* dst, int64_t dst_ld,
+                     int64_t dst_row0, cudaStream_t st);
+template <typename Src, typename Dst>
+void launch_convert_vec(const Src* src, int64_t off, int N, Dst* dst, cudaStream_t st);
+
+// a6: masked attention over the padded per-head layout [B, hk, S, d]
+template <typename Act>
+void launch_attention(const Act* Q, const Act* K, const Act* V, Act* O, const LensParam& lp, int B, int hk, int S,
+                      int d, int causal, cudaStream_t st);
+
+// GEMM epilogues
+enum { EPI_NONE = 0, EPI_BIAS = 1, EPI_BIAS_GELU = 2 };
+
+// fp32 SIMT GEMM (parity mode): D[M,N] = A[M,K] W[N,K]^T (+bias) (gelu)
+void launch_gemm_f32(const float* A, const float* W, const float* bias, float* D, int M, int N, int K, int epi,
+                     cudaStream_t st);
+
+// bf16 tcgen05 GEMM.  Operands are K-major bf16 described by TMA maps with a 64-element (128 B)
+// inner box and 128-byte swizzle: A [M,K] with a 128-row box, W [N,K] with a bn-row box (bn = the
+// tile N, 256 or 128, chosen per call by tc_pick_bn).
+bool make_tmap_kmajor(CUtensorMap* map, const void* ptr, int rows, int K, int box_rows);
+int tc_pick_bn(int M, int N);
+void launch_gemm_tc(const CUtensorMap& tmA, const CUtensorMap& tmB, int bn, const float* bias, bf16* D, int M, int N,
+                    int K, int epi, cudaStream_t st);
+int num_sms();
+
+}  // namespace energon

@@ -1,0 +1,467 @@
+// kernels_misc.cu -- the HBM-bound kernels of the DRCE path (steps a1-a3, a5, a7, a9/a12, a13)
+// plus load-time weight relayout and the in-device TP reduction of a local group.
+//
+// Every kernel reads / writes each byte of its operands once, with 16-byte (or 8-byte for bf16x4)
+// vector accesses along the contiguous hidden dimension; rows are independent (one CTA per row for
+// the LayerNorm family so the row lives in registers between the statistics and the write).
+#include "common.cuh"
+#include "kernels.h"
+
+namespace energon {
+
+// ============================================================================ a1: index maps
+// PAPER.md:368-373 (sec 4.3): every worker derives the DRCE layout from the command's seq_lens.
+// offsets = exclusive prefix sum of lens (warp-shuffle scan); for each padded cell (b, s):
+//   s < lens[b] : t = offsets[b] + s, unpack_idx[cell] = t, pack_idx[t] = cell, pos[t] = s
+//   otherwise   : unpack_idx[cell] = -1
+// Every CTA recomputes the (tiny, B <= 1024) scan in shared memory, so the whole step is one launch.
+__global__ void __launch_bounds__(256) index_maps_kernel(LensParam lp, int B, int S, int* __restrict__ offsets,
+                                                         int* __restrict__ pack_idx, int* __restrict__ pos,
+                                                         int* __restrict__ unpack_idx) {
+  __shared__ int s_off[ENERGON_MAX_B + 1];
+  __shared__ int s_len[ENERGON_MAX_B];
+  for (int b = threadIdx.x; b < B; b += blockDim.x) s_len[b] = lp.lens[b];
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    // each lane owns a contiguous chunk of ceil(B/32) sequences
+    const int lane = threadIdx.x;
+    const int per = (B + 31) / 32;
+    const int b0 = lane * per, b1 = min(B, b0 + per);
+    int local = 0;
+    for (int b = b0; b < b1; ++b) local += s_len[b];
+    int incl = local;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    int run = incl - local;  // exclusive prefix of this lane's chunk
+    for (int b = b0; b < b1; ++b) {
+      s_off[b] = run;
+      run += s_len[b];
+    }
+    if (lane == 31) s_off[B] = incl;
+  }
+  __syncthreads();
+  if (blockIdx.x == 0)
+    for (int b = threadIdx.x; b <= B; b += blockDim.x) offsets[b] = s_off[b];
+  const int cells = B * S;
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < cells; c += gridDim.x * blockDim.x) {
+    const int b = c / S, s = c - b * S;
+    if (s < s_len[b]) {
+      const int t = s_off[b] + s;
+      unpack_idx[c] = t;
+      pack_idx[t] = c;
+      pos[t] = s;
+    } else {
+      unpack_idx[c] = -1;
+    }
+  }
+}
+
+// ============================================================================ 4-wide row vectors
+template <typename T> struct Row4;
+template <> struct Row4<float> {
+  static __device__ __forceinline__ float4 load(const float* p) { return *reinterpret_cast<const float4*>(p); }
+  static __device__ __forceinline__ void store(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
+};
+template <> struct Row4<bf16> {
+  static __device__ __forceinline__ float4 load(const bf16* p) {
+    const uint2 u = *reinterpret_cast<const uint2*>(p);
+    const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+    const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+    return make_float4(a.x, a.y, b.x, b.y);
+  }
+  static __device__ __forceinline__ void store(bf16* p, float4 v) {
+    __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
+    uint2 u;
+    u.x = *reinterpret_cast<uint32_t*>(&a);
+    u.y = *reinterpret_cast<uint32_t*>(&b);
+    *reinterpret_cast<uint2*>(p) = u;
+  }
+};
+
+constexpr int LN_THREADS = 256;
+constexpr int LN_MAXV = 12;  // float4 per thread: H <= 12288
+
+// Two-pass LayerNorm statistics over a row held in registers (biased variance,
+// eps inside the square root, fp32).
+__device__ __forceinline__ void row_stats(const float4 (&v)[LN_MAXV], int nv, int H, float eps, float* red,
+                                          float& mean, float& rstd) {
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < LN_MAXV; ++i)
+    if (i < nv) s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
+  mean = block_sum(s, red) / (float)H;
+  float q = 0.f;
+#pragma unroll
+  for (int i = 0; i < LN_MAXV; ++i)
+    if (i < nv) {
+      const float a = v[i].x - mean, b = v[i].y - mean, c = v[i].z - mean, d = v[i].w - mean;
+      q += (a * a + b * b) + (c * c + d * d);
+    }
+  const float var = block_sum(q, red) / (float)H;
+  rstd = rsqrtf(var + eps);
+}
+
+__device__ __forceinline__ float4 ln_apply(float4 x, float mean, float rstd, const float* g, const float* b, int j) {
+  const float4 gg = *reinterpret_cast<const float4*>(g + j), bb = *reinterpret_cast<const float4*>(b + j);
+  return make_float4((x.x - mean) * rstd * gg.x + bb.x, (x.y - mean) * rstd * gg.y + bb.y,
+                     (x.z - mean) * rstd * gg.z + bb.z, (x.w - mean) * rstd * gg.w + bb.w);
+}
+
+// ============================================================================ a2 + a3: embed, pack, LN1
+// PAPER.md:138 embedding layer; padding is removed at the entry: only the T valid
+// rows are gathered.  X[t] = E[tok[cell]] + P[pos] (fp32 residual stream), A[t] = LN1_0(X[t]).
+// pack_idx == nullptr means the padded A/B mode (row t is cell t).  An id outside [0, V) gathers
+// row 0 and raises the device error flag (checked by energon_sync), so the kernel never faults.
+template <typename Act>
+__global__ void __launch_bounds__(LN_THREADS) embed_ln_kernel(const int* __restrict__ tok, const int* __restrict__ pack_idx,
+                                                              int S, int V, int H, const Act* __restrict__ tok_emb,
+                                                              const Act* __restrict__ pos_emb, const float* __restrict__ g,
+                                                              const float* __restrict__ b, float eps, float* __restrict__ X,
+                                                              Act* __restrict__ A, int* err_flag) {
+  __shared__ float red[32];
+  const int t = blockIdx.x;
+  const int cell = pack_idx ? pack_idx[t] : t;
+  const int s = cell % S;
+  int id = tok[cell];
+  if (id < 0 || id >= V) {
+    if (threadIdx.x == 0) *err_flag = 1;
+    id = 0;
+  }
+  const Act* e = tok_emb + (int64_t)id * H;
+  const Act* p = pos_emb + (int64_t)s * H;
+  float4 v[LN_MAXV];
+  const int nv4 = H / 4;
+  int nv = 0;
+#pragma unroll
+  for (int i = 0; i < LN_MAXV; ++i) {
+    const int c = (threadIdx.x + i * LN_THREADS);
+    if (c < nv4) {
+      const float4 a = Row4<Act>::load(e + 4 * c), q = Row4<Act>::load(p + 4 * c);
+      v[i] = make_float4(a.x + q.x, a.y + q.y, a.z + q.z, a.w + q.w);
+      Row4<float>::store(X + (int64_t)t * H + 4 * c, v[i]);
+      nv = i + 1;
+    }
+  }
+  float mean, rstd;
+  row_stats(v, nv, H, eps, red, mean, rstd);
+#pragma unroll
+  for (int i = 0; i < LN_MAXV; ++i) {
+    const int c = (threadIdx.x + i * LN_THREADS);
+    if (i < nv) Row4<Act>::store(A + (int64_t)t * H + 4 * c, ln_apply(v[i], mean, rstd, g, b, 4 * c));
+  }
+}
+
+// Hidden-state entry (energon_forward_hidden): X[t] = x[cell] (fp32), A[t] = LN1(X[t]).
+template <typename Act>
+__global__ void __launch_bounds__(LN_THREADS) gather_ln_kernel(const float* __restrict__ x, const int* __restrict__ pack_idx,
+                                                               int H, const float* __restrict__ g, const float* __restrict__ b,
+                                                               float eps, float* __restrict__ X, Act* __restrict__ A) {
+  __shared__ float red[32];
+  const int t = blockIdx.x;
+  const int cell = pack_idx ? pack_idx[t] : t;
+  float4 v[LN_MAXV];
+  int nv = 0;
+#pragma unroll
+  for (int i = 0; i < LN_MAXV; ++i) {
+    const int c = (threadIdx.x + i * LN_THREADS);
+    if (c < H / 4) {
+      v[i] = Row4<float>::load(x + (int64_t)cell * H + 4 * c);
+      Row4<float>::store(X + (int64_t)t * H + 4 * c, v[i]);
+      nv = i + 1;
+    }
+  }
+  float mean, rstd;
+  row_stats(v, nv, H, eps, red, mean, rstd);
+#pragma unroll
+  for (int i = 0; i < LN_MAXV; ++i)
+    if (i < nv) Row4<Act>::store(A + (int64_t)t * H + 4 * (threadIdx.x + i * LN_THREADS),
+                                 ln_apply(v[i], mean, rstd, g, b, 4 * (threadIdx.x + i * LN_THREADS)));
+}
+
+// ============================================================================ a9 / a12: bias + residual + LN
+// X[t] += P[t] + bias (P = the reduced row-parallel partial, "accumulated by communications",
+// PAPER.md:290; bias added once after the reduce), then A[t] = LN(X[t]).
+// With A == nullptr only the residual update is done.
+template <typename Act>
+__global__ void __launch_bounds__(LN_THREADS) residual_ln_kernel(float* __restrict__ X, const Act* __restrict__ P,
+                                                                 const float* __restrict__ bias, int H,
+                                                                 const float* __restrict__ g, const float* __restrict__ b,
+                                                                 float eps, Act* __restrict__ A) {
+  __shared__ float red[32];
+  const int t = blockIdx.x;
+  float4 v[LN_MAXV];
+  int nv = 0;
+#pragma unroll
+  for (int i = 0; i < LN_MAXV; ++i) {
+    const int c = (threadIdx.x + i * LN_THREADS);
+    if (c < H / 4) {
+      float4 x = Row4<float>::load(X + (int64_t)t * H + 4 * c);
+      const float4 p = Row4<Act>::load(P + (int64_t)t * H + 4 * c);
+      const float4 q = *reinterpret_cast<const float4*>(bias + 4 * c);
+      x.x += p.x + q.x;
+      x.y += p.y + q.y;
+      x.z += p.z + q.z;
+      x.w += p.w + q.w;
+      v[i] = x;
+      Row4<float>::store(X + (int64_t)t * H + 4 * c, x);
+      nv = i + 1;
+    }
+  }
+  if (A == nullptr) return;
+  float mean, rstd;
+  row_stats(v, nv, H, eps, red, mean, rstd);
+#pragma unroll
+  for (int i = 0; i < LN_MAXV; ++i)
+    if (i < nv) Row4<Act>::store(A + (int64_t)t * H + 4 * (threadIdx.x + i * LN_THREADS),
+                                 ln_apply(v[i], mean, rstd, g, b, 4 * (threadIdx.x + i * LN_THREADS)));
+}
+
+// ============================================================================ a13: final LN + unpack
+// out[cell] = LN_f(X[unpack_idx[cell]]) for valid cells, exactly 0 for pad cells;
+// every output row is written once.  rows_are_cells: padded A/B mode (X row = cell).
+template <typename Out>
+__global__ void __launch_bounds__(LN_THREADS) final_ln_unpack_kernel(const float* __restrict__ X, const int* __restrict__ unpack_idx,
+                                                                     int rows_are_cells, int H, const float* __restrict__ g,
+                                                                     const float* __restrict__ b, float eps, int apply_ln,
+                                                                     Out* __restrict__ out) {
+  __shared__ float red[32];
+  const int cell = blockIdx.x;
+  const int t = unpack_idx[cell];
+  Out* o = out + (int64_t)cell * H;
+  if (t < 0) {
+    for (int c = threadIdx.x; c < H / 4; c += LN_THREADS) Row4<Out>::store(o + 4 * c, make_float4(0.f, 0.f, 0.f, 0.f));
+    return;
+  }
+  const int row = rows_are_cells ? cell : t;
+  float4 v[LN_MAXV];
+  int nv = 0;
+#pragma unroll
+  for (int i = 0; i < LN_MAXV; ++i) {
+    const int c = (threadIdx.x + i * LN_THREADS);
+    if (c < H / 4) {
+      v[i] = Row4<float>::load(X + (int64_t)row * H + 4 * c);
+      nv = i + 1;
+    }
+  }
+  if (!apply_ln) {
+#pragma unroll
+    for (int i = 0; i < LN_MAXV; ++i)
+      if (i < nv) Row4<Out>::store(o + 4 * (threadIdx.x + i * LN_THREADS), v[i]);
+    return;
+  }
+  float mean, rstd;
+  row_stats(v, nv, H, eps, red, mean, rstd);
+#pragma unroll
+  for (int i = 0; i < LN_MAXV; ++i)
+    if (i < nv) Row4<Out>::store(o + 4 * (threadIdx.x + i * LN_THREADS),
+                                 ln_apply(v[i], mean, rstd, g, b, 4 * (threadIdx.x + i * LN_THREADS)));
+}
+
+// ============================================================================ a5: rebuild padding
+// Paper kernel #1 ("fuse the transpose and pad operations"): packed QKV [T, 3*Hk]
+// (per-rank column order q | k | v, head-major then d) -> Q, K, V [B, hk, S, d].
+// One thread moves one 16-byte chunk; reads are fully coalesced along the packed row, writes are
+// contiguous d-length segments.  Pad rows of Q/K/V are never written (attention never reads them).
+template <typename Act>
+__global__ void unpack_qkv_kernel(const Act* __restrict__ QKV, const int* __restrict__ pack_idx, int T, int S, int hk,
+                                  int d, Act* __restrict__ Q, Act* __restrict__ K, Act* __restrict__ Vv) {
+  constexpr int E = 16 / sizeof(Act);
+  const int Hk = hk * d;
+  const int chunks_per_row = 3 * Hk / E;
+  const int64_t total = (int64_t)T * chunks_per_row;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int t = (int)(i / chunks_per_row);
+    const int col = (int)(i - (int64_t)t * chunks_per_row) * E;
+    const int which = col / Hk;
+    const int rem = col - which * Hk;
+    const int head = rem / d, j = rem - head * d;
+    const int cell = pack_idx ? pack_idx[t] : t;
+    const int b = cell / S, s = cell - b * S;
+    Act* dst = (which == 0 ? Q : (which == 1 ? K : Vv)) + (((int64_t)b * hk + head) * S + s) * d + j;
+    *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(QKV + (int64_t)t * 3 * Hk + col);
+  }
+}
+
+// ============================================================================ a7: remove padding
+// Paper kernel #2: O [B, hk, S, d] -> packed Ctx [T, Hk] (head-major columns).
+// In the padded A/B mode (pack_idx == nullptr) pad query rows are written as 0.
+template <typename Act>
+__global__ void repack_kernel(const Act* __restrict__ O, const int* __restrict__ pack_idx,
+                              const int* __restrict__ unpack_idx, int T, int S, int hk, int d, Act* __restrict__ C) {
+  constexpr int E = 16 / sizeof(Act);
+  const int Hk = hk * d;
+  const int chunks_per_row = Hk / E;
+  const int64_t total = (int64_t)T * chunks_per_row;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int t = (int)(i / chunks_per_row);
+    const int col = (int)(i - (int64_t)t * chunks_per_row) * E;
+    const int head = col / d, j = col - head * d;
+    const int cell = pack_idx ? pack_idx[t] : t;
+    const int b = cell / S, s = cell - b * S;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (pack_idx || unpack_idx[cell] >= 0)
+      v = *reinterpret_cast<const uint4*>(O + (((int64_t)b * hk + head) * S + s) * d + j);
+    *reinterpret_cast<uint4*>(C + (int64_t)t * Hk + col) = v;
+  }
+}
+
+// ============================================================================ local TP reduction
+// In-device allreduce for a local group (energon_init_local_group): sum the k partials in rank
+// order 0..k-1 in fp32 (every rank gets bit-identical data), write back to all k.
+template <typename Act>
+__global__ void local_allreduce_kernel(PtrList parts, int k, int64_t n) {
+  constexpr int E = 16 / sizeof(Act);
+  const int64_t nv = n / E;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nv; i += (int64_t)gridDim.x * blockDim.x) {
+    float acc[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) acc[e] = 0.f;
+    for (int r = 0; r < k; ++r) {
+      Vec16<Act> v;
+      v.u = reinterpret_cast<const uint4*>(parts.p[r])[i];
+#pragma unroll
+      for (int e = 0; e < E; ++e) acc[e] += to_f32(v.e[e]);
+    }
+    Vec16<Act> o;
+#pragma unroll
+    for (int e = 0; e < E; ++e) o.e[e] = from_f32<Act>(acc[e]);
+    for (int r = 0; r < k; ++r) reinterpret_cast<uint4*>(parts.p[r])[i] = o.u;
+  }
+}
+
+// ============================================================================ load-time relayout
+// dst[n * K + k] = cvt(src[(row0 + k) * ld + col0 + n])  for n < N, k < K   (transpose == 1)
+// dst[n]         = cvt(src[col0 + n])                     for n < N         (vector)
+// Source [in, out] row-major -> destination [out, in] = K-major operand of the GEMMs.
+template <typename Dst> __device__ __forceinline__ Dst cvt(double x);
+template <> __device__ __forceinline__ float cvt<float>(double x) { return (float)x; }
+template <> __device__ __forceinline__ bf16 cvt<bf16>(double x) { return __double2bfloat16(x); }
+template <typename Dst> __device__ __forceinline__ Dst cvt(float x) { return from_f32<Dst>(x); }
+template <typename Dst> __device__ __forceinline__ Dst cvt(bf16 x);
+template <> __device__ __forceinline__ float cvt<float>(bf16 x) { return __bfloat162float(x); }
+template <> __device__ __forceinline__ bf16 cvt<bf16>(bf16 x) { return x; }
+
+template <typename Src, typename Dst>
+__global__ void relayout_kernel(const Src* __restrict__ src, int64_t ld, int64_t row0, int64_t col0, int N, int K,
+                                Dst* __restrict__ dst, int64_t dst_ld, int64_t dst_row0) {
+  __shared__ Src tile[32][33];
+  const int n0 = blockIdx.x * 32, k0 = blockIdx.y * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int k = k0 + i, n = n0 + threadIdx.x;
+    if (k < K && n < N) tile[i][threadIdx.x] = src[(row0 + k) * ld + col0 + n];
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int n = n0 + i, k = k0 + threadIdx.x;
+    if (k < K && n < N) dst[(dst_row0 + n) * dst_ld + k] = cvt<Dst>(tile[threadIdx.x][i]);
+  }
+}
+
+template <typename Src, typename Dst>
+__global__ void convert_vec_kernel(const Src* __restrict__ src, int64_t off, int N, Dst* __restrict__ dst) {
+  for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < N; n += gridDim.x * blockDim.x) dst[n] = cvt<Dst>(src[off + n]);
+}
+
+// ============================================================================ host launchers
+static inline int grid_for(int64_t work, int threads, int max_blocks) {
+  int64_t g = (work + threads - 1) / threads;
+  if (g > max_blocks) g = max_blocks;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+void launch_index_maps(const LensParam& lp, int B, int S, int* offsets, int* pack_idx, int* pos, int* unpack_idx,
+                       cudaStream_t st) {
+  const int cells = B * S;
+  index_maps_kernel<<<grid_for(cells, 256, 148 * 4), 256, 0, st>>>(lp, B, S, offsets, pack_idx, pos, unpack_idx);
+}
+
+template <typename Act>
+void launch_embed_ln(const int* tok, const int* pack_idx, int rows, int S, int V, int H, const Act* tok_emb,
+                     const Act* pos_emb, const float* g, const float* b, float eps, float* X, Act* A, int* err,
+                     cudaStream_t st) {
+  if (rows > 0) embed_ln_kernel<Act><<<rows, LN_THREADS, 0, st>>>(tok, pack_idx, S, V, H, tok_emb, pos_emb, g, b, eps, X, A, err);
+}
+
+template <typename Act>
+void launch_gather_ln(const float* x, const int* pack_idx, int rows, int H, const float* g, const float* b, float eps,
+                      float* X, Act* A, cudaStream_t st) {
+  if (rows > 0) gather_ln_kernel<Act><<<rows, LN_THREADS, 0, st>>>(x, pack_idx, H, g, b, eps, X, A);
+}
+
+template <typename Act>
+void launch_residual_ln(float* X, const Act* P, const float* bias, int rows, int H, const float* g, const float* b,
+                        float eps, Act* A, cudaStream_t st) {
+  if (rows > 0) residual_ln_kernel<Act><<<rows, LN_THREADS, 0, st>>>(X, P, bias, H, g, b, eps, A);
+}
+
+template <typename Out>
+void launch_final_ln_unpack(const float* X, const int* unpack_idx, int rows_are_cells, int cells, int H, const float* g,
+                            const float* b, float eps, int apply_ln, Out* out, cudaStream_t st) {
+  if (cells > 0)
+    final_ln_unpack_kernel<Out><<<cells, LN_THREADS, 0, st>>>(X, unpack_idx, rows_are_cells, H, g, b, eps, apply_ln, out);
+}
+
+template <typename Act>
+void launch_unpack_qkv(const Act* QKV, const int* pack_idx, int T, int S, int hk, int d, Act* Q, Act* K, Act* V,
+                       cudaStream_t st) {
+  const int64_t work = (int64_t)T * 3 * hk * d / (16 / sizeof(Act));
+  if (work > 0) unpack_qkv_kernel<Act><<<grid_for(work, 256, 148 * 16), 256, 0, st>>>(QKV, pack_idx, T, S, hk, d, Q, K, V);
+}
+
+template <typename Act>
+void launch_repack(const Act* O, const int* pack_idx, const int* unpack_idx, int T, int S, int hk, int d, Act* C,
+                   cudaStream_t st) {
+  const int64_t work = (int64_t)T * hk * d / (16 / sizeof(Act));
+  if (work > 0) repack_kernel<Act><<<grid_for(work, 256, 148 * 16), 256, 0, st>>>(O, pack_idx, unpack_idx, T, S, hk, d, C);
+}
+
+template <typename Act>
+void launch_local_allreduce(const PtrList& parts, int k, int64_t n, cudaStream_t st) {
+  const int64_t work = n / (16 / sizeof(Act));
+  if (work > 0) local_allreduce_kernel<Act><<<grid_for(work, 256, 148 * 8), 256, 0, st>>>(parts, k, n);
+}
+
+template <typename Src, typename Dst>
+void launch_relayout(const Src* src, int64_t ld, int64_t row0, int64_t col0, int N, int K, Dst* dst, int64_t dst_ld,
+                     int64_t dst_row0, cudaStream_t st) {
+  dim3 grid((N + 31) / 32, (K + 31) / 32), block(32, 8);
+  relayout_kernel<Src, Dst><<<grid, block, 0, st>>>(src, ld, row0, col0, N, K, dst, dst_ld, dst_row0);
+}
+
+template <typename Src, typename Dst>
+void launch_convert_vec(const Src* src, int64_t off, int N, Dst* dst, cudaStream_t st) {
+  convert_vec_kernel<Src, Dst><<<grid_for(N, 256, 1024), 256, 0, st>>>(src, off, N, dst);
+}
+
+// explicit instantiations
+#define INST_ACT(Act)                                                                                                   \
+  template void launch_embed_ln<Act>(const int*, const int*, int, int, int, int, const Act*, const Act*, const float*,   \
+                                     const float*, float, float*, Act*, int*, cudaStream_t);                            \
+  template void launch_gather_ln<Act>(const float*, const int*, int, int, const float*, const float*, float, float*,     \
+                                      Act*, cudaStream_t);                                                              \
+  template void launch_residual_ln<Act>(float*, const Act*, const float*, int, int, const float*, const float*, float,   \
+                                        Act*, cudaStream_t);                                                            \
+  template void launch_final_ln_unpack<Act>(const float*, const int*, int, int, int, const float*, const float*, float,  \
+                                            int, Act*, cudaStream_t);                                                   \
+  template void launch_unpack_qkv<Act>(const Act*, const int*, int, int, int, int, Act*, Act*, Act*, cudaStream_t);    \
+  template void launch_repack<Act>(const Act*, const int*, const int*, int, int, int, int, Act*, cudaStream_t);        \
+  template void launch_local_allreduce<Act>(const PtrList&, int, int64_t, cudaStream_t);
+INST_ACT(float)
+INST_ACT(bf16)
+
+#define INST_CVT(Src, Dst)                                                                                             \
+  template void launch_relayout<Src, Dst>(const Src*, int64_t, int64_t, int64_t, int, int, Dst*, int64_t, int64_t,     \
+                                          cudaStream_t);                                                                \
+  template void launch_convert_vec<Src, Dst>(const Src*, int64_t, int, Dst*, cudaStream_t);
+INST_CVT(double, float)
+INST_CVT(double, bf16)
+INST_CVT(float, float)
+INST_CVT(float, bf16)
+INST_CVT(bf16, float)
+INST_CVT(bf16, bf16)
+
+}  // namespace energon

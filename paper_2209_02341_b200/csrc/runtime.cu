@@ -1,0 +1,813 @@
+// runtime.cu -- the C ABI (include/energon.h): context, validation, weight relayout, workspace,
+// NCCL TP communicator and the per-layer launch sequence of the DRCE forward pass.
+//
+// Per layer and rank (PAPER.md:281-293 1-D TP; PAPER.md:358-373 DRCE):
+//   A   = LN1(X)                      (fused into the previous residual kernel, or the entry kernel)
+//   QKV = A . Wqkv_r^T + bqkv_r       tcgen05 GEMM, packed rows                       a4
+//   Q,K,V <- QKV  rebuild padding                                                      a5
+//   O   = attention(Q, K, V)          padded per-head layout, pad keys/queries skipped  a6
+//   Ctx <- O      remove padding                                                       a7
+//   P   = Ctx . Wo_r^T                row-parallel partial                             a8
+//   P   = allreduce(P)                NCCL (or in-device sum for a local group)         a9
+//   X  += P + bo ; A = LN2(X)                                                          a9
+//   G   = gelu(A . W1_r^T + b1_r)                                                      a10
+//   P   = G . W2_r^T ; P = allreduce(P)                                                a11, a12
+//   X  += P + b2 ; A = LN1'(X)                                                         a12
+// and once per batch: index maps (a1), embed+pack+LN1 (a2, a3), final LN + unpack (a13).
+#include <nccl.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/energon.h"
+#include "kernels.h"
+
+using namespace energon;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct LayerDev {
+  void *wqkv = nullptr, *wo = nullptr, *w1 = nullptr, *w2 = nullptr;  // [N, K] row-major (K-major operands)
+  float *bqkv = nullptr, *bo = nullptr, *b1 = nullptr, *b2 = nullptr;
+  float *ln1g = nullptr, *ln1b = nullptr, *ln2g = nullptr, *ln2b = nullptr;
+  CUtensorMap tm_qkv[2], tm_o[2], tm_1[2], tm_2[2];  // [0]: 256-row box, [1]: 128-row box
+  bool loaded = false;
+};
+
+}  // namespace
+
+struct energon_ctx {
+  energon_config cfg;
+  int k = 1, r = 0, H = 0, h = 0, d = 0, F = 0, Hk = 0, hk = 0, Fk = 0, V = 0;
+  bool bf16 = false;
+  size_t act = 4;  // bytes per activation element
+  ncclComm_t nccl = nullptr;
+  bool local_group = false;
+  // replicated embeddings / final LN
+  void* tok_emb = nullptr;
+  void* pos_emb = nullptr;
+  float *lnf_g = nullptr, *lnf_b = nullptr;
+  bool emb_loaded = false;
+  std::vector<LayerDev> layers;
+  // workspace (sized from max_tokens padded rows)
+  int *offsets = nullptr, *pack_idx = nullptr, *pos = nullptr, *unpack_idx = nullptr;
+  float* X = nullptr;
+  void *A = nullptr, *QKV = nullptr, *Q = nullptr, *K = nullptr, *Vb = nullptr, *O = nullptr, *Ctx = nullptr,
+       *P = nullptr, *G = nullptr;
+  CUtensorMap tmA_A, tmA_Ctx, tmA_G;
+  int tm_rows = -1;
+  int* err_host = nullptr;  // mapped pinned flag written by the embed kernel (bad token id)
+  int* err_dev = nullptr;
+  cudaStream_t load_stream = nullptr;
+  std::vector<void*> allocs;
+  std::string err;
+  energon_stats stats;
+  // profiling (energon_set_profiling): CUDA events around every launch on the forward stream
+  struct ProfRec {
+    cudaEvent_t a, b;
+    int cls;
+    double work;
+  };
+  bool prof = false;
+  std::vector<ProfRec> recs;
+  std::vector<cudaEvent_t> pool;
+  size_t pool_used = 0;
+  energon_profile pacc;
+};
+
+namespace {
+
+energon_status fail(energon_ctx* c, energon_status s, const std::string& msg) {
+  g_last_error = msg;
+  if (c) c->err = msg;
+  return s;
+}
+
+energon_status cuda_fail(energon_ctx* c, cudaError_t e, const char* where) {
+  return fail(c, e == cudaErrorMemoryAllocation ? ENERGON_ERR_OOM : ENERGON_ERR_CUDA,
+              std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define CU(c, expr)                                            \
+  do {                                                         \
+    cudaError_t _e = (expr);                                   \
+    if (_e != cudaSuccess) return cuda_fail((c), _e, #expr);   \
+  } while (0)
+
+template <typename T>
+energon_status dalloc(energon_ctx* c, T** p, size_t bytes, int64_t* counter) {
+  void* q = nullptr;
+  if (bytes == 0) bytes = 16;
+  cudaError_t e = cudaMalloc(&q, bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(c, ENERGON_ERR_OOM, "cudaMalloc(" + std::to_string(bytes) + " B) failed: " + cudaGetErrorString(e));
+  }
+  c->allocs.push_back(q);
+  if (counter) *counter += (int64_t)bytes;
+  *p = reinterpret_cast<T*>(q);
+  return ENERGON_OK;
+}
+
+energon_status validate_config(const energon_config* cfg) {
+  if (!cfg) return fail(nullptr, ENERGON_ERR_ARG, "cfg is NULL");
+  if (cfg->num_layers < 1 || cfg->hidden < 1 || cfg->num_heads < 1 || cfg->ffn < 1 || cfg->vocab < 1 ||
+      cfg->max_seq < 1 || cfg->max_tokens < 1)
+    return fail(nullptr, ENERGON_ERR_CONFIG, "every size in energon_config must be >= 1");
+  if (cfg->hidden % cfg->num_heads)
+    return fail(nullptr, ENERGON_ERR_CONFIG, "hidden must equal num_heads * head_dim (SPEC.md:284)");
+  if (cfg->tp_size < 1 || cfg->tp_size > 8 || cfg->tp_rank < 0 || cfg->tp_rank >= cfg->tp_size)
+    return fail(nullptr, ENERGON_ERR_CONFIG, "tp_size must be in [1,8] and 0 <= tp_rank < tp_size");
+  if (cfg->num_heads % cfg->tp_size || cfg->ffn % cfg->tp_size)
+    return fail(nullptr, ENERGON_ERR_CONFIG, "num_heads and ffn must be divisible by tp_size (SPEC.md:284)");
+  if (cfg->dtype != ENERGON_DTYPE_F32 && cfg->dtype != ENERGON_DTYPE_BF16)
+    return fail(nullptr, ENERGON_ERR_CONFIG, "dtype must be ENERGON_DTYPE_F32 or ENERGON_DTYPE_BF16");
+  if (cfg->causal != 0 && cfg->causal != 1) return fail(nullptr, ENERGON_ERR_CONFIG, "causal must be 0 or 1");
+  if (cfg->drce != 0 && cfg->drce != 1) return fail(nullptr, ENERGON_ERR_CONFIG, "drce must be 0 or 1");
+  if (!(cfg->ln_eps > 0.f)) return fail(nullptr, ENERGON_ERR_CONFIG, "ln_eps must be > 0");
+  const int d = cfg->hidden / cfg->num_heads;
+  if (cfg->hidden % 8 || d % 8 || (cfg->ffn / cfg->tp_size) % 8 || cfg->hidden > 12288)
+    return fail(nullptr, ENERGON_ERR_SHAPE,
+                "unsupported shape: hidden, head_dim and ffn/tp_size must be multiples of 8, hidden <= 12288");
+  return ENERGON_OK;
+}
+
+energon_status setup(energon_ctx* c) {
+  const energon_config& g = c->cfg;
+  c->k = g.tp_size;
+  c->r = g.tp_rank;
+  c->H = g.hidden;
+  c->h = g.num_heads;
+  c->d = g.hidden / g.num_heads;
+  c->F = g.ffn;
+  c->V = g.vocab;
+  c->Hk = c->H / c->k;
+  c->hk = c->h / c->k;
+  c->Fk = c->F / c->k;
+  c->bf16 = g.dtype == ENERGON_DTYPE_BF16;
+  c->act = c->bf16 ? 2 : 4;
+  memset(&c->stats, 0, sizeof(c->stats));
+  memset(&c->pacc, 0, sizeof(c->pacc));
+  CU(c, cudaSetDevice(g.device));
+  CU(c, cudaStreamCreateWithFlags(&c->load_stream, cudaStreamNonBlocking));
+  CU(c, cudaHostAlloc(&c->err_host, sizeof(int), cudaHostAllocMapped));
+  *c->err_host = 0;
+  CU(c, cudaHostGetDevicePointer(&c->err_dev, c->err_host, 0));
+  c->layers.resize(g.num_layers);
+  // workspace: every buffer is sized for max_tokens rows (padded rows when drce == 0)
+  const size_t R = (size_t)g.max_tokens, a = c->act;
+  int64_t* ws = &c->stats.workspace_bytes;
+  energon_status s;
+  if ((s = dalloc(c, &c->offsets, sizeof(int) * (ENERGON_MAX_BATCH + 1), ws)) ||
+      (s = dalloc(c, &c->pack_idx, sizeof(int) * R, ws)) || (s = dalloc(c, &c->pos, sizeof(int) * R, ws)) ||
+      (s = dalloc(c, &c->unpack_idx, sizeof(int) * R, ws)) || (s = dalloc(c, &c->X, sizeof(float) * R * c->H, ws)) ||
+      (s = dalloc(c, &c->A, a * R * c->H, ws)) || (s = dalloc(c, &c->QKV, a * R * 3 * c->Hk, ws)) ||
+      (s = dalloc(c, &c->Q, a * R * c->Hk, ws)) || (s = dalloc(c, &c->K, a * R * c->Hk, ws)) ||
+      (s = dalloc(c, &c->Vb, a * R * c->Hk, ws)) || (s = dalloc(c, &c->O, a * R * c->Hk, ws)) ||
+      (s = dalloc(c, &c->Ctx, a * R * c->Hk, ws)) || (s = dalloc(c, &c->P, a * R * c->H, ws)) ||
+      (s = dalloc(c, &c->G, a * R * c->Fk, ws)))
+    return s;
+  return ENERGON_OK;
+}
+
+void release(energon_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->cfg.device);
+  cudaDeviceSynchronize();
+  for (void* p : c->allocs) cudaFree(p);
+  c->allocs.clear();
+  if (c->err_host) cudaFreeHost(c->err_host);
+  if (c->load_stream) cudaStreamDestroy(c->load_stream);
+  for (cudaEvent_t e : c->pool) cudaEventDestroy(e);
+  if (c->nccl) ncclCommDestroy(c->nccl);
+  delete c;
+}
+
+// ----------------------------------------------------------------------------- weight loading
+template <typename Src, typename Dst>
+energon_status put_matrix_t(energon_ctx* c, const void* src, bool on_dev, int64_t src_rows, int64_t ld, int64_t row0,
+                            int64_t col0, int N, int K, void* dst, int64_t dst_row0) {
+  const Src* s = reinterpret_cast<const Src*>(src);
+  void* stage = nullptr;
+  if (!on_dev) {
+    const size_t bytes = sizeof(Src) * (size_t)src_rows * (size_t)ld;
+    CU(c, cudaMalloc(&stage, bytes));
+    CU(c, cudaMemcpyAsync(stage, src, bytes, cudaMemcpyHostToDevice, c->load_stream));
+    s = reinterpret_cast<const Src*>(stage);
+  }
+  launch_relayout<Src, Dst>(s, ld, row0, col0, N, K, reinterpret_cast<Dst*>(dst), K, dst_row0, c->load_stream);
+  c->stats.kernel_launches++;
+  CU(c, cudaGetLastError());
+  if (stage) {
+    CU(c, cudaStreamSynchronize(c->load_stream));
+    CU(c, cudaFree(stage));
+  }
+  return ENERGON_OK;
+}
+
+template <typename Src, typename Dst>
+energon_status put_vector_t(energon_ctx* c, const void* src, bool on_dev, int64_t src_n, int64_t off, int N, Dst* dst) {
+  const Src* s = reinterpret_cast<const Src*>(src);
+  void* stage = nullptr;
+  if (!on_dev) {
+    CU(c, cudaMalloc(&stage, sizeof(Src) * (size_t)src_n));
+    CU(c, cudaMemcpyAsync(stage, src, sizeof(Src) * (size_t)src_n, cudaMemcpyHostToDevice, c->load_stream));
+    s = reinterpret_cast<const Src*>(stage);
+  }
+  launch_convert_vec<Src, Dst>(s, off, N, dst, c->load_stream);
+  c->stats.kernel_launches++;
+  CU(c, cudaGetLastError());
+  if (stage) {
+    CU(c, cudaStreamSynchronize(c->load_stream));
+    CU(c, cudaFree(stage));
+  }
+  return ENERGON_OK;
+}
+
+// dispatch on (src dtype, ctx activation dtype)
+energon_status put_matrix(energon_ctx* c, int sd, const void* src, bool on_dev, int64_t src_rows, int64_t ld,
+                          int64_t row0, int64_t col0, int N, int K, void* dst, int64_t dst_row0) {
+  if (c->bf16) {
+    if (sd == ENERGON_DTYPE_F64) return put_matrix_t<double, bf16>(c, src, on_dev, src_rows, ld, row0, col0, N, K, dst, dst_row0);
+    if (sd == ENERGON_DTYPE_F32) return put_matrix_t<float, bf16>(c, src, on_dev, src_rows, ld, row0, col0, N, K, dst, dst_row0);
+    return put_matrix_t<bf16, bf16>(c, src, on_dev, src_rows, ld, row0, col0, N, K, dst, dst_row0);
+  }
+  if (sd == ENERGON_DTYPE_F64) return put_matrix_t<double, float>(c, src, on_dev, src_rows, ld, row0, col0, N, K, dst, dst_row0);
+  if (sd == ENERGON_DTYPE_F32) return put_matrix_t<float, float>(c, src, on_dev, src_rows, ld, row0, col0, N, K, dst, dst_row0);
+  return put_matrix_t<bf16, float>(c, src, on_dev, src_rows, ld, row0, col0, N, K, dst, dst_row0);
+}
+
+template <typename Dst>
+energon_status put_vector(energon_ctx* c, int sd, const void* src, bool on_dev, int64_t src_n, int64_t off, int N,
+                          Dst* dst) {
+  if (sd == ENERGON_DTYPE_F64) return put_vector_t<double, Dst>(c, src, on_dev, src_n, off, N, dst);
+  if (sd == ENERGON_DTYPE_F32) return put_vector_t<float, Dst>(c, src, on_dev, src_n, off, N, dst);
+  return put_vector_t<bf16, Dst>(c, src, on_dev, src_n, off, N, dst);
+}
+
+// ----------------------------------------------------------------------------- profiling scopes
+enum { P_GEMM = 0, P_ATTN = 1, P_MEM = 2, P_COMM = 3 };
+
+cudaEvent_t next_event(energon_ctx* c) {
+  if (c->pool_used == c->pool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    c->pool.push_back(e);
+  }
+  return c->pool[c->pool_used++];
+}
+
+struct Prof {
+  energon_ctx* c;
+  cudaStream_t st;
+  int cls;
+  double work;
+  cudaEvent_t a = nullptr;
+  Prof(energon_ctx* c_, cudaStream_t st_, int cls_, double work_) : c(c_), st(st_), cls(cls_), work(work_) {
+    if (c->prof) {
+      a = next_event(c);
+      cudaEventRecord(a, st);
+    }
+  }
+  ~Prof() {
+    if (c->prof) {
+      cudaEvent_t b = next_event(c);
+      cudaEventRecord(b, st);
+      c->recs.push_back({a, b, cls, work});
+    }
+  }
+};
+
+// ----------------------------------------------------------------------------- forward
+struct Call {
+  const int32_t* tokens;  // token entry (energon_forward)
+  const float* x_in;      // hidden entry (energon_forward_hidden)
+  const int32_t* lens;
+  int B, S, l0, l1, final_ln;
+  void* out;
+  bool out_f32;
+  cudaStream_t st;
+};
+
+energon_status check_ready(energon_ctx* c) {
+  if (!c->emb_loaded) return fail(c, ENERGON_ERR_NOT_LOADED, "embeddings not loaded");
+  for (size_t l = 0; l < c->layers.size(); ++l)
+    if (!c->layers[l].loaded) return fail(c, ENERGON_ERR_NOT_LOADED, "layer " + std::to_string(l) + " not loaded");
+  if (*c->err_host) return fail(c, ENERGON_ERR_TOKEN, "a token id outside [0, vocab) was seen by a previous forward");
+  return ENERGON_OK;
+}
+
+energon_status validate_call(energon_ctx* c, const Call& a, int64_t* T_out) {
+  if (!a.lens || !a.out) return fail(c, ENERGON_ERR_ARG, "seq_lens / out must not be NULL");
+  if (!a.tokens && !a.x_in) return fail(c, ENERGON_ERR_ARG, "tokens must not be NULL");
+  if (a.B < 1) return fail(c, ENERGON_ERR_ARG, "batch must be >= 1");
+  if (a.B > ENERGON_MAX_BATCH) return fail(c, ENERGON_ERR_CAPACITY, "batch exceeds ENERGON_MAX_BATCH");
+  if (a.S < 1 || a.S > c->cfg.max_seq)
+    return fail(c, ENERGON_ERR_LENGTH, "max_len must be in [1, max_seq] (SPEC.md:133)");
+  if ((int64_t)a.B * a.S > c->cfg.max_tokens)
+    return fail(c, ENERGON_ERR_CAPACITY, "batch * max_len exceeds max_tokens");
+  if (a.l0 < 0 || a.l1 > c->cfg.num_layers || a.l0 > a.l1) return fail(c, ENERGON_ERR_ARG, "bad layer range");
+  int64_t T = 0;
+  for (int b = 0; b < a.B; ++b) {
+    if (a.lens[b] < 1 || a.lens[b] > a.S)
+      return fail(c, ENERGON_ERR_LENGTH,
+                  "seq_lens[" + std::to_string(b) + "]=" + std::to_string(a.lens[b]) + " not in [1, max_len]");
+    T += a.lens[b];
+  }
+  *T_out = T;
+  return ENERGON_OK;
+}
+
+template <typename Act>
+energon_status allreduce(energon_ctx** cs, int n, int rows, cudaStream_t st) {
+  energon_ctx* c0 = cs[0];
+  if (c0->k == 1) return ENERGON_OK;
+  const size_t count = (size_t)rows * c0->H;
+  Prof p(c0, st, P_COMM, (double)count * c0->act);
+  if (c0->local_group) {
+    PtrList pl;
+    for (int i = 0; i < n; ++i) pl.p[i] = cs[i]->P;
+    launch_local_allreduce<Act>(pl, n, (int64_t)count, st);
+    c0->stats.kernel_launches++;
+  } else {
+    ncclResult_t e = ncclAllReduce(c0->P, c0->P, count, c0->bf16 ? ncclBfloat16 : ncclFloat, ncclSum, c0->nccl, st);
+    if (e != ncclSuccess) return fail(c0, ENERGON_ERR_NCCL, std::string("ncclAllReduce: ") + ncclGetErrorString(e));
+  }
+  for (int i = 0; i < n; ++i) cs[i]->stats.allreduce_calls++;
+  return ENERGON_OK;
+}
+
+template <typename Act>
+void gemm(energon_ctx* c, const CUtensorMap& tmA, const CUtensorMap* tmB, const void* A, const void* W,
+          const float* bias, void* D, int M, int N, int K, int epi, cudaStream_t st) {
+  Prof p(c, st, P_GEMM, 2.0 * M * N * K);
+  if constexpr (sizeof(Act) == 2) {
+    const int bn = tc_pick_bn(M, N);
+    launch_gemm_tc(tmA, tmB[bn == 256 ? 0 : 1], bn, bias, reinterpret_cast<bf16*>(D), M, N, K, epi, st);
+  } else {
+    launch_gemm_f32(reinterpret_cast<const float*>(A), reinterpret_cast<const float*>(W), bias,
+                    reinterpret_cast<float*>(D), M, N, K, epi, st);
+  }
+  c->stats.kernel_launches++;
+}
+
+template <typename Act>
+energon_status forward_t(energon_ctx** cs, int n, const Call& a, int64_t T) {
+  cudaStream_t st = a.st;
+  energon_ctx* c0 = cs[0];
+  const energon_config& g = c0->cfg;
+  const bool drce = g.drce == 1;
+  const int rows = drce ? (int)T : a.B * a.S;
+  const float eps = g.ln_eps;
+  const double act = (double)sizeof(Act), H = c0->H, Hk = c0->Hk;
+  LensParam lp;
+  double allowed = 0.0;  // sum over sequences of visible (query, key) pairs
+  for (int b = 0; b < a.B; ++b) {
+    lp.lens[b] = a.lens[b];
+    const double L = a.lens[b];
+    allowed += g.causal ? L * (L + 1) / 2 : L * L;
+  }
+
+  for (int i = 0; i < n; ++i) {
+    energon_ctx* c = cs[i];
+    c->stats.last_tokens = T;
+    c->stats.last_rows = rows;
+    {
+      Prof p(c, st, P_MEM, 4.0 * (a.B + 1) + 8.0 * T + 4.0 * a.B * a.S);
+      launch_index_maps(lp, a.B, a.S, c->offsets, c->pack_idx, c->pos, c->unpack_idx, st);
+    }
+    c->stats.kernel_launches++;
+    if (sizeof(Act) == 2 && c->tm_rows != rows) {
+      if (!make_tmap_kmajor(&c->tmA_A, c->A, rows, c->H, 128) ||
+          !make_tmap_kmajor(&c->tmA_Ctx, c->Ctx, rows, c->Hk, 128) ||
+          !make_tmap_kmajor(&c->tmA_G, c->G, rows, c->Fk, 128))
+        return fail(c, ENERGON_ERR_CUDA, "cuTensorMapEncodeTiled failed for an activation operand");
+      c->tm_rows = rows;
+    }
+    const int* pidx = drce ? c->pack_idx : nullptr;
+    const LayerDev& L0 = c->layers[a.l0 < g.num_layers ? a.l0 : 0];
+    const float* g1 = a.l0 < a.l1 ? L0.ln1g : c->lnf_g;
+    const float* b1 = a.l0 < a.l1 ? L0.ln1b : c->lnf_b;
+    {
+      // reads: ids + 2 embedding rows (or one fp32 row); writes: X (fp32) + A
+      Prof p(c, st, P_MEM, a.tokens ? rows * (4.0 + H * (2 * act + 4 + act)) : rows * H * (4 + 4 + act));
+      if (a.tokens)
+        launch_embed_ln<Act>(a.tokens, pidx, rows, a.S, c->V, c->H, reinterpret_cast<const Act*>(c->tok_emb),
+                             reinterpret_cast<const Act*>(c->pos_emb), g1, b1, eps, c->X, reinterpret_cast<Act*>(c->A),
+                             c->err_dev, st);
+      else
+        launch_gather_ln<Act>(a.x_in, pidx, rows, c->H, g1, b1, eps, c->X, reinterpret_cast<Act*>(c->A), st);
+    }
+    c->stats.kernel_launches++;
+  }
+
+  for (int l = a.l0; l < a.l1; ++l) {
+    // ---- attention module: column-parallel QKV, local heads, row-parallel out-proj
+    for (int i = 0; i < n; ++i) {
+      energon_ctx* c = cs[i];
+      const LayerDev& L = c->layers[l];
+      const int* pidx = drce ? c->pack_idx : nullptr;
+      gemm<Act>(c, c->tmA_A, L.tm_qkv, c->A, L.wqkv, L.bqkv, c->QKV, rows, 3 * c->Hk, c->H, EPI_BIAS, st);
+      {
+        Prof p(c, st, P_MEM, 2.0 * rows * 3 * Hk * act);
+        launch_unpack_qkv<Act>(reinterpret_cast<const Act*>(c->QKV), pidx, rows, a.S, c->hk, c->d,
+                               reinterpret_cast<Act*>(c->Q), reinterpret_cast<Act*>(c->K), reinterpret_cast<Act*>(c->Vb),
+                               st);
+      }
+      {
+        Prof p(c, st, P_ATTN, 4.0 * c->d * allowed * c->hk);
+        launch_attention<Act>(reinterpret_cast<const Act*>(c->Q), reinterpret_cast<const Act*>(c->K),
+                              reinterpret_cast<const Act*>(c->Vb), reinterpret_cast<Act*>(c->O), lp, a.B, c->hk, a.S,
+                              c->d, g.causal, st);
+      }
+      {
+        Prof p(c, st, P_MEM, 2.0 * rows * Hk * act);
+        launch_repack<Act>(reinterpret_cast<const Act*>(c->O), pidx, c->unpack_idx, rows, a.S, c->hk, c->d,
+                           reinterpret_cast<Act*>(c->Ctx), st);
+      }
+      c->stats.kernel_launches += 3;
+      gemm<Act>(c, c->tmA_Ctx, L.tm_o, c->Ctx, L.wo, nullptr, c->P, rows, c->H, c->Hk, EPI_NONE, st);
+    }
+    energon_status s = allreduce<Act>(cs, n, rows, st);
+    if (s) return s;
+    // ---- MLP module: column-parallel W1 (+GeLU), row-parallel W2
+    for (int i = 0; i < n; ++i) {
+      energon_ctx* c = cs[i];
+      const LayerDev& L = c->layers[l];
+      {
+        Prof p(c, st, P_MEM, rows * H * (8.0 + 2 * act));
+        launch_residual_ln<Act>(c->X, reinterpret_cast<const Act*>(c->P), L.bo, rows, c->H, L.ln2g, L.ln2b, eps,
+                                reinterpret_cast<Act*>(c->A), st);
+      }
+      c->stats.kernel_launches++;
+      gemm<Act>(c, c->tmA_A, L.tm_1, c->A, L.w1, L.b1, c->G, rows, c->Fk, c->H, EPI_BIAS_GELU, st);
+      gemm<Act>(c, c->tmA_G, L.tm_2, c->G, L.w2, nullptr, c->P, rows, c->H, c->Fk, EPI_NONE, st);
+    }
+    s = allreduce<Act>(cs, n, rows, st);
+    if (s) return s;
+    for (int i = 0; i < n; ++i) {
+      energon_ctx* c = cs[i];
+      const LayerDev& L = c->layers[l];
+      const bool last = (l + 1 == a.l1);
+      const LayerDev& Ln = c->layers[last ? l : l + 1];
+      {
+        Prof p(c, st, P_MEM, rows * H * (8.0 + (last ? 1 : 2) * act));
+        launch_residual_ln<Act>(c->X, reinterpret_cast<const Act*>(c->P), L.b2, rows, c->H, Ln.ln1g, Ln.ln1b, eps,
+                                last ? nullptr : reinterpret_cast<Act*>(c->A), st);
+      }
+      c->stats.kernel_launches++;
+    }
+  }
+
+  // ---- a13: final LN + unpack (every rank holds the replicated result; a local group writes once)
+  energon_ctx* c = cs[0];
+  const int apply_ln = a.final_ln;
+  {
+    Prof p(c, st, P_MEM, 4.0 * a.B * a.S + 4.0 * T * H + (double)a.B * a.S * H * (a.out_f32 ? 4 : act));
+    if (a.out_f32)
+      launch_final_ln_unpack<float>(c->X, c->unpack_idx, drce ? 0 : 1, a.B * a.S, c->H, c->lnf_g, c->lnf_b, eps,
+                                    apply_ln, reinterpret_cast<float*>(a.out), st);
+    else
+      launch_final_ln_unpack<Act>(c->X, c->unpack_idx, drce ? 0 : 1, a.B * a.S, c->H, c->lnf_g, c->lnf_b, eps, apply_ln,
+                                  reinterpret_cast<Act*>(a.out), st);
+  }
+  c->stats.kernel_launches++;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(c0, e, "kernel launch");
+  for (int i = 0; i < n; ++i) cs[i]->stats.forwards++;
+  return ENERGON_OK;
+}
+
+energon_status run(energon_ctx** cs, int n, const Call& a) {
+  energon_ctx* c0 = cs[0];
+  cudaError_t e = cudaSetDevice(c0->cfg.device);
+  if (e != cudaSuccess) return cuda_fail(c0, e, "cudaSetDevice");
+  for (int i = 0; i < n; ++i) {
+    energon_status s = check_ready(cs[i]);
+    if (s) return s;
+  }
+  int64_t T = 0;
+  energon_status s = validate_call(c0, a, &T);
+  if (s) return s;
+  return c0->bf16 ? forward_t<bf16>(cs, n, a, T) : forward_t<float>(cs, n, a, T);
+}
+
+}  // namespace
+
+// ============================================================================ C ABI
+extern "C" {
+
+const char* energon_status_string(energon_status s) {
+  switch (s) {
+    case ENERGON_OK: return "ENERGON_OK";
+    case ENERGON_ERR_ARG: return "ENERGON_ERR_ARG";
+    case ENERGON_ERR_CONFIG: return "ENERGON_ERR_CONFIG";
+    case ENERGON_ERR_SHAPE: return "ENERGON_ERR_SHAPE";
+    case ENERGON_ERR_LENGTH: return "ENERGON_ERR_LENGTH";
+    case ENERGON_ERR_TOKEN: return "ENERGON_ERR_TOKEN";
+    case ENERGON_ERR_CAPACITY: return "ENERGON_ERR_CAPACITY";
+    case ENERGON_ERR_NOT_LOADED: return "ENERGON_ERR_NOT_LOADED";
+    case ENERGON_ERR_CUDA: return "ENERGON_ERR_CUDA";
+    case ENERGON_ERR_NCCL: return "ENERGON_ERR_NCCL";
+    case ENERGON_ERR_OOM: return "ENERGON_ERR_OOM";
+  }
+  return "ENERGON_ERR_UNKNOWN";
+}
+
+const char* energon_last_error(const energon_ctx* ctx) { return ctx ? ctx->err.c_str() : g_last_error.c_str(); }
+
+energon_status energon_get_unique_id(void* out) {
+  if (!out) return fail(nullptr, ENERGON_ERR_ARG, "out is NULL");
+  ncclUniqueId id;
+  ncclResult_t e = ncclGetUniqueId(&id);
+  if (e != ncclSuccess) return fail(nullptr, ENERGON_ERR_NCCL, std::string("ncclGetUniqueId: ") + ncclGetErrorString(e));
+  memcpy(out, &id, sizeof(id));
+  return ENERGON_OK;
+}
+
+energon_status energon_init(const energon_config* cfg, const void* uid, energon_ctx** out) {
+  if (!out) return fail(nullptr, ENERGON_ERR_ARG, "out is NULL");
+  *out = nullptr;
+  energon_status s = validate_config(cfg);
+  if (s) return s;
+  if (cfg->tp_size > 1 && !uid) return fail(nullptr, ENERGON_ERR_ARG, "nccl_unique_id required when tp_size > 1");
+  energon_ctx* c = new energon_ctx();
+  c->cfg = *cfg;
+  if ((s = setup(c))) {
+    g_last_error = c->err;
+    release(c);
+    return s;
+  }
+  if (cfg->tp_size > 1) {
+    ncclUniqueId id;
+    memcpy(&id, uid, sizeof(id));
+    ncclResult_t e = ncclCommInitRank(&c->nccl, cfg->tp_size, id, cfg->tp_rank);
+    if (e != ncclSuccess) {
+      c->nccl = nullptr;
+      fail(c, ENERGON_ERR_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(e));
+      release(c);
+      return ENERGON_ERR_NCCL;
+    }
+  }
+  *out = c;
+  return ENERGON_OK;
+}
+
+energon_status energon_init_local_group(const energon_config* cfg, int32_t k, energon_ctx** out_k) {
+  if (!out_k || !cfg) return fail(nullptr, ENERGON_ERR_ARG, "NULL argument");
+  if (k < 1 || k > 8) return fail(nullptr, ENERGON_ERR_CONFIG, "k must be in [1, 8]");
+  for (int i = 0; i < k; ++i) out_k[i] = nullptr;
+  for (int i = 0; i < k; ++i) {
+    energon_config ci = *cfg;
+    ci.tp_size = k;
+    ci.tp_rank = i;
+    energon_status s = validate_config(&ci);
+    if (s == ENERGON_OK) {
+      energon_ctx* c = new energon_ctx();
+      c->cfg = ci;
+      c->local_group = true;
+      s = setup(c);
+      if (s) {
+        g_last_error = c->err;
+        release(c);
+      } else {
+        out_k[i] = c;
+      }
+    }
+    if (s) {
+      for (int j = 0; j < i; ++j) {
+        release(out_k[j]);
+        out_k[j] = nullptr;
+      }
+      return s;
+    }
+  }
+  return ENERGON_OK;
+}
+
+energon_status energon_load_embeddings(energon_ctx* c, const void* tok_emb, const void* pos_emb, const void* lnf_g,
+                                       const void* lnf_b, int32_t sd, int32_t on_dev) {
+  if (!c || !tok_emb || !pos_emb || !lnf_g || !lnf_b) return fail(c, ENERGON_ERR_ARG, "NULL argument");
+  if (sd < 0 || sd > 2) return fail(c, ENERGON_ERR_ARG, "src_dtype must be F32, BF16 or F64");
+  CU(c, cudaSetDevice(c->cfg.device));
+  const int64_t VH = (int64_t)c->V * c->H, PH = (int64_t)c->cfg.max_seq * c->H;
+  energon_status s;
+  if (!c->tok_emb) {
+    if ((s = dalloc(c, &c->tok_emb, c->act * VH, &c->stats.weight_bytes)) ||
+        (s = dalloc(c, &c->pos_emb, c->act * PH, &c->stats.weight_bytes)) ||
+        (s = dalloc(c, &c->lnf_g, sizeof(float) * c->H, &c->stats.weight_bytes)) ||
+        (s = dalloc(c, &c->lnf_b, sizeof(float) * c->H, &c->stats.weight_bytes)))
+      return s;
+  }
+  const bool dev = on_dev != 0;
+  if (c->bf16) {
+    if ((s = put_vector<bf16>(c, sd, tok_emb, dev, VH, 0, (int)VH, reinterpret_cast<bf16*>(c->tok_emb))) ||
+        (s = put_vector<bf16>(c, sd, pos_emb, dev, PH, 0, (int)PH, reinterpret_cast<bf16*>(c->pos_emb))))
+      return s;
+  } else {
+    if ((s = put_vector<float>(c, sd, tok_emb, dev, VH, 0, (int)VH, reinterpret_cast<float*>(c->tok_emb))) ||
+        (s = put_vector<float>(c, sd, pos_emb, dev, PH, 0, (int)PH, reinterpret_cast<float*>(c->pos_emb))))
+      return s;
+  }
+  if ((s = put_vector<float>(c, sd, lnf_g, dev, c->H, 0, c->H, c->lnf_g)) ||
+      (s = put_vector<float>(c, sd, lnf_b, dev, c->H, 0, c->H, c->lnf_b)))
+    return s;
+  CU(c, cudaStreamSynchronize(c->load_stream));
+  c->emb_loaded = true;
+  return ENERGON_OK;
+}
+
+energon_status energon_load_layer_weights(energon_ctx* c, int32_t layer, const energon_layer_weights* w, int32_t sd,
+                                          int32_t on_dev, int32_t layout) {
+  if (!c || !w) return fail(c, ENERGON_ERR_ARG, "NULL argument");
+  if (layer < 0 || layer >= c->cfg.num_layers) return fail(c, ENERGON_ERR_ARG, "layer index out of range");
+  if (sd < 0 || sd > 2) return fail(c, ENERGON_ERR_ARG, "src_dtype must be F32, BF16 or F64");
+  if (layout != ENERGON_FULL && layout != ENERGON_RANK_SHARD) return fail(c, ENERGON_ERR_ARG, "bad src_layout");
+  const void* ptrs[16] = {w->wq, w->wk, w->wv, w->wo, w->bq, w->bk, w->bv, w->bo,
+                          w->w1, w->b1, w->w2, w->b2, w->ln1_g, w->ln1_b, w->ln2_g, w->ln2_b};
+  for (int i = 0; i < 16; ++i)
+    if (!ptrs[i]) return fail(c, ENERGON_ERR_ARG, "a layer weight pointer is NULL");
+  CU(c, cudaSetDevice(c->cfg.device));
+  LayerDev& L = c->layers[layer];
+  const int H = c->H, F = c->F, Hk = c->Hk, Fk = c->Fk, r = c->r;
+  const size_t a = c->act;
+  energon_status s;
+  int64_t* wb = &c->stats.weight_bytes;
+  if (!L.wqkv) {
+    if ((s = dalloc(c, &L.wqkv, a * 3 * Hk * H, wb)) || (s = dalloc(c, &L.wo, a * (size_t)H * Hk, wb)) ||
+        (s = dalloc(c, &L.w1, a * (size_t)Fk * H, wb)) || (s = dalloc(c, &L.w2, a * (size_t)H * Fk, wb)) ||
+        (s = dalloc(c, &L.bqkv, sizeof(float) * 3 * Hk, wb)) || (s = dalloc(c, &L.bo, sizeof(float) * H, wb)) ||
+        (s = dalloc(c, &L.b1, sizeof(float) * Fk, wb)) || (s = dalloc(c, &L.b2, sizeof(float) * H, wb)) ||
+        (s = dalloc(c, &L.ln1g, sizeof(float) * H, wb)) || (s = dalloc(c, &L.ln1b, sizeof(float) * H, wb)) ||
+        (s = dalloc(c, &L.ln2g, sizeof(float) * H, wb)) || (s = dalloc(c, &L.ln2b, sizeof(float) * H, wb)))
+      return s;
+  }
+  const bool full = layout == ENERGON_FULL, dev = on_dev != 0;
+  // column-parallel: this rank's heads / FFN columns; row-parallel: the matching rows
+  const int64_t qk_ld = full ? H : Hk, qk_col0 = full ? (int64_t)r * Hk : 0;
+  const int64_t o_rows = full ? H : Hk, o_row0 = full ? (int64_t)r * Hk : 0;
+  const int64_t w1_ld = full ? F : Fk, w1_col0 = full ? (int64_t)r * Fk : 0;
+  const int64_t w2_rows = full ? F : Fk, w2_row0 = full ? (int64_t)r * Fk : 0;
+  const int64_t bq_n = full ? H : Hk, bq_off = full ? (int64_t)r * Hk : 0;
+  const int64_t b1_n = full ? F : Fk, b1_off = full ? (int64_t)r * Fk : 0;
+  if ((s = put_matrix(c, sd, w->wq, dev, H, qk_ld, 0, qk_col0, Hk, H, L.wqkv, 0)) ||
+      (s = put_matrix(c, sd, w->wk, dev, H, qk_ld, 0, qk_col0, Hk, H, L.wqkv, Hk)) ||
+      (s = put_matrix(c, sd, w->wv, dev, H, qk_ld, 0, qk_col0, Hk, H, L.wqkv, 2 * Hk)) ||
+      (s = put_matrix(c, sd, w->wo, dev, o_rows, H, o_row0, 0, H, Hk, L.wo, 0)) ||
+      (s = put_matrix(c, sd, w->w1, dev, H, w1_ld, 0, w1_col0, Fk, H, L.w1, 0)) ||
+      (s = put_matrix(c, sd, w->w2, dev, w2_rows, H, w2_row0, 0, H, Fk, L.w2, 0)) ||
+      (s = put_vector<float>(c, sd, w->bq, dev, bq_n, bq_off, Hk, L.bqkv)) ||
+      (s = put_vector<float>(c, sd, w->bk, dev, bq_n, bq_off, Hk, L.bqkv + Hk)) ||
+      (s = put_vector<float>(c, sd, w->bv, dev, bq_n, bq_off, Hk, L.bqkv + 2 * Hk)) ||
+      (s = put_vector<float>(c, sd, w->bo, dev, H, 0, H, L.bo)) ||
+      (s = put_vector<float>(c, sd, w->b1, dev, b1_n, b1_off, Fk, L.b1)) ||
+      (s = put_vector<float>(c, sd, w->b2, dev, H, 0, H, L.b2)) ||
+      (s = put_vector<float>(c, sd, w->ln1_g, dev, H, 0, H, L.ln1g)) ||
+      (s = put_vector<float>(c, sd, w->ln1_b, dev, H, 0, H, L.ln1b)) ||
+      (s = put_vector<float>(c, sd, w->ln2_g, dev, H, 0, H, L.ln2g)) ||
+      (s = put_vector<float>(c, sd, w->ln2_b, dev, H, 0, H, L.ln2b)))
+    return s;
+  CU(c, cudaStreamSynchronize(c->load_stream));
+  if (c->bf16) {
+    const int boxes[2] = {256, 128};
+    for (int i = 0; i < 2; ++i) {
+      if (!make_tmap_kmajor(&L.tm_qkv[i], L.wqkv, 3 * Hk, H, boxes[i]) ||
+          !make_tmap_kmajor(&L.tm_o[i], L.wo, H, Hk, boxes[i]) || !make_tmap_kmajor(&L.tm_1[i], L.w1, Fk, H, boxes[i]) ||
+          !make_tmap_kmajor(&L.tm_2[i], L.w2, H, Fk, boxes[i]))
+        return fail(c, ENERGON_ERR_CUDA, "cuTensorMapEncodeTiled failed for a weight operand");
+    }
+  }
+  L.loaded = true;
+  return ENERGON_OK;
+}
+
+energon_status energon_forward(energon_ctx* c, const int32_t* tokens, const int32_t* lens, int32_t B, int32_t S,
+                               void* out, void* stream) {
+  if (!c) return fail(nullptr, ENERGON_ERR_ARG, "ctx is NULL");
+  if (!tokens) return fail(c, ENERGON_ERR_ARG, "tokens is NULL");
+  Call a{tokens, nullptr, lens, B, S, 0, c->cfg.num_layers, c->cfg.final_ln, out, false, (cudaStream_t)stream};
+  energon_ctx* cs[1] = {c};
+  return run(cs, 1, a);
+}
+
+energon_status energon_forward_group(energon_ctx** cs, int32_t k, const int32_t* tokens, const int32_t* lens,
+                                     int32_t B, int32_t S, void* out, void* stream) {
+  if (!cs || k < 1 || k > 8) return fail(nullptr, ENERGON_ERR_ARG, "bad context list");
+  for (int i = 0; i < k; ++i)
+    if (!cs[i] || cs[i]->cfg.tp_size != k || cs[i]->cfg.tp_rank != i || (k > 1 && !cs[i]->local_group))
+      return fail(nullptr, ENERGON_ERR_ARG, "contexts must be ranks 0..k-1 of one local group");
+  if (!tokens) return fail(cs[0], ENERGON_ERR_ARG, "tokens is NULL");
+  Call a{tokens, nullptr, lens, B, S, 0, cs[0]->cfg.num_layers, cs[0]->cfg.final_ln, out, false, (cudaStream_t)stream};
+  return run(cs, k, a);
+}
+
+energon_status energon_forward_hidden(energon_ctx* c, const float* x, const int32_t* lens, int32_t B, int32_t S,
+                                      int32_t l0, int32_t l1, int32_t apply_final_ln, float* out, void* stream) {
+  if (!c) return fail(nullptr, ENERGON_ERR_ARG, "ctx is NULL");
+  if (!x) return fail(c, ENERGON_ERR_ARG, "x is NULL");
+  Call a{nullptr, x, lens, B, S, l0, l1, apply_final_ln, out, true, (cudaStream_t)stream};
+  energon_ctx* cs[1] = {c};
+  return run(cs, 1, a);
+}
+
+energon_status energon_sync(energon_ctx* c) {
+  if (!c) return fail(nullptr, ENERGON_ERR_ARG, "ctx is NULL");
+  CU(c, cudaSetDevice(c->cfg.device));
+  CU(c, cudaDeviceSynchronize());
+  if (c->nccl) {
+    ncclResult_t ae = ncclSuccess;
+    ncclCommGetAsyncError(c->nccl, &ae);
+    if (ae != ncclSuccess) return fail(c, ENERGON_ERR_NCCL, std::string("NCCL async error: ") + ncclGetErrorString(ae));
+  }
+  if (*c->err_host) {
+    *c->err_host = 0;
+    return fail(c, ENERGON_ERR_TOKEN, "a token id outside [0, vocab) was seen on the device (SPEC.md:151)");
+  }
+  return ENERGON_OK;
+}
+
+energon_status energon_get_stats(const energon_ctx* c, energon_stats* out) {
+  if (!c || !out) return fail(nullptr, ENERGON_ERR_ARG, "NULL argument");
+  *out = c->stats;
+  return ENERGON_OK;
+}
+
+void energon_destroy(energon_ctx* c) { release(c); }
+
+energon_status energon_set_profiling(energon_ctx* c, int32_t enable) {
+  if (!c) return fail(nullptr, ENERGON_ERR_ARG, "ctx is NULL");
+  CU(c, cudaSetDevice(c->cfg.device));
+  if (enable) {
+    CU(c, cudaDeviceSynchronize());
+    c->recs.clear();
+    c->pool_used = 0;
+    memset(&c->pacc, 0, sizeof(c->pacc));
+  }
+  c->prof = enable != 0;
+  return ENERGON_OK;
+}
+
+energon_status energon_get_profile(energon_ctx* c, energon_profile* out) {
+  if (!c || !out) return fail(c, ENERGON_ERR_ARG, "NULL argument");
+  CU(c, cudaSetDevice(c->cfg.device));
+  for (auto& r : c->recs) {
+    CU(c, cudaEventSynchronize(r.b));
+    float ms = 0.f;
+    CU(c, cudaEventElapsedTime(&ms, r.a, r.b));
+    energon_profile& p = c->pacc;
+    switch (r.cls) {
+      case P_GEMM: p.gemm_ms += ms; p.gemm_flops += r.work; p.gemm_launches++; break;
+      case P_ATTN: p.attn_ms += ms; p.attn_flops += r.work; p.attn_launches++; break;
+      case P_MEM: p.mem_ms += ms; p.mem_bytes += r.work; p.mem_launches++; break;
+      default: p.comm_ms += ms; p.comm_bytes += r.work; p.comm_calls++; break;
+    }
+  }
+  c->recs.clear();
+  c->pool_used = 0;
+  *out = c->pacc;
+  return ENERGON_OK;
+}
+
+energon_status energon_index_maps(const int32_t* lens, int32_t B, int32_t S, int32_t* offsets, int32_t* pack_idx,
+                                  int32_t* pos, int32_t* unpack_idx, void* stream) {
+  if (!lens || !offsets || !pack_idx || !pos || !unpack_idx) return fail(nullptr, ENERGON_ERR_ARG, "NULL argument");
+  if (B < 1 || B > ENERGON_MAX_BATCH || S < 1) return fail(nullptr, ENERGON_ERR_ARG, "bad batch / max_len");
+  LensParam lp;
+  for (int b = 0; b < B; ++b) {
+    if (lens[b] < 1 || lens[b] > S) return fail(nullptr, ENERGON_ERR_LENGTH, "seq_lens not in [1, max_len]");
+    lp.lens[b] = lens[b];
+  }
+  launch_index_maps(lp, B, S, offsets, pack_idx, pos, unpack_idx, (cudaStream_t)stream);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(nullptr, e, "index_maps");
+  return ENERGON_OK;
+}
+
+energon_status energon_gemm(int32_t dtype, const void* A, const void* W, const float* bias, void* D, int32_t M,
+                            int32_t N, int32_t K, int32_t epi, void* stream) {
+  if (!A || !W || !D) return fail(nullptr, ENERGON_ERR_ARG, "NULL argument");
+  if (M < 1 || N < 1 || K < 1 || epi < 0 || epi > 2 || (epi > 0 && !bias))
+    return fail(nullptr, ENERGON_ERR_ARG, "bad GEMM arguments");
+  if (dtype == ENERGON_DTYPE_F32) {
+    launch_gemm_f32(reinterpret_cast<const float*>(A), reinterpret_cast<const float*>(W), bias,
+                    reinterpret_cast<float*>(D), M, N, K, epi, (cudaStream_t)stream);
+  } else if (dtype == ENERGON_DTYPE_BF16) {
+    if (K % 8 || N % 8) return fail(nullptr, ENERGON_ERR_SHAPE, "bf16 GEMM needs K and N multiples of 8");
+    const int bn = tc_pick_bn(M, N);
+    CUtensorMap ta, tb;
+    if (!make_tmap_kmajor(&ta, A, M, K, 128) || !make_tmap_kmajor(&tb, W, N, K, bn))
+      return fail(nullptr, ENERGON_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+    launch_gemm_tc(ta, tb, bn, bias, reinterpret_cast<bf16*>(D), M, N, K, epi, (cudaStream_t)stream);
+  } else {
+    return fail(nullptr, ENERGON_ERR_ARG, "dtype must be F32 or BF16");
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(nullptr, e, "gemm");
+  return ENERGON_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,229 @@
+"""Thin ctypes binding of the energon C ABI (include/energon.h).
+
+Argument marshalling only: every step of the forward pass runs in the CUDA kernels of
+libenergon.so.  torch is used for device memory, streams and process groups.  There is no
+fallback: if the library is missing or the device is not a B200 this module raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+SO_PATH = os.path.join(HERE, "lib", "libenergon.so")
+
+ENERGON_OK = 0
+STATUS = {0: "ENERGON_OK", -1: "ENERGON_ERR_ARG", -2: "ENERGON_ERR_CONFIG", -3: "ENERGON_ERR_SHAPE",
+          -4: "ENERGON_ERR_LENGTH", -5: "ENERGON_ERR_TOKEN", -6: "ENERGON_ERR_CAPACITY",
+          -7: "ENERGON_ERR_NOT_LOADED", -8: "ENERGON_ERR_CUDA", -9: "ENERGON_ERR_NCCL", -10: "ENERGON_ERR_OOM"}
+DTYPE_F32, DTYPE_BF16, DTYPE_F64 = 0, 1, 2
+FULL, RANK_SHARD = 0, 1
+MAX_BATCH = 1024
+LAYER_TENSORS = ("wq", "wk", "wv", "wo", "bq", "bk", "bv", "bo",
+                 "w1", "b1", "w2", "b2", "ln1_g", "ln1_b", "ln2_g", "ln2_b")
+
+# symbols include/energon.h declares (checked by tests/test_abi.py)
+EXPORTS = ("energon_get_unique_id", "energon_init", "energon_init_local_group", "energon_load_embeddings",
+           "energon_load_layer_weights", "energon_forward", "energon_forward_group", "energon_forward_hidden",
+           "energon_sync", "energon_get_stats", "energon_last_error", "energon_status_string", "energon_destroy",
+           "energon_index_maps", "energon_gemm", "energon_set_profiling", "energon_get_profile")
+
+
+class EnergonError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class Config(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int32) for n in ("num_layers", "hidden", "num_heads", "ffn", "vocab", "max_seq",
+                                              "causal", "dtype", "drce", "tp_size", "tp_rank", "device",
+                                              "max_tokens", "final_ln")] + [("ln_eps", ctypes.c_float)]
+
+
+class LayerWeights(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_void_p) for n in LAYER_TENSORS]
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int64) for n in ("forwards", "allreduce_calls", "kernel_launches", "last_tokens",
+                                              "last_rows", "weight_bytes", "workspace_bytes")]
+
+
+class Profile(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_double) for n in ("gemm_ms", "attn_ms", "mem_ms", "comm_ms", "gemm_flops",
+                                               "attn_flops", "mem_bytes", "comm_bytes")] + \
+               [(n, ctypes.c_int64) for n in ("gemm_launches", "attn_launches", "mem_launches", "comm_calls")]
+
+
+_lib = None
+
+
+def load_library(path: str = SO_PATH):
+    """dlopen libenergon.so and declare every prototype.  Raises if it is absent (no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"{path} not built: run `python -m paper_2209_02341_b200.build` "
+                          "(the CUDA library is required; there is no CPU fallback)")
+    L = ctypes.CDLL(path)
+    P, I32, St = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int
+    L.energon_get_unique_id.argtypes = [P]
+    L.energon_init.argtypes = [ctypes.POINTER(Config), P, ctypes.POINTER(P)]
+    L.energon_init_local_group.argtypes = [ctypes.POINTER(Config), I32, ctypes.POINTER(P)]
+    L.energon_load_embeddings.argtypes = [P, P, P, P, P, I32, I32]
+    L.energon_load_layer_weights.argtypes = [P, I32, ctypes.POINTER(LayerWeights), I32, I32, I32]
+    L.energon_forward.argtypes = [P, P, ctypes.POINTER(ctypes.c_int32), I32, I32, P, P]
+    L.energon_forward_group.argtypes = [ctypes.POINTER(P), I32, P, ctypes.POINTER(ctypes.c_int32), I32, I32, P, P]
+    L.energon_forward_hidden.argtypes = [P, P, ctypes.POINTER(ctypes.c_int32), I32, I32, I32, I32, I32, P, P]
+    L.energon_sync.argtypes = [P]
+    L.energon_get_stats.argtypes = [P, ctypes.POINTER(Stats)]
+    L.energon_last_error.argtypes = [P]
+    L.energon_last_error.restype = ctypes.c_char_p
+    L.energon_status_string.argtypes = [St]
+    L.energon_status_string.restype = ctypes.c_char_p
+    L.energon_destroy.argtypes = [P]
+    L.energon_destroy.restype = None
+    L.energon_index_maps.argtypes = [ctypes.POINTER(ctypes.c_int32), I32, I32, P, P, P, P, P]
+    L.energon_gemm.argtypes = [I32, P, P, P, P, I32, I32, I32, I32, P]
+    L.energon_set_profiling.argtypes = [P, I32]
+    L.energon_get_profile.argtypes = [P, ctypes.POINTER(Profile)]
+    for name in EXPORTS:
+        fn = getattr(L, name)
+        if fn.restype is ctypes.c_int:  # default restype: energon_status
+            fn.restype = St
+    _lib = L
+    return L
+
+
+def _check(status: int, ctx=None):
+    if status != ENERGON_OK:
+        msg = load_library().energon_last_error(ctx).decode()
+        raise EnergonError(status, msg)
+
+
+def _lens(seq_lens):
+    arr = (ctypes.c_int32 * len(seq_lens))(*[int(x) for x in seq_lens])
+    return arr
+
+
+def _stream(stream):
+    if stream is None:
+        import torch
+        return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    if isinstance(stream, int):
+        return ctypes.c_void_p(stream)
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def _src_dtype(t):
+    import torch
+    return {torch.float32: DTYPE_F32, torch.bfloat16: DTYPE_BF16, torch.float64: DTYPE_F64}[t.dtype]
+
+
+def make_config(num_layers, hidden, num_heads, ffn, vocab, max_seq, max_tokens, dtype="bf16", causal=1, drce=1,
+                tp_size=1, tp_rank=0, device=0, final_ln=1, ln_eps=1e-5) -> Config:
+    return Config(num_layers, hidden, num_heads, ffn, vocab, max_seq, causal,
+                  DTYPE_BF16 if dtype == "bf16" else DTYPE_F32, drce, tp_size, tp_rank, device, max_tokens,
+                  final_ln, ln_eps)
+
+
+# ----------------------------------------------------------------------------- ABI wrappers (same names)
+def energon_get_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(load_library().energon_get_unique_id(buf))
+    return buf.raw
+
+
+def energon_init(cfg: Config, unique_id: bytes | None = None) -> ctypes.c_void_p:
+    ctx = ctypes.c_void_p()
+    uid = ctypes.create_string_buffer(unique_id, 128) if unique_id is not None else None
+    _check(load_library().energon_init(ctypes.byref(cfg), uid, ctypes.byref(ctx)))
+    return ctx
+
+
+def energon_init_local_group(cfg: Config, k: int) -> list:
+    arr = (ctypes.c_void_p * k)()
+    _check(load_library().energon_init_local_group(ctypes.byref(cfg), k, arr))
+    return [ctypes.c_void_p(arr[i]) for i in range(k)]
+
+
+def energon_load_embeddings(ctx, tok_emb, pos_emb, lnf_g, lnf_b):
+    """torch tensors (all the same dtype, all on the GPU or all on the host)."""
+    on_dev = int(tok_emb.is_cuda)
+    _check(load_library().energon_load_embeddings(ctx, _ptr(tok_emb), _ptr(pos_emb), _ptr(lnf_g), _ptr(lnf_b),
+                                                  _src_dtype(tok_emb), on_dev), ctx)
+
+
+def energon_load_layer_weights(ctx, layer: int, w: dict, layout: int = FULL):
+    """w: dict name -> torch tensor ([in, out] row-major, one dtype, one device)."""
+    first = w["wq"]
+    lw = LayerWeights(*[w[n].data_ptr() for n in LAYER_TENSORS])
+    _check(load_library().energon_load_layer_weights(ctx, layer, ctypes.byref(lw), _src_dtype(first),
+                                                     int(first.is_cuda), layout), ctx)
+
+
+def energon_forward(ctx, tokens, seq_lens, out, stream=None):
+    B, S = tokens.shape
+    _check(load_library().energon_forward(ctx, _ptr(tokens), _lens(seq_lens), B, S, _ptr(out), _stream(stream)), ctx)
+
+
+def energon_forward_group(ctxs, tokens, seq_lens, out, stream=None):
+    B, S = tokens.shape
+    arr = (ctypes.c_void_p * len(ctxs))(*[c.value for c in ctxs])
+    _check(load_library().energon_forward_group(arr, len(ctxs), _ptr(tokens), _lens(seq_lens), B, S, _ptr(out),
+                                                _stream(stream)), ctxs[0])
+
+
+def energon_forward_hidden(ctx, x, seq_lens, layer_begin, layer_end, apply_final_ln, out, stream=None):
+    B, S, _ = x.shape
+    _check(load_library().energon_forward_hidden(ctx, _ptr(x), _lens(seq_lens), B, S, layer_begin, layer_end,
+                                                 int(apply_final_ln), _ptr(out), _stream(stream)), ctx)
+
+
+def energon_sync(ctx):
+    _check(load_library().energon_sync(ctx), ctx)
+
+
+def energon_get_stats(ctx) -> dict:
+    s = Stats()
+    _check(load_library().energon_get_stats(ctx, ctypes.byref(s)), ctx)
+    return {n: getattr(s, n) for n, _ in Stats._fields_}
+
+
+def energon_set_profiling(ctx, enable: bool):
+    _check(load_library().energon_set_profiling(ctx, int(enable)), ctx)
+
+
+def energon_get_profile(ctx) -> dict:
+    p = Profile()
+    _check(load_library().energon_get_profile(ctx, ctypes.byref(p)), ctx)
+    return {n: getattr(p, n) for n, _ in Profile._fields_}
+
+
+def energon_last_error(ctx=None) -> str:
+    return load_library().energon_last_error(ctx).decode()
+
+
+def energon_destroy(ctx):
+    load_library().energon_destroy(ctx)
+
+
+def energon_index_maps(seq_lens, max_len, offsets, pack_idx, pos, unpack_idx, stream=None):
+    _check(load_library().energon_index_maps(_lens(seq_lens), len(seq_lens), max_len, _ptr(offsets), _ptr(pack_idx),
+                                             _ptr(pos), _ptr(unpack_idx), _stream(stream)))
+
+
+def energon_gemm(A, W, bias, D, epilogue=0, stream=None):
+    """D[M,N] = A[M,K] . W[N,K]^T (+bias) (gelu): fp32 SIMT or bf16 tcgen05 by A's dtype."""
+    import torch
+    M, K = A.shape
+    N = W.shape[0]
+    dt = DTYPE_BF16 if A.dtype == torch.bfloat16 else DTYPE_F32
+    _check(load_library().energon_gemm(dt, _ptr(A), _ptr(W), _ptr(bias), _ptr(D), M, N, K, epilogue,
+                                       _stream(stream)))

@@ -235,3 +235,32 @@ def model_host(L, H, F, V, max_seq, seed, bf16, layer_ids=None):
     layers = [{n: layer_tensor_host(n, l, H, F, seed, bf16) for n in LAYER_TENSORS} for l in ids]
     emb = {n: emb_tensor_host(n, H, V, max_seq, seed, bf16) for n in EMB_TENSORS}
     return layers, emb
+
+
+# BASELINE.json configs, concretised in SURVEY.md 8(d): model shapes and batch recipes.
+SHAPES = {
+    "tiny": dict(L=1, H=64, h=4, F=256, V=256, max_seq=16),                 # config 1
+    "gpt2s": dict(L=12, H=768, h=12, F=3072, V=50257, max_seq=1024),        # config 2
+    "gpt3_13b": dict(L=40, H=5120, h=40, F=20480, V=50257, max_seq=2048),   # config 3
+    "opt30b": dict(L=48, H=7168, h=56, F=28672, V=50272, max_seq=2048),     # config 4
+    "opt66b": dict(L=64, H=9216, h=72, F=36864, V=50272, max_seq=2048),     # config 5
+}
+BATCHES = {
+    "tiny": dict(B=4, S=16, lengths="random", p=None),
+    "gpt2s": dict(B=32, S=128, lengths="random", p=None),
+    "gpt3_13b": dict(B=16, S=512, lengths="exact_p", p=0.5),
+    "opt30b": dict(B=32, S=1024, lengths="exact_p", p=0.5),
+    "opt66b": dict(B=32, S=1024, lengths="exact_p", p=0.5),
+}
+
+
+def batch_lengths(name: str, seed: int, p=None, regime: str | None = None) -> list:
+    cfg = BATCHES[name]
+    B, S = cfg["B"], cfg["S"]
+    mode = regime or cfg["lengths"]
+    if mode == "random":
+        return random_lengths(B, S, seed)
+    pp = cfg["p"] if p is None else p
+    if mode == "paper":
+        return paper_lengths(B, S, pp)
+    return exact_p_lengths(B, S, pp, seed)

@@ -1,0 +1,71 @@
+"""CPU checks of the C-ABI boundary: the library loads, exports every symbol include/energon.h
+declares, and rejects bad configurations on the host before touching the device."""
+import ctypes
+import os
+import re
+
+import pytest
+
+from paper_2209_02341_b200 import build, energon
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    build()
+    return energon.load_library()
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "energon.h")).read()
+    return sorted(set(re.findall(r"ENERGON_API\s+[\w\s\*]+?\b(energon_\w+)\s*\(", src)))
+
+
+def test_header_declares_the_binding_names():
+    assert declared_symbols() == sorted(energon.EXPORTS)
+
+
+def test_library_exports_every_declared_symbol(lib):
+    for name in declared_symbols():
+        assert hasattr(lib, name), name
+
+
+def test_status_strings(lib):
+    for code, name in energon.STATUS.items():
+        assert lib.energon_status_string(code).decode() == name
+
+
+@pytest.mark.parametrize("field,value,status", [
+    ("num_heads", 5, -2),      # 64 % 5 != 0: H != h*d
+    ("tp_size", 3, -2),        # 4 heads % 3
+    ("tp_rank", 2, -2),        # rank >= tp_size
+    ("dtype", 7, -2),
+    ("num_layers", 0, -2),
+    ("hidden", 12, -2),        # 12 % 4 == 0 but hidden=12/h=4 -> d=3: shape check
+])
+def test_init_rejects_bad_config_on_host(lib, field, value, status):
+    cfg = energon.make_config(1, 64, 4, 256, 256, 16, 64, dtype="f32", tp_size=2 if field == "tp_rank" else 1)
+    setattr(cfg, field, value)
+    ctx = ctypes.c_void_p()
+    rc = lib.energon_init(ctypes.byref(cfg), None, ctypes.byref(ctx))
+    if field == "hidden":
+        assert rc == -3  # ENERGON_ERR_SHAPE: head_dim 3 not a multiple of 8
+    else:
+        assert rc == status
+    assert not ctx.value
+    assert lib.energon_last_error(None).decode()
+
+
+def test_tp_without_unique_id_rejected(lib):
+    cfg = energon.make_config(1, 64, 4, 256, 256, 16, 64, dtype="f32", tp_size=2)
+    ctx = ctypes.c_void_p()
+    assert lib.energon_init(ctypes.byref(cfg), None, ctypes.byref(ctx)) == -1
+
+
+def test_index_maps_validates_lengths_on_host(lib):
+    lens = (ctypes.c_int32 * 2)(3, 0)
+    dummy = ctypes.c_void_p(16)
+    assert lib.energon_index_maps(lens, 2, 4, dummy, dummy, dummy, dummy, None) == -4
+    lens = (ctypes.c_int32 * 2)(3, 5)
+    assert lib.energon_index_maps(lens, 2, 4, dummy, dummy, dummy, dummy, None) == -4

@@ -1,0 +1,287 @@
+"""GPU parity of the CUDA path (through the C ABI) against the fp64 oracle.
+
+Bars (BASELINE.json north_star): index maps bit-exact; max-abs-rel <= 1e-4 in
+the fp32 mode and <= 2e-2 in the bf16 mode.  Inputs are seeded synthetic batches with the
+shapes of the paper's workloads.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from gpu_helpers import (SHAPES, destroy, make_engine, max_abs_rel, oracle_model, run_forward, torch_dtype)
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOL = {"f32": 1e-4, "bf16": 2e-2}
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2209_02341_b200 import build, energon
+    build()
+    energon.load_library()
+    synth.build(device=True)
+
+
+def E():
+    from paper_2209_02341_b200 import energon
+    return energon
+
+
+# ----------------------------------------------------------------------------- generator
+@pytest.mark.parametrize("bf16", [False, True])
+def test_synth_device_bits_equal_host(bf16):
+    n = 100003
+    t = torch.empty(n, dtype=torch.bfloat16 if bf16 else torch.float32, device="cuda")
+    synth.fill_device(t, 7, 2, 3, 0.02, 0.0, bf16)
+    h = synth.host_tensor((n,), 7, 2, 3, 0.02, 0.0, bf16, dtype="bf16" if bf16 else np.float32)
+    got = t.cpu()
+    if bf16:
+        assert np.array_equal(got.view(torch.int16).numpy().view(np.uint16), h)
+    else:
+        assert np.array_equal(got.numpy().view(np.uint32), h.view(np.uint32))
+
+
+# ----------------------------------------------------------------------------- a1 index maps
+@pytest.mark.parametrize("lens,S", [
+    ([2, 3], 4), ([1], 3), ([5, 5, 5], 5), ([1] * 7, 9),
+    (synth.random_lengths(32, 128, 0), 128),
+    (synth.exact_p_lengths(16, 512, 0.5, 0), 512),
+    (synth.random_lengths(1024, 64, 3), 64),
+    (synth.exact_p_lengths(32, 1024, 0.75, 1), 1024),
+])
+def test_index_maps_bitexact(lens, S):
+    B = len(lens)
+    off = torch.full((B + 1,), -7, dtype=torch.int32, device="cuda")
+    pack = torch.full((B * S,), -7, dtype=torch.int32, device="cuda")
+    pos = torch.full((B * S,), -7, dtype=torch.int32, device="cuda")
+    unpack = torch.full((B * S,), -7, dtype=torch.int32, device="cuda")
+    E().energon_index_maps(lens, S, off, pack, pos, unpack)
+    torch.cuda.synchronize()
+    o_off, o_pack, o_pos, o_unpack = oracle.index_maps(lens, S)
+    T = int(o_off[-1])
+    assert np.array_equal(off.cpu().numpy(), o_off)
+    assert np.array_equal(pack.cpu().numpy()[:T], o_pack)
+    assert np.array_equal(pos.cpu().numpy()[:T], o_pos)
+    assert np.array_equal(unpack.cpu().numpy(), o_unpack)
+    assert (pack.cpu().numpy()[T:] == -7).all()  # nothing written past T
+
+
+# ----------------------------------------------------------------------------- a4/a8/a10/a11 GEMMs
+def _gemm_case(M, N, K, dtype, epi, seed=0):
+    tdt = torch_dtype(dtype)
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    A = (torch.rand(M, K, generator=g) * 2 - 1).to(tdt)
+    W = ((torch.rand(N, K, generator=g) * 2 - 1) * 0.05).to(tdt)
+    bias = (torch.rand(N, generator=g) * 2 - 1).float()
+    D = torch.full((M, N), float("nan"), dtype=tdt, device="cuda")
+    E().energon_gemm(A.cuda(), W.cuda(), bias.cuda() if epi else None, D, epilogue=epi)
+    torch.cuda.synchronize()
+    ref = oracle.matmul(A.double().numpy(), W.double().numpy().T)
+    if epi:
+        ref = ref + bias.double().numpy()
+    if epi == 2:
+        ref = np.vectorize(oracle.gelu)(ref)
+    return D.float().cpu().numpy().astype(np.float64), ref
+
+
+@pytest.mark.parametrize("M,N,K", [
+    (1, 64, 64), (77, 136, 72), (128, 256, 64), (129, 264, 128), (300, 392, 640), (1000, 1920, 512),
+    (513, 768, 3072), (2064, 2304, 768),
+])
+def test_gemm_bf16_tcgen05_vs_oracle(M, N, K):
+    got, ref = _gemm_case(M, N, K, "bf16", 0)
+    err = np.abs(got - ref)
+    # bf16 output rounding (2^-9 relative) + fp32 accumulation
+    assert (err <= 4e-3 * np.abs(ref) + 1e-4 * np.abs(ref).max()).all(), err.max()
+
+
+@pytest.mark.parametrize("epi", [1, 2])
+def test_gemm_bf16_epilogues(epi):
+    got, ref = _gemm_case(200, 264, 192, "bf16", epi, seed=1)
+    assert (np.abs(got - ref) <= 4e-3 * np.abs(ref) + 1e-4 * np.abs(ref).max()).all()
+
+
+@pytest.mark.parametrize("M,N,K,epi", [(30, 192, 64, 1), (30, 256, 64, 2), (77, 64, 256, 0), (130, 130, 70, 1)])
+def test_gemm_f32_vs_oracle(M, N, K, epi):
+    got, ref = _gemm_case(M, N, K, "f32", epi)
+    assert np.abs(got - ref).max() <= 1e-5 * np.abs(ref).max()
+
+
+def test_gemm_bf16_large_vs_cublas():
+    """Library cross-check (tests only): 4096 x 5120 x 5120 against torch.matmul (cuBLAS, fp32)."""
+    M, N, K = 4096, 5120, 5120
+    A = (torch.randn(M, K, device="cuda") * 0.5).bfloat16()
+    W = (torch.randn(N, K, device="cuda") * 0.02).bfloat16()
+    D = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    E().energon_gemm(A, W, None, D)
+    ref = A.float() @ W.float().t()
+    err = (D.float() - ref).abs()
+    assert (err <= 4e-3 * ref.abs() + 1e-3 * ref.abs().max()).all().item(), err.max().item()
+
+
+# ----------------------------------------------------------------------------- full stack, config 1
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("causal", [1, 0])
+@pytest.mark.parametrize("drce", [1, 0])
+def test_forward_tiny_vs_oracle(dtype, causal, drce):
+    """BASELINE config 1 (1 layer, H=64, 4 heads, B=4, S=16, random lengths)."""
+    shape = SHAPES["tiny"]
+    B, S, seed = 4, 16, 0
+    lens = synth.random_lengths(B, S, seed)
+    tok = synth.tokens(B, S, shape["V"], lens, seed)
+    ctxs = make_engine(shape, seed, dtype, B * S, drce=drce, causal=causal)
+    try:
+        y = run_forward(ctxs, tok, lens, dtype, shape["H"])
+    finally:
+        destroy(ctxs)
+    layers, emb = oracle_model(shape, seed, dtype)
+    cfg = oracle.make_cfg(shape["L"], shape["H"], shape["h"], shape["F"], causal=causal)
+    ref = oracle.forward_padded(cfg, layers, emb, tok, lens)
+    assert max_abs_rel(y, ref, lens) <= TOL[dtype]
+    for b, n in enumerate(lens):
+        assert not y[b, n:].any()  # pad rows exactly 0
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("k", [2, 4])
+def test_forward_local_tp_vs_oracle(dtype, k):
+    """1-D TP over k shards on one GPU (in-device rank-order reduction): equals the serial oracle."""
+    shape = dict(SHAPES["tiny"], L=2, V=300, max_seq=40)
+    B, S, seed = 5, 33, 4
+    lens = synth.random_lengths(B, S, seed)
+    tok = synth.tokens(B, S, shape["V"], lens, seed)
+    ctxs = make_engine(shape, seed, dtype, B * S, k=k)
+    try:
+        y = run_forward(ctxs, tok, lens, dtype, shape["H"])
+        st = E().energon_get_stats(ctxs[0])
+    finally:
+        destroy(ctxs)
+    assert st["allreduce_calls"] == 2 * shape["L"]  # SPEC.md:315 exactly 2 per layer
+    layers, emb = oracle_model(shape, seed, dtype)
+    cfg = oracle.make_cfg(shape["L"], shape["H"], shape["h"], shape["F"])
+    ref = oracle.forward_padded(cfg, layers, emb, tok, lens)
+    assert max_abs_rel(y, ref, lens) <= TOL[dtype]
+
+
+def test_forward_multi_tile_f32():
+    """fp32 mode across several GEMM / attention tiles and a ragged tail (H=256, S=200)."""
+    shape = dict(L=2, H=256, h=4, F=1024, V=1000, max_seq=256)
+    B, S, seed = 6, 200, 11
+    lens = synth.random_lengths(B, S, seed)
+    tok = synth.tokens(B, S, shape["V"], lens, seed)
+    ctxs = make_engine(shape, seed, "f32", B * S)
+    try:
+        y = run_forward(ctxs, tok, lens, "f32", shape["H"])
+    finally:
+        destroy(ctxs)
+    layers, emb = oracle_model(shape, seed, "f32")
+    cfg = oracle.make_cfg(shape["L"], shape["H"], shape["h"], shape["F"])
+    ref = oracle.forward_drce(cfg, layers, emb, tok, lens)
+    assert max_abs_rel(y, ref, lens) <= 1e-4
+
+
+# ----------------------------------------------------------------------------- config 2 (GPT-2 small)
+def test_forward_gpt2s_sampled_sequences():
+    """BASELINE config 2 at full size (12 layers, H=768, B=32, S=128, bf16) on the GPU; the oracle
+    recomputes 4 sampled sequences (P12: sequence independence) -- longest, shortest, two more."""
+    shape = SHAPES["gpt2s"]
+    B, S, seed = 32, 128, 0
+    lens = synth.random_lengths(B, S, seed)
+    tok = synth.tokens(B, S, shape["V"], lens, seed)
+    ctxs = make_engine(shape, seed, "bf16", B * S)
+    try:
+        y = run_forward(ctxs, tok, lens, "bf16", shape["H"])
+    finally:
+        destroy(ctxs)
+    order = np.argsort(lens)
+    sel = [int(order[-1]), int(order[0]), 5, 17]
+    layers, emb = oracle_model(shape, seed, "bf16")
+    cfg = oracle.make_cfg(shape["L"], shape["H"], shape["h"], shape["F"])
+    Ssel = max(lens[i] for i in sel)
+    ref = oracle.forward_drce(cfg, layers, emb, tok[sel][:, :Ssel], [lens[i] for i in sel])
+    err = max_abs_rel(y[sel][:, :Ssel], ref, [lens[i] for i in sel])
+    assert err <= 2e-2, err
+
+
+# ----------------------------------------------------------------------------- config 3, teacher-forced
+def test_gpt3_13b_layer_teacher_forced():
+    """BASELINE config 3 shape (H=5120, 40 heads, B=16, S=512, p=0.5, bf16) at full size: one layer
+    through energon_forward_hidden on the whole batch; the oracle recomputes that layer for the
+    shortest sequence from the same fp32 input."""
+    shape = SHAPES["gpt3_13b"]
+    B, S, seed = 16, 512, 0
+    lens = synth.exact_p_lengths(B, S, 0.5, seed)
+    H = shape["H"]
+    ctxs = make_engine(shape, seed, "bf16", B * S, L=1)
+    try:
+        g = torch.Generator(device="cpu").manual_seed(3)
+        x = (torch.randn(B, S, H, generator=g) * 0.5).float()
+        out = torch.full((B, S, H), float("nan"), device="cuda")
+        E().energon_forward_hidden(ctxs[0], x.cuda(), lens, 0, 1, 0, out)
+        E().energon_sync(ctxs[0])
+        y = out.cpu().double().numpy()
+    finally:
+        destroy(ctxs)
+    b = int(np.argmin(lens))
+    n = lens[b]
+    layers, _ = oracle_model(shape, seed, "bf16", layer_ids=[0], L=1)
+    cfg = oracle.make_cfg(1, H, shape["h"], shape["F"])
+    ref = oracle.layers_padded(cfg, layers, 0, 1, x[b:b + 1, :n].double().numpy(), [n])
+    err = max_abs_rel(y[b:b + 1, :n], ref, [n])
+    assert err <= 2e-2, err
+    assert not y[b, n:].any()
+
+
+# ----------------------------------------------------------------------------- error paths on the device
+def test_bad_token_surfaces_on_sync():
+    shape = SHAPES["tiny"]
+    ctxs = make_engine(shape, 0, "f32", 64)
+    try:
+        tok = torch.tensor([[1, 2, 99999, 4]], dtype=torch.int32, device="cuda")
+        out = torch.empty(1, 4, shape["H"], device="cuda")
+        E().energon_forward(ctxs[0], tok, [4], out)
+        with pytest.raises(E().EnergonError) as ei:
+            E().energon_sync(ctxs[0])
+        assert ei.value.status == -5
+        E().energon_sync(ctxs[0])  # cleared
+    finally:
+        destroy(ctxs)
+
+
+def test_host_validation_no_side_effects():
+    shape = SHAPES["tiny"]
+    ctxs = make_engine(shape, 0, "f32", 64)
+    try:
+        tok = torch.ones(4, 16, dtype=torch.int32, device="cuda")
+        out = torch.zeros(4, 16, shape["H"], device="cuda")
+        before = E().energon_get_stats(ctxs[0])
+        for lens, code in (([0, 1, 1, 1], -4), ([17, 1, 1, 1], -4)):
+            with pytest.raises(E().EnergonError) as ei:
+                E().energon_forward(ctxs[0], tok, lens, out)
+            assert ei.value.status == code
+        with pytest.raises(E().EnergonError) as ei:
+            E().energon_forward(ctxs[0], torch.ones(5, 16, dtype=torch.int32, device="cuda"), [1] * 5,
+                                torch.zeros(5, 16, shape["H"], device="cuda"))
+        assert ei.value.status == -6  # 5*16 > max_tokens
+        assert E().energon_get_stats(ctxs[0]) == before
+        assert not out.any()
+    finally:
+        destroy(ctxs)
+
+
+def test_not_loaded():
+    from paper_2209_02341_b200 import energon
+    cfg = energon.make_config(1, 64, 4, 256, 256, 16, 64, dtype="f32")
+    ctx = energon.energon_init(cfg)
+    try:
+        with pytest.raises(energon.EnergonError) as ei:
+            energon.energon_forward(ctx, torch.ones(1, 4, dtype=torch.int32, device="cuda"), [4],
+                                    torch.empty(1, 4, 64, device="cuda"))
+        assert ei.value.status == -7
+    finally:
+        energon.energon_destroy(ctx)
