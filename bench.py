@@ -255,11 +255,16 @@ def energon_arm(args, world, rank, local):
     barrier()
     torch.cuda.synchronize()
     clocks.start()
+    prof_range = os.environ.get("ENERGON_PROFILE_RANGE") == "1"  # ncu --profile-from-start off
+    if prof_range:
+        torch.cuda.cudart().cudaProfilerStart()
     evs[0].record(stream)
     for i in range(args.steps):
         energon.energon_forward(ctx, tok, lens, out, stream)
         evs[i + 1].record(stream)
     torch.cuda.synchronize()
+    if prof_range:
+        torch.cuda.cudart().cudaProfilerStop()
     barrier()
     clk = clocks.stop()
     energon.energon_sync(ctx)

@@ -198,6 +198,12 @@ ENERGON_API void energon_destroy(energon_ctx* ctx);
  */
 ENERGON_API energon_status energon_index_maps(const int32_t* lens, int32_t batch, int32_t max_len, int32_t* offsets_d,
                                   int32_t* pack_idx_d, int32_t* pos_d, int32_t* unpack_idx_d, void* stream);
+/*   energon_attention: a6 on the padded per-head layout Q, K, V, O [batch, heads, max_len, head_dim]
+ *     (dtype F32: SIMT fp32; BF16: mma.sync tensor-core kernel for head_dim 64 / 128); rows
+ *     s >= lens[b] of O are not written. */
+ENERGON_API energon_status energon_attention(int32_t dtype, const void* Q_d, const void* K_d, const void* V_d, void* O_d,
+                                             const int32_t* lens, int32_t batch, int32_t heads, int32_t max_len,
+                                             int32_t head_dim, int32_t causal, void* stream);
 ENERGON_API energon_status energon_gemm(int32_t dtype, const void* A_d, const void* W_d, const float* bias_d, void* D_d,
                             int32_t M, int32_t N, int32_t K, int32_t epilogue, void* stream);
 

@@ -266,6 +266,225 @@ __global__ void __launch_bounds__(256, 1)
   }
 }
 
+// ----------------------------------------------------------------------------- 2-CTA (cta_group::2) kernel
+// A CTA pair (cluster of 2 on one TPC) computes a 256 x 256 tile with tcgen05.mma.cta_group::2
+// (M = 256, N = 256, K = 16): each CTA stages its 128 rows of A and its 128 rows (of N) of W, so the
+// pair reads 64 KB of operands per 64-deep K step for 2 x 128 x 256 outputs -- twice the operand
+// reuse of the 1-CTA 128 x 256 tile.  The leader CTA's MMA warp issues for both; TMA loads of both
+// CTAs complete on the leader's full barrier; MMA commits multicast to both CTAs' empty / tmem-full
+// barriers; both CTAs' epilogue warps arrive on the leader's tmem-empty barrier.
+// Tiles are rasterised in groups of `group_m` 256-row panels so that the A panels of a group stay
+// L2-resident while the group sweeps N.
+constexpr int TC2_STAGES = 6;
+constexpr int TC2_HALF_BYTES = 128 * TC_BK * 2;  // 16 KB: one CTA's half of A or of W per stage
+constexpr int TC2_SMEM = TC2_STAGES * 2 * TC2_HALF_BYTES + 1024 + 256;
+constexpr uint32_t TC2_IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(256 >> 3) << 17) |
+                               ((uint32_t)(256 >> 4) << 24);
+constexpr uint32_t PEER_MASK = 0xFEFFFFFFu;  // shared::cluster address of the same offset in CTA 0
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tma_load_2d_2sm(const CUtensorMap* map, uint32_t dst, uint32_t bar_leader, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], "
+      "[%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_leader), "r"(x), "r"(y)
+      : "memory");
+}
+__device__ __forceinline__ void umma_bf16_2sm(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit_2sm_mc(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t addr) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(addr) : "memory");
+}
+
+__device__ __forceinline__ void raster(int tile, int num_m, int num_n, int group_m, int& m_blk, int& n_blk) {
+  const int per_group = group_m * num_n;
+  const int g = tile / per_group;
+  const int first_m = g * group_m;
+  const int gsize = min(group_m, num_m - first_m);
+  const int r = tile - g * per_group;
+  m_blk = first_m + r % gsize;
+  n_blk = r / gsize;
+}
+
+template <int EPI>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
+    gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    bf16* __restrict__ D, const float* __restrict__ bias, int M, int N, int K, int group_m) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + TC2_STAGES * TC2_HALF_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + TC2_STAGES * TC2_HALF_BYTES);
+  uint64_t* empty = full + TC2_STAGES;
+  uint64_t* tfull = empty + TC2_STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const int num_m = (M + 255) / 256, num_n = (N + 255) / 256;
+  const int num_tiles = num_m * num_n;
+  const int nkb = (K + TC_BK - 1) / TC_BK;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int i = 0; i < TC2_STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 8);  // 4 epilogue warps x 2 CTAs
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                 "n"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = cid; tile < num_tiles; tile += ncl) {
+        int m_blk, n_blk;
+        raster(tile, num_m, num_n, group_m, m_blk, n_blk);
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          const uint32_t fb = smem_u32(&full[stage]) & PEER_MASK;
+          if (leader) mbar_expect_tx(&full[stage], 4 * TC2_HALF_BYTES);
+          tma_load_2d_2sm(&tmA, smem_u32(sA + stage * TC2_HALF_BYTES), fb, kb * TC_BK, m_blk * 256 + (int)rank * 128);
+          tma_load_2d_2sm(&tmB, smem_u32(sB + stage * TC2_HALF_BYTES), fb, kb * TC_BK, n_blk * 256 + (int)rank * 128);
+          if (++stage == TC2_STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int tile = cid; tile < num_tiles; tile += ncl) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + (uint32_t)(acc * 256);
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint64_t a0 = umma_desc_sw128(smem_u32(sA + stage * TC2_HALF_BYTES));
+          const uint64_t b0 = umma_desc_sw128(smem_u32(sB + stage * TC2_HALF_BYTES));
+#pragma unroll
+          for (int k = 0; k < TC_BK / 16; ++k) umma_bf16_2sm(d_tmem, a0 + 2 * k, b0 + 2 * k, TC2_IDESC, (kb | k) != 0);
+          umma_commit_2sm_mc(&empty[stage]);
+          if (++stage == TC2_STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit_2sm_mc(&tfull[acc]);
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    const int q = warp - 4;
+    const uint32_t tempty_leader = smem_u32(&tempty[0]) & PEER_MASK;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = cid; tile < num_tiles; tile += ncl) {
+      int m_blk, n_blk;
+      raster(tile, num_m, num_n, group_m, m_blk, n_blk);
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const int row = m_blk * 256 + (int)rank * 128 + q * 32 + lane;
+      bf16* drow = D + (int64_t)row * N;
+#pragma unroll 1
+      for (int c = 0; c < 256 / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * 256 + c * 32), r);
+        const int n0 = n_blk * 256 + c * 32;
+        if (row < M && n0 < N) {
+          float v[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+          if (EPI >= EPI_BIAS) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 4) {
+              if (n0 + j < N) {
+                const float4 bb = __ldg(reinterpret_cast<const float4*>(bias + n0 + j));
+                v[j] += bb.x;
+                v[j + 1] += bb.y;
+                v[j + 2] += bb.z;
+                v[j + 3] += bb.w;
+              }
+            }
+          }
+          if (EPI == EPI_BIAS_GELU) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = gelu_tanh(v[j]);
+          }
+#pragma unroll
+          for (int j = 0; j < 32; j += 8) {
+            if (n0 + j < N) {
+              uint4 o;
+              o.x = pack_bf16x2(v[j], v[j + 1]);
+              o.y = pack_bf16x2(v[j + 2], v[j + 3]);
+              o.z = pack_bf16x2(v[j + 4], v[j + 5]);
+              o.w = pack_bf16x2(v[j + 6], v[j + 7]);
+              *reinterpret_cast<uint4*>(drow + n0 + j) = o;
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tempty_leader + (uint32_t)(acc * sizeof(uint64_t)));
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(512));
+  }
+}
+
 // ----------------------------------------------------------------------------- host side
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -304,14 +523,30 @@ int num_sms() {
 }
 
 int tc_pick_bn(int M, int N) {
-  // Prefer 256-wide tiles; fall back to 128 when N is small or 256 wastes a large part of the last wave.
-  if (N <= 128) return 128;
-  const int sms = num_sms();
-  const int mt = (M + TC_BM - 1) / TC_BM;
-  const long t256 = (long)mt * ((N + 255) / 256), t128 = (long)mt * ((N + 127) / 128);
-  // wave-quantised cost in units of a 128-wide tile
-  const double c256 = 2.0 * ((t256 + sms - 1) / sms), c128 = 1.0 * ((t128 + sms - 1) / sms);
-  return (c128 < c256) ? 128 : 256;
+  // 2-CTA 256 x 256 tiles (bn == 512 encodes "pair") whenever both dimensions can fill them;
+  // otherwise the 1-CTA kernel with 256- or 128-wide tiles.
+  if (M > 128 && N >= 256) return 512;
+  return N <= 128 ? 128 : 256;
+}
+
+template <int EPI>
+static void launch_pair_epi(const CUtensorMap& tmA, const CUtensorMap& tmB, const float* bias, bf16* D, int M, int N,
+                            int K, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(gemm_tc2_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC2_SMEM);
+    attr = true;
+  }
+  const int num_m = (M + 255) / 256, num_n = (N + 255) / 256;
+  const int tiles = num_m * num_n;
+  const int pairs = num_sms() / 2;
+  const int grid = 2 * (tiles < pairs ? tiles : pairs);
+  // group of A panels kept L2-resident while the group sweeps N (about 48 MB of A per group)
+  const double panel = 256.0 * K * 2;
+  int group_m = (int)(48.0e6 / panel);
+  if (group_m < 1) group_m = 1;
+  if (group_m > num_m) group_m = num_m;
+  gemm_tc2_kernel<EPI><<<grid, 256, TC2_SMEM, st>>>(tmA, tmB, D, bias, M, N, K, group_m);
 }
 
 template <int BN, int EPI>
@@ -331,7 +566,11 @@ static void launch_bn_epi(const CUtensorMap& tmA, const CUtensorMap& tmB, const 
 void launch_gemm_tc(const CUtensorMap& tmA, const CUtensorMap& tmB, int bn, const float* bias, bf16* D, int M, int N,
                     int K, int epi, cudaStream_t st) {
   if (M <= 0 || N <= 0) return;
-  if (bn == 256) {
+  if (bn == 512) {
+    if (epi == EPI_NONE) launch_pair_epi<EPI_NONE>(tmA, tmB, bias, D, M, N, K, st);
+    else if (epi == EPI_BIAS) launch_pair_epi<EPI_BIAS>(tmA, tmB, bias, D, M, N, K, st);
+    else launch_pair_epi<EPI_BIAS_GELU>(tmA, tmB, bias, D, M, N, K, st);
+  } else if (bn == 256) {
     if (epi == EPI_NONE) launch_bn_epi<256, EPI_NONE>(tmA, tmB, bias, D, M, N, K, st);
     else if (epi == EPI_BIAS) launch_bn_epi<256, EPI_BIAS>(tmA, tmB, bias, D, M, N, K, st);
     else launch_bn_epi<256, EPI_BIAS_GELU>(tmA, tmB, bias, D, M, N, K, st);

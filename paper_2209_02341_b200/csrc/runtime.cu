@@ -346,7 +346,7 @@ void gemm(energon_ctx* c, const CUtensorMap& tmA, const CUtensorMap* tmB, const 
           const float* bias, void* D, int M, int N, int K, int epi, cudaStream_t st) {
   Prof p(c, st, P_GEMM, 2.0 * M * N * K);
   if constexpr (sizeof(Act) == 2) {
-    const int bn = tc_pick_bn(M, N);
+    const int bn = tc_pick_bn(M, N);  // 512: 2-CTA pair kernel (128-row W box), 256 / 128: 1-CTA
     launch_gemm_tc(tmA, tmB[bn == 256 ? 0 : 1], bn, bias, reinterpret_cast<bf16*>(D), M, N, K, epi, st);
   } else {
     launch_gemm_f32(reinterpret_cast<const float*>(A), reinterpret_cast<const float*>(W), bias,
@@ -787,6 +787,32 @@ energon_status energon_index_maps(const int32_t* lens, int32_t B, int32_t S, int
   return ENERGON_OK;
 }
 
+energon_status energon_attention(int32_t dtype, const void* Q, const void* K, const void* V, void* O,
+                                 const int32_t* lens, int32_t B, int32_t hk, int32_t S, int32_t d, int32_t causal,
+                                 void* stream) {
+  if (!Q || !K || !V || !O || !lens) return fail(nullptr, ENERGON_ERR_ARG, "NULL argument");
+  if (B < 1 || B > ENERGON_MAX_BATCH || hk < 1 || S < 1 || d < 1 || d % 8 || (causal != 0 && causal != 1))
+    return fail(nullptr, ENERGON_ERR_ARG, "bad attention arguments");
+  LensParam lp;
+  for (int b = 0; b < B; ++b) {
+    if (lens[b] < 1 || lens[b] > S) return fail(nullptr, ENERGON_ERR_LENGTH, "seq_lens not in [1, max_len]");
+    lp.lens[b] = lens[b];
+  }
+  if (dtype == ENERGON_DTYPE_F32)
+    launch_attention<float>(reinterpret_cast<const float*>(Q), reinterpret_cast<const float*>(K),
+                            reinterpret_cast<const float*>(V), reinterpret_cast<float*>(O), lp, B, hk, S, d, causal,
+                            (cudaStream_t)stream);
+  else if (dtype == ENERGON_DTYPE_BF16)
+    launch_attention<bf16>(reinterpret_cast<const bf16*>(Q), reinterpret_cast<const bf16*>(K),
+                           reinterpret_cast<const bf16*>(V), reinterpret_cast<bf16*>(O), lp, B, hk, S, d, causal,
+                           (cudaStream_t)stream);
+  else
+    return fail(nullptr, ENERGON_ERR_ARG, "dtype must be F32 or BF16");
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(nullptr, e, "attention");
+  return ENERGON_OK;
+}
+
 energon_status energon_gemm(int32_t dtype, const void* A, const void* W, const float* bias, void* D, int32_t M,
                             int32_t N, int32_t K, int32_t epi, void* stream) {
   if (!A || !W || !D) return fail(nullptr, ENERGON_ERR_ARG, "NULL argument");
@@ -799,7 +825,7 @@ energon_status energon_gemm(int32_t dtype, const void* A, const void* W, const f
     if (K % 8 || N % 8) return fail(nullptr, ENERGON_ERR_SHAPE, "bf16 GEMM needs K and N multiples of 8");
     const int bn = tc_pick_bn(M, N);
     CUtensorMap ta, tb;
-    if (!make_tmap_kmajor(&ta, A, M, K, 128) || !make_tmap_kmajor(&tb, W, N, K, bn))
+    if (!make_tmap_kmajor(&ta, A, M, K, 128) || !make_tmap_kmajor(&tb, W, N, K, bn == 256 ? 256 : 128))
       return fail(nullptr, ENERGON_ERR_CUDA, "cuTensorMapEncodeTiled failed");
     launch_gemm_tc(ta, tb, bn, bias, reinterpret_cast<bf16*>(D), M, N, K, epi, (cudaStream_t)stream);
   } else {

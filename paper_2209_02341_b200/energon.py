@@ -26,7 +26,7 @@ LAYER_TENSORS = ("wq", "wk", "wv", "wo", "bq", "bk", "bv", "bo",
 EXPORTS = ("energon_get_unique_id", "energon_init", "energon_init_local_group", "energon_load_embeddings",
            "energon_load_layer_weights", "energon_forward", "energon_forward_group", "energon_forward_hidden",
            "energon_sync", "energon_get_stats", "energon_last_error", "energon_status_string", "energon_destroy",
-           "energon_index_maps", "energon_gemm", "energon_set_profiling", "energon_get_profile")
+           "energon_index_maps", "energon_gemm", "energon_attention", "energon_set_profiling", "energon_get_profile")
 
 
 class EnergonError(RuntimeError):
@@ -87,6 +87,7 @@ def load_library(path: str = SO_PATH):
     L.energon_destroy.restype = None
     L.energon_index_maps.argtypes = [ctypes.POINTER(ctypes.c_int32), I32, I32, P, P, P, P, P]
     L.energon_gemm.argtypes = [I32, P, P, P, P, I32, I32, I32, I32, P]
+    L.energon_attention.argtypes = [I32, P, P, P, P, ctypes.POINTER(ctypes.c_int32), I32, I32, I32, I32, I32, P]
     L.energon_set_profiling.argtypes = [P, I32]
     L.energon_get_profile.argtypes = [P, ctypes.POINTER(Profile)]
     for name in EXPORTS:
@@ -227,3 +228,12 @@ def energon_gemm(A, W, bias, D, epilogue=0, stream=None):
     dt = DTYPE_BF16 if A.dtype == torch.bfloat16 else DTYPE_F32
     _check(load_library().energon_gemm(dt, _ptr(A), _ptr(W), _ptr(bias), _ptr(D), M, N, K, epilogue,
                                        _stream(stream)))
+
+
+def energon_attention(Q, K, V, O, seq_lens, causal=1, stream=None):
+    """a6 on [B, heads, S, d] tensors (fp32 SIMT or bf16 tensor-core by Q's dtype)."""
+    import torch
+    B, hk, S, d = Q.shape
+    dt = DTYPE_BF16 if Q.dtype == torch.bfloat16 else DTYPE_F32
+    _check(load_library().energon_attention(dt, _ptr(Q), _ptr(K), _ptr(V), _ptr(O), _lens(seq_lens), B, hk, S, d,
+                                            causal, _stream(stream)))

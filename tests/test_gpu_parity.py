@@ -285,3 +285,33 @@ def test_not_loaded():
         assert ei.value.status == -7
     finally:
         energon.energon_destroy(ctx)
+
+
+# ----------------------------------------------------------------------------- a6 attention kernel
+@pytest.mark.parametrize("dtype,d", [("bf16", 128), ("bf16", 64), ("f32", 64), ("bf16", 16)])
+@pytest.mark.parametrize("causal", [1, 0])
+def test_attention_kernel_vs_oracle(dtype, d, causal):
+    """Lengths straddling the 64-row tiles (1, 63, 64, 65, 130, S) incl. NaN in every pad row of K/V."""
+    B, hk, S = 6, 3, 150
+    lens = [1, 63, 64, 65, 130, 150]
+    g = torch.Generator(device="cpu").manual_seed(d + causal)
+    tdt = torch_dtype(dtype)
+    Qh, Kh, Vh = ((torch.randn(B, hk, S, d, generator=g) * s).to(tdt) for s in (1.0, 1.0, 1.0))
+    for b, n in enumerate(lens):  # pad rows never written by a5: poison them
+        Kh[b, :, n:] = float("nan")
+        Vh[b, :, n:] = float("nan")
+        Qh[b, :, n:] = float("nan")
+    O = torch.full((B, hk, S, d), 7.0, dtype=tdt, device="cuda")
+    E().energon_attention(Qh.cuda(), Kh.cuda(), Vh.cuda(), O, lens, causal=causal)
+    torch.cuda.synchronize()
+    got = O.float().cpu().numpy().astype(np.float64)
+    # oracle layout [B, S, H] with head i = columns [i d, (i+1) d)
+    to_bsh = lambda t: t.double().permute(0, 2, 1, 3).reshape(B, S, hk * d).numpy()
+    ref = oracle.attention(np.nan_to_num(to_bsh(Qh)), np.nan_to_num(to_bsh(Kh)), np.nan_to_num(to_bsh(Vh)),
+                           hk, lens, causal)
+    ref = ref.reshape(B, S, hk, d).transpose(0, 2, 1, 3)
+    tol = 1e-5 if dtype == "f32" else 2e-2
+    for b, n in enumerate(lens):
+        assert np.isfinite(got[b, :, :n]).all()
+        assert np.abs(got[b, :, :n] - ref[b, :, :n]).max() <= tol * max(1.0, np.abs(ref[b, :, :n]).max())
+        assert (got[b, :, n:] == 7.0).all()  # pad query rows untouched
