@@ -110,6 +110,7 @@ __device__ __forceinline__ uint32_t pack2(float a, float b) {
 template <int D>
 __global__ void __launch_bounds__(128) attention_fa_kernel(const bf16* __restrict__ Q, const bf16* __restrict__ K,
                                                            const bf16* __restrict__ V, bf16* __restrict__ O,
+                                                           bf16* __restrict__ Cp, const int* __restrict__ offsets,
                                                            LensParam lp, int hk, int S, int causal, float scale_log2) {
   constexpr int BM = 64, BN = 64, CH = D / 8, KS = D / 16, NT = BN / 8, DT = D / 8;
   static_assert(CH >= 8, "swizzle needs >= 8 chunks per row");
@@ -246,19 +247,27 @@ __global__ void __launch_bounds__(128) attention_fa_kernel(const bf16* __restric
   l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
   l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
   const float inv0 = 1.f / l0, inv1 = 1.f / l1;
+  // a7 fused (Cp != nullptr): write the packed row offsets[b] + s, columns head*D.. of [T, hk*D]
+  bf16 *dst0, *dst1;
+  if (Cp) {
+    const int64_t t0 = __ldg(offsets + b);
+    dst0 = Cp + (t0 + row0) * (int64_t)(hk * D) + head * D;
+    dst1 = Cp + (t0 + row1) * (int64_t)(hk * D) + head * D;
+  } else {
+    dst0 = O + base + (int64_t)row0 * D;
+    dst1 = O + base + (int64_t)row1 * D;
+  }
 #pragma unroll
   for (int i = 0; i < DT; ++i) {
     const int col = i * 8 + (lane & 3) * 2;
-    if (row0 < len)
-      *reinterpret_cast<uint32_t*>(O + base + (int64_t)row0 * D + col) = pack2(o[i][0] * inv0, o[i][1] * inv0);
-    if (row1 < len)
-      *reinterpret_cast<uint32_t*>(O + base + (int64_t)row1 * D + col) = pack2(o[i][2] * inv1, o[i][3] * inv1);
+    if (row0 < len) *reinterpret_cast<uint32_t*>(dst0 + col) = pack2(o[i][0] * inv0, o[i][1] * inv0);
+    if (row1 < len) *reinterpret_cast<uint32_t*>(dst1 + col) = pack2(o[i][2] * inv1, o[i][3] * inv1);
   }
 }
 
 template <int D>
-static void launch_fa(const bf16* Q, const bf16* K, const bf16* V, bf16* O, const LensParam& lp, int B, int hk, int S,
-                      int causal, cudaStream_t st) {
+static void launch_fa(const bf16* Q, const bf16* K, const bf16* V, bf16* O, bf16* Cp, const int* offsets,
+                      const LensParam& lp, int B, int hk, int S, int causal, cudaStream_t st) {
   const int smem = (64 + 4 * 64) * D * 2;
   static bool attr = false;
   if (!attr) {
@@ -267,17 +276,24 @@ static void launch_fa(const bf16* Q, const bf16* K, const bf16* V, bf16* O, cons
   }
   dim3 grid((S + 63) / 64, hk, B);
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)D);
-  attention_fa_kernel<D><<<grid, 128, smem, st>>>(Q, K, V, O, lp, hk, S, causal, scale_log2);
+  attention_fa_kernel<D><<<grid, 128, smem, st>>>(Q, K, V, O, Cp, offsets, lp, hk, S, causal, scale_log2);
 }
 
 template <typename Act>
 void launch_attention(const Act* Q, const Act* K, const Act* V, Act* O, const LensParam& lp, int B, int hk, int S, int d,
                       int causal, cudaStream_t st) {
   if constexpr (sizeof(Act) == 2) {
-    if (d == 128) return launch_fa<128>(Q, K, V, O, lp, B, hk, S, causal, st);
-    if (d == 64) return launch_fa<64>(Q, K, V, O, lp, B, hk, S, causal, st);
+    if (d == 128) return launch_fa<128>(Q, K, V, O, nullptr, nullptr, lp, B, hk, S, causal, st);
+    if (d == 64) return launch_fa<64>(Q, K, V, O, nullptr, nullptr, lp, B, hk, S, causal, st);
   }
   launch_attention_simt<Act>(Q, K, V, O, lp, B, hk, S, d, causal, st);
+}
+
+bool launch_attention_packed(const bf16* Q, const bf16* K, const bf16* V, bf16* ctx_packed, const int* offsets,
+                             const LensParam& lp, int B, int hk, int S, int d, int causal, cudaStream_t st) {
+  if (d == 128) return launch_fa<128>(Q, K, V, nullptr, ctx_packed, offsets, lp, B, hk, S, causal, st), true;
+  if (d == 64) return launch_fa<64>(Q, K, V, nullptr, ctx_packed, offsets, lp, B, hk, S, causal, st), true;
+  return false;
 }
 
 template void launch_attention<float>(const float*, const float*, const float*, float*, const LensParam&, int, int, int,

@@ -15,6 +15,7 @@
 // Tiles are walked m-fastest so the activation panel stays L2-resident while the weights stream
 // through once.  M and N tails are handled by TMA out-of-bounds zero fill + predicated stores.
 #include <cudaTypedefs.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -103,16 +104,37 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// GeLU-tanh for the bf16 epilogue: hardware tanh.approx (rel. err ~2^-11, below the
+// bf16 output rounding of 2^-9).  The fp32 parity path keeps tanhf.
+__device__ __forceinline__ float gelu_fast(float x) {
+  const float u = 0.7978845608f * (x + 0.044715f * x * x * x);
+  float t;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(u));
+  return 0.5f * x * (1.f + t);
+}
+
 __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
   __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&v);
+}
+
+// a5 fused into the QKV epilogue: packed row t, column n0 (32-aligned, inside one head since
+// d % 32 == 0) of the per-rank [q | k | v] block -> &{Q,K,V}[b, head, s, j] (PAPER.md:373 kernel #1).
+__device__ __forceinline__ bf16* qkv_dst(const QkvScatter& qs, int row, int n0, int N) {
+  const int Hk = N / 3;
+  const int which = n0 / Hk, rem = n0 - which * Hk;
+  const int head = rem / qs.d, j = rem - head * qs.d;
+  const int cell = qs.pack_idx ? __ldg(qs.pack_idx + row) : row;
+  const int b = cell / qs.S, s = cell - b * qs.S;
+  bf16* base = which == 0 ? qs.q : (which == 1 ? qs.k : qs.v);
+  return base + (((int64_t)b * qs.hk + head) * qs.S + s) * qs.d + j;
 }
 
 // ----------------------------------------------------------------------------- the kernel
 template <int BN, int EPI>
 __global__ void __launch_bounds__(256, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, bf16* __restrict__ D,
-                   const float* __restrict__ bias, int M, int N, int K) {
+                   const float* __restrict__ bias, int M, int N, int K, const QkvScatter qs) {
   using C = TcCfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -234,8 +256,10 @@ __global__ void __launch_bounds__(256, 1)
           }
           if (EPI == EPI_BIAS_GELU) {
 #pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = gelu_tanh(v[j]);
+            for (int j = 0; j < 32; ++j) v[j] = gelu_fast(v[j]);
           }
+          bf16* dst = drow + n0;
+          if (EPI == EPI_BIAS_QKV) dst = qkv_dst(qs, row, n0, N);
 #pragma unroll
           for (int j = 0; j < 32; j += 8) {
             if (n0 + j < N) {
@@ -244,7 +268,7 @@ __global__ void __launch_bounds__(256, 1)
               o.y = pack_bf16x2(v[j + 2], v[j + 3]);
               o.z = pack_bf16x2(v[j + 4], v[j + 5]);
               o.w = pack_bf16x2(v[j + 6], v[j + 7]);
-              *reinterpret_cast<uint4*>(drow + n0 + j) = o;
+              *reinterpret_cast<uint4*>(dst + j) = o;
             }
           }
         }
@@ -275,11 +299,15 @@ __global__ void __launch_bounds__(256, 1)
 // barriers; both CTAs' epilogue warps arrive on the leader's tmem-empty barrier.
 // Tiles are rasterised in groups of `group_m` 256-row panels so that the A panels of a group stay
 // L2-resident while the group sweeps N.
-constexpr int TC2_STAGES = 6;
-constexpr int TC2_HALF_BYTES = 128 * TC_BK * 2;  // 16 KB: one CTA's half of A or of W per stage
-constexpr int TC2_SMEM = TC2_STAGES * 2 * TC2_HALF_BYTES + 1024 + 256;
-constexpr uint32_t TC2_IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(256 >> 3) << 17) |
-                               ((uint32_t)(256 >> 4) << 24);
+template <int BN> struct Tc2Cfg {
+  static constexpr int A_BYTES = 128 * TC_BK * 2;      // this CTA's 128 rows of A per stage
+  static constexpr int B_BYTES = (BN / 2) * TC_BK * 2;  // this CTA's BN/2 rows of W per stage
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = (200 * 1024) / STAGE_BYTES;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+  static constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                                    ((uint32_t)(256 >> 4) << 24);
+};
 constexpr uint32_t PEER_MASK = 0xFEFFFFFFu;  // shared::cluster address of the same offset in CTA 0
 
 __device__ __forceinline__ uint32_t cluster_ctarank() {
@@ -323,17 +351,19 @@ __device__ __forceinline__ void raster(int tile, int num_m, int num_n, int group
   n_blk = r / gsize;
 }
 
-template <int EPI>
+template <int BN, int EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                    bf16* __restrict__ D, const float* __restrict__ bias, int M, int N, int K, int group_m) {
+                    bf16* __restrict__ D, const float* __restrict__ bias, int M, int N, int K, int group_m,
+                    const QkvScatter qs) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  using C = Tc2Cfg<BN>;
   uint8_t* sA = smem;
-  uint8_t* sB = smem + TC2_STAGES * TC2_HALF_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + TC2_STAGES * TC2_HALF_BYTES);
-  uint64_t* empty = full + TC2_STAGES;
-  uint64_t* tfull = empty + TC2_STAGES;
+  uint8_t* sB = smem + C::STAGES * C::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + C::STAGES * C::B_BYTES);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
 
@@ -341,14 +371,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   const uint32_t rank = cluster_ctarank();
   const bool leader = rank == 0;
   const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
-  const int num_m = (M + 255) / 256, num_n = (N + 255) / 256;
+  const int num_m = (M + 255) / 256, num_n = (N + BN - 1) / BN;
   const int num_tiles = num_m * num_n;
   const int nkb = (K + TC_BK - 1) / TC_BK;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
-    for (int i = 0; i < TC2_STAGES; ++i) {
+    for (int i = 0; i < C::STAGES; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
     }
@@ -378,10 +408,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           const uint32_t fb = smem_u32(&full[stage]) & PEER_MASK;
-          if (leader) mbar_expect_tx(&full[stage], 4 * TC2_HALF_BYTES);
-          tma_load_2d_2sm(&tmA, smem_u32(sA + stage * TC2_HALF_BYTES), fb, kb * TC_BK, m_blk * 256 + (int)rank * 128);
-          tma_load_2d_2sm(&tmB, smem_u32(sB + stage * TC2_HALF_BYTES), fb, kb * TC_BK, n_blk * 256 + (int)rank * 128);
-          if (++stage == TC2_STAGES) {
+          if (leader) mbar_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
+          tma_load_2d_2sm(&tmA, smem_u32(sA + stage * C::A_BYTES), fb, kb * TC_BK, m_blk * 256 + (int)rank * 128);
+          tma_load_2d_2sm(&tmB, smem_u32(sB + stage * C::B_BYTES), fb, kb * TC_BK, n_blk * BN + (int)rank * (BN / 2));
+          if (++stage == C::STAGES) {
             stage = 0;
             phase ^= 1;
           }
@@ -397,16 +427,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       for (int tile = cid; tile < num_tiles; tile += ncl) {
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + (uint32_t)(acc * 256);
+        const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const uint64_t a0 = umma_desc_sw128(smem_u32(sA + stage * TC2_HALF_BYTES));
-          const uint64_t b0 = umma_desc_sw128(smem_u32(sB + stage * TC2_HALF_BYTES));
+          const uint64_t a0 = umma_desc_sw128(smem_u32(sA + stage * C::A_BYTES));
+          const uint64_t b0 = umma_desc_sw128(smem_u32(sB + stage * C::B_BYTES));
 #pragma unroll
-          for (int k = 0; k < TC_BK / 16; ++k) umma_bf16_2sm(d_tmem, a0 + 2 * k, b0 + 2 * k, TC2_IDESC, (kb | k) != 0);
+          for (int k = 0; k < TC_BK / 16; ++k) umma_bf16_2sm(d_tmem, a0 + 2 * k, b0 + 2 * k, C::IDESC, (kb | k) != 0);
           umma_commit_2sm_mc(&empty[stage]);
-          if (++stage == TC2_STAGES) {
+          if (++stage == C::STAGES) {
             stage = 0;
             phase ^= 1;
           }
@@ -431,10 +461,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       const int row = m_blk * 256 + (int)rank * 128 + q * 32 + lane;
       bf16* drow = D + (int64_t)row * N;
 #pragma unroll 1
-      for (int c = 0; c < 256 / 32; ++c) {
+      for (int c = 0; c < BN / 32; ++c) {
         uint32_t r[32];
-        tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * 256 + c * 32), r);
-        const int n0 = n_blk * 256 + c * 32;
+        tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c * 32), r);
+        const int n0 = n_blk * BN + c * 32;
         if (row < M && n0 < N) {
           float v[32];
 #pragma unroll
@@ -453,8 +483,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
           }
           if (EPI == EPI_BIAS_GELU) {
 #pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = gelu_tanh(v[j]);
+            for (int j = 0; j < 32; ++j) v[j] = gelu_fast(v[j]);
           }
+          bf16* dst = drow + n0;
+          if (EPI == EPI_BIAS_QKV) dst = qkv_dst(qs, row, n0, N);
 #pragma unroll
           for (int j = 0; j < 32; j += 8) {
             if (n0 + j < N) {
@@ -463,7 +495,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
               o.y = pack_bf16x2(v[j + 2], v[j + 3]);
               o.z = pack_bf16x2(v[j + 4], v[j + 5]);
               o.w = pack_bf16x2(v[j + 6], v[j + 7]);
-              *reinterpret_cast<uint4*>(drow + n0 + j) = o;
+              *reinterpret_cast<uint4*>(dst + j) = o;
             }
           }
         }
@@ -522,22 +554,32 @@ int num_sms() {
   return n;
 }
 
+// Tile choice.  Codes: 1256 / 1192 / 1128 = 2-CTA pair with a 256 x {256, 192, 128} tile (the W
+// tensor map then has a BN/2-row box), 256 / 128 = 1-CTA 128 x {256, 128} tile.  Measured on B200
+// (profiles/r01_tile_sweep.log) the 256 x 256 pair tile is the fastest on every DRCE GEMM shape at
+// TP 1..8 even where a narrower tile would quantise into fewer waves, so it is used whenever both
+// dimensions can fill it; the 1-CTA kernel covers M <= 128 or N < 256.
 int tc_pick_bn(int M, int N) {
-  // 2-CTA 256 x 256 tiles (bn == 512 encodes "pair") whenever both dimensions can fill them;
-  // otherwise the 1-CTA kernel with 256- or 128-wide tiles.
-  if (M > 128 && N >= 256) return 512;
+  if (const char* f = getenv("ENERGON_GEMM_TILE")) {  // test hook: force a tile code
+    const int code = atoi(f);
+    if (code == 1256 || code == 1192 || code == 1128 || code == 256 || code == 128) return code;
+  }
+  if (M > 128 && N >= 256) return 1256;
   return N <= 128 ? 128 : 256;
 }
 
-template <int EPI>
+int tc_w_box(int code) { return code > 1000 ? (code - 1000) / 2 : code; }
+
+template <int BN, int EPI>
 static void launch_pair_epi(const CUtensorMap& tmA, const CUtensorMap& tmB, const float* bias, bf16* D, int M, int N,
-                            int K, cudaStream_t st) {
+                            int K, cudaStream_t st, const QkvScatter& qs) {
+  using C = Tc2Cfg<BN>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(gemm_tc2_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC2_SMEM);
+    cudaFuncSetAttribute(gemm_tc2_kernel<BN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     attr = true;
   }
-  const int num_m = (M + 255) / 256, num_n = (N + 255) / 256;
+  const int num_m = (M + 255) / 256, num_n = (N + BN - 1) / BN;
   const int tiles = num_m * num_n;
   const int pairs = num_sms() / 2;
   const int grid = 2 * (tiles < pairs ? tiles : pairs);
@@ -546,12 +588,12 @@ static void launch_pair_epi(const CUtensorMap& tmA, const CUtensorMap& tmB, cons
   int group_m = (int)(48.0e6 / panel);
   if (group_m < 1) group_m = 1;
   if (group_m > num_m) group_m = num_m;
-  gemm_tc2_kernel<EPI><<<grid, 256, TC2_SMEM, st>>>(tmA, tmB, D, bias, M, N, K, group_m);
+  gemm_tc2_kernel<BN, EPI><<<grid, 256, C::SMEM, st>>>(tmA, tmB, D, bias, M, N, K, group_m, qs);
 }
 
 template <int BN, int EPI>
 static void launch_bn_epi(const CUtensorMap& tmA, const CUtensorMap& tmB, const float* bias, bf16* D, int M, int N,
-                          int K, cudaStream_t st) {
+                          int K, cudaStream_t st, const QkvScatter& qs) {
   using C = TcCfg<BN>;
   static bool attr = false;
   if (!attr) {
@@ -560,24 +602,35 @@ static void launch_bn_epi(const CUtensorMap& tmA, const CUtensorMap& tmB, const 
   }
   const int tiles = ((M + TC_BM - 1) / TC_BM) * ((N + BN - 1) / BN);
   const int grid = tiles < num_sms() ? tiles : num_sms();
-  gemm_tc_kernel<BN, EPI><<<grid, 256, C::SMEM, st>>>(tmA, tmB, D, bias, M, N, K);
+  gemm_tc_kernel<BN, EPI><<<grid, 256, C::SMEM, st>>>(tmA, tmB, D, bias, M, N, K, qs);
 }
 
+#define DISPATCH_EPI(F, BNARGS)                                                  \
+  switch (epi) {                                                                 \
+    case EPI_NONE: F<BNARGS EPI_NONE>(tmA, tmB, bias, D, M, N, K, st, qs); break; \
+    case EPI_BIAS: F<BNARGS EPI_BIAS>(tmA, tmB, bias, D, M, N, K, st, qs); break; \
+    case EPI_BIAS_GELU: F<BNARGS EPI_BIAS_GELU>(tmA, tmB, bias, D, M, N, K, st, qs); break; \
+    default: F<BNARGS EPI_BIAS_QKV>(tmA, tmB, bias, D, M, N, K, st, qs); break;   \
+  }
+#define BN256 256,
+#define BN192 192,
+#define BN128 128,
+
 void launch_gemm_tc(const CUtensorMap& tmA, const CUtensorMap& tmB, int bn, const float* bias, bf16* D, int M, int N,
-                    int K, int epi, cudaStream_t st) {
+                    int K, int epi, cudaStream_t st, const QkvScatter* qkv) {
   if (M <= 0 || N <= 0) return;
-  if (bn == 512) {
-    if (epi == EPI_NONE) launch_pair_epi<EPI_NONE>(tmA, tmB, bias, D, M, N, K, st);
-    else if (epi == EPI_BIAS) launch_pair_epi<EPI_BIAS>(tmA, tmB, bias, D, M, N, K, st);
-    else launch_pair_epi<EPI_BIAS_GELU>(tmA, tmB, bias, D, M, N, K, st);
+  QkvScatter qs{};
+  if (qkv) qs = *qkv;
+  if (bn == 1256) {
+    DISPATCH_EPI(launch_pair_epi, BN256)
+  } else if (bn == 1192) {
+    DISPATCH_EPI(launch_pair_epi, BN192)
+  } else if (bn == 1128) {
+    DISPATCH_EPI(launch_pair_epi, BN128)
   } else if (bn == 256) {
-    if (epi == EPI_NONE) launch_bn_epi<256, EPI_NONE>(tmA, tmB, bias, D, M, N, K, st);
-    else if (epi == EPI_BIAS) launch_bn_epi<256, EPI_BIAS>(tmA, tmB, bias, D, M, N, K, st);
-    else launch_bn_epi<256, EPI_BIAS_GELU>(tmA, tmB, bias, D, M, N, K, st);
+    DISPATCH_EPI(launch_bn_epi, BN256)
   } else {
-    if (epi == EPI_NONE) launch_bn_epi<128, EPI_NONE>(tmA, tmB, bias, D, M, N, K, st);
-    else if (epi == EPI_BIAS) launch_bn_epi<128, EPI_BIAS>(tmA, tmB, bias, D, M, N, K, st);
-    else launch_bn_epi<128, EPI_BIAS_GELU>(tmA, tmB, bias, D, M, N, K, st);
+    DISPATCH_EPI(launch_bn_epi, BN128)
   }
 }
 

@@ -56,12 +56,22 @@ template <typename Src, typename Dst>
 void launch_convert_vec(const Src* src, int64_t off, int N, Dst* dst, cudaStream_t st);
 
 // a6: masked attention over the padded per-head layout [B, hk, S, d]
+// ctx_packed != nullptr fuses a7: O rows are written straight to the packed [T, hk*d] layout at
+// row offsets[b] + s (bf16 tensor-core path only; returns false if the fused form is unsupported).
 template <typename Act>
 void launch_attention(const Act* Q, const Act* K, const Act* V, Act* O, const LensParam& lp, int B, int hk, int S,
                       int d, int causal, cudaStream_t st);
+bool launch_attention_packed(const bf16* Q, const bf16* K, const bf16* V, bf16* ctx_packed, const int* offsets,
+                             const LensParam& lp, int B, int hk, int S, int d, int causal, cudaStream_t st);
 
-// GEMM epilogues
-enum { EPI_NONE = 0, EPI_BIAS = 1, EPI_BIAS_GELU = 2 };
+// GEMM epilogues.  EPI_BIAS_QKV = bias, then a5 fused: the packed QKV row t / column block is
+// scattered straight into the padded per-head Q, K, V [B, hk, S, d] (needs d % 32 == 0).
+enum { EPI_NONE = 0, EPI_BIAS = 1, EPI_BIAS_GELU = 2, EPI_BIAS_QKV = 3 };
+struct QkvScatter {
+  const int* pack_idx;  // packed row -> padded cell (nullptr: identity, padded A/B mode)
+  bf16 *q, *k, *v;
+  int S, hk, d;
+};
 
 // fp32 SIMT GEMM (parity mode): D[M,N] = A[M,K] W[N,K]^T (+bias) (gelu)
 void launch_gemm_f32(const float* A, const float* W, const float* bias, float* D, int M, int N, int K, int epi,
@@ -71,9 +81,10 @@ void launch_gemm_f32(const float* A, const float* W, const float* bias, float* D
 // inner box and 128-byte swizzle: A [M,K] with a 128-row box, W [N,K] with a bn-row box (bn = the
 // tile N, 256 or 128, chosen per call by tc_pick_bn).
 bool make_tmap_kmajor(CUtensorMap* map, const void* ptr, int rows, int K, int box_rows);
-int tc_pick_bn(int M, int N);
+int tc_pick_bn(int M, int N);  // tile code (see gemm_tc.cu)
+int tc_w_box(int code);        // row box of the W tensor map the code needs (256, 128, 96 or 64)
 void launch_gemm_tc(const CUtensorMap& tmA, const CUtensorMap& tmB, int bn, const float* bias, bf16* D, int M, int N,
-                    int K, int epi, cudaStream_t st);
+                    int K, int epi, cudaStream_t st, const QkvScatter* qkv = nullptr);
 int num_sms();
 
 }  // namespace energon

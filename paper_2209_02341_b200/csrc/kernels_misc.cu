@@ -82,10 +82,12 @@ template <> struct Row4<bf16> {
 };
 
 constexpr int LN_THREADS = 256;
-constexpr int LN_MAXV = 12;  // float4 per thread: H <= 12288
+// Each LayerNorm-family kernel is instantiated for NV = ceil(H / 4 / 256) float4 per thread (1..12,
+// H <= 12288), so the row stays in exactly as many registers as it needs (occupancy).
 
 // Two-pass LayerNorm statistics over a row held in registers (biased variance,
 // eps inside the square root, fp32).
+template <int LN_MAXV>
 __device__ __forceinline__ void row_stats(const float4 (&v)[LN_MAXV], int nv, int H, float eps, float* red,
                                           float& mean, float& rstd) {
   float s = 0.f;
@@ -115,7 +117,7 @@ __device__ __forceinline__ float4 ln_apply(float4 x, float mean, float rstd, con
 // rows are gathered.  X[t] = E[tok[cell]] + P[pos] (fp32 residual stream), A[t] = LN1_0(X[t]).
 // pack_idx == nullptr means the padded A/B mode (row t is cell t).  An id outside [0, V) gathers
 // row 0 and raises the device error flag (checked by energon_sync), so the kernel never faults.
-template <typename Act>
+template <typename Act, int LN_MAXV>
 __global__ void __launch_bounds__(LN_THREADS) embed_ln_kernel(const int* __restrict__ tok, const int* __restrict__ pack_idx,
                                                               int S, int V, int H, const Act* __restrict__ tok_emb,
                                                               const Act* __restrict__ pos_emb, const float* __restrict__ g,
@@ -155,7 +157,7 @@ __global__ void __launch_bounds__(LN_THREADS) embed_ln_kernel(const int* __restr
 }
 
 // Hidden-state entry (energon_forward_hidden): X[t] = x[cell] (fp32), A[t] = LN1(X[t]).
-template <typename Act>
+template <typename Act, int LN_MAXV>
 __global__ void __launch_bounds__(LN_THREADS) gather_ln_kernel(const float* __restrict__ x, const int* __restrict__ pack_idx,
                                                                int H, const float* __restrict__ g, const float* __restrict__ b,
                                                                float eps, float* __restrict__ X, Act* __restrict__ A) {
@@ -185,7 +187,7 @@ __global__ void __launch_bounds__(LN_THREADS) gather_ln_kernel(const float* __re
 // X[t] += P[t] + bias (P = the reduced row-parallel partial, "accumulated by communications",
 // PAPER.md:290; bias added once after the reduce), then A[t] = LN(X[t]).
 // With A == nullptr only the residual update is done.
-template <typename Act>
+template <typename Act, int LN_MAXV>
 __global__ void __launch_bounds__(LN_THREADS) residual_ln_kernel(float* __restrict__ X, const Act* __restrict__ P,
                                                                  const float* __restrict__ bias, int H,
                                                                  const float* __restrict__ g, const float* __restrict__ b,
@@ -222,7 +224,7 @@ __global__ void __launch_bounds__(LN_THREADS) residual_ln_kernel(float* __restri
 // ============================================================================ a13: final LN + unpack
 // out[cell] = LN_f(X[unpack_idx[cell]]) for valid cells, exactly 0 for pad cells;
 // every output row is written once.  rows_are_cells: padded A/B mode (X row = cell).
-template <typename Out>
+template <typename Out, int LN_MAXV>
 __global__ void __launch_bounds__(LN_THREADS) final_ln_unpack_kernel(const float* __restrict__ X, const int* __restrict__ unpack_idx,
                                                                      int rows_are_cells, int H, const float* __restrict__ g,
                                                                      const float* __restrict__ b, float eps, int apply_ln,
@@ -379,30 +381,49 @@ void launch_index_maps(const LensParam& lp, int B, int S, int* offsets, int* pac
   index_maps_kernel<<<grid_for(cells, 256, 148 * 4), 256, 0, st>>>(lp, B, S, offsets, pack_idx, pos, unpack_idx);
 }
 
+#define NV_DISPATCH(H, KERNEL_CALL)                                         \
+  switch ((((H) / 4) + LN_THREADS - 1) / LN_THREADS) {                      \
+    case 1: { constexpr int NVX = 1; KERNEL_CALL; } break;                  \
+    case 2: { constexpr int NVX = 2; KERNEL_CALL; } break;                  \
+    case 3: { constexpr int NVX = 3; KERNEL_CALL; } break;                  \
+    case 4: { constexpr int NVX = 4; KERNEL_CALL; } break;                  \
+    case 5: { constexpr int NVX = 5; KERNEL_CALL; } break;                  \
+    case 6: { constexpr int NVX = 6; KERNEL_CALL; } break;                  \
+    case 7: { constexpr int NVX = 7; KERNEL_CALL; } break;                  \
+    case 8: { constexpr int NVX = 8; KERNEL_CALL; } break;                  \
+    case 9: { constexpr int NVX = 9; KERNEL_CALL; } break;                  \
+    case 10: { constexpr int NVX = 10; KERNEL_CALL; } break;                \
+    case 11: { constexpr int NVX = 11; KERNEL_CALL; } break;                \
+    default: { constexpr int NVX = 12; KERNEL_CALL; } break;                \
+  }
+
 template <typename Act>
 void launch_embed_ln(const int* tok, const int* pack_idx, int rows, int S, int V, int H, const Act* tok_emb,
                      const Act* pos_emb, const float* g, const float* b, float eps, float* X, Act* A, int* err,
                      cudaStream_t st) {
-  if (rows > 0) embed_ln_kernel<Act><<<rows, LN_THREADS, 0, st>>>(tok, pack_idx, S, V, H, tok_emb, pos_emb, g, b, eps, X, A, err);
+  if (rows > 0)
+    NV_DISPATCH(H, (embed_ln_kernel<Act, NVX><<<rows, LN_THREADS, 0, st>>>(tok, pack_idx, S, V, H, tok_emb, pos_emb, g, b,
+                                                                           eps, X, A, err)))
 }
 
 template <typename Act>
 void launch_gather_ln(const float* x, const int* pack_idx, int rows, int H, const float* g, const float* b, float eps,
                       float* X, Act* A, cudaStream_t st) {
-  if (rows > 0) gather_ln_kernel<Act><<<rows, LN_THREADS, 0, st>>>(x, pack_idx, H, g, b, eps, X, A);
+  if (rows > 0) NV_DISPATCH(H, (gather_ln_kernel<Act, NVX><<<rows, LN_THREADS, 0, st>>>(x, pack_idx, H, g, b, eps, X, A)))
 }
 
 template <typename Act>
 void launch_residual_ln(float* X, const Act* P, const float* bias, int rows, int H, const float* g, const float* b,
                         float eps, Act* A, cudaStream_t st) {
-  if (rows > 0) residual_ln_kernel<Act><<<rows, LN_THREADS, 0, st>>>(X, P, bias, H, g, b, eps, A);
+  if (rows > 0) NV_DISPATCH(H, (residual_ln_kernel<Act, NVX><<<rows, LN_THREADS, 0, st>>>(X, P, bias, H, g, b, eps, A)))
 }
 
 template <typename Out>
 void launch_final_ln_unpack(const float* X, const int* unpack_idx, int rows_are_cells, int cells, int H, const float* g,
                             const float* b, float eps, int apply_ln, Out* out, cudaStream_t st) {
   if (cells > 0)
-    final_ln_unpack_kernel<Out><<<cells, LN_THREADS, 0, st>>>(X, unpack_idx, rows_are_cells, H, g, b, eps, apply_ln, out);
+    NV_DISPATCH(H, (final_ln_unpack_kernel<Out, NVX><<<cells, LN_THREADS, 0, st>>>(X, unpack_idx, rows_are_cells, H, g, b,
+                                                                                   eps, apply_ln, out)))
 }
 
 template <typename Act>

@@ -16,6 +16,7 @@
 // and once per batch: index maps (a1), embed+pack+LN1 (a2, a3), final LN + unpack (a13).
 #include <nccl.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <string>
@@ -30,11 +31,14 @@ namespace {
 
 thread_local std::string g_last_error;
 
+const int kBoxes[4] = {256, 128, 96, 64};
+int box_slot(int box) { return box == 256 ? 0 : box == 128 ? 1 : box == 96 ? 2 : 3; }
+
 struct LayerDev {
   void *wqkv = nullptr, *wo = nullptr, *w1 = nullptr, *w2 = nullptr;  // [N, K] row-major (K-major operands)
   float *bqkv = nullptr, *bo = nullptr, *b1 = nullptr, *b2 = nullptr;
   float *ln1g = nullptr, *ln1b = nullptr, *ln2g = nullptr, *ln2b = nullptr;
-  CUtensorMap tm_qkv[2], tm_o[2], tm_1[2], tm_2[2];  // [0]: 256-row box, [1]: 128-row box
+  CUtensorMap tm_qkv[4], tm_o[4], tm_1[4], tm_2[4];  // W row box 256 / 128 / 96 / 64 (box_slot())
   bool loaded = false;
 };
 
@@ -47,6 +51,7 @@ struct energon_ctx {
   size_t act = 4;  // bytes per activation element
   ncclComm_t nccl = nullptr;
   bool local_group = false;
+  bool fuse = true;  // fused a5 / a7 (ENERGON_NO_FUSE=1 disables, for A/B and tests)
   // replicated embeddings / final LN
   void* tok_emb = nullptr;
   void* pos_emb = nullptr;
@@ -152,6 +157,7 @@ energon_status setup(energon_ctx* c) {
   c->act = c->bf16 ? 2 : 4;
   memset(&c->stats, 0, sizeof(c->stats));
   memset(&c->pacc, 0, sizeof(c->pacc));
+  if (const char* e = getenv("ENERGON_NO_FUSE")) c->fuse = e[0] != '1';
   CU(c, cudaSetDevice(g.device));
   CU(c, cudaStreamCreateWithFlags(&c->load_stream, cudaStreamNonBlocking));
   CU(c, cudaHostAlloc(&c->err_host, sizeof(int), cudaHostAllocMapped));
@@ -343,11 +349,11 @@ energon_status allreduce(energon_ctx** cs, int n, int rows, cudaStream_t st) {
 
 template <typename Act>
 void gemm(energon_ctx* c, const CUtensorMap& tmA, const CUtensorMap* tmB, const void* A, const void* W,
-          const float* bias, void* D, int M, int N, int K, int epi, cudaStream_t st) {
+          const float* bias, void* D, int M, int N, int K, int epi, cudaStream_t st, const QkvScatter* qs = nullptr) {
   Prof p(c, st, P_GEMM, 2.0 * M * N * K);
   if constexpr (sizeof(Act) == 2) {
-    const int bn = tc_pick_bn(M, N);  // 512: 2-CTA pair kernel (128-row W box), 256 / 128: 1-CTA
-    launch_gemm_tc(tmA, tmB[bn == 256 ? 0 : 1], bn, bias, reinterpret_cast<bf16*>(D), M, N, K, epi, st);
+    const int code = tc_pick_bn(M, N);
+    launch_gemm_tc(tmA, tmB[box_slot(tc_w_box(code))], code, bias, reinterpret_cast<bf16*>(D), M, N, K, epi, st, qs);
   } else {
     launch_gemm_f32(reinterpret_cast<const float*>(A), reinterpret_cast<const float*>(W), bias,
                     reinterpret_cast<float*>(D), M, N, K, epi, st);
@@ -364,6 +370,11 @@ energon_status forward_t(energon_ctx** cs, int n, const Call& a, int64_t T) {
   const int rows = drce ? (int)T : a.B * a.S;
   const float eps = g.ln_eps;
   const double act = (double)sizeof(Act), H = c0->H, Hk = c0->Hk;
+  // Fused forms of the paper's two layout kernels on the bf16 tensor-core path:
+  // a5 inside the QKV GEMM epilogue, a7 inside the attention epilogue (DRCE mode only; the padded
+  // A/B mode keeps the standalone repack because it must zero the pad query rows).
+  const bool fuse_a5 = sizeof(Act) == 2 && c0->fuse && (c0->d == 64 || c0->d == 128);
+  const bool fuse_a7 = fuse_a5 && drce;
   LensParam lp;
   double allowed = 0.0;  // sum over sequences of visible (query, key) pairs
   for (int b = 0; b < a.B; ++b) {
@@ -411,25 +422,40 @@ energon_status forward_t(energon_ctx** cs, int n, const Call& a, int64_t T) {
       energon_ctx* c = cs[i];
       const LayerDev& L = c->layers[l];
       const int* pidx = drce ? c->pack_idx : nullptr;
-      gemm<Act>(c, c->tmA_A, L.tm_qkv, c->A, L.wqkv, L.bqkv, c->QKV, rows, 3 * c->Hk, c->H, EPI_BIAS, st);
-      {
+      if (fuse_a5) {
+        // a4 + a5: the QKV epilogue scatters straight into the padded per-head Q, K, V
+        QkvScatter qs{pidx, reinterpret_cast<bf16*>(c->Q), reinterpret_cast<bf16*>(c->K),
+                      reinterpret_cast<bf16*>(c->Vb), a.S, c->hk, c->d};
+        gemm<Act>(c, c->tmA_A, L.tm_qkv, c->A, L.wqkv, L.bqkv, nullptr, rows, 3 * c->Hk, c->H, EPI_BIAS_QKV, st, &qs);
+      } else {
+        gemm<Act>(c, c->tmA_A, L.tm_qkv, c->A, L.wqkv, L.bqkv, c->QKV, rows, 3 * c->Hk, c->H, EPI_BIAS, st);
         Prof p(c, st, P_MEM, 2.0 * rows * 3 * Hk * act);
         launch_unpack_qkv<Act>(reinterpret_cast<const Act*>(c->QKV), pidx, rows, a.S, c->hk, c->d,
                                reinterpret_cast<Act*>(c->Q), reinterpret_cast<Act*>(c->K), reinterpret_cast<Act*>(c->Vb),
                                st);
+        c->stats.kernel_launches++;
       }
-      {
+      if (fuse_a7) {
+        // a6 + a7: attention writes its rows straight into the packed context [T, Hk]
         Prof p(c, st, P_ATTN, 4.0 * c->d * allowed * c->hk);
-        launch_attention<Act>(reinterpret_cast<const Act*>(c->Q), reinterpret_cast<const Act*>(c->K),
-                              reinterpret_cast<const Act*>(c->Vb), reinterpret_cast<Act*>(c->O), lp, a.B, c->hk, a.S,
-                              c->d, g.causal, st);
+        launch_attention_packed(reinterpret_cast<const bf16*>(c->Q), reinterpret_cast<const bf16*>(c->K),
+                                reinterpret_cast<const bf16*>(c->Vb), reinterpret_cast<bf16*>(c->Ctx), c->offsets, lp,
+                                a.B, c->hk, a.S, c->d, g.causal, st);
+        c->stats.kernel_launches++;
+      } else {
+        {
+          Prof p(c, st, P_ATTN, 4.0 * c->d * allowed * c->hk);
+          launch_attention<Act>(reinterpret_cast<const Act*>(c->Q), reinterpret_cast<const Act*>(c->K),
+                                reinterpret_cast<const Act*>(c->Vb), reinterpret_cast<Act*>(c->O), lp, a.B, c->hk, a.S,
+                                c->d, g.causal, st);
+        }
+        {
+          Prof p(c, st, P_MEM, 2.0 * rows * Hk * act);
+          launch_repack<Act>(reinterpret_cast<const Act*>(c->O), pidx, c->unpack_idx, rows, a.S, c->hk, c->d,
+                             reinterpret_cast<Act*>(c->Ctx), st);
+        }
+        c->stats.kernel_launches += 2;
       }
-      {
-        Prof p(c, st, P_MEM, 2.0 * rows * Hk * act);
-        launch_repack<Act>(reinterpret_cast<const Act*>(c->O), pidx, c->unpack_idx, rows, a.S, c->hk, c->d,
-                           reinterpret_cast<Act*>(c->Ctx), st);
-      }
-      c->stats.kernel_launches += 3;
       gemm<Act>(c, c->tmA_Ctx, L.tm_o, c->Ctx, L.wo, nullptr, c->P, rows, c->H, c->Hk, EPI_NONE, st);
     }
     energon_status s = allreduce<Act>(cs, n, rows, st);
@@ -673,11 +699,10 @@ energon_status energon_load_layer_weights(energon_ctx* c, int32_t layer, const e
     return s;
   CU(c, cudaStreamSynchronize(c->load_stream));
   if (c->bf16) {
-    const int boxes[2] = {256, 128};
-    for (int i = 0; i < 2; ++i) {
-      if (!make_tmap_kmajor(&L.tm_qkv[i], L.wqkv, 3 * Hk, H, boxes[i]) ||
-          !make_tmap_kmajor(&L.tm_o[i], L.wo, H, Hk, boxes[i]) || !make_tmap_kmajor(&L.tm_1[i], L.w1, Fk, H, boxes[i]) ||
-          !make_tmap_kmajor(&L.tm_2[i], L.w2, H, Fk, boxes[i]))
+    for (int i = 0; i < 4; ++i) {
+      if (!make_tmap_kmajor(&L.tm_qkv[i], L.wqkv, 3 * Hk, H, kBoxes[i]) ||
+          !make_tmap_kmajor(&L.tm_o[i], L.wo, H, Hk, kBoxes[i]) || !make_tmap_kmajor(&L.tm_1[i], L.w1, Fk, H, kBoxes[i]) ||
+          !make_tmap_kmajor(&L.tm_2[i], L.w2, H, Fk, kBoxes[i]))
         return fail(c, ENERGON_ERR_CUDA, "cuTensorMapEncodeTiled failed for a weight operand");
     }
   }
@@ -823,11 +848,11 @@ energon_status energon_gemm(int32_t dtype, const void* A, const void* W, const f
                     reinterpret_cast<float*>(D), M, N, K, epi, (cudaStream_t)stream);
   } else if (dtype == ENERGON_DTYPE_BF16) {
     if (K % 8 || N % 8) return fail(nullptr, ENERGON_ERR_SHAPE, "bf16 GEMM needs K and N multiples of 8");
-    const int bn = tc_pick_bn(M, N);
+    const int code = tc_pick_bn(M, N);
     CUtensorMap ta, tb;
-    if (!make_tmap_kmajor(&ta, A, M, K, 128) || !make_tmap_kmajor(&tb, W, N, K, bn == 256 ? 256 : 128))
+    if (!make_tmap_kmajor(&ta, A, M, K, 128) || !make_tmap_kmajor(&tb, W, N, K, tc_w_box(code)))
       return fail(nullptr, ENERGON_ERR_CUDA, "cuTensorMapEncodeTiled failed");
-    launch_gemm_tc(ta, tb, bn, bias, reinterpret_cast<bf16*>(D), M, N, K, epi, (cudaStream_t)stream);
+    launch_gemm_tc(ta, tb, code, bias, reinterpret_cast<bf16*>(D), M, N, K, epi, (cudaStream_t)stream);
   } else {
     return fail(nullptr, ENERGON_ERR_ARG, "dtype must be F32 or BF16");
   }

@@ -315,3 +315,50 @@ def test_attention_kernel_vs_oracle(dtype, d, causal):
         assert np.isfinite(got[b, :, :n]).all()
         assert np.abs(got[b, :, :n] - ref[b, :, :n]).max() <= tol * max(1.0, np.abs(ref[b, :, :n]).max())
         assert (got[b, :, n:] == 7.0).all()  # pad query rows untouched
+
+
+# ----------------------------------------------------------------------------- fused a5 / a7
+@pytest.mark.parametrize("drce", [1, 0])
+def test_fused_layout_kernels_bitexact(drce, monkeypatch):
+    """a5 fused into the QKV epilogue and a7 fused into attention produce the same bits as the
+    standalone paper kernels."""
+    shape = dict(SHAPES["gpt2s"], L=2)
+    B, S, seed = 8, 96, 2
+    lens = synth.random_lengths(B, S, seed)
+    tok = synth.tokens(B, S, shape["V"], lens, seed)
+    outs = []
+    for nofuse in ("0", "1"):
+        monkeypatch.setenv("ENERGON_NO_FUSE", nofuse)
+        ctxs = make_engine(shape, seed, "bf16", B * S, drce=drce)
+        try:
+            outs.append(run_forward(ctxs, tok, lens, "bf16", shape["H"]))
+        finally:
+            destroy(ctxs)
+    assert np.array_equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("k", [2, 4])
+def test_forward_local_tp_fused_d64(k):
+    """Local TP with head_dim 64 (fused a5/a7 path) against the oracle, bf16."""
+    shape = dict(L=2, H=256, h=4, F=1024, V=500, max_seq=64)
+    B, S, seed = 5, 64, 9
+    lens = synth.random_lengths(B, S, seed)
+    tok = synth.tokens(B, S, shape["V"], lens, seed)
+    ctxs = make_engine(shape, seed, "bf16", B * S, k=k)
+    try:
+        y = run_forward(ctxs, tok, lens, "bf16", shape["H"])
+    finally:
+        destroy(ctxs)
+    layers, emb = oracle_model(shape, seed, "bf16")
+    cfg = oracle.make_cfg(shape["L"], shape["H"], shape["h"], shape["F"])
+    ref = oracle.forward_padded(cfg, layers, emb, tok, lens)
+    assert max_abs_rel(y, ref, lens) <= 2e-2
+
+
+@pytest.mark.parametrize("code", [1256, 1192, 1128, 256, 128])
+@pytest.mark.parametrize("M,N,K,epi", [(700, 1000, 320, 1), (257, 392, 640, 2), (4096, 640, 128, 0)])
+def test_gemm_every_tile_shape(code, M, N, K, epi, monkeypatch):
+    """Every tcgen05 tile variant (2-CTA 256x{256,192,128}, 1-CTA 128x{256,128}) on ragged shapes."""
+    monkeypatch.setenv("ENERGON_GEMM_TILE", str(code))
+    got, ref = _gemm_case(M, N, K, "bf16", epi, seed=code)
+    assert (np.abs(got - ref) <= 4e-3 * np.abs(ref) + 1e-4 * np.abs(ref).max()).all()
