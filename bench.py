@@ -208,11 +208,9 @@ def energon_arm(args, world, rank, local):
                               dtype="bf16", drce=args.drce, tp_size=world, tp_rank=rank, device=local)
     uid = None
     if world > 1:
-        buf = torch.zeros(128, dtype=torch.uint8, device="cuda")
-        if rank == 0:
-            buf.copy_(torch.frombuffer(bytearray(energon.energon_get_unique_id()), dtype=torch.uint8))
-        dist.broadcast(buf, 0)
-        uid = bytes(buf.cpu().numpy().tobytes())
+        from paper_2209_02341_b200 import dist as edist
+        uid = edist.broadcast_bytes(energon.energon_get_unique_id() if rank == 0 else None, 128, device="cuda")
+        lens = edist.broadcast_lengths(lens, device="cuda")  # the engine command's seq_lens
     ctx = energon.energon_init(cfg, uid)
 
     # weights: generated on the device by the seeded counter-based generator, loaded unsharded
@@ -239,9 +237,8 @@ def energon_arm(args, world, rank, local):
     def max_over_ranks(x: float) -> float:
         if dist is None:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        from paper_2209_02341_b200 import dist as edist
+        return edist.max_over_ranks(x, device="cuda")
 
     for _ in range(args.warmup):
         energon.energon_forward(ctx, tok, lens, out, stream)

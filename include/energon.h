@@ -122,7 +122,19 @@ typedef struct {
   int64_t gemm_launches, attn_launches, mem_launches, comm_calls;
 } energon_profile;
 
+/*
+ * This rank's share under 1-D TP: heads
+ * [head0, head0 + heads) -> columns [qkv_col0, qkv_col0 + qkv_cols) of wq / wk / wv and rows of wo;
+ * FFN columns [ffn_col0, ffn_col0 + ffn_cols) of w1 / b1 and rows of w2.
+ */
+typedef struct {
+  int32_t head0, heads, qkv_col0, qkv_cols, ffn_col0, ffn_cols;
+} energon_shard;
+
 typedef struct energon_ctx energon_ctx;
+
+/* Host-only: the shard of cfg->tp_rank (validates cfg like energon_init; touches no device). */
+ENERGON_API energon_status energon_shard_plan(const energon_config* cfg, energon_shard* out);
 
 /* 128-byte NCCL unique id for a TP group (call on one rank, broadcast the bytes). */
 ENERGON_API energon_status energon_get_unique_id(void* out_128_bytes);

@@ -546,6 +546,20 @@ const char* energon_status_string(energon_status s) {
 
 const char* energon_last_error(const energon_ctx* ctx) { return ctx ? ctx->err.c_str() : g_last_error.c_str(); }
 
+energon_status energon_shard_plan(const energon_config* cfg, energon_shard* out) {
+  if (!out) return fail(nullptr, ENERGON_ERR_ARG, "out is NULL");
+  energon_status s = validate_config(cfg);
+  if (s) return s;
+  const int k = cfg->tp_size, r = cfg->tp_rank, hk = cfg->num_heads / k, d = cfg->hidden / cfg->num_heads;
+  out->head0 = r * hk;
+  out->heads = hk;
+  out->qkv_col0 = r * hk * d;
+  out->qkv_cols = hk * d;
+  out->ffn_col0 = r * (cfg->ffn / k);
+  out->ffn_cols = cfg->ffn / k;
+  return ENERGON_OK;
+}
+
 energon_status energon_get_unique_id(void* out) {
   if (!out) return fail(nullptr, ENERGON_ERR_ARG, "out is NULL");
   ncclUniqueId id;
@@ -674,12 +688,15 @@ energon_status energon_load_layer_weights(energon_ctx* c, int32_t layer, const e
   }
   const bool full = layout == ENERGON_FULL, dev = on_dev != 0;
   // column-parallel: this rank's heads / FFN columns; row-parallel: the matching rows
-  const int64_t qk_ld = full ? H : Hk, qk_col0 = full ? (int64_t)r * Hk : 0;
-  const int64_t o_rows = full ? H : Hk, o_row0 = full ? (int64_t)r * Hk : 0;
-  const int64_t w1_ld = full ? F : Fk, w1_col0 = full ? (int64_t)r * Fk : 0;
-  const int64_t w2_rows = full ? F : Fk, w2_row0 = full ? (int64_t)r * Fk : 0;
-  const int64_t bq_n = full ? H : Hk, bq_off = full ? (int64_t)r * Hk : 0;
-  const int64_t b1_n = full ? F : Fk, b1_off = full ? (int64_t)r * Fk : 0;
+  energon_shard sh;
+  energon_shard_plan(&c->cfg, &sh);
+  (void)r;
+  const int64_t qk_ld = full ? H : Hk, qk_col0 = full ? sh.qkv_col0 : 0;
+  const int64_t o_rows = full ? H : Hk, o_row0 = full ? sh.qkv_col0 : 0;
+  const int64_t w1_ld = full ? F : Fk, w1_col0 = full ? sh.ffn_col0 : 0;
+  const int64_t w2_rows = full ? F : Fk, w2_row0 = full ? sh.ffn_col0 : 0;
+  const int64_t bq_n = full ? H : Hk, bq_off = full ? sh.qkv_col0 : 0;
+  const int64_t b1_n = full ? F : Fk, b1_off = full ? sh.ffn_col0 : 0;
   if ((s = put_matrix(c, sd, w->wq, dev, H, qk_ld, 0, qk_col0, Hk, H, L.wqkv, 0)) ||
       (s = put_matrix(c, sd, w->wk, dev, H, qk_ld, 0, qk_col0, Hk, H, L.wqkv, Hk)) ||
       (s = put_matrix(c, sd, w->wv, dev, H, qk_ld, 0, qk_col0, Hk, H, L.wqkv, 2 * Hk)) ||

@@ -26,7 +26,8 @@ LAYER_TENSORS = ("wq", "wk", "wv", "wo", "bq", "bk", "bv", "bo",
 EXPORTS = ("energon_get_unique_id", "energon_init", "energon_init_local_group", "energon_load_embeddings",
            "energon_load_layer_weights", "energon_forward", "energon_forward_group", "energon_forward_hidden",
            "energon_sync", "energon_get_stats", "energon_last_error", "energon_status_string", "energon_destroy",
-           "energon_index_maps", "energon_gemm", "energon_attention", "energon_set_profiling", "energon_get_profile")
+           "energon_index_maps", "energon_gemm", "energon_attention", "energon_set_profiling", "energon_get_profile",
+           "energon_shard_plan")
 
 
 class EnergonError(RuntimeError):
@@ -43,6 +44,10 @@ class Config(ctypes.Structure):
 
 class LayerWeights(ctypes.Structure):
     _fields_ = [(n, ctypes.c_void_p) for n in LAYER_TENSORS]
+
+
+class Shard(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int32) for n in ("head0", "heads", "qkv_col0", "qkv_cols", "ffn_col0", "ffn_cols")]
 
 
 class Stats(ctypes.Structure):
@@ -88,6 +93,7 @@ def load_library(path: str = SO_PATH):
     L.energon_index_maps.argtypes = [ctypes.POINTER(ctypes.c_int32), I32, I32, P, P, P, P, P]
     L.energon_gemm.argtypes = [I32, P, P, P, P, I32, I32, I32, I32, P]
     L.energon_attention.argtypes = [I32, P, P, P, P, ctypes.POINTER(ctypes.c_int32), I32, I32, I32, I32, I32, P]
+    L.energon_shard_plan.argtypes = [ctypes.POINTER(Config), ctypes.POINTER(Shard)]
     L.energon_set_profiling.argtypes = [P, I32]
     L.energon_get_profile.argtypes = [P, ctypes.POINTER(Profile)]
     for name in EXPORTS:
@@ -135,6 +141,12 @@ def make_config(num_layers, hidden, num_heads, ffn, vocab, max_seq, max_tokens, 
 
 
 # ----------------------------------------------------------------------------- ABI wrappers (same names)
+def energon_shard_plan(cfg: Config) -> dict:
+    sh = Shard()
+    _check(load_library().energon_shard_plan(ctypes.byref(cfg), ctypes.byref(sh)))
+    return {n: getattr(sh, n) for n, _ in Shard._fields_}
+
+
 def energon_get_unique_id() -> bytes:
     buf = ctypes.create_string_buffer(128)
     _check(load_library().energon_get_unique_id(buf))
