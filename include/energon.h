@@ -192,6 +192,14 @@ ENERGON_API energon_status energon_forward_hidden(energon_ctx* ctx, const float*
 /* Block until the context's work is done; surfaces sticky CUDA / NCCL / token errors. */
 ENERGON_API energon_status energon_sync(energon_ctx* ctx);
 ENERGON_API energon_status energon_get_stats(const energon_ctx* ctx, energon_stats* out);
+/*
+ * Runtime options (take effect at the next forward; host-only, no device work):
+ *   ENERGON_OPT_DRCE   1 = packed linears (the method), 0 = padded A/B ("pure EnergonAI",
+ *                      PAPER.md:567-571); the workspace is sized for max_tokens padded rows either way.
+ */
+enum { ENERGON_OPT_DRCE = 1 };
+ENERGON_API energon_status energon_set_option(energon_ctx* ctx, int32_t option, int32_t value);
+
 /* Enable (1) / disable (0) per-launch CUDA-event timing; enabling resets the accumulators. */
 ENERGON_API energon_status energon_set_profiling(energon_ctx* ctx, int32_t enable);
 /* Synchronise the recorded events and return the accumulated profile. */

@@ -351,11 +351,78 @@ __device__ __forceinline__ void raster(int tile, int num_m, int num_n, int group
   n_blk = r / gsize;
 }
 
+// Work decomposition of the pair kernel.  Tiles [0, full) are whole-K units (data parallel);
+// when the last wave would leave clusters idle, each of the `rem` tail tiles is split into
+// `splits` K-ranges that run concurrently on the otherwise idle clusters ("stream-K tail").  A
+// split unit writes its fp32 partial tile to `ws`; the last split to arrive (per tile and CTA,
+// counted in `counters`, which self-reset) sums the partials in split order 0..splits-1
+// (deterministic) and runs the epilogue.
+struct TailPlan {
+  int full;    // whole tiles
+  int splits;  // K-splits per tail tile (0: no tail split)
+  float* ws;   // [rem * splits][2][128][BN] fp32 partials
+  int* counters;  // [rem][2]
+};
+
+__device__ __forceinline__ void unit_decode(int u, const TailPlan& tp, int nkb, int& tile, int& kb0, int& kb1,
+                                            int& split, int& tail) {
+  if (tp.splits == 0 || u < tp.full) {
+    tile = u;
+    kb0 = 0;
+    kb1 = nkb;
+    split = -1;
+    tail = -1;
+    return;
+  }
+  const int j = u - tp.full;
+  tail = j / tp.splits;
+  split = j - tail * tp.splits;
+  tile = tp.full + tail;
+  kb0 = (int)(((long)nkb * split) / tp.splits);
+  kb1 = (int)(((long)nkb * (split + 1)) / tp.splits);
+}
+
+template <int EPI>
+__device__ __forceinline__ void epi_store(float (&v)[32], int row, int n0, int M, int N, bf16* __restrict__ D,
+                                          const float* __restrict__ bias, const QkvScatter& qs) {
+  if (row >= M || n0 >= N) return;
+  if (EPI >= EPI_BIAS) {
+#pragma unroll
+    for (int j = 0; j < 32; j += 4) {
+      if (n0 + j < N) {
+        const float4 bb = __ldg(reinterpret_cast<const float4*>(bias + n0 + j));
+        v[j] += bb.x;
+        v[j + 1] += bb.y;
+        v[j + 2] += bb.z;
+        v[j + 3] += bb.w;
+      }
+    }
+  }
+  if (EPI == EPI_BIAS_GELU) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = gelu_fast(v[j]);
+  }
+  bf16* dst = (EPI == EPI_BIAS_QKV) ? qkv_dst(qs, row, n0, N) : D + (int64_t)row * N + n0;
+#pragma unroll
+  for (int j = 0; j < 32; j += 8) {
+    if (n0 + j < N) {
+      uint4 o;
+      o.x = pack_bf16x2(v[j], v[j + 1]);
+      o.y = pack_bf16x2(v[j + 2], v[j + 3]);
+      o.z = pack_bf16x2(v[j + 4], v[j + 5]);
+      o.w = pack_bf16x2(v[j + 6], v[j + 7]);
+      *reinterpret_cast<uint4*>(dst + j) = o;
+    }
+  }
+}
+
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
 template <int BN, int EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     bf16* __restrict__ D, const float* __restrict__ bias, int M, int N, int K, int group_m,
-                    const QkvScatter qs) {
+                    const QkvScatter qs, const TailPlan tp) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   using C = Tc2Cfg<BN>;
@@ -366,6 +433,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+  int* fix_flag = reinterpret_cast<int*>(tmem_holder + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
@@ -374,6 +442,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   const int num_m = (M + 255) / 256, num_n = (N + BN - 1) / BN;
   const int num_tiles = num_m * num_n;
   const int nkb = (K + TC_BK - 1) / TC_BK;
+  const int num_units = tp.splits ? tp.full + (num_tiles - tp.full) * tp.splits : num_tiles;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -402,10 +471,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = cid; tile < num_tiles; tile += ncl) {
+      for (int u = cid; u < num_units; u += ncl) {
+        int tile, kb0, kb1, split, tail;
+        unit_decode(u, tp, nkb, tile, kb0, kb1, split, tail);
         int m_blk, n_blk;
         raster(tile, num_m, num_n, group_m, m_blk, n_blk);
-        for (int kb = 0; kb < nkb; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           const uint32_t fb = smem_u32(&full[stage]) & PEER_MASK;
           if (leader) mbar_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
@@ -424,17 +495,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int tile = cid; tile < num_tiles; tile += ncl) {
+      for (int u = cid; u < num_units; u += ncl) {
+        int tile, kb0, kb1, split, tail;
+        unit_decode(u, tp, nkb, tile, kb0, kb1, split, tail);
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
-        for (int kb = 0; kb < nkb; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint64_t a0 = umma_desc_sw128(smem_u32(sA + stage * C::A_BYTES));
           const uint64_t b0 = umma_desc_sw128(smem_u32(sB + stage * C::B_BYTES));
 #pragma unroll
-          for (int k = 0; k < TC_BK / 16; ++k) umma_bf16_2sm(d_tmem, a0 + 2 * k, b0 + 2 * k, C::IDESC, (kb | k) != 0);
+          for (int k = 0; k < TC_BK / 16; ++k)
+            umma_bf16_2sm(d_tmem, a0 + 2 * k, b0 + 2 * k, C::IDESC, (kb > kb0 || k > 0) ? 1u : 0u);
           umma_commit_2sm_mc(&empty[stage]);
           if (++stage == C::STAGES) {
             stage = 0;
@@ -450,54 +524,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     }
   } else if (warp >= 4) {
     const int q = warp - 4;
+    const int etid = threadIdx.x - 128;  // 0..127: this thread's TMEM lane / tile row
     const uint32_t tempty_leader = smem_u32(&tempty[0]) & PEER_MASK;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int tile = cid; tile < num_tiles; tile += ncl) {
+    for (int u = cid; u < num_units; u += ncl) {
+      int tile, kb0, kb1, split, tail;
+      unit_decode(u, tp, nkb, tile, kb0, kb1, split, tail);
       int m_blk, n_blk;
       raster(tile, num_m, num_n, group_m, m_blk, n_blk);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const int row = m_blk * 256 + (int)rank * 128 + q * 32 + lane;
-      bf16* drow = D + (int64_t)row * N;
+      const int row = m_blk * 256 + (int)rank * 128 + etid;
+      // split unit: this CTA's 128 x BN partial goes to the workspace
+      float* part = (split >= 0) ? tp.ws + ((size_t)(tail * tp.splits + split) * 2 + rank) * 128 * BN + (size_t)etid * BN
+                                 : nullptr;
 #pragma unroll 1
       for (int c = 0; c < BN / 32; ++c) {
         uint32_t r[32];
         tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c * 32), r);
-        const int n0 = n_blk * BN + c * 32;
-        if (row < M && n0 < N) {
+        if (split >= 0) {
+#pragma unroll
+          for (int j = 0; j < 32; j += 4)
+            __stcg(reinterpret_cast<float4*>(part + c * 32 + j),
+                   make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]), __uint_as_float(r[j + 2]),
+                               __uint_as_float(r[j + 3])));
+        } else {
           float v[32];
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-          if (EPI >= EPI_BIAS) {
-#pragma unroll
-            for (int j = 0; j < 32; j += 4) {
-              if (n0 + j < N) {
-                const float4 bb = __ldg(reinterpret_cast<const float4*>(bias + n0 + j));
-                v[j] += bb.x;
-                v[j + 1] += bb.y;
-                v[j + 2] += bb.z;
-                v[j + 3] += bb.w;
-              }
-            }
-          }
-          if (EPI == EPI_BIAS_GELU) {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = gelu_fast(v[j]);
-          }
-          bf16* dst = drow + n0;
-          if (EPI == EPI_BIAS_QKV) dst = qkv_dst(qs, row, n0, N);
-#pragma unroll
-          for (int j = 0; j < 32; j += 8) {
-            if (n0 + j < N) {
-              uint4 o;
-              o.x = pack_bf16x2(v[j], v[j + 1]);
-              o.y = pack_bf16x2(v[j + 2], v[j + 3]);
-              o.z = pack_bf16x2(v[j + 4], v[j + 5]);
-              o.w = pack_bf16x2(v[j + 6], v[j + 7]);
-              *reinterpret_cast<uint4*>(dst + j) = o;
-            }
-          }
+          epi_store<EPI>(v, row, n_blk * BN + c * 32, M, N, D, bias, qs);
         }
       }
       tc_fence_before();
@@ -506,6 +562,39 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
+      }
+      if (split >= 0) {
+        // publish the partial; the last of the `splits` arrivals reduces (fixed order) + epilogue
+        __threadfence();
+        epi_bar();
+        if (etid == 0) {
+          const int old = atomicAdd(tp.counters + tail * 2 + rank, 1);
+          *fix_flag = (old == tp.splits - 1);
+          if (old == tp.splits - 1) tp.counters[tail * 2 + rank] = 0;  // self-reset for the next launch
+        }
+        epi_bar();
+        if (*fix_flag) {
+          __threadfence();
+#pragma unroll 1
+          for (int c = 0; c < BN / 32; ++c) {
+            float v[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = 0.f;
+            for (int sp = 0; sp < tp.splits; ++sp) {
+              const float* ps = tp.ws + ((size_t)(tail * tp.splits + sp) * 2 + rank) * 128 * BN + (size_t)etid * BN + c * 32;
+#pragma unroll
+              for (int j = 0; j < 32; j += 4) {
+                const float4 x = __ldcg(reinterpret_cast<const float4*>(ps + j));
+                v[j] += x.x;
+                v[j + 1] += x.y;
+                v[j + 2] += x.z;
+                v[j + 3] += x.w;
+              }
+            }
+            epi_store<EPI>(v, row, n_blk * BN + c * 32, M, N, D, bias, qs);
+          }
+        }
+        epi_bar();  // fix_flag is reused by the next split unit
       }
     }
   }
@@ -568,6 +657,33 @@ int tc_pick_bn(int M, int N) {
   return N <= 128 ? 128 : 256;
 }
 
+// fp32 partial-tile workspace + self-resetting arrival counters of the stream-K tail, one per device
+// (GEMMs of one device are stream-ordered on the forward stream; concurrent GEMMs on other streams of
+// the same device would need their own workspace).
+struct TailWorkspace {
+  float* ws = nullptr;
+  int* counters = nullptr;
+};
+static TailWorkspace& tail_workspace(int pairs, int bn) {
+  static TailWorkspace per_dev[16];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  TailWorkspace& w = per_dev[dev & 15];
+  if (!w.ws) {
+    const size_t units = (size_t)pairs;  // rem * splits <= pairs
+    if (cudaMalloc(&w.ws, units * 2 * 128 * 256 * sizeof(float)) != cudaSuccess ||
+        cudaMalloc(&w.counters, units * 2 * sizeof(int)) != cudaSuccess) {
+      cudaGetLastError();
+      w.ws = nullptr;
+      return w;
+    }
+    cudaMemset(w.counters, 0, units * 2 * sizeof(int));
+    cudaDeviceSynchronize();  // one-time: counters are zero before any stream uses them
+  }
+  (void)bn;
+  return w;
+}
+
 int tc_w_box(int code) { return code > 1000 ? (code - 1000) / 2 : code; }
 
 template <int BN, int EPI>
@@ -583,12 +699,26 @@ static void launch_pair_epi(const CUtensorMap& tmA, const CUtensorMap& tmB, cons
   const int tiles = num_m * num_n;
   const int pairs = num_sms() / 2;
   const int grid = 2 * (tiles < pairs ? tiles : pairs);
+  const int nkb = (K + TC_BK - 1) / TC_BK;
+  TailPlan tp{tiles, 0, nullptr, nullptr};
+  const int rem = tiles % pairs;
+  // Split the tail only when a tile is long (K >= 10240): the fp32 fix-up costs ~10-15 us, which
+  // outweighs the saved fraction of a wave for shorter K (profiles/r01_tile_sweep_streamk.log).
+  if (tiles > pairs && rem > 0 && nkb >= 160 && !getenv("ENERGON_NO_STREAMK")) {
+    int splits = pairs / rem;
+    if (splits > nkb / 4) splits = nkb / 4;  // at least 4 K-blocks per split
+    if (splits > 8) splits = 8;
+    if (splits >= 2) {
+      TailWorkspace& w = tail_workspace(pairs, BN);
+      if (w.ws) tp = TailPlan{tiles - rem, splits, w.ws, w.counters};
+    }
+  }
   // group of A panels kept L2-resident while the group sweeps N (about 48 MB of A per group)
   const double panel = 256.0 * K * 2;
   int group_m = (int)(48.0e6 / panel);
   if (group_m < 1) group_m = 1;
   if (group_m > num_m) group_m = num_m;
-  gemm_tc2_kernel<BN, EPI><<<grid, 256, C::SMEM, st>>>(tmA, tmB, D, bias, M, N, K, group_m, qs);
+  gemm_tc2_kernel<BN, EPI><<<grid, 256, C::SMEM, st>>>(tmA, tmB, D, bias, M, N, K, group_m, qs, tp);
 }
 
 template <int BN, int EPI>

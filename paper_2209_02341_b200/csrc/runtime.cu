@@ -780,6 +780,17 @@ energon_status energon_get_stats(const energon_ctx* c, energon_stats* out) {
 
 void energon_destroy(energon_ctx* c) { release(c); }
 
+energon_status energon_set_option(energon_ctx* c, int32_t option, int32_t value) {
+  if (!c) return fail(nullptr, ENERGON_ERR_ARG, "ctx is NULL");
+  if (option == ENERGON_OPT_DRCE) {
+    if (value != 0 && value != 1) return fail(c, ENERGON_ERR_ARG, "ENERGON_OPT_DRCE takes 0 or 1");
+    c->cfg.drce = value;
+    c->tm_rows = -1;  // activation tensor maps depend on the row count
+    return ENERGON_OK;
+  }
+  return fail(c, ENERGON_ERR_ARG, "unknown option");
+}
+
 energon_status energon_set_profiling(energon_ctx* c, int32_t enable) {
   if (!c) return fail(nullptr, ENERGON_ERR_ARG, "ctx is NULL");
   CU(c, cudaSetDevice(c->cfg.device));

@@ -19,6 +19,7 @@ STATUS = {0: "ENERGON_OK", -1: "ENERGON_ERR_ARG", -2: "ENERGON_ERR_CONFIG", -3: 
 DTYPE_F32, DTYPE_BF16, DTYPE_F64 = 0, 1, 2
 FULL, RANK_SHARD = 0, 1
 MAX_BATCH = 1024
+OPT_DRCE = 1
 LAYER_TENSORS = ("wq", "wk", "wv", "wo", "bq", "bk", "bv", "bo",
                  "w1", "b1", "w2", "b2", "ln1_g", "ln1_b", "ln2_g", "ln2_b")
 
@@ -27,7 +28,7 @@ EXPORTS = ("energon_get_unique_id", "energon_init", "energon_init_local_group", 
            "energon_load_layer_weights", "energon_forward", "energon_forward_group", "energon_forward_hidden",
            "energon_sync", "energon_get_stats", "energon_last_error", "energon_status_string", "energon_destroy",
            "energon_index_maps", "energon_gemm", "energon_attention", "energon_set_profiling", "energon_get_profile",
-           "energon_shard_plan")
+           "energon_shard_plan", "energon_set_option")
 
 
 class EnergonError(RuntimeError):
@@ -95,6 +96,7 @@ def load_library(path: str = SO_PATH):
     L.energon_attention.argtypes = [I32, P, P, P, P, ctypes.POINTER(ctypes.c_int32), I32, I32, I32, I32, I32, P]
     L.energon_shard_plan.argtypes = [ctypes.POINTER(Config), ctypes.POINTER(Shard)]
     L.energon_set_profiling.argtypes = [P, I32]
+    L.energon_set_option.argtypes = [P, I32, I32]
     L.energon_get_profile.argtypes = [P, ctypes.POINTER(Profile)]
     for name in EXPORTS:
         fn = getattr(L, name)
@@ -207,6 +209,10 @@ def energon_get_stats(ctx) -> dict:
     s = Stats()
     _check(load_library().energon_get_stats(ctx, ctypes.byref(s)), ctx)
     return {n: getattr(s, n) for n, _ in Stats._fields_}
+
+
+def energon_set_option(ctx, option: int, value: int):
+    _check(load_library().energon_set_option(ctx, option, int(value)), ctx)
 
 
 def energon_set_profiling(ctx, enable: bool):

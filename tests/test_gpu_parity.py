@@ -362,3 +362,31 @@ def test_gemm_every_tile_shape(code, M, N, K, epi, monkeypatch):
     monkeypatch.setenv("ENERGON_GEMM_TILE", str(code))
     got, ref = _gemm_case(M, N, K, "bf16", epi, seed=code)
     assert (np.abs(got - ref) <= 4e-3 * np.abs(ref) + 1e-4 * np.abs(ref).max()).all()
+
+
+@pytest.mark.parametrize("M,N,K,epi", [(2304, 2560, 10240, 2), (1200, 3800, 10240, 1)])
+def test_gemm_streamk_tail(M, N, K, epi, monkeypatch):
+    """Tail tiles split along K across idle clusters (90 tiles -> 16 tail tiles x 4 splits; 75 tiles ->
+    1 x 8): correct vs the oracle, deterministic run to run, close to the unsplit kernel."""
+    tdt = torch.bfloat16
+    g = torch.Generator(device="cpu").manual_seed(M + N)
+    A = (torch.rand(M, K, generator=g) * 2 - 1).to(tdt)
+    W = ((torch.rand(N, K, generator=g) * 2 - 1) * 0.05).to(tdt)
+    bias = (torch.rand(N, generator=g) * 2 - 1).float()
+    Ad, Wd, bd = A.cuda(), W.cuda(), bias.cuda()
+
+    def run():
+        D = torch.full((M, N), float("nan"), dtype=tdt, device="cuda")
+        E().energon_gemm(Ad, Wd, bd, D, epilogue=epi)
+        torch.cuda.synchronize()
+        return D.float().cpu().numpy().astype(np.float64)
+
+    got, got2 = run(), run()
+    monkeypatch.setenv("ENERGON_NO_STREAMK", "1")
+    got3 = run()
+    ref = oracle.matmul(A.double().numpy(), W.double().numpy().T) + bias.double().numpy()
+    if epi == 2:
+        ref = np.vectorize(oracle.gelu)(ref)
+    assert (np.abs(got - ref) <= 4e-3 * np.abs(ref) + 1e-4 * np.abs(ref).max()).all()
+    assert np.array_equal(got, got2)
+    assert np.abs(got3 - got).max() <= 8e-3 * np.abs(ref).max()
