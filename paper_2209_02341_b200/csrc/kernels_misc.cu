@@ -4,6 +4,8 @@
 // Every kernel reads / writes each byte of its operands once, with 16-byte (or 8-byte for bf16x4)
 // vector accesses along the contiguous hidden dimension; rows are independent (one CTA per row for
 // the LayerNorm family so the row lives in registers between the statistics and the write).
+#include <stdlib.h>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -187,29 +189,38 @@ __global__ void __launch_bounds__(LN_THREADS) gather_ln_kernel(const float* __re
 // X[t] += P[t] + bias (P = the reduced row-parallel partial, "accumulated by communications",
 // PAPER.md:290; bias added once after the reduce), then A[t] = LN(X[t]).
 // With A == nullptr only the residual update is done.
-template <typename Act, int LN_MAXV>
-__global__ void __launch_bounds__(LN_THREADS) residual_ln_kernel(float* __restrict__ X, const Act* __restrict__ P,
-                                                                 const float* __restrict__ bias, int H,
-                                                                 const float* __restrict__ g, const float* __restrict__ b,
-                                                                 float eps, Act* __restrict__ A) {
+template <typename Act, int LN_MAXV, int TPR>
+__global__ void __launch_bounds__(TPR) residual_ln_kernel(float* __restrict__ X, const Act* __restrict__ P,
+                                                          const float* __restrict__ bias, int H,
+                                                          const float* __restrict__ g, const float* __restrict__ b,
+                                                          float eps, Act* __restrict__ A) {
   __shared__ float red[32];
   const int t = blockIdx.x;
   float4 v[LN_MAXV];
   int nv = 0;
+  float* xrow = X + (int64_t)t * H;
+  const Act* prow = P + (int64_t)t * H;
+  // issue every load of the row before any arithmetic (memory-level parallelism)
+  float4 pv[LN_MAXV];
 #pragma unroll
   for (int i = 0; i < LN_MAXV; ++i) {
-    const int c = (threadIdx.x + i * LN_THREADS);
+    const int c = (threadIdx.x + i * TPR);
     if (c < H / 4) {
-      float4 x = Row4<float>::load(X + (int64_t)t * H + 4 * c);
-      const float4 p = Row4<Act>::load(P + (int64_t)t * H + 4 * c);
-      const float4 q = *reinterpret_cast<const float4*>(bias + 4 * c);
-      x.x += p.x + q.x;
-      x.y += p.y + q.y;
-      x.z += p.z + q.z;
-      x.w += p.w + q.w;
-      v[i] = x;
-      Row4<float>::store(X + (int64_t)t * H + 4 * c, x);
+      v[i] = __ldcs(reinterpret_cast<const float4*>(xrow) + c);
+      pv[i] = Row4<Act>::load(prow + 4 * c);
       nv = i + 1;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < LN_MAXV; ++i) {
+    if (i < nv) {
+      const int c = (threadIdx.x + i * TPR);
+      const float4 q = *reinterpret_cast<const float4*>(bias + 4 * c);
+      v[i].x += pv[i].x + q.x;
+      v[i].y += pv[i].y + q.y;
+      v[i].z += pv[i].z + q.z;
+      v[i].w += pv[i].w + q.w;
+      Row4<float>::store(xrow + 4 * c, v[i]);
     }
   }
   if (A == nullptr) return;
@@ -217,8 +228,8 @@ __global__ void __launch_bounds__(LN_THREADS) residual_ln_kernel(float* __restri
   row_stats(v, nv, H, eps, red, mean, rstd);
 #pragma unroll
   for (int i = 0; i < LN_MAXV; ++i)
-    if (i < nv) Row4<Act>::store(A + (int64_t)t * H + 4 * (threadIdx.x + i * LN_THREADS),
-                                 ln_apply(v[i], mean, rstd, g, b, 4 * (threadIdx.x + i * LN_THREADS)));
+    if (i < nv) Row4<Act>::store(A + (int64_t)t * H + 4 * (threadIdx.x + i * TPR),
+                                 ln_apply(v[i], mean, rstd, g, b, 4 * (threadIdx.x + i * TPR)));
 }
 
 // ============================================================================ a13: final LN + unpack
@@ -412,10 +423,46 @@ void launch_gather_ln(const float* x, const int* pack_idx, int rows, int H, cons
   if (rows > 0) NV_DISPATCH(H, (gather_ln_kernel<Act, NVX><<<rows, LN_THREADS, 0, st>>>(x, pack_idx, H, g, b, eps, X, A)))
 }
 
+#define NV_DISPATCH_T(H, TPRV, KERNEL_CALL)                                 \
+  switch ((((H) / 4) + (TPRV) - 1) / (TPRV)) {                              \
+    case 1: { constexpr int NVX = 1; KERNEL_CALL; } break;                  \
+    case 2: { constexpr int NVX = 2; KERNEL_CALL; } break;                  \
+    case 3: { constexpr int NVX = 3; KERNEL_CALL; } break;                  \
+    case 4: { constexpr int NVX = 4; KERNEL_CALL; } break;                  \
+    case 5: { constexpr int NVX = 5; KERNEL_CALL; } break;                  \
+    case 6: { constexpr int NVX = 6; KERNEL_CALL; } break;                  \
+    case 7: { constexpr int NVX = 7; KERNEL_CALL; } break;                  \
+    case 8: { constexpr int NVX = 8; KERNEL_CALL; } break;                  \
+    case 9: { constexpr int NVX = 9; KERNEL_CALL; } break;                  \
+    case 10: { constexpr int NVX = 10; KERNEL_CALL; } break;                \
+    case 11: { constexpr int NVX = 11; KERNEL_CALL; } break;                \
+    default: { constexpr int NVX = 12; KERNEL_CALL; } break;                \
+  }
+
+// Threads per row for the residual + LN kernel: 256 by default; ENERGON_LN_TPR=128|512 for
+// experiments (128 only when the row fits in 12 float4 per thread).
+static int ln_tpr(int H) {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("ENERGON_LN_TPR");
+    v = e ? atoi(e) : 256;
+    if (v != 128 && v != 256 && v != 512) v = 256;
+  }
+  if (v == 128 && H / 4 > 128 * 12) return 256;
+  return v;
+}
+
 template <typename Act>
 void launch_residual_ln(float* X, const Act* P, const float* bias, int rows, int H, const float* g, const float* b,
                         float eps, Act* A, cudaStream_t st) {
-  if (rows > 0) NV_DISPATCH(H, (residual_ln_kernel<Act, NVX><<<rows, LN_THREADS, 0, st>>>(X, P, bias, H, g, b, eps, A)))
+  if (rows <= 0) return;
+  const int tpr = ln_tpr(H);
+  if (tpr == 128)
+    NV_DISPATCH_T(H, 128, (residual_ln_kernel<Act, NVX, 128><<<rows, 128, 0, st>>>(X, P, bias, H, g, b, eps, A)))
+  else if (tpr == 512)
+    NV_DISPATCH_T(H, 512, (residual_ln_kernel<Act, NVX, 512><<<rows, 512, 0, st>>>(X, P, bias, H, g, b, eps, A)))
+  else
+    NV_DISPATCH_T(H, 256, (residual_ln_kernel<Act, NVX, 256><<<rows, 256, 0, st>>>(X, P, bias, H, g, b, eps, A)))
 }
 
 template <typename Out>

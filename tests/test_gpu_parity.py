@@ -390,3 +390,33 @@ def test_gemm_streamk_tail(M, N, K, epi, monkeypatch):
     assert (np.abs(got - ref) <= 4e-3 * np.abs(ref) + 1e-4 * np.abs(ref).max()).all()
     assert np.array_equal(got, got2)
     assert np.abs(got3 - got).max() <= 8e-3 * np.abs(ref).max()
+
+
+# ----------------------------------------------------------------------------- configs 4 and 5, teacher-forced
+@pytest.mark.parametrize("name,p", [("opt30b", 0.5), ("opt66b", 0.75), ("opt66b", 0.0)])
+def test_opt_layer_teacher_forced(name, p):
+    """BASELINE configs 4 / 5 shapes (H=7168 / 9216, d=128, B=32, S=1024, padding p): one layer of
+    the stack on the whole batch through energon_forward_hidden; the oracle recomputes it for the
+    shortest sequence (P12), from the same fp32 input, within 2e-2."""
+    shape = SHAPES[name]
+    B, S, seed = 32, 1024, 1
+    lens = synth.exact_p_lengths(B, S, p, seed)
+    H = shape["H"]
+    ctxs = make_engine(shape, seed, "bf16", B * S, L=1)
+    try:
+        g = torch.Generator(device="cpu").manual_seed(5)
+        x = (torch.randn(B, S, H, generator=g) * 0.5).float()
+        out = torch.full((B, S, H), float("nan"), device="cuda")
+        E().energon_forward_hidden(ctxs[0], x.cuda(), lens, 0, 1, 0, out)
+        E().energon_sync(ctxs[0])
+        b = int(np.argmin(lens))
+        n = min(lens[b], 96)  # causal prefix of the shortest sequence (P13) keeps the oracle fast
+        y = out[b:b + 1, :n].cpu().double().numpy()
+        assert not out[b, lens[b]:].any().item()
+    finally:
+        destroy(ctxs)
+    layers, _ = oracle_model(shape, seed, "bf16", layer_ids=[0], L=1)
+    cfg = oracle.make_cfg(1, H, shape["h"], shape["F"])
+    ref = oracle.layers_padded(cfg, layers, 0, 1, x[b:b + 1, :n].double().numpy(), [n])
+    err = max_abs_rel(y, ref, [n])
+    assert err <= 2e-2, err
