@@ -16,6 +16,7 @@
 // through once.  M and N tails are handled by TMA out-of-bounds zero fill + predicated stores.
 #include <cudaTypedefs.h>
 #include <stdlib.h>
+#include <string.h>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -304,7 +305,8 @@ template <int BN> struct Tc2Cfg {
   static constexpr int B_BYTES = (BN / 2) * TC_BK * 2;  // this CTA's BN/2 rows of W per stage
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES = (200 * 1024) / STAGE_BYTES;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+  static constexpr int STG_BYTES = 4 * 2 * 32 * 32 * 2;  // epilogue staging: 4 warps x 2 x [32 rows x 32 cols] bf16
+  static constexpr int SMEM = STAGES * STAGE_BYTES + STG_BYTES + 1024 + 256;
   static constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
                                     ((uint32_t)(256 >> 4) << 24);
 };
@@ -383,6 +385,58 @@ __device__ __forceinline__ void unit_decode(int u, const TailPlan& tp, int nkb, 
 }
 
 template <int EPI>
+__device__ __forceinline__ void epi_math(float (&v)[32], int n0, int N, const float* __restrict__ bias) {
+  if (EPI >= EPI_BIAS) {
+#pragma unroll
+    for (int j = 0; j < 32; j += 4) {
+      if (n0 + j < N) {
+        const float4 bb = __ldg(reinterpret_cast<const float4*>(bias + n0 + j));
+        v[j] += bb.x;
+        v[j + 1] += bb.y;
+        v[j + 2] += bb.z;
+        v[j + 3] += bb.w;
+      }
+    }
+  }
+  if (EPI == EPI_BIAS_GELU) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = gelu_fast(v[j]);
+  }
+}
+
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t src, int x, int y) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(src), "r"(x), "r"(y)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+// Stage one warp's 32 rows x 32 columns (bf16) in shared memory with the 64-byte swizzle the TMA map
+// uses (16-byte chunk j of row r lives at chunk j ^ ((r >> 1) & 3): 4-way instead of 16-way bank
+// conflicts) and store it with one TMA bulk-tensor store; out-of-range rows / columns are clipped.
+__device__ __forceinline__ void epi_tma_store(const float (&v)[32], uint8_t* stg, int lane, const CUtensorMap* tmD,
+                                              int n0, int row0) {
+  const uint32_t base = (uint32_t)__cvta_generic_to_shared(stg) + lane * 64;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const uint32_t a = base + ((j ^ ((lane >> 1) & 3)) << 4);
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(pack_bf16x2(v[8 * j], v[8 * j + 1])),
+                 "r"(pack_bf16x2(v[8 * j + 2], v[8 * j + 3])), "r"(pack_bf16x2(v[8 * j + 4], v[8 * j + 5])),
+                 "r"(pack_bf16x2(v[8 * j + 6], v[8 * j + 7]))
+                 : "memory");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncwarp();
+  if (lane == 0) {
+    tma_store_2d(tmD, (uint32_t)__cvta_generic_to_shared(stg), n0, row0);
+    bulk_commit();
+  }
+}
+
+template <int EPI>
 __device__ __forceinline__ void epi_store(float (&v)[32], int row, int n0, int M, int N, bf16* __restrict__ D,
                                           const float* __restrict__ bias, const QkvScatter& qs) {
   if (row >= M || n0 >= N) return;
@@ -422,13 +476,15 @@ template <int BN, int EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     bf16* __restrict__ D, const float* __restrict__ bias, int M, int N, int K, int group_m,
-                    const QkvScatter qs, const TailPlan tp) {
+                    const QkvScatter qs, const TailPlan tp, const __grid_constant__ CUtensorMap tmD) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   using C = Tc2Cfg<BN>;
+  constexpr bool TMA_ST = (EPI != EPI_BIAS_QKV);  // QKV scatters (a5); everything else leaves by TMA store
   uint8_t* sA = smem;
   uint8_t* sB = smem + C::STAGES * C::A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + C::STAGES * C::B_BYTES);
+  uint8_t* sStg = sB + C::STAGES * C::B_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sStg + C::STG_BYTES);
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
@@ -526,6 +582,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     const int q = warp - 4;
     const int etid = threadIdx.x - 128;  // 0..127: this thread's TMEM lane / tile row
     const uint32_t tempty_leader = smem_u32(&tempty[0]) & PEER_MASK;
+    uint8_t* my_stg = sStg + q * 2 * 2048;
+    uint32_t nst = 0;  // TMA stores issued by this warp (double-buffered staging)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int u = cid; u < num_units; u += ncl) {
@@ -553,7 +611,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
           float v[32];
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-          epi_store<EPI>(v, row, n_blk * BN + c * 32, M, N, D, bias, qs);
+          if constexpr (TMA_ST) {
+            epi_math<EPI>(v, n_blk * BN + c * 32, N, bias);
+            if (nst >= 2) {  // the store that used this buffer two chunks ago has read it
+              if (lane == 0) bulk_wait_read1();
+              __syncwarp();
+            }
+            epi_tma_store(v, my_stg + (nst & 1) * 2048, lane, &tmD, n_blk * BN + c * 32,
+                          m_blk * 256 + (int)rank * 128 + q * 32);
+            ++nst;
+          } else {
+            epi_store<EPI>(v, row, n_blk * BN + c * 32, M, N, D, bias, qs);
+          }
         }
       }
       tc_fence_before();
@@ -597,6 +666,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
         epi_bar();  // fix_flag is reused by the next split unit
       }
     }
+    if (TMA_ST && lane == 0) bulk_wait_all();  // stores complete before the CTA's smem goes away
   }
   tc_fence_before();
   cluster_sync_all();
@@ -628,6 +698,20 @@ bool make_tmap_kmajor(CUtensorMap* map, const void* ptr, int rows, int K, int bo
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+// Output map for the TMA-store epilogue: D [rows, N] bf16 row-major, 32 x 32 box, 64-byte swizzle.
+bool make_tmap_store(CUtensorMap* map, const void* ptr, int rows, int N) {
+  auto enc = encode_fn();
+  if (!enc || rows <= 0 || N <= 0 || (N % 8) != 0 || (reinterpret_cast<uintptr_t>(ptr) & 15)) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)N, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)N * 2};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
@@ -688,7 +772,7 @@ int tc_w_box(int code) { return code > 1000 ? (code - 1000) / 2 : code; }
 
 template <int BN, int EPI>
 static void launch_pair_epi(const CUtensorMap& tmA, const CUtensorMap& tmB, const float* bias, bf16* D, int M, int N,
-                            int K, cudaStream_t st, const QkvScatter& qs) {
+                            int K, cudaStream_t st, const QkvScatter& qs, const CUtensorMap* tmD) {
   using C = Tc2Cfg<BN>;
   static bool attr = false;
   if (!attr) {
@@ -718,12 +802,19 @@ static void launch_pair_epi(const CUtensorMap& tmA, const CUtensorMap& tmB, cons
   int group_m = (int)(48.0e6 / panel);
   if (group_m < 1) group_m = 1;
   if (group_m > num_m) group_m = num_m;
-  gemm_tc2_kernel<BN, EPI><<<grid, 256, C::SMEM, st>>>(tmA, tmB, D, bias, M, N, K, group_m, qs, tp);
+  CUtensorMap md;
+  if (tmD) {
+    md = *tmD;
+  } else {
+    memset(&md, 0, sizeof(md));
+    if (EPI != EPI_BIAS_QKV && !make_tmap_store(&md, D, M, N)) return;  // caller checks cudaGetLastError
+  }
+  gemm_tc2_kernel<BN, EPI><<<grid, 256, C::SMEM, st>>>(tmA, tmB, D, bias, M, N, K, group_m, qs, tp, md);
 }
 
 template <int BN, int EPI>
 static void launch_bn_epi(const CUtensorMap& tmA, const CUtensorMap& tmB, const float* bias, bf16* D, int M, int N,
-                          int K, cudaStream_t st, const QkvScatter& qs) {
+                          int K, cudaStream_t st, const QkvScatter& qs, const CUtensorMap* /*tmD*/) {
   using C = TcCfg<BN>;
   static bool attr = false;
   if (!attr) {
@@ -737,17 +828,17 @@ static void launch_bn_epi(const CUtensorMap& tmA, const CUtensorMap& tmB, const 
 
 #define DISPATCH_EPI(F, BNARGS)                                                  \
   switch (epi) {                                                                 \
-    case EPI_NONE: F<BNARGS EPI_NONE>(tmA, tmB, bias, D, M, N, K, st, qs); break; \
-    case EPI_BIAS: F<BNARGS EPI_BIAS>(tmA, tmB, bias, D, M, N, K, st, qs); break; \
-    case EPI_BIAS_GELU: F<BNARGS EPI_BIAS_GELU>(tmA, tmB, bias, D, M, N, K, st, qs); break; \
-    default: F<BNARGS EPI_BIAS_QKV>(tmA, tmB, bias, D, M, N, K, st, qs); break;   \
+    case EPI_NONE: F<BNARGS EPI_NONE>(tmA, tmB, bias, D, M, N, K, st, qs, tmD); break; \
+    case EPI_BIAS: F<BNARGS EPI_BIAS>(tmA, tmB, bias, D, M, N, K, st, qs, tmD); break; \
+    case EPI_BIAS_GELU: F<BNARGS EPI_BIAS_GELU>(tmA, tmB, bias, D, M, N, K, st, qs, tmD); break; \
+    default: F<BNARGS EPI_BIAS_QKV>(tmA, tmB, bias, D, M, N, K, st, qs, tmD); break;   \
   }
 #define BN256 256,
 #define BN192 192,
 #define BN128 128,
 
 void launch_gemm_tc(const CUtensorMap& tmA, const CUtensorMap& tmB, int bn, const float* bias, bf16* D, int M, int N,
-                    int K, int epi, cudaStream_t st, const QkvScatter* qkv) {
+                    int K, int epi, cudaStream_t st, const QkvScatter* qkv, const CUtensorMap* tmD) {
   if (M <= 0 || N <= 0) return;
   QkvScatter qs{};
   if (qkv) qs = *qkv;

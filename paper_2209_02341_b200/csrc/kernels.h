@@ -83,8 +83,10 @@ void launch_gemm_f32(const float* A, const float* W, const float* bias, float* D
 bool make_tmap_kmajor(CUtensorMap* map, const void* ptr, int rows, int K, int box_rows);
 int tc_pick_bn(int M, int N);  // tile code (see gemm_tc.cu)
 int tc_w_box(int code);        // row box of the W tensor map the code needs (256, 128, 96 or 64)
+bool make_tmap_store(CUtensorMap* map, const void* ptr, int rows, int N);  // D map of the TMA-store epilogue
+// tmD: the output map (make_tmap_store) or nullptr to build it per call.
 void launch_gemm_tc(const CUtensorMap& tmA, const CUtensorMap& tmB, int bn, const float* bias, bf16* D, int M, int N,
-                    int K, int epi, cudaStream_t st, const QkvScatter* qkv = nullptr);
+                    int K, int epi, cudaStream_t st, const QkvScatter* qkv = nullptr, const CUtensorMap* tmD = nullptr);
 int num_sms();
 
 }  // namespace energon

@@ -64,6 +64,7 @@ struct energon_ctx {
   void *A = nullptr, *QKV = nullptr, *Q = nullptr, *K = nullptr, *Vb = nullptr, *O = nullptr, *Ctx = nullptr,
        *P = nullptr, *G = nullptr;
   CUtensorMap tmA_A, tmA_Ctx, tmA_G;
+  CUtensorMap tmD_P, tmD_G;  // TMA-store output maps of the out/down (P) and up (G) GEMMs
   int tm_rows = -1;
   int* err_host = nullptr;  // mapped pinned flag written by the embed kernel (bad token id)
   int* err_dev = nullptr;
@@ -349,11 +350,13 @@ energon_status allreduce(energon_ctx** cs, int n, int rows, cudaStream_t st) {
 
 template <typename Act>
 void gemm(energon_ctx* c, const CUtensorMap& tmA, const CUtensorMap* tmB, const void* A, const void* W,
-          const float* bias, void* D, int M, int N, int K, int epi, cudaStream_t st, const QkvScatter* qs = nullptr) {
+          const float* bias, void* D, int M, int N, int K, int epi, cudaStream_t st, const QkvScatter* qs = nullptr,
+          const CUtensorMap* tmD = nullptr) {
   Prof p(c, st, P_GEMM, 2.0 * M * N * K);
   if constexpr (sizeof(Act) == 2) {
     const int code = tc_pick_bn(M, N);
-    launch_gemm_tc(tmA, tmB[box_slot(tc_w_box(code))], code, bias, reinterpret_cast<bf16*>(D), M, N, K, epi, st, qs);
+    launch_gemm_tc(tmA, tmB[box_slot(tc_w_box(code))], code, bias, reinterpret_cast<bf16*>(D), M, N, K, epi, st, qs,
+                   tmD);
   } else {
     launch_gemm_f32(reinterpret_cast<const float*>(A), reinterpret_cast<const float*>(W), bias,
                     reinterpret_cast<float*>(D), M, N, K, epi, st);
@@ -395,7 +398,8 @@ energon_status forward_t(energon_ctx** cs, int n, const Call& a, int64_t T) {
     if (sizeof(Act) == 2 && c->tm_rows != rows) {
       if (!make_tmap_kmajor(&c->tmA_A, c->A, rows, c->H, 128) ||
           !make_tmap_kmajor(&c->tmA_Ctx, c->Ctx, rows, c->Hk, 128) ||
-          !make_tmap_kmajor(&c->tmA_G, c->G, rows, c->Fk, 128))
+          !make_tmap_kmajor(&c->tmA_G, c->G, rows, c->Fk, 128) || !make_tmap_store(&c->tmD_P, c->P, rows, c->H) ||
+          !make_tmap_store(&c->tmD_G, c->G, rows, c->Fk))
         return fail(c, ENERGON_ERR_CUDA, "cuTensorMapEncodeTiled failed for an activation operand");
       c->tm_rows = rows;
     }
@@ -456,7 +460,7 @@ energon_status forward_t(energon_ctx** cs, int n, const Call& a, int64_t T) {
         }
         c->stats.kernel_launches += 2;
       }
-      gemm<Act>(c, c->tmA_Ctx, L.tm_o, c->Ctx, L.wo, nullptr, c->P, rows, c->H, c->Hk, EPI_NONE, st);
+      gemm<Act>(c, c->tmA_Ctx, L.tm_o, c->Ctx, L.wo, nullptr, c->P, rows, c->H, c->Hk, EPI_NONE, st, nullptr, &c->tmD_P);
     }
     energon_status s = allreduce<Act>(cs, n, rows, st);
     if (s) return s;
@@ -470,8 +474,8 @@ energon_status forward_t(energon_ctx** cs, int n, const Call& a, int64_t T) {
                                 reinterpret_cast<Act*>(c->A), st);
       }
       c->stats.kernel_launches++;
-      gemm<Act>(c, c->tmA_A, L.tm_1, c->A, L.w1, L.b1, c->G, rows, c->Fk, c->H, EPI_BIAS_GELU, st);
-      gemm<Act>(c, c->tmA_G, L.tm_2, c->G, L.w2, nullptr, c->P, rows, c->H, c->Fk, EPI_NONE, st);
+      gemm<Act>(c, c->tmA_A, L.tm_1, c->A, L.w1, L.b1, c->G, rows, c->Fk, c->H, EPI_BIAS_GELU, st, nullptr, &c->tmD_G);
+      gemm<Act>(c, c->tmA_G, L.tm_2, c->G, L.w2, nullptr, c->P, rows, c->H, c->Fk, EPI_NONE, st, nullptr, &c->tmD_P);
     }
     s = allreduce<Act>(cs, n, rows, st);
     if (s) return s;
