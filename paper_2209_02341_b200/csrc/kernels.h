@@ -24,13 +24,14 @@ struct PtrList {
 void launch_index_maps(const LensParam& lp, int B, int S, int* offsets, int* pack_idx, int* pos, int* unpack_idx,
                        cudaStream_t st);
 // a2 + a3
+// rows [row0, row0 + rows) of the packed layout
 template <typename Act>
-void launch_embed_ln(const int* tok, const int* pack_idx, int rows, int S, int V, int H, const Act* tok_emb,
+void launch_embed_ln(const int* tok, const int* pack_idx, int row0, int rows, int S, int V, int H, const Act* tok_emb,
                      const Act* pos_emb, const float* g, const float* b, float eps, float* X, Act* A, int* err,
                      cudaStream_t st);
 template <typename Act>
-void launch_gather_ln(const float* x, const int* pack_idx, int rows, int H, const float* g, const float* b, float eps,
-                      float* X, Act* A, cudaStream_t st);
+void launch_gather_ln(const float* x, const int* pack_idx, int row0, int rows, int H, const float* g, const float* b,
+                      float eps, float* X, Act* A, cudaStream_t st);
 // a9 / a12
 template <typename Act>
 void launch_residual_ln(float* X, const Act* P, const float* bias, int rows, int H, const float* g, const float* b,
@@ -48,6 +49,9 @@ void launch_repack(const Act* O, const int* pack_idx, const int* unpack_idx, int
                    cudaStream_t st);
 template <typename Act>
 void launch_local_allreduce(const PtrList& parts, int k, int64_t n, cudaStream_t st);
+template <typename Act>
+void launch_local_reduce_scatter(const PtrList& parts, int k, int64_t shard, cudaStream_t st);
+void launch_local_all_gather(const PtrList& parts, int k, int64_t shard_bytes, cudaStream_t st);
 // load-time relayout
 template <typename Src, typename Dst>
 void launch_relayout(const Src* src, int64_t ld, int64_t row0, int64_t col0, int N, int K, Dst* dst, int64_t dst_ld,

@@ -11,6 +11,13 @@
 
 namespace energon {
 
+static inline int grid_for(int64_t work, int threads, int max_blocks) {
+  int64_t g = (work + threads - 1) / threads;
+  if (g > max_blocks) g = max_blocks;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
 // ============================================================================ a1: index maps
 // PAPER.md:368-373 (sec 4.3): every worker derives the DRCE layout from the command's seq_lens.
 // offsets = exclusive prefix sum of lens (warp-shuffle scan); for each padded cell (b, s):
@@ -121,12 +128,12 @@ __device__ __forceinline__ float4 ln_apply(float4 x, float mean, float rstd, con
 // row 0 and raises the device error flag (checked by energon_sync), so the kernel never faults.
 template <typename Act, int LN_MAXV>
 __global__ void __launch_bounds__(LN_THREADS) embed_ln_kernel(const int* __restrict__ tok, const int* __restrict__ pack_idx,
-                                                              int S, int V, int H, const Act* __restrict__ tok_emb,
+                                                              int row0, int S, int V, int H, const Act* __restrict__ tok_emb,
                                                               const Act* __restrict__ pos_emb, const float* __restrict__ g,
                                                               const float* __restrict__ b, float eps, float* __restrict__ X,
                                                               Act* __restrict__ A, int* err_flag) {
   __shared__ float red[32];
-  const int t = blockIdx.x;
+  const int t = row0 + blockIdx.x;
   const int cell = pack_idx ? pack_idx[t] : t;
   const int s = cell % S;
   int id = tok[cell];
@@ -161,10 +168,11 @@ __global__ void __launch_bounds__(LN_THREADS) embed_ln_kernel(const int* __restr
 // Hidden-state entry (energon_forward_hidden): X[t] = x[cell] (fp32), A[t] = LN1(X[t]).
 template <typename Act, int LN_MAXV>
 __global__ void __launch_bounds__(LN_THREADS) gather_ln_kernel(const float* __restrict__ x, const int* __restrict__ pack_idx,
-                                                               int H, const float* __restrict__ g, const float* __restrict__ b,
-                                                               float eps, float* __restrict__ X, Act* __restrict__ A) {
+                                                               int row0, int H, const float* __restrict__ g,
+                                                               const float* __restrict__ b, float eps, float* __restrict__ X,
+                                                               Act* __restrict__ A) {
   __shared__ float red[32];
-  const int t = blockIdx.x;
+  const int t = row0 + blockIdx.x;
   const int cell = pack_idx ? pack_idx[t] : t;
   float4 v[LN_MAXV];
   int nv = 0;
@@ -345,6 +353,56 @@ __global__ void local_allreduce_kernel(PtrList parts, int k, int64_t n) {
   }
 }
 
+// Local-group reduce-scatter (sequence-parallel schedule): shard s (= rank s) of every partial,
+// `shard` elements starting at s * shard, is summed over the k ranks in rank order (fp32) and
+// written to rank s's buffer only -- the semantics of ncclReduceScatter in place.
+template <typename Act>
+__global__ void local_reduce_scatter_kernel(PtrList parts, int k, int64_t shard) {
+  constexpr int E = 16 / sizeof(Act);
+  const int64_t nv = shard / E;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nv * k; i += (int64_t)gridDim.x * blockDim.x) {
+    const int s = (int)(i / nv);
+    const int64_t off = (int64_t)s * nv + (i - (int64_t)s * nv);
+    float acc[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) acc[e] = 0.f;
+    for (int r = 0; r < k; ++r) {
+      Vec16<Act> v;
+      v.u = reinterpret_cast<const uint4*>(parts.p[r])[off];
+#pragma unroll
+      for (int e = 0; e < E; ++e) acc[e] += to_f32(v.e[e]);
+    }
+    Vec16<Act> o;
+#pragma unroll
+    for (int e = 0; e < E; ++e) o.e[e] = from_f32<Act>(acc[e]);
+    reinterpret_cast<uint4*>(parts.p[s])[off] = o.u;
+  }
+}
+
+// Local-group all-gather: rank s's shard (shard_bytes at s * shard_bytes) is copied into every
+// other rank's buffer -- the semantics of ncclAllGather in place.
+__global__ void local_all_gather_kernel(PtrList parts, int k, int64_t shard_bytes) {
+  const int64_t nv = shard_bytes / 16;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nv * k; i += (int64_t)gridDim.x * blockDim.x) {
+    const int s = (int)(i / nv);
+    const int64_t off = (int64_t)s * nv + (i - (int64_t)s * nv);
+    const uint4 v = reinterpret_cast<const uint4*>(parts.p[s])[off];
+    for (int r = 0; r < k; ++r)
+      if (r != s) reinterpret_cast<uint4*>(parts.p[r])[off] = v;
+  }
+}
+
+template <typename Act>
+void launch_local_reduce_scatter(const PtrList& parts, int k, int64_t shard, cudaStream_t st) {
+  const int64_t work = shard / (16 / sizeof(Act)) * k;
+  if (work > 0) local_reduce_scatter_kernel<Act><<<grid_for(work, 256, 148 * 8), 256, 0, st>>>(parts, k, shard);
+}
+
+void launch_local_all_gather(const PtrList& parts, int k, int64_t shard_bytes, cudaStream_t st) {
+  const int64_t work = shard_bytes / 16 * k;
+  if (work > 0) local_all_gather_kernel<<<grid_for(work, 256, 148 * 8), 256, 0, st>>>(parts, k, shard_bytes);
+}
+
 // ============================================================================ load-time relayout
 // dst[n * K + k] = cvt(src[(row0 + k) * ld + col0 + n])  for n < N, k < K   (transpose == 1)
 // dst[n]         = cvt(src[col0 + n])                     for n < N         (vector)
@@ -379,12 +437,6 @@ __global__ void convert_vec_kernel(const Src* __restrict__ src, int64_t off, int
 }
 
 // ============================================================================ host launchers
-static inline int grid_for(int64_t work, int threads, int max_blocks) {
-  int64_t g = (work + threads - 1) / threads;
-  if (g > max_blocks) g = max_blocks;
-  if (g < 1) g = 1;
-  return (int)g;
-}
 
 void launch_index_maps(const LensParam& lp, int B, int S, int* offsets, int* pack_idx, int* pos, int* unpack_idx,
                        cudaStream_t st) {
@@ -409,18 +461,19 @@ void launch_index_maps(const LensParam& lp, int B, int S, int* offsets, int* pac
   }
 
 template <typename Act>
-void launch_embed_ln(const int* tok, const int* pack_idx, int rows, int S, int V, int H, const Act* tok_emb,
+void launch_embed_ln(const int* tok, const int* pack_idx, int row0, int rows, int S, int V, int H, const Act* tok_emb,
                      const Act* pos_emb, const float* g, const float* b, float eps, float* X, Act* A, int* err,
                      cudaStream_t st) {
   if (rows > 0)
-    NV_DISPATCH(H, (embed_ln_kernel<Act, NVX><<<rows, LN_THREADS, 0, st>>>(tok, pack_idx, S, V, H, tok_emb, pos_emb, g, b,
-                                                                           eps, X, A, err)))
+    NV_DISPATCH(H, (embed_ln_kernel<Act, NVX><<<rows, LN_THREADS, 0, st>>>(tok, pack_idx, row0, S, V, H, tok_emb, pos_emb,
+                                                                           g, b, eps, X, A, err)))
 }
 
 template <typename Act>
-void launch_gather_ln(const float* x, const int* pack_idx, int rows, int H, const float* g, const float* b, float eps,
-                      float* X, Act* A, cudaStream_t st) {
-  if (rows > 0) NV_DISPATCH(H, (gather_ln_kernel<Act, NVX><<<rows, LN_THREADS, 0, st>>>(x, pack_idx, H, g, b, eps, X, A)))
+void launch_gather_ln(const float* x, const int* pack_idx, int row0, int rows, int H, const float* g, const float* b,
+                      float eps, float* X, Act* A, cudaStream_t st) {
+  if (rows > 0)
+    NV_DISPATCH(H, (gather_ln_kernel<Act, NVX><<<rows, LN_THREADS, 0, st>>>(x, pack_idx, row0, H, g, b, eps, X, A)))
 }
 
 #define NV_DISPATCH_T(H, TPRV, KERNEL_CALL)                                 \
@@ -507,10 +560,11 @@ void launch_convert_vec(const Src* src, int64_t off, int N, Dst* dst, cudaStream
 
 // explicit instantiations
 #define INST_ACT(Act)                                                                                                   \
-  template void launch_embed_ln<Act>(const int*, const int*, int, int, int, int, const Act*, const Act*, const float*,   \
-                                     const float*, float, float*, Act*, int*, cudaStream_t);                            \
-  template void launch_gather_ln<Act>(const float*, const int*, int, int, const float*, const float*, float, float*,     \
-                                      Act*, cudaStream_t);                                                              \
+  template void launch_embed_ln<Act>(const int*, const int*, int, int, int, int, int, const Act*, const Act*,            \
+                                     const float*, const float*, float, float*, Act*, int*, cudaStream_t);              \
+  template void launch_gather_ln<Act>(const float*, const int*, int, int, int, const float*, const float*, float,        \
+                                      float*, Act*, cudaStream_t);                                                      \
+  template void launch_local_reduce_scatter<Act>(const PtrList&, int, int64_t, cudaStream_t);                          \
   template void launch_residual_ln<Act>(float*, const Act*, const float*, int, int, const float*, const float*, float,   \
                                         Act*, cudaStream_t);                                                            \
   template void launch_final_ln_unpack<Act>(const float*, const int*, int, int, int, const float*, const float*, float,  \

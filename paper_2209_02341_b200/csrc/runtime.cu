@@ -19,6 +19,7 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <algorithm>
 #include <string>
 #include <vector>
 
@@ -52,6 +53,7 @@ struct energon_ctx {
   ncclComm_t nccl = nullptr;
   bool local_group = false;
   bool fuse = true;  // fused a5 / a7 (ENERGON_NO_FUSE=1 disables, for A/B and tests)
+  bool sp = true;    // k > 1: sequence-parallel schedule (reduce-scatter / LN on own rows / all-gather)
   // replicated embeddings / final LN
   void* tok_emb = nullptr;
   void* pos_emb = nullptr;
@@ -166,7 +168,8 @@ energon_status setup(energon_ctx* c) {
   CU(c, cudaHostGetDevicePointer(&c->err_dev, c->err_host, 0));
   c->layers.resize(g.num_layers);
   // workspace: every buffer is sized for max_tokens rows (padded rows when drce == 0)
-  const size_t R = (size_t)g.max_tokens, a = c->act;
+  // + 8 rows: the sequence-parallel schedule pads the row count to a multiple of k (<= 8)
+  const size_t R = (size_t)g.max_tokens + 8, a = c->act;
   int64_t* ws = &c->stats.workspace_bytes;
   energon_status s;
   if ((s = dalloc(c, &c->offsets, sizeof(int) * (ENERGON_MAX_BATCH + 1), ws)) ||
@@ -178,6 +181,14 @@ energon_status setup(energon_ctx* c) {
       (s = dalloc(c, &c->Ctx, a * R * c->Hk, ws)) || (s = dalloc(c, &c->P, a * R * c->H, ws)) ||
       (s = dalloc(c, &c->G, a * R * c->Fk, ws)))
     return s;
+  // zero every activation buffer once: rows a schedule reads but never writes (sequence-parallel
+  // padding rows, unwritten Ctx rows) stay finite
+  for (void* p : c->allocs) CU(c, cudaMemset(p, 0, 16));
+  CU(c, cudaMemset(c->X, 0, sizeof(float) * R * c->H));
+  CU(c, cudaMemset(c->A, 0, a * R * c->H));
+  CU(c, cudaMemset(c->P, 0, a * R * c->H));
+  CU(c, cudaMemset(c->Ctx, 0, a * R * c->Hk));
+  CU(c, cudaDeviceSynchronize());
   return ENERGON_OK;
 }
 
@@ -329,22 +340,56 @@ energon_status validate_call(energon_ctx* c, const Call& a, int64_t* T_out) {
   return ENERGON_OK;
 }
 
+// ----------------------------------------------------------------------------- TP exchanges
+// "accumulated by communications": one reduction per pair of linears.  AR schedule:
+// allreduce of the packed [rows, H] partial.  SP schedule (k > 1, default): reduce-scatter of the
+// partial over row shards of rpr rows, so each rank adds bias + residual and normalises only its
+// rows, then all-gather of the normalised rows for the next column-parallel GEMM -- the same bytes
+// on the wire as the allreduce, 1/k of the memory-bound work per rank.
 template <typename Act>
-energon_status allreduce(energon_ctx** cs, int n, int rows, cudaStream_t st) {
+energon_status tp_reduce(energon_ctx** cs, int n, int rows, int rpr, bool sp, cudaStream_t st) {
   energon_ctx* c0 = cs[0];
   if (c0->k == 1) return ENERGON_OK;
-  const size_t count = (size_t)rows * c0->H;
+  const ncclDataType_t dt = c0->bf16 ? ncclBfloat16 : ncclFloat;
+  const size_t count = sp ? (size_t)rpr * c0->k * c0->H : (size_t)rows * c0->H;
   Prof p(c0, st, P_COMM, (double)count * c0->act);
   if (c0->local_group) {
     PtrList pl;
     for (int i = 0; i < n; ++i) pl.p[i] = cs[i]->P;
-    launch_local_allreduce<Act>(pl, n, (int64_t)count, st);
+    if (sp) launch_local_reduce_scatter<Act>(pl, n, (int64_t)rpr * c0->H, st);
+    else launch_local_allreduce<Act>(pl, n, (int64_t)count, st);
     c0->stats.kernel_launches++;
   } else {
-    ncclResult_t e = ncclAllReduce(c0->P, c0->P, count, c0->bf16 ? ncclBfloat16 : ncclFloat, ncclSum, c0->nccl, st);
-    if (e != ncclSuccess) return fail(c0, ENERGON_ERR_NCCL, std::string("ncclAllReduce: ") + ncclGetErrorString(e));
+    ncclResult_t e;
+    if (sp) {
+      Act* P = reinterpret_cast<Act*>(c0->P);
+      e = ncclReduceScatter(P, P + (size_t)c0->r * rpr * c0->H, (size_t)rpr * c0->H, dt, ncclSum, c0->nccl, st);
+    } else {
+      e = ncclAllReduce(c0->P, c0->P, count, dt, ncclSum, c0->nccl, st);
+    }
+    if (e != ncclSuccess) return fail(c0, ENERGON_ERR_NCCL, std::string("NCCL reduction: ") + ncclGetErrorString(e));
   }
   for (int i = 0; i < n; ++i) cs[i]->stats.allreduce_calls++;
+  return ENERGON_OK;
+}
+
+// all-gather of each rank's rpr-row shard of buf (A: activation dtype, or X: fp32), in place
+template <typename T>
+energon_status tp_gather(energon_ctx** cs, int n, int rpr, bool x_buf, cudaStream_t st) {
+  energon_ctx* c0 = cs[0];
+  const size_t elems = (size_t)rpr * c0->H;
+  Prof p(c0, st, P_COMM, (double)elems * sizeof(T) * (c0->k - 1));
+  if (c0->local_group) {
+    PtrList pl;
+    for (int i = 0; i < n; ++i) pl.p[i] = x_buf ? (void*)cs[i]->X : cs[i]->A;
+    launch_local_all_gather(pl, n, (int64_t)(elems * sizeof(T)), st);
+    c0->stats.kernel_launches++;
+  } else {
+    T* b = reinterpret_cast<T*>(x_buf ? (void*)c0->X : c0->A);
+    const ncclDataType_t dt = sizeof(T) == 4 ? ncclFloat : ncclBfloat16;
+    ncclResult_t e = ncclAllGather(b + (size_t)c0->r * elems, b, elems, dt, c0->nccl, st);
+    if (e != ncclSuccess) return fail(c0, ENERGON_ERR_NCCL, std::string("ncclAllGather: ") + ncclGetErrorString(e));
+  }
   return ENERGON_OK;
 }
 
@@ -378,6 +423,11 @@ energon_status forward_t(energon_ctx** cs, int n, const Call& a, int64_t T) {
   // A/B mode keeps the standalone repack because it must zero the pad query rows).
   const bool fuse_a5 = sizeof(Act) == 2 && c0->fuse && (c0->d == 64 || c0->d == 128);
   const bool fuse_a7 = fuse_a5 && drce;
+  // TP schedule: row shard [r0, r0 + sn) of each rank (the whole range without sequence parallelism)
+  const bool sp = c0->k > 1 && c0->sp;
+  const int rpr = sp ? (rows + c0->k - 1) / c0->k : rows;
+  auto shard0 = [&](const energon_ctx* c) { return sp ? std::min(rows, c->r * rpr) : 0; };
+  auto shardn = [&](const energon_ctx* c) { return sp ? std::max(0, std::min(rows, (c->r + 1) * rpr) - c->r * rpr) : rows; };
   LensParam lp;
   double allowed = 0.0;  // sum over sequences of visible (query, key) pairs
   for (int b = 0; b < a.B; ++b) {
@@ -408,16 +458,21 @@ energon_status forward_t(energon_ctx** cs, int n, const Call& a, int64_t T) {
     const float* g1 = a.l0 < a.l1 ? L0.ln1g : c->lnf_g;
     const float* b1 = a.l0 < a.l1 ? L0.ln1b : c->lnf_b;
     {
-      // reads: ids + 2 embedding rows (or one fp32 row); writes: X (fp32) + A
-      Prof p(c, st, P_MEM, a.tokens ? rows * (4.0 + H * (2 * act + 4 + act)) : rows * H * (4 + 4 + act));
+      // reads: ids + 2 embedding rows (or one fp32 row); writes: X (fp32) + A -- this rank's rows
+      const int r0 = shard0(c), sn = shardn(c);
+      Prof p(c, st, P_MEM, a.tokens ? sn * (4.0 + H * (2 * act + 4 + act)) : sn * H * (4 + 4 + act));
       if (a.tokens)
-        launch_embed_ln<Act>(a.tokens, pidx, rows, a.S, c->V, c->H, reinterpret_cast<const Act*>(c->tok_emb),
+        launch_embed_ln<Act>(a.tokens, pidx, r0, sn, a.S, c->V, c->H, reinterpret_cast<const Act*>(c->tok_emb),
                              reinterpret_cast<const Act*>(c->pos_emb), g1, b1, eps, c->X, reinterpret_cast<Act*>(c->A),
                              c->err_dev, st);
       else
-        launch_gather_ln<Act>(a.x_in, pidx, rows, c->H, g1, b1, eps, c->X, reinterpret_cast<Act*>(c->A), st);
+        launch_gather_ln<Act>(a.x_in, pidx, r0, sn, c->H, g1, b1, eps, c->X, reinterpret_cast<Act*>(c->A), st);
     }
     c->stats.kernel_launches++;
+  }
+  if (sp) {
+    energon_status s = tp_gather<Act>(cs, n, rpr, false, st);
+    if (s) return s;
   }
 
   for (int l = a.l0; l < a.l1; ++l) {
@@ -462,35 +517,48 @@ energon_status forward_t(energon_ctx** cs, int n, const Call& a, int64_t T) {
       }
       gemm<Act>(c, c->tmA_Ctx, L.tm_o, c->Ctx, L.wo, nullptr, c->P, rows, c->H, c->Hk, EPI_NONE, st, nullptr, &c->tmD_P);
     }
-    energon_status s = allreduce<Act>(cs, n, rows, st);
+    energon_status s = tp_reduce<Act>(cs, n, rows, rpr, sp, st);
     if (s) return s;
+    // ---- a9: bias + residual + LN2 on this rank's rows, then (SP) all-gather of the LN output
+    for (int i = 0; i < n; ++i) {
+      energon_ctx* c = cs[i];
+      const LayerDev& L = c->layers[l];
+      const size_t o = (size_t)shard0(c) * c->H;
+      const int sn = shardn(c);
+      Prof p(c, st, P_MEM, sn * H * (8.0 + 2 * act));
+      launch_residual_ln<Act>(c->X + o, reinterpret_cast<const Act*>(c->P) + o, L.bo, sn, c->H, L.ln2g, L.ln2b, eps,
+                              reinterpret_cast<Act*>(c->A) + o, st);
+      c->stats.kernel_launches++;
+    }
+    if (sp && (s = tp_gather<Act>(cs, n, rpr, false, st))) return s;
     // ---- MLP module: column-parallel W1 (+GeLU), row-parallel W2
     for (int i = 0; i < n; ++i) {
       energon_ctx* c = cs[i];
       const LayerDev& L = c->layers[l];
-      {
-        Prof p(c, st, P_MEM, rows * H * (8.0 + 2 * act));
-        launch_residual_ln<Act>(c->X, reinterpret_cast<const Act*>(c->P), L.bo, rows, c->H, L.ln2g, L.ln2b, eps,
-                                reinterpret_cast<Act*>(c->A), st);
-      }
-      c->stats.kernel_launches++;
       gemm<Act>(c, c->tmA_A, L.tm_1, c->A, L.w1, L.b1, c->G, rows, c->Fk, c->H, EPI_BIAS_GELU, st, nullptr, &c->tmD_G);
       gemm<Act>(c, c->tmA_G, L.tm_2, c->G, L.w2, nullptr, c->P, rows, c->H, c->Fk, EPI_NONE, st, nullptr, &c->tmD_P);
     }
-    s = allreduce<Act>(cs, n, rows, st);
+    s = tp_reduce<Act>(cs, n, rows, rpr, sp, st);
     if (s) return s;
+    // ---- a12: bias + residual (+ LN1 of the next layer) on this rank's rows
+    const bool last = (l + 1 == a.l1);
     for (int i = 0; i < n; ++i) {
       energon_ctx* c = cs[i];
       const LayerDev& L = c->layers[l];
-      const bool last = (l + 1 == a.l1);
       const LayerDev& Ln = c->layers[last ? l : l + 1];
-      {
-        Prof p(c, st, P_MEM, rows * H * (8.0 + (last ? 1 : 2) * act));
-        launch_residual_ln<Act>(c->X, reinterpret_cast<const Act*>(c->P), L.b2, rows, c->H, Ln.ln1g, Ln.ln1b, eps,
-                                last ? nullptr : reinterpret_cast<Act*>(c->A), st);
-      }
+      const size_t o = (size_t)shard0(c) * c->H;
+      const int sn = shardn(c);
+      Prof p(c, st, P_MEM, sn * H * (8.0 + (last ? 1 : 2) * act));
+      launch_residual_ln<Act>(c->X + o, reinterpret_cast<const Act*>(c->P) + o, L.b2, sn, c->H, Ln.ln1g, Ln.ln1b, eps,
+                              last ? nullptr : reinterpret_cast<Act*>(c->A) + o, st);
       c->stats.kernel_launches++;
     }
+    if (sp && !last && (s = tp_gather<Act>(cs, n, rpr, false, st))) return s;
+  }
+  if (sp) {
+    // the final LN / unpack needs every row of the residual stream on every rank
+    energon_status s = tp_gather<float>(cs, n, rpr, true, st);
+    if (s) return s;
   }
 
   // ---- a13: final LN + unpack (every rank holds the replicated result; a local group writes once)
@@ -790,6 +858,11 @@ energon_status energon_set_option(energon_ctx* c, int32_t option, int32_t value)
     if (value != 0 && value != 1) return fail(c, ENERGON_ERR_ARG, "ENERGON_OPT_DRCE takes 0 or 1");
     c->cfg.drce = value;
     c->tm_rows = -1;  // activation tensor maps depend on the row count
+    return ENERGON_OK;
+  }
+  if (option == ENERGON_OPT_TP_SP) {
+    if (value != 0 && value != 1) return fail(c, ENERGON_ERR_ARG, "ENERGON_OPT_TP_SP takes 0 or 1");
+    c->sp = value != 0;
     return ENERGON_OK;
   }
   return fail(c, ENERGON_ERR_ARG, "unknown option");

@@ -149,13 +149,17 @@ def test_forward_tiny_vs_oracle(dtype, causal, drce):
 
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
 @pytest.mark.parametrize("k", [2, 4])
-def test_forward_local_tp_vs_oracle(dtype, k):
-    """1-D TP over k shards on one GPU (in-device rank-order reduction): equals the serial oracle."""
+@pytest.mark.parametrize("sp", [1, 0])
+def test_forward_local_tp_vs_oracle(dtype, k, sp):
+    """1-D TP over k shards on one GPU (in-device rank-order reductions), both schedules: allreduce
+    (sp=0) and reduce-scatter / LN on own rows / all-gather (sp=1); equals the serial oracle."""
     shape = dict(SHAPES["tiny"], L=2, V=300, max_seq=40)
     B, S, seed = 5, 33, 4
     lens = synth.random_lengths(B, S, seed)
     tok = synth.tokens(B, S, shape["V"], lens, seed)
     ctxs = make_engine(shape, seed, dtype, B * S, k=k)
+    for c in ctxs:
+        E().energon_set_option(c, E().OPT_TP_SP, sp)
     try:
         y = run_forward(ctxs, tok, lens, dtype, shape["H"])
         st = E().energon_get_stats(ctxs[0])
@@ -338,13 +342,15 @@ def test_fused_layout_kernels_bitexact(drce, monkeypatch):
 
 
 @pytest.mark.parametrize("k", [2, 4])
-def test_forward_local_tp_fused_d64(k):
-    """Local TP with head_dim 64 (fused a5/a7 path) against the oracle, bf16."""
+@pytest.mark.parametrize("drce", [1, 0])
+def test_forward_local_tp_fused_d64(k, drce):
+    """Local TP with head_dim 64 (fused a5/a7 path), sequence-parallel schedule, DRCE on / off,
+    against the oracle, bf16."""
     shape = dict(L=2, H=256, h=4, F=1024, V=500, max_seq=64)
     B, S, seed = 5, 64, 9
     lens = synth.random_lengths(B, S, seed)
     tok = synth.tokens(B, S, shape["V"], lens, seed)
-    ctxs = make_engine(shape, seed, "bf16", B * S, k=k)
+    ctxs = make_engine(shape, seed, "bf16", B * S, k=k, drce=drce)
     try:
         y = run_forward(ctxs, tok, lens, "bf16", shape["H"])
     finally:
