@@ -20,6 +20,8 @@ template <typename Act>
 __global__ void __launch_bounds__(128) attention_simt_kernel(const Act* __restrict__ Q, const Act* __restrict__ K,
                                                              const Act* __restrict__ V, Act* __restrict__ O, LensParam lp,
                                                              int hk, int S, int d, int causal, float scale) {
+  pdl_trigger();
+  pdl_wait();
   extern __shared__ float sm[];
   float* q = sm;        // [d]
   float* sc = sm + d;   // [S]
@@ -69,7 +71,7 @@ void launch_attention_simt(const Act* Q, const Act* K, const Act* V, Act* O, con
   if (B <= 0) return;
   dim3 grid(S, hk, B);
   const size_t smem = sizeof(float) * (size_t)(d + S);
-  attention_simt_kernel<Act><<<grid, 128, smem, st>>>(Q, K, V, O, lp, hk, S, d, causal, 1.f / sqrtf((float)d));
+  launch_k(attention_simt_kernel<Act>, dim3(grid), dim3(128), smem, st, Q, K, V, O, lp, hk, S, d, causal, 1.f / sqrtf((float)d));
 }
 
 // ----------------------------------------------------------------------------- tensor-core kernel (bf16)
@@ -113,6 +115,8 @@ __global__ void __launch_bounds__(128) attention_fa_kernel(const bf16* __restric
                                                            const bf16* __restrict__ V, bf16* __restrict__ O,
                                                            bf16* __restrict__ Cp, const int* __restrict__ offsets,
                                                            LensParam lp, int hk, int S, int causal, float scale_log2) {
+  pdl_trigger();
+  pdl_wait();
   constexpr int BM = 64, BN = 64, CH = D / 8, KS = D / 16, NT = BN / 8, DT = D / 8;
   static_assert(CH >= 8, "swizzle needs >= 8 chunks per row");
   extern __shared__ __align__(128) uint8_t sm_raw[];
@@ -282,6 +286,8 @@ __global__ void __launch_bounds__(128, 4) attention_fa2_kernel(const bf16* __res
                                                                const bf16* __restrict__ V, bf16* __restrict__ O,
                                                                bf16* __restrict__ Cp, const int* __restrict__ offsets,
                                                                LensParam lp, int hk, int S, int causal, float scale_log2) {
+  pdl_trigger();
+  pdl_wait();
   constexpr int BM = 64, BN = 64, CH = D / 8, KS = D / 16, NT = BN / 8, DT = D / 8;
   static_assert(CH >= 8, "swizzle needs >= 8 chunks per row");
   extern __shared__ __align__(128) uint8_t sm_raw[];
@@ -440,7 +446,7 @@ static void launch_fa(const bf16* Q, const bf16* K, const bf16* V, bf16* O, bf16
       cudaFuncSetAttribute(attention_fa_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       attr = true;
     }
-    attention_fa_kernel<D><<<grid, 128, smem, st>>>(Q, K, V, O, Cp, offsets, lp, hk, S, causal, scale_log2);
+    launch_k(attention_fa_kernel<D>, dim3(grid), dim3(128), smem, st, Q, K, V, O, Cp, offsets, lp, hk, S, causal, scale_log2);
   } else {
     const int smem = (64 + 2 * 64) * D * 2;
     static bool attr = false;
@@ -448,7 +454,7 @@ static void launch_fa(const bf16* Q, const bf16* K, const bf16* V, bf16* O, bf16
       cudaFuncSetAttribute(attention_fa2_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       attr = true;
     }
-    attention_fa2_kernel<D><<<grid, 128, smem, st>>>(Q, K, V, O, Cp, offsets, lp, hk, S, causal, scale_log2);
+    launch_k(attention_fa2_kernel<D>, dim3(grid), dim3(128), smem, st, Q, K, V, O, Cp, offsets, lp, hk, S, causal, scale_log2);
   }
 }
 

@@ -32,6 +32,13 @@ __device__ __forceinline__ uint4 ld_nc_v4(const void* p) {
   return r;
 }
 
+// ----------------------------------------------------------------------------- programmatic dependent launch
+// Every energon kernel is launched with programmatic stream serialization (launch_k in kernels.h):
+// it may start while the previous kernel on the stream drains, runs its prologue, and waits here
+// before touching any global data the previous kernel produces or consumes.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // ----------------------------------------------------------------------------- reductions
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll

@@ -11,6 +11,8 @@ constexpr int SG_BM = 64, SG_BN = 64, SG_BK = 16;
 __global__ void __launch_bounds__(256) gemm_f32_kernel(const float* __restrict__ A, const float* __restrict__ W,
                                                        const float* __restrict__ bias, float* __restrict__ D, int M,
                                                        int N, int K, int epi) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ float As[SG_BK][SG_BM + 4];
   __shared__ float Ws[SG_BK][SG_BN + 4];
   const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
@@ -59,7 +61,7 @@ void launch_gemm_f32(const float* A, const float* W, const float* bias, float* D
                      cudaStream_t st) {
   if (M <= 0 || N <= 0) return;
   dim3 grid((N + SG_BN - 1) / SG_BN, (M + SG_BM - 1) / SG_BM);
-  gemm_f32_kernel<<<grid, 256, 0, st>>>(A, W, bias, D, M, N, K, epi);
+  launch_k(gemm_f32_kernel, dim3(grid), dim3(256), 0, st, A, W, bias, D, M, N, K, epi);
 }
 
 }  // namespace energon

@@ -136,6 +136,7 @@ template <int BN, int EPI>
 __global__ void __launch_bounds__(256, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, bf16* __restrict__ D,
                    const float* __restrict__ bias, int M, int N, int K, const QkvScatter qs) {
+  pdl_trigger();
   using C = TcCfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -177,6 +178,7 @@ __global__ void __launch_bounds__(256, 1)
 
   if (warp == 0) {
     if (lane == 0) {
+      pdl_wait();  // inputs of this GEMM are written by the previous kernel
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
@@ -225,6 +227,7 @@ __global__ void __launch_bounds__(256, 1)
       }
     }
   } else if (warp >= 4) {
+    pdl_wait();  // outputs: the previous kernel must be done with them
     const int q = warp - 4;  // TMEM lane quadrant this warp may access
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -477,6 +480,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     bf16* __restrict__ D, const float* __restrict__ bias, int M, int N, int K, int group_m,
                     const QkvScatter qs, const TailPlan tp, const __grid_constant__ CUtensorMap tmD) {
+  pdl_trigger();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   using C = Tc2Cfg<BN>;
@@ -525,6 +529,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
 
   if (warp == 0) {
     if (lane == 0) {
+      pdl_wait();  // inputs of this GEMM are written by the previous kernel
       int stage = 0;
       uint32_t phase = 0;
       for (int u = cid; u < num_units; u += ncl) {
@@ -579,6 +584,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       }
     }
   } else if (warp >= 4) {
+    pdl_wait();  // outputs: the previous kernel must be done with them
     const int q = warp - 4;
     const int etid = threadIdx.x - 128;  // 0..127: this thread's TMEM lane / tile row
     const uint32_t tempty_leader = smem_u32(&tempty[0]) & PEER_MASK;
@@ -809,7 +815,7 @@ static void launch_pair_epi(const CUtensorMap& tmA, const CUtensorMap& tmB, cons
     memset(&md, 0, sizeof(md));
     if (EPI != EPI_BIAS_QKV && !make_tmap_store(&md, D, M, N)) return;  // caller checks cudaGetLastError
   }
-  gemm_tc2_kernel<BN, EPI><<<grid, 256, C::SMEM, st>>>(tmA, tmB, D, bias, M, N, K, group_m, qs, tp, md);
+  launch_k(gemm_tc2_kernel<BN, EPI>, dim3(grid), dim3(256), C::SMEM, st, tmA, tmB, D, bias, M, N, K, group_m, qs, tp, md);
 }
 
 template <int BN, int EPI>
@@ -823,7 +829,7 @@ static void launch_bn_epi(const CUtensorMap& tmA, const CUtensorMap& tmB, const 
   }
   const int tiles = ((M + TC_BM - 1) / TC_BM) * ((N + BN - 1) / BN);
   const int grid = tiles < num_sms() ? tiles : num_sms();
-  gemm_tc_kernel<BN, EPI><<<grid, 256, C::SMEM, st>>>(tmA, tmB, D, bias, M, N, K, qs);
+  launch_k(gemm_tc_kernel<BN, EPI>, dim3(grid), dim3(256), C::SMEM, st, tmA, tmB, D, bias, M, N, K, qs);
 }
 
 #define DISPATCH_EPI(F, BNARGS)                                                  \

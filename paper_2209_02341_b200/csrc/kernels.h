@@ -7,9 +7,31 @@
 
 #define ENERGON_MAX_B 1024
 
+#include <utility>
+
 namespace energon {
 
 typedef __nv_bfloat16 bf16;
+
+bool pdl_enabled();  // ENERGON_NO_PDL=1 disables programmatic dependent launch (A/B)
+
+// Launch with programmatic stream serialization (PDL): the kernel may begin while the previous
+// kernel in the stream finishes; it calls pdl_wait() before its first dependent global access.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                            Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 // seq_lens passed by value as a kernel parameter (4 KB): no host->device copy, no sync.
 struct LensParam {

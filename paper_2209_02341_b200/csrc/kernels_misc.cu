@@ -27,6 +27,8 @@ static inline int grid_for(int64_t work, int threads, int max_blocks) {
 __global__ void __launch_bounds__(256) index_maps_kernel(LensParam lp, int B, int S, int* __restrict__ offsets,
                                                          int* __restrict__ pack_idx, int* __restrict__ pos,
                                                          int* __restrict__ unpack_idx) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ int s_off[ENERGON_MAX_B + 1];
   __shared__ int s_len[ENERGON_MAX_B];
   for (int b = threadIdx.x; b < B; b += blockDim.x) s_len[b] = lp.lens[b];
@@ -132,6 +134,8 @@ __global__ void __launch_bounds__(LN_THREADS) embed_ln_kernel(const int* __restr
                                                               const Act* __restrict__ pos_emb, const float* __restrict__ g,
                                                               const float* __restrict__ b, float eps, float* __restrict__ X,
                                                               Act* __restrict__ A, int* err_flag) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ float red[32];
   const int t = row0 + blockIdx.x;
   const int cell = pack_idx ? pack_idx[t] : t;
@@ -171,6 +175,8 @@ __global__ void __launch_bounds__(LN_THREADS) gather_ln_kernel(const float* __re
                                                                int row0, int H, const float* __restrict__ g,
                                                                const float* __restrict__ b, float eps, float* __restrict__ X,
                                                                Act* __restrict__ A) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ float red[32];
   const int t = row0 + blockIdx.x;
   const int cell = pack_idx ? pack_idx[t] : t;
@@ -202,6 +208,8 @@ __global__ void __launch_bounds__(TPR) residual_ln_kernel(float* __restrict__ X,
                                                           const float* __restrict__ bias, int H,
                                                           const float* __restrict__ g, const float* __restrict__ b,
                                                           float eps, Act* __restrict__ A) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ float red[32];
   const int t = blockIdx.x;
   float4 v[LN_MAXV];
@@ -248,6 +256,8 @@ __global__ void __launch_bounds__(LN_THREADS) final_ln_unpack_kernel(const float
                                                                      int rows_are_cells, int H, const float* __restrict__ g,
                                                                      const float* __restrict__ b, float eps, int apply_ln,
                                                                      Out* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ float red[32];
   const int cell = blockIdx.x;
   const int t = unpack_idx[cell];
@@ -289,6 +299,8 @@ __global__ void __launch_bounds__(LN_THREADS) final_ln_unpack_kernel(const float
 template <typename Act>
 __global__ void unpack_qkv_kernel(const Act* __restrict__ QKV, const int* __restrict__ pack_idx, int T, int S, int hk,
                                   int d, Act* __restrict__ Q, Act* __restrict__ K, Act* __restrict__ Vv) {
+  pdl_trigger();
+  pdl_wait();
   constexpr int E = 16 / sizeof(Act);
   const int Hk = hk * d;
   const int chunks_per_row = 3 * Hk / E;
@@ -312,6 +324,8 @@ __global__ void unpack_qkv_kernel(const Act* __restrict__ QKV, const int* __rest
 template <typename Act>
 __global__ void repack_kernel(const Act* __restrict__ O, const int* __restrict__ pack_idx,
                               const int* __restrict__ unpack_idx, int T, int S, int hk, int d, Act* __restrict__ C) {
+  pdl_trigger();
+  pdl_wait();
   constexpr int E = 16 / sizeof(Act);
   const int Hk = hk * d;
   const int chunks_per_row = Hk / E;
@@ -334,6 +348,8 @@ __global__ void repack_kernel(const Act* __restrict__ O, const int* __restrict__
 // order 0..k-1 in fp32 (every rank gets bit-identical data), write back to all k.
 template <typename Act>
 __global__ void local_allreduce_kernel(PtrList parts, int k, int64_t n) {
+  pdl_trigger();
+  pdl_wait();
   constexpr int E = 16 / sizeof(Act);
   const int64_t nv = n / E;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nv; i += (int64_t)gridDim.x * blockDim.x) {
@@ -358,6 +374,8 @@ __global__ void local_allreduce_kernel(PtrList parts, int k, int64_t n) {
 // written to rank s's buffer only -- the semantics of ncclReduceScatter in place.
 template <typename Act>
 __global__ void local_reduce_scatter_kernel(PtrList parts, int k, int64_t shard) {
+  pdl_trigger();
+  pdl_wait();
   constexpr int E = 16 / sizeof(Act);
   const int64_t nv = shard / E;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nv * k; i += (int64_t)gridDim.x * blockDim.x) {
@@ -382,6 +400,8 @@ __global__ void local_reduce_scatter_kernel(PtrList parts, int k, int64_t shard)
 // Local-group all-gather: rank s's shard (shard_bytes at s * shard_bytes) is copied into every
 // other rank's buffer -- the semantics of ncclAllGather in place.
 __global__ void local_all_gather_kernel(PtrList parts, int k, int64_t shard_bytes) {
+  pdl_trigger();
+  pdl_wait();
   const int64_t nv = shard_bytes / 16;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nv * k; i += (int64_t)gridDim.x * blockDim.x) {
     const int s = (int)(i / nv);
@@ -395,12 +415,12 @@ __global__ void local_all_gather_kernel(PtrList parts, int k, int64_t shard_byte
 template <typename Act>
 void launch_local_reduce_scatter(const PtrList& parts, int k, int64_t shard, cudaStream_t st) {
   const int64_t work = shard / (16 / sizeof(Act)) * k;
-  if (work > 0) local_reduce_scatter_kernel<Act><<<grid_for(work, 256, 148 * 8), 256, 0, st>>>(parts, k, shard);
+  if (work > 0) launch_k(local_reduce_scatter_kernel<Act>, dim3(grid_for(work, 256, 148 * 8)), dim3(256), 0, st, parts, k, shard);
 }
 
 void launch_local_all_gather(const PtrList& parts, int k, int64_t shard_bytes, cudaStream_t st) {
   const int64_t work = shard_bytes / 16 * k;
-  if (work > 0) local_all_gather_kernel<<<grid_for(work, 256, 148 * 8), 256, 0, st>>>(parts, k, shard_bytes);
+  if (work > 0) launch_k(local_all_gather_kernel, dim3(grid_for(work, 256, 148 * 8)), dim3(256), 0, st, parts, k, shard_bytes);
 }
 
 // ============================================================================ load-time relayout
@@ -418,6 +438,8 @@ template <> __device__ __forceinline__ bf16 cvt<bf16>(bf16 x) { return x; }
 template <typename Src, typename Dst>
 __global__ void relayout_kernel(const Src* __restrict__ src, int64_t ld, int64_t row0, int64_t col0, int N, int K,
                                 Dst* __restrict__ dst, int64_t dst_ld, int64_t dst_row0) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ Src tile[32][33];
   const int n0 = blockIdx.x * 32, k0 = blockIdx.y * 32;
   for (int i = threadIdx.y; i < 32; i += blockDim.y) {
@@ -433,6 +455,8 @@ __global__ void relayout_kernel(const Src* __restrict__ src, int64_t ld, int64_t
 
 template <typename Src, typename Dst>
 __global__ void convert_vec_kernel(const Src* __restrict__ src, int64_t off, int N, Dst* __restrict__ dst) {
+  pdl_trigger();
+  pdl_wait();
   for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < N; n += gridDim.x * blockDim.x) dst[n] = cvt<Dst>(src[off + n]);
 }
 
@@ -441,7 +465,7 @@ __global__ void convert_vec_kernel(const Src* __restrict__ src, int64_t off, int
 void launch_index_maps(const LensParam& lp, int B, int S, int* offsets, int* pack_idx, int* pos, int* unpack_idx,
                        cudaStream_t st) {
   const int cells = B * S;
-  index_maps_kernel<<<grid_for(cells, 256, 148 * 4), 256, 0, st>>>(lp, B, S, offsets, pack_idx, pos, unpack_idx);
+  launch_k(index_maps_kernel, dim3(grid_for(cells, 256, 148 * 4)), dim3(256), 0, st, lp, B, S, offsets, pack_idx, pos, unpack_idx);
 }
 
 #define NV_DISPATCH(H, KERNEL_CALL)                                         \
@@ -465,7 +489,7 @@ void launch_embed_ln(const int* tok, const int* pack_idx, int row0, int rows, in
                      const Act* pos_emb, const float* g, const float* b, float eps, float* X, Act* A, int* err,
                      cudaStream_t st) {
   if (rows > 0)
-    NV_DISPATCH(H, (embed_ln_kernel<Act, NVX><<<rows, LN_THREADS, 0, st>>>(tok, pack_idx, row0, S, V, H, tok_emb, pos_emb,
+    NV_DISPATCH(H, (launch_k(embed_ln_kernel<Act, NVX>, dim3(rows), dim3(LN_THREADS), 0, st, tok, pack_idx, row0, S, V, H, tok_emb, pos_emb,
                                                                            g, b, eps, X, A, err)))
 }
 
@@ -473,7 +497,7 @@ template <typename Act>
 void launch_gather_ln(const float* x, const int* pack_idx, int row0, int rows, int H, const float* g, const float* b,
                       float eps, float* X, Act* A, cudaStream_t st) {
   if (rows > 0)
-    NV_DISPATCH(H, (gather_ln_kernel<Act, NVX><<<rows, LN_THREADS, 0, st>>>(x, pack_idx, row0, H, g, b, eps, X, A)))
+    NV_DISPATCH(H, (launch_k(gather_ln_kernel<Act, NVX>, dim3(rows), dim3(LN_THREADS), 0, st, x, pack_idx, row0, H, g, b, eps, X, A)))
 }
 
 #define NV_DISPATCH_T(H, TPRV, KERNEL_CALL)                                 \
@@ -511,51 +535,51 @@ void launch_residual_ln(float* X, const Act* P, const float* bias, int rows, int
   if (rows <= 0) return;
   const int tpr = ln_tpr(H);
   if (tpr == 128)
-    NV_DISPATCH_T(H, 128, (residual_ln_kernel<Act, NVX, 128><<<rows, 128, 0, st>>>(X, P, bias, H, g, b, eps, A)))
+    NV_DISPATCH_T(H, 128, (launch_k(residual_ln_kernel<Act, NVX, 128>, dim3(rows), dim3(128), 0, st, X, P, bias, H, g, b, eps, A)))
   else if (tpr == 512)
-    NV_DISPATCH_T(H, 512, (residual_ln_kernel<Act, NVX, 512><<<rows, 512, 0, st>>>(X, P, bias, H, g, b, eps, A)))
+    NV_DISPATCH_T(H, 512, (launch_k(residual_ln_kernel<Act, NVX, 512>, dim3(rows), dim3(512), 0, st, X, P, bias, H, g, b, eps, A)))
   else
-    NV_DISPATCH_T(H, 256, (residual_ln_kernel<Act, NVX, 256><<<rows, 256, 0, st>>>(X, P, bias, H, g, b, eps, A)))
+    NV_DISPATCH_T(H, 256, (launch_k(residual_ln_kernel<Act, NVX, 256>, dim3(rows), dim3(256), 0, st, X, P, bias, H, g, b, eps, A)))
 }
 
 template <typename Out>
 void launch_final_ln_unpack(const float* X, const int* unpack_idx, int rows_are_cells, int cells, int H, const float* g,
                             const float* b, float eps, int apply_ln, Out* out, cudaStream_t st) {
   if (cells > 0)
-    NV_DISPATCH(H, (final_ln_unpack_kernel<Out, NVX><<<cells, LN_THREADS, 0, st>>>(X, unpack_idx, rows_are_cells, H, g, b,
-                                                                                   eps, apply_ln, out)))
+    NV_DISPATCH(H, (launch_k(final_ln_unpack_kernel<Out, NVX>, dim3(cells), dim3(LN_THREADS), 0, st, X, unpack_idx,
+                             rows_are_cells, H, g, b, eps, apply_ln, out)))
 }
 
 template <typename Act>
 void launch_unpack_qkv(const Act* QKV, const int* pack_idx, int T, int S, int hk, int d, Act* Q, Act* K, Act* V,
                        cudaStream_t st) {
   const int64_t work = (int64_t)T * 3 * hk * d / (16 / sizeof(Act));
-  if (work > 0) unpack_qkv_kernel<Act><<<grid_for(work, 256, 148 * 16), 256, 0, st>>>(QKV, pack_idx, T, S, hk, d, Q, K, V);
+  if (work > 0) launch_k(unpack_qkv_kernel<Act>, dim3(grid_for(work, 256, 148 * 16)), dim3(256), 0, st, QKV, pack_idx, T, S, hk, d, Q, K, V);
 }
 
 template <typename Act>
 void launch_repack(const Act* O, const int* pack_idx, const int* unpack_idx, int T, int S, int hk, int d, Act* C,
                    cudaStream_t st) {
   const int64_t work = (int64_t)T * hk * d / (16 / sizeof(Act));
-  if (work > 0) repack_kernel<Act><<<grid_for(work, 256, 148 * 16), 256, 0, st>>>(O, pack_idx, unpack_idx, T, S, hk, d, C);
+  if (work > 0) launch_k(repack_kernel<Act>, dim3(grid_for(work, 256, 148 * 16)), dim3(256), 0, st, O, pack_idx, unpack_idx, T, S, hk, d, C);
 }
 
 template <typename Act>
 void launch_local_allreduce(const PtrList& parts, int k, int64_t n, cudaStream_t st) {
   const int64_t work = n / (16 / sizeof(Act));
-  if (work > 0) local_allreduce_kernel<Act><<<grid_for(work, 256, 148 * 8), 256, 0, st>>>(parts, k, n);
+  if (work > 0) launch_k(local_allreduce_kernel<Act>, dim3(grid_for(work, 256, 148 * 8)), dim3(256), 0, st, parts, k, n);
 }
 
 template <typename Src, typename Dst>
 void launch_relayout(const Src* src, int64_t ld, int64_t row0, int64_t col0, int N, int K, Dst* dst, int64_t dst_ld,
                      int64_t dst_row0, cudaStream_t st) {
   dim3 grid((N + 31) / 32, (K + 31) / 32), block(32, 8);
-  relayout_kernel<Src, Dst><<<grid, block, 0, st>>>(src, ld, row0, col0, N, K, dst, dst_ld, dst_row0);
+  launch_k(relayout_kernel<Src, Dst>, dim3(grid), dim3(block), 0, st, src, ld, row0, col0, N, K, dst, dst_ld, dst_row0);
 }
 
 template <typename Src, typename Dst>
 void launch_convert_vec(const Src* src, int64_t off, int N, Dst* dst, cudaStream_t st) {
-  convert_vec_kernel<Src, Dst><<<grid_for(N, 256, 1024), 256, 0, st>>>(src, off, N, dst);
+  launch_k(convert_vec_kernel<Src, Dst>, dim3(grid_for(N, 256, 1024)), dim3(256), 0, st, src, off, N, dst);
 }
 
 // explicit instantiations

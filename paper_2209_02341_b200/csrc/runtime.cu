@@ -28,6 +28,17 @@
 
 using namespace energon;
 
+namespace energon {
+bool pdl_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("ENERGON_NO_PDL");
+    v = (e && e[0] == '1') ? 0 : 1;
+  }
+  return v == 1;
+}
+}  // namespace energon
+
 namespace {
 
 thread_local std::string g_last_error;

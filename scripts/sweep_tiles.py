@@ -4,10 +4,12 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2209_02341_b200 import energon
 energon.load_library()
-T = 4096
+T = int(os.environ.get("T", 4096))
+H0 = int(os.environ.get("H", 5120))
+TPS = [int(x) for x in os.environ.get("TPS", "1,2,4,8").split(",")]
 res = {}
-for k in (1, 2, 4, 8):
-    H = 5120
+for k in TPS:
+    H = H0
     shapes = {"qkv": (T, 3 * H // k, H), "out": (T, H, H // k), "up": (T, 4 * H // k, H), "down": (T, H, 4 * H // k)}
     for name, (M, N, K) in shapes.items():
         A = (torch.randn(M, K, device="cuda") * 0.5).bfloat16()
