@@ -92,7 +92,8 @@ typedef struct {
  * caller passes pre-sliced shards in the same [in,out] layout (wq [H,H/k],
  * bq [H/k], wo [H/k,H], w1 [H,F/k], b1 [F/k], w2 [F/k,H]); bo, b2 and the LN
  * vectors are always full (added once after the reduce on every rank, C9).
- * Sources are read during the call only (they may be freed afterwards).
+ * Sources are read during the call only (they may be freed afterwards); the call first waits for
+ * all work already issued to the device, so sources written on any stream are complete.
  */
 typedef struct {
   const void *wq, *wk, *wv, *wo, *bq, *bk, *bv, *bo, *w1, *b1, *w2, *b2, *ln1_g, *ln1_b, *ln2_g, *ln2_b;

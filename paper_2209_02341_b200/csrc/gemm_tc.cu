@@ -524,6 +524,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   }
   tc_fence_before();
   cluster_sync_all();
+  __syncthreads();  // also a CTA barrier: orders the tcgen05.alloc write of tmem_holder for every checker
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
 

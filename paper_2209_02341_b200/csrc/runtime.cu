@@ -717,6 +717,9 @@ energon_status energon_load_embeddings(energon_ctx* c, const void* tok_emb, cons
   if (!c || !tok_emb || !pos_emb || !lnf_g || !lnf_b) return fail(c, ENERGON_ERR_ARG, "NULL argument");
   if (sd < 0 || sd > 2) return fail(c, ENERGON_ERR_ARG, "src_dtype must be F32, BF16 or F64");
   CU(c, cudaSetDevice(c->cfg.device));
+  // the sources may have been produced on any stream of this device (e.g. the legacy default stream,
+  // which the non-blocking load stream does not wait for): finish all prior work first
+  CU(c, cudaDeviceSynchronize());
   const int64_t VH = (int64_t)c->V * c->H, PH = (int64_t)c->cfg.max_seq * c->H;
   energon_status s;
   if (!c->tok_emb) {
@@ -755,6 +758,7 @@ energon_status energon_load_layer_weights(energon_ctx* c, int32_t layer, const e
   for (int i = 0; i < 16; ++i)
     if (!ptrs[i]) return fail(c, ENERGON_ERR_ARG, "a layer weight pointer is NULL");
   CU(c, cudaSetDevice(c->cfg.device));
+  CU(c, cudaDeviceSynchronize());  // sources may come from any stream (see energon_load_embeddings)
   LayerDev& L = c->layers[layer];
   const int H = c->H, F = c->F, Hk = c->Hk, Fk = c->Fk, r = c->r;
   const size_t a = c->act;
