@@ -429,14 +429,21 @@ __global__ void __launch_bounds__(128, 4) attention_fa2_kernel(const bf16* __res
   }
 }
 
+int attention_impl() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("ENERGON_ATTN");
+    v = e ? atoi(e) : 3;
+    if (v < 1 || v > 3) v = 3;
+  }
+  return v;
+}
+
 template <int D>
 static void launch_fa(const bf16* Q, const bf16* K, const bf16* V, bf16* O, bf16* Cp, const int* offsets,
                       const LensParam& lp, int B, int hk, int S, int causal, cudaStream_t st) {
-  static int gen = -1;
-  if (gen < 0) {
-    const char* e = getenv("ENERGON_ATTN");  // 1 = first-generation kernel (A/B), default 2
-    gen = (e && e[0] == '1') ? 1 : 2;
-  }
+  if (attention_impl() == 3 && launch_attention_tc(Q, K, V, Cp, offsets, O, lp, B, hk, S, D, causal, st)) return;
+  const int gen = attention_impl() == 1 ? 1 : 2;
   dim3 grid((S + 63) / 64, hk, B);
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)D);
   if (gen == 1) {

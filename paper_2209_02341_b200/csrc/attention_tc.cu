@@ -1,0 +1,327 @@
+// attention_tc.cu -- a6 (+ a7 fused) on the 5th-generation tensor cores: masked softmax attention
+// over the rebuilt padded per-head layout Q, K, V [B, hk, S, d] ("the multi-head
+// attention module still requires the padding area"), writing the packed context
+// rows [T, hk*d] at offsets[b] + s (PAPER.md:373 kernel #2 fused).
+//
+// One CTA = 128 query rows of one (sequence, head); 6 warps:
+//   warp 0    TMA producer: the Q tile once, then K and V tiles of 64 keys (single-buffered each;
+//             the next K tile streams in while the current tile's softmax and P.V run)
+//   warp 1    MMA issuer (one thread): S = Q K^T  (M=128, N=64, K=d; K-major A and B)
+//                                      O += P V    (M=128, N=d, K=64; A = P from shared memory,
+//                                                   B = V, MN-major)  -- accumulators in TMEM
+//   warps 2-5 softmax: thread i owns query row i (TMEM lane i): tcgen05.ld its 64 scores, masks
+//             (t >= len, causal t > s), runs the online softmax in fp32 / exp2 and writes its P row
+//             (bf16, 128B-swizzled) to shared memory; O stays in TMEM and is rescaled only when the
+//             row maximum grew by more than 2^8 (exact: P values are bounded by 256).
+// Key tiles stop at min(len, q0 + 128) (causal) or len; query tiles with q0 >= len exit at once.
+// Rows t >= len of the last V tile are zeroed in shared memory before P.V, so pad rows of V that a5
+// never wrote (possibly NaN) cannot reach the output even as 0 * NaN.
+#include "common.cuh"
+#include "kernels.h"
+#include "tc_ptx.cuh"
+
+namespace energon {
+
+__device__ __forceinline__ float ex2f(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,"
+      "%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
+      "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+      "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
+// MN-major (N contiguous) 128B-swizzled operand: 64-element rows of 128 B; SBO = 1024 B between
+// 8-row groups along K, LBO = distance between 64-wide blocks along N.
+__device__ __forceinline__ uint64_t umma_desc_sw128_mn(uint32_t saddr, uint32_t lbo_bytes) {
+  uint64_t d = (uint64_t)((saddr & 0x3FFFFu) >> 4);
+  d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)(1024u >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
+template <int D>
+struct AttnCfg {
+  static constexpr int BM = 128, BN = 64, DH = D / 64;
+  static constexpr int Q_BYTES = BM * D * 2;  // DH blocks of [128 rows x 64] (16 KB each)
+  static constexpr int K_BYTES = BN * D * 2;  // DH blocks of [64 keys x 64]
+  static constexpr int V_BYTES = BN * D * 2;
+  static constexpr int P_BYTES = BM * BN * 2;  // [128 rows x 64 keys], one swizzle block
+  static constexpr int SMEM = Q_BYTES + K_BYTES + V_BYTES + P_BYTES + 1024 + 256;
+  static constexpr int TMEM_COLS = (BN + D) <= 128 ? 128 : 256;  // S at col 0, O at col BN
+  // S = Q K^T: M=128, N=BN, both K-major
+  static constexpr uint32_t IDESC_S = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                                      ((uint32_t)(BM >> 4) << 24);
+  // O += P V: M=128, N=D, A K-major, B MN-major (bit 16)
+  static constexpr uint32_t IDESC_O = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | ((uint32_t)(D >> 3) << 17) |
+                                      ((uint32_t)(BM >> 4) << 24);
+};
+
+template <int D>
+__global__ void __launch_bounds__(192, 2)
+    attention_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                        const __grid_constant__ CUtensorMap tmV, bf16* __restrict__ Cp, const int* __restrict__ offsets,
+                        bf16* __restrict__ Opad, LensParam lp, int hk, int S, int causal, float scale_log2) {
+  using C = AttnCfg<D>;
+  constexpr int BM = C::BM, BN = C::BN, DH = C::DH;
+  pdl_trigger();
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sK = sQ + C::Q_BYTES;
+  uint8_t* sV = sK + C::K_BYTES;
+  uint8_t* sP = sV + C::V_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + C::P_BYTES);
+  uint64_t* q_full = bars + 0;
+  uint64_t* k_full = bars + 1;
+  uint64_t* v_full = bars + 2;
+  uint64_t* k_empty = bars + 3;
+  uint64_t* v_empty = bars + 4;
+  uint64_t* s_full = bars + 5;
+  uint64_t* s_empty = bars + 6;
+  uint64_t* p_full = bars + 7;
+  uint64_t* o_full = bars + 8;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 9);
+
+  const int qt = gridDim.x - 1 - blockIdx.x;  // longest-running query tiles first
+  const int head = blockIdx.y, b = blockIdx.z;
+  const int len = lp.lens[b];
+  const int q0 = qt * BM;
+  if (q0 >= len) return;  // uniform over the CTA: before any barrier / TMEM use
+  const int kv_end = causal ? min(len, q0 + BM) : len;
+  const int nkv = (kv_end + BN - 1) / BN;
+  const int row_base = (b * hk + head) * S;  // first row of this (sequence, head) in the [B*hk*S, D] view
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmQ);
+    tma_prefetch_desc(&tmK);
+    tma_prefetch_desc(&tmV);
+    mbar_init(q_full, 1);
+    mbar_init(k_full, 1);
+    mbar_init(v_full, 1);
+    mbar_init(k_empty, 1);
+    mbar_init(v_empty, 1);
+    mbar_init(s_full, 1);
+    mbar_init(s_empty, 4);
+    mbar_init(p_full, 4);
+    mbar_init(o_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                 "n"(C::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+  const uint32_t tS = tmem_base, tO = tmem_base + BN;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      pdl_wait();
+      mbar_expect_tx(q_full, C::Q_BYTES);
+#pragma unroll
+      for (int h = 0; h < DH; ++h) tma_load_2d(&tmQ, smem_u32(sQ + h * BM * 128), q_full, h * 64, row_base + q0);
+      for (int j = 0; j < nkv; ++j) {
+        const uint32_t par = j & 1;
+        mbar_wait(k_empty, par ^ 1);
+        mbar_expect_tx(k_full, C::K_BYTES);
+#pragma unroll
+        for (int h = 0; h < DH; ++h) tma_load_2d(&tmK, smem_u32(sK + h * BN * 128), k_full, h * 64, row_base + j * BN);
+        mbar_wait(v_empty, par ^ 1);
+        mbar_expect_tx(v_full, C::V_BYTES);
+#pragma unroll
+        for (int h = 0; h < DH; ++h) tma_load_2d(&tmV, smem_u32(sV + h * BN * 128), v_full, h * 64, row_base + j * BN);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      mbar_wait(q_full, 0);
+      for (int j = 0; j < nkv; ++j) {
+        const uint32_t par = j & 1;
+        // ---- S = Q K^T
+        mbar_wait(k_full, par);
+        mbar_wait(s_empty, par ^ 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * 0 + (kk & 3) * 32;
+          const uint64_t a = umma_desc_sw128(smem_u32(sQ + (kk >> 2) * BM * 128 + off));
+          const uint64_t bb = umma_desc_sw128(smem_u32(sK + (kk >> 2) * BN * 128 + off));
+          umma_bf16(tS, a, bb, C::IDESC_S, kk > 0 ? 1u : 0u);
+        }
+        umma_commit(k_empty);
+        umma_commit(s_full);
+        // ---- O += P V
+        mbar_wait(p_full, par);
+        mbar_wait(v_full, par);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < BN / 16; ++kk) {
+          const uint64_t a = umma_desc_sw128(smem_u32(sP + kk * 32));
+          const uint64_t bb = umma_desc_sw128_mn(smem_u32(sV + kk * 16 * 128), BN * 128);
+          umma_bf16(tO, a, bb, C::IDESC_O, (j > 0 || kk > 0) ? 1u : 0u);
+        }
+        umma_commit(v_empty);
+        umma_commit(o_full);
+      }
+    }
+  } else {
+    // ---------------- softmax warps: thread owns query row r (= TMEM lane r)
+    const int qd = warp & 3;  // TMEM lane quadrant of this warp
+    const int r = qd * 32 + lane;
+    const int srow = q0 + r;  // position in the sequence
+    const uint32_t lane_off = (uint32_t)(qd * 32) << 16;
+    float m_ref = -INFINITY, l = 0.f;
+    for (int j = 0; j < nkv; ++j) {
+      const uint32_t par = j & 1;
+      const int k0 = j * BN;
+      mbar_wait(s_full, par);
+      tc_fence_after();
+      uint32_t sr[2][32];
+      tmem_ld32(tS + lane_off + 0, sr[0]);
+      tmem_ld32(tS + lane_off + 32, sr[1]);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(s_empty);
+      // mask + tile max (scaled log2 domain)
+      float mt = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < BN; ++c) {
+        const int t = k0 + c;
+        float v = __uint_as_float(sr[c >> 5][c & 31]) * scale_log2;
+        if (t >= len || (causal && t > srow)) v = -INFINITY;
+        sr[c >> 5][c & 31] = __float_as_uint(v);
+        mt = fmaxf(mt, v);
+      }
+      // P_{j-1} . V_{j-1} must be done before P is overwritten or O rescaled
+      if (j > 0) {
+        mbar_wait(o_full, par ^ 1);
+        tc_fence_after();
+      }
+      if (mt > m_ref + 8.f) {  // first tile, or the max grew by more than 2^8: move the reference
+        const float alpha = (m_ref == -INFINITY) ? 0.f : ex2f(m_ref - mt);
+        if (j > 0) {
+#pragma unroll 1
+          for (int c = 0; c < D; c += 32) {
+            uint32_t o[32];
+            tmem_ld32(tO + lane_off + c, o);
+#pragma unroll
+            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+            tmem_st32(tO + lane_off + c, o);
+          }
+        }
+        l *= alpha;
+        m_ref = mt;
+      }
+      const float base = (m_ref == -INFINITY) ? 0.f : m_ref;
+      // P row (bf16) -> shared memory, 128B swizzle: 16-byte chunk c of row r at chunk c ^ (r & 7)
+      uint8_t* prow = sP + r * 128;
+#pragma unroll
+      for (int c8 = 0; c8 < BN / 8; ++c8) {
+        float p[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          p[e] = ex2f(__uint_as_float(sr[(c8 * 8 + e) >> 5][(c8 * 8 + e) & 31]) - base);
+          l += p[e];
+        }
+        uint4 pk;
+        pk.x = pack_bf16x2(p[0], p[1]);
+        pk.y = pack_bf16x2(p[2], p[3]);
+        pk.z = pack_bf16x2(p[4], p[5]);
+        pk.w = pack_bf16x2(p[6], p[7]);
+        *reinterpret_cast<uint4*>(prow + ((c8 ^ (r & 7)) << 4)) = pk;
+      }
+      // zero the V rows of keys >= len in a partial last tile (never-written pad rows may hold NaN)
+      if (k0 + BN > len) {
+        mbar_wait(v_full, par);
+        if (r < BN && k0 + r >= len) {
+#pragma unroll
+          for (int h = 0; h < DH; ++h) {
+            uint4* vr = reinterpret_cast<uint4*>(sV + h * BN * 128 + r * 128);
+#pragma unroll
+            for (int c = 0; c < 8; ++c) vr[c] = make_uint4(0, 0, 0, 0);
+          }
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic-proxy smem writes -> tcgen05.mma
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p_full);
+    }
+    // ---------------- epilogue: O / l -> packed context row offsets[b] + srow (valid rows only)
+    mbar_wait(o_full, (nkv - 1) & 1);
+    tc_fence_after();
+    const float inv = 1.f / l;
+    const bool valid = srow < len;
+    // packed context row (a7 fused) or, without Cp, the padded O [B, hk, S, D] row
+    bf16* dst = Cp ? Cp + ((int64_t)__ldg(offsets + b) + srow) * (int64_t)(hk * D) + head * D
+                   : Opad + ((int64_t)row_base + srow) * D;
+#pragma unroll 1
+    for (int c = 0; c < D; c += 32) {
+      uint32_t o[32];
+      tmem_ld32(tO + lane_off + c, o);
+      if (valid) {
+#pragma unroll
+        for (int e = 0; e < 32; e += 8) {
+          uint4 pk;
+          pk.x = pack_bf16x2(__uint_as_float(o[e]) * inv, __uint_as_float(o[e + 1]) * inv);
+          pk.y = pack_bf16x2(__uint_as_float(o[e + 2]) * inv, __uint_as_float(o[e + 3]) * inv);
+          pk.z = pack_bf16x2(__uint_as_float(o[e + 4]) * inv, __uint_as_float(o[e + 5]) * inv);
+          pk.w = pack_bf16x2(__uint_as_float(o[e + 6]) * inv, __uint_as_float(o[e + 7]) * inv);
+          *reinterpret_cast<uint4*>(dst + c + e) = pk;
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(C::TMEM_COLS));
+  }
+}
+
+template <int D>
+static bool launch_tc(const bf16* Q, const bf16* K, const bf16* V, bf16* Cp, const int* offsets, bf16* Opad,
+                      const LensParam& lp, int B, int hk, int S, int causal, cudaStream_t st) {
+  using C = AttnCfg<D>;
+  const int rows = B * hk * S;
+  CUtensorMap mq, mk, mv;
+  if (!make_tmap_kmajor(&mq, Q, rows, D, C::BM) || !make_tmap_kmajor(&mk, K, rows, D, C::BN) ||
+      !make_tmap_kmajor(&mv, V, rows, D, C::BN))
+    return false;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(attention_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    attr = true;
+  }
+  dim3 grid((S + C::BM - 1) / C::BM, hk, B);
+  const float scale_log2 = 1.4426950408889634f / sqrtf((float)D);
+  launch_k(attention_tc_kernel<D>, grid, dim3(192), C::SMEM, st, mq, mk, mv, Cp, offsets, Opad, lp, hk, S, causal,
+           scale_log2);
+  return true;
+}
+
+bool launch_attention_tc(const bf16* Q, const bf16* K, const bf16* V, bf16* ctx_packed, const int* offsets,
+                         bf16* O_padded, const LensParam& lp, int B, int hk, int S, int d, int causal, cudaStream_t st) {
+  if (d == 128) return launch_tc<128>(Q, K, V, ctx_packed, offsets, O_padded, lp, B, hk, S, causal, st);
+  if (d == 64) return launch_tc<64>(Q, K, V, ctx_packed, offsets, O_padded, lp, B, hk, S, causal, st);
+  return false;
+}
+
+}  // namespace energon

@@ -89,6 +89,10 @@ void launch_attention(const Act* Q, const Act* K, const Act* V, Act* O, const Le
                       int d, int causal, cudaStream_t st);
 bool launch_attention_packed(const bf16* Q, const bf16* K, const bf16* V, bf16* ctx_packed, const int* offsets,
                              const LensParam& lp, int B, int hk, int S, int d, int causal, cudaStream_t st);
+// tcgen05 / TMEM attention (d = 64 or 128): packed output (ctx_packed + offsets) or padded O.
+bool launch_attention_tc(const bf16* Q, const bf16* K, const bf16* V, bf16* ctx_packed, const int* offsets,
+                         bf16* O_padded, const LensParam& lp, int B, int hk, int S, int d, int causal, cudaStream_t st);
+int attention_impl();  // ENERGON_ATTN: 3 = tcgen05 (default), 2 = mma.sync v2, 1 = mma.sync v1
 
 // GEMM epilogues.  EPI_BIAS_QKV = bias, then a5 fused: the packed QKV row t / column block is
 // scattered straight into the padded per-head Q, K, V [B, hk, S, d] (needs d % 32 == 0).
@@ -106,7 +110,7 @@ void launch_gemm_f32(const float* A, const float* W, const float* bias, float* D
 // bf16 tcgen05 GEMM.  Operands are K-major bf16 described by TMA maps with a 64-element (128 B)
 // inner box and 128-byte swizzle: A [M,K] with a 128-row box, W [N,K] with a bn-row box (bn = the
 // tile N, 256 or 128, chosen per call by tc_pick_bn).
-bool make_tmap_kmajor(CUtensorMap* map, const void* ptr, int rows, int K, int box_rows);
+bool make_tmap_kmajor(CUtensorMap* map, const void* ptr, int rows, int K, int box_rows);  // inner box 64, SW128
 int tc_pick_bn(int M, int N);  // tile code (see gemm_tc.cu)
 int tc_w_box(int code);        // row box of the W tensor map the code needs (256, 128, 96 or 64)
 bool make_tmap_store(CUtensorMap* map, const void* ptr, int rows, int N);  // D map of the TMA-store epilogue
