@@ -49,6 +49,9 @@ def parse():
     ap.add_argument("--no-ab", action="store_true", help="skip the DRCE-off (padded) A/B")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-tokens", type=int, default=192)
+    ap.add_argument("--local-tp", type=int, default=0,
+                    help="emulate TP=k on ONE GPU with a local group (ranks serialised; per-rank kernel "
+                         "shapes and ncu evidence of TP=k, not a TP=k latency)")
     return ap.parse_args()
 
 
@@ -182,6 +185,44 @@ def workload_config(args, shape, bcfg, lens, world):
 
 
 # ============================================================================= energon (GPU) arm
+class Engine:
+    """One rank's context, or a local group of k contexts on this GPU (--local-tp)."""
+
+    def __init__(self, energon, ctxs):
+        self.e, self.ctxs = energon, ctxs
+
+    def forward(self, tok, lens, out, stream):
+        if len(self.ctxs) == 1:
+            self.e.energon_forward(self.ctxs[0], tok, lens, out, stream)
+        else:
+            self.e.energon_forward_group(self.ctxs, tok, lens, out, stream)
+
+    def set_option(self, opt, v):
+        for c in self.ctxs:
+            self.e.energon_set_option(c, opt, v)
+
+    def set_profiling(self, on):
+        for c in self.ctxs:
+            self.e.energon_set_profiling(c, on)
+
+    def profile(self):
+        tot = {}
+        for c in self.ctxs:
+            for k, v in self.e.energon_get_profile(c).items():
+                tot[k] = tot.get(k, 0) + v
+        return tot
+
+    def launches(self):
+        return sum(self.e.energon_get_stats(c)["kernel_launches"] for c in self.ctxs)
+
+    def sync(self):
+        self.e.energon_sync(self.ctxs[0])
+
+    def destroy(self):
+        for c in self.ctxs:
+            self.e.energon_destroy(c)
+
+
 def energon_arm(args, world, rank, local):
     import numpy as np
     import torch
@@ -212,17 +253,23 @@ def energon_arm(args, world, rank, local):
         from paper_2209_02341_b200 import dist as edist
         uid = edist.broadcast_bytes(energon.energon_get_unique_id() if rank == 0 else None, 128, device="cuda")
         lens = edist.broadcast_lengths(lens, device="cuda")  # the engine command's seq_lens
-    ctx = energon.energon_init(cfg, uid)
+    if args.local_tp > 1:
+        ctxs = energon.energon_init_local_group(cfg, args.local_tp)
+    else:
+        ctxs = [energon.energon_init(cfg, uid)]
+    eng = Engine(energon, ctxs)
 
     # weights: generated on the device by the seeded counter-based generator, loaded unsharded
     emb = {n: synth.emb_tensor_device(n, H, shape["V"], shape["max_seq"], args.seed, True, torch.bfloat16)
            for n in synth.EMB_TENSORS}
-    energon.energon_load_embeddings(ctx, emb["tok_emb"], emb["pos_emb"], emb["lnf_g"], emb["lnf_b"])
+    for c in ctxs:
+        energon.energon_load_embeddings(c, emb["tok_emb"], emb["pos_emb"], emb["lnf_g"], emb["lnf_b"])
     del emb
     for l in range(shape["L"]):
         w = {n: synth.layer_tensor_device(n, l, H, shape["F"], args.seed, True, torch.bfloat16)
              for n in synth.LAYER_TENSORS}
-        energon.energon_load_layer_weights(ctx, l, w)
+        for c in ctxs:
+            energon.energon_load_layer_weights(c, l, w)
         del w
     torch.cuda.synchronize()
     torch.cuda.empty_cache()
@@ -242,11 +289,11 @@ def energon_arm(args, world, rank, local):
         return edist.max_over_ranks(x, device="cuda")
 
     for _ in range(args.warmup):
-        energon.energon_forward(ctx, tok, lens, out, stream)
-    energon.energon_sync(ctx)
+        eng.forward(tok, lens, out, stream)
+    eng.sync()
 
     # ---------------- device-timed region: inputs resident in HBM (no per-launch instrumentation)
-    launches0 = energon.energon_get_stats(ctx)["kernel_launches"]
+    launches0 = eng.launches()
     clocks = ClockSampler(local)
     evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     barrier()
@@ -257,33 +304,33 @@ def energon_arm(args, world, rank, local):
         torch.cuda.cudart().cudaProfilerStart()
     evs[0].record(stream)
     for i in range(args.steps):
-        energon.energon_forward(ctx, tok, lens, out, stream)
+        eng.forward(tok, lens, out, stream)
         evs[i + 1].record(stream)
     torch.cuda.synchronize()
     if prof_range:
         torch.cuda.cudart().cudaProfilerStop()
     barrier()
     clk = clocks.stop()
-    energon.energon_sync(ctx)
+    eng.sync()
     step_ms = [evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)]
     total_ms = max_over_ranks(evs[0].elapsed_time(evs[-1]))
-    launches = energon.energon_get_stats(ctx)["kernel_launches"] - launches0
+    launches = eng.launches() - launches0
 
     # ---------------- instrumented pass: the same K steps with CUDA events around every launch on
     # the forward stream (energon_set_profiling) -> per-kernel-class device time for the roofline
-    energon.energon_set_profiling(ctx, True)
+    eng.set_profiling(True)
     barrier()
     torch.cuda.synchronize()
     p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     p0.record(stream)
     for i in range(args.steps):
-        energon.energon_forward(ctx, tok, lens, out, stream)
+        eng.forward(tok, lens, out, stream)
     p1.record(stream)
     torch.cuda.synchronize()
     barrier()
-    prof = energon.energon_get_profile(ctx)
+    prof = eng.profile()
     prof_ms = p0.elapsed_time(p1) / args.steps
-    energon.energon_set_profiling(ctx, False)
+    eng.set_profiling(False)
     value = T * args.steps / (total_ms * 1e-3)
 
     # ---------------- end-to-end: host tokens -> device, forward, result -> host, every step
@@ -295,7 +342,7 @@ def energon_arm(args, world, rank, local):
 
         def e2e_step():
             tok_d.copy_(tok_h, non_blocking=True)
-            energon.energon_forward(ctx, tok_d, lens, out, stream)
+            eng.forward(tok_d, lens, out, stream)
             out_h.copy_(out, non_blocking=True)
 
         e2e_step()
@@ -312,13 +359,13 @@ def energon_arm(args, world, rank, local):
         e2e_ms = max_over_ranks(e0.elapsed_time(e1))
         e2e = {"value": T * args.steps / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": tok_h.numel() * 4,
                "d2h_bytes_per_step": out_h.numel() * 2, "ms_per_step": e2e_ms / args.steps}
-    energon.energon_sync(ctx)
+    eng.sync()
 
     # ---------------- DRCE A/B: the same batch with the linears on all B*S padded rows
     drce_ab = None
     if not args.no_ab and args.drce:
-        energon.energon_set_option(ctx, energon.OPT_DRCE, 0)
-        energon.energon_forward(ctx, tok, lens, out, stream)
+        eng.set_option(energon.OPT_DRCE, 0)
+        eng.forward(tok, lens, out, stream)
         torch.cuda.synchronize()
         a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         nab = max(2, args.steps // 2)
@@ -326,18 +373,18 @@ def energon_arm(args, world, rank, local):
         torch.cuda.synchronize()
         a0.record(stream)
         for _ in range(nab):
-            energon.energon_forward(ctx, tok, lens, out, stream)
+            eng.forward(tok, lens, out, stream)
         a1.record(stream)
         torch.cuda.synchronize()
         barrier()
         off_ms = max_over_ranks(a0.elapsed_time(a1)) / nab
-        energon.energon_set_option(ctx, energon.OPT_DRCE, 1)
+        eng.set_option(energon.OPT_DRCE, 1)
         on_ms = total_ms / args.steps
         drce_ab = {"drce_on_ms": on_ms, "drce_off_ms": off_ms, "latency_reduction": 1 - on_ms / off_ms,
                    "valid_tok_s_off": T / (off_ms * 1e-3), "padding_ratio": 1 - T / (B * S),
                    "ideal_reduction": 1 - T / (B * S),
                    "note": "paper: up to 46.8% latency reduction at p=0.5 on A100 (PAPER.md:567-579)"}
-    energon.energon_sync(ctx)
+    eng.sync()
 
     pk = peaks()
     gemm_ms_avg = prof["gemm_ms"] / max(prof["gemm_launches"], 1)
@@ -376,7 +423,8 @@ def energon_arm(args, world, rank, local):
                   min(len(step_ms) - 1, int(round(0.95 * (len(step_ms) - 1))))],
               "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
               "data": "synthetic (seeded counter-based generator; random-init weights of the GPT-3-13B shape)",
-              "config": workload_config(args, shape, bcfg, lens, world), "clocks": clk, "e2e": e2e,
+              "config": workload_config(args, shape, bcfg, lens, world if args.local_tp <= 1 else args.local_tp),
+              "clocks": clk, "e2e": e2e,
               "gpu_launches": int(launches), "roofline": roofline, "phases": phases, "drce_ab": drce_ab}
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -389,9 +437,12 @@ def energon_arm(args, world, rank, local):
                                   "kind": "oracle",
                                   "sample": f"fp64 oracle, layer 0 of {L} over the first {n} tokens of the longest "
                                             f"sequence ({dt:.1f} s), tokens/s extrapolated by the layer count"}
+    if args.local_tp > 1:
+        result["local_tp_emulation"] = (f"TP={args.local_tp} ranks run serially on ONE GPU (in-device reductions): "
+                                        "per-rank kernel shapes of TP=k, not a TP=k latency")
     if rank == 0:
         print(json.dumps(result), flush=True)
-    energon.energon_destroy(ctx)
+    eng.destroy()
     if dist is not None:
         dist.destroy_process_group()
 

@@ -226,8 +226,11 @@ template <int BN> struct Tc2Cfg {
   static constexpr int A_BYTES = 128 * TC_BK * 2;      // this CTA's 128 rows of A per stage
   static constexpr int B_BYTES = (BN / 2) * TC_BK * 2;  // this CTA's BN/2 rows of W per stage
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (200 * 1024) / STAGE_BYTES;
-  static constexpr int STG_BYTES = 4 * 2 * 32 * 32 * 2;  // epilogue staging: 4 warps x 2 x [32 rows x 32 cols] bf16
+  static constexpr int EPI_WARPS = 8;  // two warpgroups, each owning half of a tile's columns
+  static constexpr int STG_BYTES = EPI_WARPS * 2 * 32 * 32 * 2;  // staging: per warp 2 x [32 rows x 32 cols] bf16
+  // as many operand stages as fit in the 227 KB opt-in shared memory next to the staging buffers
+  static constexpr int STAGES_FIT = (227 * 1024 - STG_BYTES - 1024 - 256) / STAGE_BYTES;
+  static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
   static constexpr int SMEM = STAGES * STAGE_BYTES + STG_BYTES + 1024 + 256;
   static constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
                                     ((uint32_t)(256 >> 4) << 24);
@@ -392,10 +395,10 @@ __device__ __forceinline__ void epi_store(float (&v)[32], int row, int n0, int M
   }
 }
 
-__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }  // the 8 epilogue warps
 
 template <int BN, int EPI>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     bf16* __restrict__ D, const float* __restrict__ bias, int M, int N, int K, int group_m,
                     const QkvScatter qs, const TailPlan tp, const __grid_constant__ CUtensorMap tmD) {
@@ -432,7 +435,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 8);  // 4 epilogue warps x 2 CTAs
+      mbar_init(&tempty[i], 2 * C::EPI_WARPS);  // epilogue warps x 2 CTAs
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -505,10 +508,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     }
   } else if (warp >= 4) {
     pdl_wait();  // outputs: the previous kernel must be done with them
-    const int q = warp - 4;
-    const int etid = threadIdx.x - 128;  // 0..127: this thread's TMEM lane / tile row
+    const int q = warp & 3;                 // TMEM lane quadrant this warp may access
+    const int eg = (warp - 4) >> 2;         // epilogue warpgroup: columns [eg * BN/2, (eg+1) * BN/2)
+    const int etid = q * 32 + lane;         // this thread's TMEM lane / tile row
+    constexpr int CH = BN / 32 / 2;         // 32-column chunks per warpgroup
+    const int c0 = eg * CH;
     const uint32_t tempty_leader = smem_u32(&tempty[0]) & PEER_MASK;
-    uint8_t* my_stg = sStg + q * 2 * 2048;
+    uint8_t* my_stg = sStg + (warp - 4) * 2 * 2048;
     uint32_t nst = 0;  // TMA stores issued by this warp (double-buffered staging)
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -524,7 +530,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       float* part = (split >= 0) ? tp.ws + ((size_t)(tail * tp.splits + split) * 2 + rank) * 128 * BN + (size_t)etid * BN
                                  : nullptr;
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
+      for (int c = c0; c < c0 + CH; ++c) {
         uint32_t r[32];
         tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c * 32), r);
         if (split >= 0) {
@@ -562,7 +568,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
         // publish the partial; the last of the `splits` arrivals reduces (fixed order) + epilogue
         __threadfence();
         epi_bar();
-        if (etid == 0) {
+        if (warp == 4 && lane == 0) {
           const int old = atomicAdd(tp.counters + tail * 2 + rank, 1);
           *fix_flag = (old == tp.splits - 1);
           if (old == tp.splits - 1) tp.counters[tail * 2 + rank] = 0;  // self-reset for the next launch
@@ -571,7 +577,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
         if (*fix_flag) {
           __threadfence();
 #pragma unroll 1
-          for (int c = 0; c < BN / 32; ++c) {
+          for (int c = c0; c < c0 + CH; ++c) {
             float v[32];
 #pragma unroll
             for (int j = 0; j < 32; ++j) v[j] = 0.f;
@@ -735,7 +741,8 @@ static void launch_pair_epi(const CUtensorMap& tmA, const CUtensorMap& tmB, cons
     memset(&md, 0, sizeof(md));
     if (EPI != EPI_BIAS_QKV && !make_tmap_store(&md, D, M, N)) return;  // caller checks cudaGetLastError
   }
-  launch_k(gemm_tc2_kernel<BN, EPI>, dim3(grid), dim3(256), C::SMEM, st, tmA, tmB, D, bias, M, N, K, group_m, qs, tp, md);
+  launch_k(gemm_tc2_kernel<BN, EPI>, dim3(grid), dim3(128 + 32 * C::EPI_WARPS), C::SMEM, st, tmA, tmB, D, bias, M, N, K,
+           group_m, qs, tp, md);
 }
 
 template <int BN, int EPI>
