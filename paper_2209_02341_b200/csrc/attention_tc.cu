@@ -3,7 +3,8 @@
 // attention module still requires the padding area"), writing the packed context
 // rows [T, hk*d] at offsets[b] + s (PAPER.md:373 kernel #2 fused).
 //
-// One CTA = 128 query rows of one (sequence, head); 6 warps:
+// Persistent: each CTA (2 per SM) loops over a heaviest-first list of work items, one item = 128 query
+// rows of one (sequence, head), so the next item's Q / K loads overlap the current item's tail; 6 warps:
 //   warp 0    TMA producer: the Q tile once, then K and V tiles of 64 keys (single-buffered each;
 //             the next K tile streams in while the current tile's softmax and P.V run)
 //   warp 1    MMA issuer (one thread): S = Q K^T  (M=128, N=64, K=d; K-major A and B)
@@ -16,9 +17,13 @@
 // Key tiles stop at min(len, q0 + 128) (causal) or len; query tiles with q0 >= len exit at once.
 // Rows t >= len of the last V tile are zeroed in shared memory before P.V, so pad rows of V that a5
 // never wrote (possibly NaN) cannot reach the output even as 0 * NaN.
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 #include "tc_ptx.cuh"
+
+#define ATTN_MAX_PAIRS 2048
 
 namespace energon {
 
@@ -58,7 +63,8 @@ struct AttnCfg {
   static constexpr int K_BYTES = BN * D * 2;  // DH blocks of [64 keys x 64]
   static constexpr int V_BYTES = BN * D * 2;
   static constexpr int P_BYTES = BM * BN * 2;  // [128 rows x 64 keys], one swizzle block
-  static constexpr int SMEM = Q_BYTES + K_BYTES + V_BYTES + P_BYTES + 1024 + 256;
+  static constexpr int K_STAGES = 2;  // K double-buffered: K_{j+1} streams in while S_j runs
+  static constexpr int SMEM = Q_BYTES + K_STAGES * K_BYTES + V_BYTES + P_BYTES + 1024 + 256;
   static constexpr int TMEM_COLS = (BN + D) <= 128 ? 128 : 256;  // S at col 0, O at col BN
   // S = Q K^T: M=128, N=BN, both K-major
   static constexpr uint32_t IDESC_S = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
@@ -68,11 +74,19 @@ struct AttnCfg {
                                       ((uint32_t)(BM >> 4) << 24);
 };
 
+// Work list of the persistent kernel: (sequence b, query tile qt) pairs with qt * 128 < len_b, sorted
+// heaviest first (most key tiles) on the host; item w = (pair w / hk, head w % hk).
+struct AttnWork {
+  int npairs;
+  uint32_t pair[ATTN_MAX_PAIRS];  // (b << 16) | qt
+};
+
 template <int D>
 __global__ void __launch_bounds__(192, 2)
     attention_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                         const __grid_constant__ CUtensorMap tmV, bf16* __restrict__ Cp, const int* __restrict__ offsets,
-                        bf16* __restrict__ Opad, LensParam lp, int hk, int S, int causal, float scale_log2) {
+                        bf16* __restrict__ Opad, const __grid_constant__ LensParam lp, int hk, int S, int causal,
+                        float scale_log2, const __grid_constant__ AttnWork work) {
   using C = AttnCfg<D>;
   constexpr int BM = C::BM, BN = C::BN, DH = C::DH;
   pdl_trigger();
@@ -80,43 +94,41 @@ __global__ void __launch_bounds__(192, 2)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;
   uint8_t* sK = sQ + C::Q_BYTES;
-  uint8_t* sV = sK + C::K_BYTES;
+  uint8_t* sV = sK + C::K_STAGES * C::K_BYTES;
   uint8_t* sP = sV + C::V_BYTES;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sP + C::P_BYTES);
   uint64_t* q_full = bars + 0;
-  uint64_t* k_full = bars + 1;
+  uint64_t* q_empty = bars + 1;
   uint64_t* v_full = bars + 2;
-  uint64_t* k_empty = bars + 3;
-  uint64_t* v_empty = bars + 4;
-  uint64_t* s_full = bars + 5;
-  uint64_t* s_empty = bars + 6;
-  uint64_t* p_full = bars + 7;
-  uint64_t* o_full = bars + 8;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 9);
+  uint64_t* v_empty = bars + 3;
+  uint64_t* s_full = bars + 4;
+  uint64_t* s_empty = bars + 5;
+  uint64_t* p_full = bars + 6;
+  uint64_t* o_full = bars + 7;
+  uint64_t* o_empty = bars + 8;
+  uint64_t* k_full = bars + 9;    // [K_STAGES]
+  uint64_t* k_empty = bars + 11;  // [K_STAGES]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 13);
 
-  const int qt = gridDim.x - 1 - blockIdx.x;  // longest-running query tiles first
-  const int head = blockIdx.y, b = blockIdx.z;
-  const int len = lp.lens[b];
-  const int q0 = qt * BM;
-  if (q0 >= len) return;  // uniform over the CTA: before any barrier / TMEM use
-  const int kv_end = causal ? min(len, q0 + BM) : len;
-  const int nkv = (kv_end + BN - 1) / BN;
-  const int row_base = (b * hk + head) * S;  // first row of this (sequence, head) in the [B*hk*S, D] view
-
+  const int items = work.npairs * hk;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmQ);
     tma_prefetch_desc(&tmK);
     tma_prefetch_desc(&tmV);
     mbar_init(q_full, 1);
-    mbar_init(k_full, 1);
+    mbar_init(q_empty, 1);
+    for (int i = 0; i < C::K_STAGES; ++i) {
+      mbar_init(&k_full[i], 1);
+      mbar_init(&k_empty[i], 1);
+    }
     mbar_init(v_full, 1);
-    mbar_init(k_empty, 1);
     mbar_init(v_empty, 1);
     mbar_init(s_full, 1);
     mbar_init(s_empty, 4);
     mbar_init(p_full, 4);
     mbar_init(o_full, 1);
+    mbar_init(o_empty, 4);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -130,162 +142,209 @@ __global__ void __launch_bounds__(192, 2)
   const uint32_t tmem_base = *tmem_holder;
   const uint32_t tS = tmem_base, tO = tmem_base + BN;
 
+  // decode item w -> (b, head, q0, number of key tiles)
+  auto decode = [&](int w, int& b, int& head, int& q0, int& nkv, int& len) {
+    const uint32_t pr = work.pair[w / hk];
+    head = w % hk;
+    b = (int)(pr >> 16);
+    q0 = (int)(pr & 0xFFFFu) * BM;
+    len = lp.lens[b];
+    const int kv_end = causal ? min(len, q0 + BM) : len;
+    nkv = (kv_end + BN - 1) / BN;
+  };
+
   if (warp == 0) {
     if (lane == 0) {
+      // ---------------- TMA producer: per item Q once, then K_0, K_1, V_0, K_2, V_1, ... (g = global tile)
       pdl_wait();
-      mbar_expect_tx(q_full, C::Q_BYTES);
+      int g = 0, qi = 0;
+      for (int w = blockIdx.x; w < items; w += gridDim.x, ++qi) {
+        int b, head, q0, nkv, len;
+        decode(w, b, head, q0, nkv, len);
+        const int row_base = (b * hk + head) * S;
+        mbar_wait(q_empty, (qi & 1) ^ 1);  // the previous item's last S has consumed Q
+        mbar_expect_tx(q_full, C::Q_BYTES);
 #pragma unroll
-      for (int h = 0; h < DH; ++h) tma_load_2d(&tmQ, smem_u32(sQ + h * BM * 128), q_full, h * 64, row_base + q0);
-      for (int j = 0; j < nkv; ++j) {
-        const uint32_t par = j & 1;
-        mbar_wait(k_empty, par ^ 1);
-        mbar_expect_tx(k_full, C::K_BYTES);
+        for (int h = 0; h < DH; ++h) tma_load_2d(&tmQ, smem_u32(sQ + h * BM * 128), q_full, h * 64, row_base + q0);
+        auto load_k = [&](int gt, int j) {
+          const int ks = gt & 1;
+          mbar_wait(&k_empty[ks], ((gt >> 1) & 1) ^ 1);
+          mbar_expect_tx(&k_full[ks], C::K_BYTES);
 #pragma unroll
-        for (int h = 0; h < DH; ++h) tma_load_2d(&tmK, smem_u32(sK + h * BN * 128), k_full, h * 64, row_base + j * BN);
-        mbar_wait(v_empty, par ^ 1);
-        mbar_expect_tx(v_full, C::V_BYTES);
+          for (int h = 0; h < DH; ++h)
+            tma_load_2d(&tmK, smem_u32(sK + ks * C::K_BYTES + h * BN * 128), &k_full[ks], h * 64, row_base + j * BN);
+        };
+        load_k(g, 0);
+        for (int j = 0; j < nkv; ++j) {
+          if (j + 1 < nkv) load_k(g + j + 1, j + 1);
+          mbar_wait(v_empty, ((g + j) & 1) ^ 1);
+          mbar_expect_tx(v_full, C::V_BYTES);
 #pragma unroll
-        for (int h = 0; h < DH; ++h) tma_load_2d(&tmV, smem_u32(sV + h * BN * 128), v_full, h * 64, row_base + j * BN);
+          for (int h = 0; h < DH; ++h)
+            tma_load_2d(&tmV, smem_u32(sV + h * BN * 128), v_full, h * 64, row_base + j * BN);
+        }
+        g += nkv;
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      mbar_wait(q_full, 0);
-      for (int j = 0; j < nkv; ++j) {
-        const uint32_t par = j & 1;
-        // ---- S = Q K^T
-        mbar_wait(k_full, par);
-        mbar_wait(s_empty, par ^ 1);
-        tc_fence_after();
+      // ---------------- MMA issuer
+      int g = 0, qi = 0;
+      for (int w = blockIdx.x; w < items; w += gridDim.x, ++qi) {
+        int b, head, q0, nkv, len;
+        decode(w, b, head, q0, nkv, len);
+        mbar_wait(q_full, qi & 1);
+        for (int j = 0; j < nkv; ++j, ++g) {
+          const uint32_t par = g & 1;
+          const int ks = g & 1;
+          // ---- S = Q K^T
+          mbar_wait(&k_full[ks], (g >> 1) & 1);
+          mbar_wait(s_empty, par ^ 1);
+          tc_fence_after();
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t off = (kk >> 2) * 0 + (kk & 3) * 32;
-          const uint64_t a = umma_desc_sw128(smem_u32(sQ + (kk >> 2) * BM * 128 + off));
-          const uint64_t bb = umma_desc_sw128(smem_u32(sK + (kk >> 2) * BN * 128 + off));
-          umma_bf16(tS, a, bb, C::IDESC_S, kk > 0 ? 1u : 0u);
-        }
-        umma_commit(k_empty);
-        umma_commit(s_full);
-        // ---- O += P V
-        mbar_wait(p_full, par);
-        mbar_wait(v_full, par);
-        tc_fence_after();
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint32_t off = (kk & 3) * 32;
+            const uint64_t a = umma_desc_sw128(smem_u32(sQ + (kk >> 2) * BM * 128 + off));
+            const uint64_t bb = umma_desc_sw128(smem_u32(sK + ks * C::K_BYTES + (kk >> 2) * BN * 128 + off));
+            umma_bf16(tS, a, bb, C::IDESC_S, kk > 0 ? 1u : 0u);
+          }
+          umma_commit(&k_empty[ks]);
+          if (j + 1 == nkv) umma_commit(q_empty);
+          umma_commit(s_full);
+          // ---- O += P V
+          mbar_wait(p_full, par);
+          mbar_wait(v_full, par);
+          if (j == 0) mbar_wait(o_empty, (qi & 1) ^ 1);  // the previous item's epilogue has read O
+          tc_fence_after();
 #pragma unroll
-        for (int kk = 0; kk < BN / 16; ++kk) {
-          const uint64_t a = umma_desc_sw128(smem_u32(sP + kk * 32));
-          const uint64_t bb = umma_desc_sw128_mn(smem_u32(sV + kk * 16 * 128), BN * 128);
-          umma_bf16(tO, a, bb, C::IDESC_O, (j > 0 || kk > 0) ? 1u : 0u);
+          for (int kk = 0; kk < BN / 16; ++kk) {
+            const uint64_t a = umma_desc_sw128(smem_u32(sP + kk * 32));
+            const uint64_t bb = umma_desc_sw128_mn(smem_u32(sV + kk * 16 * 128), BN * 128);
+            umma_bf16(tO, a, bb, C::IDESC_O, (j > 0 || kk > 0) ? 1u : 0u);
+          }
+          umma_commit(v_empty);
+          umma_commit(o_full);
         }
-        umma_commit(v_empty);
-        umma_commit(o_full);
       }
     }
   } else {
     // ---------------- softmax warps: thread owns query row r (= TMEM lane r)
-    const int qd = warp & 3;  // TMEM lane quadrant of this warp
+    const int qd = warp & 3;
     const int r = qd * 32 + lane;
-    const int srow = q0 + r;  // position in the sequence
     const uint32_t lane_off = (uint32_t)(qd * 32) << 16;
-    float m_ref = -INFINITY, l = 0.f;
-    for (int j = 0; j < nkv; ++j) {
-      const uint32_t par = j & 1;
-      const int k0 = j * BN;
-      mbar_wait(s_full, par);
-      tc_fence_after();
-      uint32_t sr[2][32];
-      tmem_ld32(tS + lane_off + 0, sr[0]);
-      tmem_ld32(tS + lane_off + 32, sr[1]);
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(s_empty);
-      // mask + tile max (scaled log2 domain)
-      float mt = -INFINITY;
-#pragma unroll
-      for (int c = 0; c < BN; ++c) {
-        const int t = k0 + c;
-        float v = __uint_as_float(sr[c >> 5][c & 31]) * scale_log2;
-        if (t >= len || (causal && t > srow)) v = -INFINITY;
-        sr[c >> 5][c & 31] = __float_as_uint(v);
-        mt = fmaxf(mt, v);
-      }
-      // P_{j-1} . V_{j-1} must be done before P is overwritten or O rescaled
-      if (j > 0) {
-        mbar_wait(o_full, par ^ 1);
+    int g = 0;
+    for (int w = blockIdx.x; w < items; w += gridDim.x) {
+      int b, head, q0, nkv, len;
+      decode(w, b, head, q0, nkv, len);
+      const int srow = q0 + r;
+      float m_ref = -INFINITY, l = 0.f;
+      for (int j = 0; j < nkv; ++j, ++g) {
+        const uint32_t par = g & 1;
+        const int k0 = j * BN;
+        mbar_wait(s_full, par);
         tc_fence_after();
-      }
-      if (mt > m_ref + 8.f) {  // first tile, or the max grew by more than 2^8: move the reference
-        const float alpha = (m_ref == -INFINITY) ? 0.f : ex2f(m_ref - mt);
-        if (j > 0) {
+        uint32_t sr[2][32];
+        tmem_ld32(tS + lane_off + 0, sr[0]);
+        tmem_ld32(tS + lane_off + 32, sr[1]);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(s_empty);
+        // tile max over the raw scores (scale > 0 commutes with max); mask only on tiles that cross
+        // len or the causal diagonal of this warp's rows (warp-uniform test)
+        float mt = -INFINITY;
+        const bool need_mask = (k0 + BN > len) || (causal && k0 + BN - 1 > q0 + qd * 32);
+        if (need_mask) {
+#pragma unroll
+          for (int c = 0; c < BN; ++c) {
+            const int t = k0 + c;
+            float v = __uint_as_float(sr[c >> 5][c & 31]);
+            if (t >= len || (causal && t > srow)) v = -INFINITY;
+            sr[c >> 5][c & 31] = __float_as_uint(v);
+            mt = fmaxf(mt, v);
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < BN; ++c) mt = fmaxf(mt, __uint_as_float(sr[c >> 5][c & 31]));
+        }
+        mt *= scale_log2;
+        if (j > 0) {  // P_{g-1} . V_{g-1} done before P is overwritten or O rescaled
+          mbar_wait(o_full, par ^ 1);
+          tc_fence_after();
+        }
+        if (mt > m_ref + 8.f) {  // first tile, or the max grew by more than 2^8: move the reference
+          const float alpha = (m_ref == -INFINITY) ? 0.f : ex2f(m_ref - mt);
+          if (j > 0) {
 #pragma unroll 1
-          for (int c = 0; c < D; c += 32) {
-            uint32_t o[32];
-            tmem_ld32(tO + lane_off + c, o);
+            for (int c = 0; c < D; c += 32) {
+              uint32_t o[32];
+              tmem_ld32(tO + lane_off + c, o);
 #pragma unroll
-            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
-            tmem_st32(tO + lane_off + c, o);
+              for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+              tmem_st32(tO + lane_off + c, o);
+            }
+          }
+          l *= alpha;
+          m_ref = mt;
+        }
+        const float base = (m_ref == -INFINITY) ? 0.f : m_ref;
+        uint8_t* prow = sP + r * 128;  // 128B swizzle: chunk c of row r at c ^ (r & 7)
+#pragma unroll
+        for (int c8 = 0; c8 < BN / 8; ++c8) {
+          float p[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            p[e] = ex2f(fmaf(__uint_as_float(sr[(c8 * 8 + e) >> 5][(c8 * 8 + e) & 31]), scale_log2, -base));
+            l += p[e];
+          }
+          uint4 pk;
+          pk.x = pack_bf16x2(p[0], p[1]);
+          pk.y = pack_bf16x2(p[2], p[3]);
+          pk.z = pack_bf16x2(p[4], p[5]);
+          pk.w = pack_bf16x2(p[6], p[7]);
+          *reinterpret_cast<uint4*>(prow + ((c8 ^ (r & 7)) << 4)) = pk;
+        }
+        if (k0 + BN > len) {  // zero V rows of keys >= len (pad rows a5 never wrote may hold NaN)
+          mbar_wait(v_full, par);
+          if (r < BN && k0 + r >= len) {
+#pragma unroll
+            for (int h = 0; h < DH; ++h) {
+              uint4* vr = reinterpret_cast<uint4*>(sV + h * BN * 128 + r * 128);
+#pragma unroll
+              for (int c = 0; c < 8; ++c) vr[c] = make_uint4(0, 0, 0, 0);
+            }
           }
         }
-        l *= alpha;
-        m_ref = mt;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(p_full);
       }
-      const float base = (m_ref == -INFINITY) ? 0.f : m_ref;
-      // P row (bf16) -> shared memory, 128B swizzle: 16-byte chunk c of row r at chunk c ^ (r & 7)
-      uint8_t* prow = sP + r * 128;
+      // ---------------- item epilogue: O / l -> packed context row (or padded O row)
+      mbar_wait(o_full, (g - 1) & 1);
+      tc_fence_after();
+      const float inv = 1.f / l;
+      const bool valid = srow < len;
+      bf16* dst = Cp ? Cp + ((int64_t)__ldg(offsets + b) + srow) * (int64_t)(hk * D) + head * D
+                     : Opad + ((int64_t)(b * hk + head) * S + srow) * D;
+#pragma unroll 1
+      for (int c = 0; c < D; c += 32) {
+        uint32_t o[32];
+        tmem_ld32(tO + lane_off + c, o);
+        if (valid) {
 #pragma unroll
-      for (int c8 = 0; c8 < BN / 8; ++c8) {
-        float p[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          p[e] = ex2f(__uint_as_float(sr[(c8 * 8 + e) >> 5][(c8 * 8 + e) & 31]) - base);
-          l += p[e];
-        }
-        uint4 pk;
-        pk.x = pack_bf16x2(p[0], p[1]);
-        pk.y = pack_bf16x2(p[2], p[3]);
-        pk.z = pack_bf16x2(p[4], p[5]);
-        pk.w = pack_bf16x2(p[6], p[7]);
-        *reinterpret_cast<uint4*>(prow + ((c8 ^ (r & 7)) << 4)) = pk;
-      }
-      // zero the V rows of keys >= len in a partial last tile (never-written pad rows may hold NaN)
-      if (k0 + BN > len) {
-        mbar_wait(v_full, par);
-        if (r < BN && k0 + r >= len) {
-#pragma unroll
-          for (int h = 0; h < DH; ++h) {
-            uint4* vr = reinterpret_cast<uint4*>(sV + h * BN * 128 + r * 128);
-#pragma unroll
-            for (int c = 0; c < 8; ++c) vr[c] = make_uint4(0, 0, 0, 0);
+          for (int e = 0; e < 32; e += 8) {
+            uint4 pk;
+            pk.x = pack_bf16x2(__uint_as_float(o[e]) * inv, __uint_as_float(o[e + 1]) * inv);
+            pk.y = pack_bf16x2(__uint_as_float(o[e + 2]) * inv, __uint_as_float(o[e + 3]) * inv);
+            pk.z = pack_bf16x2(__uint_as_float(o[e + 4]) * inv, __uint_as_float(o[e + 5]) * inv);
+            pk.w = pack_bf16x2(__uint_as_float(o[e + 6]) * inv, __uint_as_float(o[e + 7]) * inv);
+            *reinterpret_cast<uint4*>(dst + c + e) = pk;
           }
         }
       }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic-proxy smem writes -> tcgen05.mma
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(p_full);
-    }
-    // ---------------- epilogue: O / l -> packed context row offsets[b] + srow (valid rows only)
-    mbar_wait(o_full, (nkv - 1) & 1);
-    tc_fence_after();
-    const float inv = 1.f / l;
-    const bool valid = srow < len;
-    // packed context row (a7 fused) or, without Cp, the padded O [B, hk, S, D] row
-    bf16* dst = Cp ? Cp + ((int64_t)__ldg(offsets + b) + srow) * (int64_t)(hk * D) + head * D
-                   : Opad + ((int64_t)row_base + srow) * D;
-#pragma unroll 1
-    for (int c = 0; c < D; c += 32) {
-      uint32_t o[32];
-      tmem_ld32(tO + lane_off + c, o);
-      if (valid) {
-#pragma unroll
-        for (int e = 0; e < 32; e += 8) {
-          uint4 pk;
-          pk.x = pack_bf16x2(__uint_as_float(o[e]) * inv, __uint_as_float(o[e + 1]) * inv);
-          pk.y = pack_bf16x2(__uint_as_float(o[e + 2]) * inv, __uint_as_float(o[e + 3]) * inv);
-          pk.z = pack_bf16x2(__uint_as_float(o[e + 4]) * inv, __uint_as_float(o[e + 5]) * inv);
-          pk.w = pack_bf16x2(__uint_as_float(o[e + 6]) * inv, __uint_as_float(o[e + 7]) * inv);
-          *reinterpret_cast<uint4*>(dst + c + e) = pk;
-        }
-      }
+      if (lane == 0) mbar_arrive(o_empty);
     }
   }
   tc_fence_before();
@@ -300,6 +359,23 @@ template <int D>
 static bool launch_tc(const bf16* Q, const bf16* K, const bf16* V, bf16* Cp, const int* offsets, bf16* Opad,
                       const LensParam& lp, int B, int hk, int S, int causal, cudaStream_t st) {
   using C = AttnCfg<D>;
+  // heaviest-first work list of (sequence, query tile) pairs, built from the host copy of the lengths
+  static AttnWork work;  // 8 KB kernel parameter; host-side staging only (copied at launch)
+  int n = 0;
+  auto cost = [&](int b, int qt) {
+    const int len = lp.lens[b];
+    const int kv_end = causal ? std::min(len, (qt + 1) * C::BM) : len;
+    return (kv_end + C::BN - 1) / C::BN;
+  };
+  for (int b = 0; b < B; ++b)
+    for (int qt = 0; qt * C::BM < lp.lens[b]; ++qt) {
+      if (n >= ATTN_MAX_PAIRS) return false;
+      work.pair[n++] = ((uint32_t)b << 16) | (uint32_t)qt;
+    }
+  work.npairs = n;
+  std::stable_sort(work.pair, work.pair + n, [&](uint32_t x, uint32_t y) {
+    return cost((int)(x >> 16), (int)(x & 0xFFFF)) > cost((int)(y >> 16), (int)(y & 0xFFFF));
+  });
   const int rows = B * hk * S;
   CUtensorMap mq, mk, mv;
   if (!make_tmap_kmajor(&mq, Q, rows, D, C::BM) || !make_tmap_kmajor(&mk, K, rows, D, C::BN) ||
@@ -310,10 +386,13 @@ static bool launch_tc(const bf16* Q, const bf16* K, const bf16* V, bf16* Cp, con
     cudaFuncSetAttribute(attention_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     attr = true;
   }
-  dim3 grid((S + C::BM - 1) / C::BM, hk, B);
+  const int items = n * hk;
+  const int slots = 2 * num_sms();  // 2 CTAs per SM (shared memory and 256 TMEM columns each)
+  const int grid = items < slots ? items : slots;
+  if (grid <= 0) return true;
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)D);
-  launch_k(attention_tc_kernel<D>, grid, dim3(192), C::SMEM, st, mq, mk, mv, Cp, offsets, Opad, lp, hk, S, causal,
-           scale_log2);
+  launch_k(attention_tc_kernel<D>, dim3(grid), dim3(192), C::SMEM, st, mq, mk, mv, Cp, offsets, Opad, lp, hk, S,
+           causal, scale_log2, work);
   return true;
 }
 
