@@ -426,3 +426,39 @@ def test_opt_layer_teacher_forced(name, p):
     ref = oracle.layers_padded(cfg, layers, 0, 1, x[b:b + 1, :n].double().numpy(), [n])
     err = max_abs_rel(y, ref, [n])
     assert err <= 2e-2, err
+
+
+# ----------------------------------------------------------------------------- edge cases
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+@pytest.mark.parametrize("case", ["all_len_1", "max_len_1", "one_long_sequence", "max_batch"])
+def test_forward_edge_cases(dtype, case):
+    """Degenerate batches: every sequence of length 1, max_len 1, a single 1024-token sequence
+    (several query tiles of the persistent attention), and the maximum batch of 1024 sequences."""
+    shape = dict(L=2, H=256, h=2, F=1024, V=512, max_seq=1024)
+    if case == "all_len_1":
+        B, S, lens = 7, 32, [1] * 7
+    elif case == "max_len_1":
+        B, S, lens = 5, 1, [1] * 5
+    elif case == "one_long_sequence":
+        B, S, lens = 1, 1024, [1024]
+    else:
+        B, S = 1024, 4
+        lens = synth.random_lengths(B, S, 5)
+    seed = 13
+    tok = synth.tokens(B, S, shape["V"], lens, seed)
+    ctxs = make_engine(shape, seed, dtype, B * S)
+    try:
+        y = run_forward(ctxs, tok, lens, dtype, shape["H"])
+    finally:
+        destroy(ctxs)
+    layers, emb = oracle_model(shape, seed, dtype)
+    cfg = oracle.make_cfg(shape["L"], shape["H"], shape["h"], shape["F"])
+    if case == "one_long_sequence":  # causal prefix (P13) keeps the oracle fast
+        n = 192
+        ref = oracle.forward_drce(cfg, layers, emb, tok[:, :n], [n])
+        assert max_abs_rel(y[:, :n], ref, [n]) <= TOL[dtype]
+    else:
+        ref = oracle.forward_drce(cfg, layers, emb, tok, lens)
+        assert max_abs_rel(y, ref, lens) <= TOL[dtype]
+    for b, n in enumerate(lens):
+        assert not y[b, n:].any()
