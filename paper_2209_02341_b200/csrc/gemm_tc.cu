@@ -338,6 +338,20 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t sr
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+
+// one warp's 32 rows x 32 columns -> bf16 staging buffer, 64-byte swizzle (chunk j of row r at j ^ ((r >> 1) & 3))
+__device__ __forceinline__ void epi_stage(const float (&v)[32], uint8_t* stg, int lane) {
+  const uint32_t base = (uint32_t)__cvta_generic_to_shared(stg) + lane * 64;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const uint32_t a = base + ((j ^ ((lane >> 1) & 3)) << 4);
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(pack_bf16x2(v[8 * j], v[8 * j + 1])),
+                 "r"(pack_bf16x2(v[8 * j + 2], v[8 * j + 3])), "r"(pack_bf16x2(v[8 * j + 4], v[8 * j + 5])),
+                 "r"(pack_bf16x2(v[8 * j + 6], v[8 * j + 7]))
+                 : "memory");
+  }
+}
 
 // Stage one warp's 32 rows x 32 columns (bf16) in shared memory with the 64-byte swizzle the TMA map
 // uses (16-byte chunk j of row r lives at chunk j ^ ((r >> 1) & 3): 4-way instead of 16-way bank
@@ -529,37 +543,68 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       // split unit: this CTA's 128 x BN partial goes to the workspace
       float* part = (split >= 0) ? tp.ws + ((size_t)(tail * tp.splits + split) * 2 + rank) * 128 * BN + (size_t)etid * BN
                                  : nullptr;
+      const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
+      if (TMA_ST && split < 0) {
+        // two 32-column chunks per step: both TMEM loads in flight, one proxy fence and one wait for the
+        // staging buffers per pair; the accumulator is released right after the tile's last TMEM load
 #pragma unroll 1
-      for (int c = c0; c < c0 + CH; ++c) {
-        uint32_t r[32];
-        tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c * 32), r);
-        if (split >= 0) {
+        for (int c = c0; c < c0 + CH; c += 2) {
+          const bool two = c + 1 < c0 + CH;
+          uint32_t r0[32], r1[32];
+          tmem_ld32_nowait(tbase + (uint32_t)(c * 32), r0);
+          if (two) tmem_ld32_nowait(tbase + (uint32_t)((c + 1) * 32), r1);
+          tmem_wait_ld();
+          if (c + 2 >= c0 + CH) {  // last TMEM read of this tile
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(tempty_leader + (uint32_t)(acc * sizeof(uint64_t)));
+          }
+          float v0[32], v1[32];
 #pragma unroll
-          for (int j = 0; j < 32; j += 4)
-            __stcg(reinterpret_cast<float4*>(part + c * 32 + j),
-                   make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]), __uint_as_float(r[j + 2]),
-                               __uint_as_float(r[j + 3])));
-        } else {
-          float v[32];
+          for (int j = 0; j < 32; ++j) {
+            v0[j] = __uint_as_float(r0[j]);
+            v1[j] = __uint_as_float(r1[j]);
+          }
+          epi_math<EPI>(v0, n_blk * BN + c * 32, N, bias);
+          if (two) epi_math<EPI>(v1, n_blk * BN + (c + 1) * 32, N, bias);
+          if (nst > 0) {  // the previous pair's stores have finished reading the staging buffers
+            if (lane == 0) bulk_wait_read0();
+            __syncwarp();
+          }
+          const int rowt = m_blk * 256 + (int)rank * 128 + q * 32;
+          epi_stage(v0, my_stg, lane);
+          if (two) epi_stage(v1, my_stg + 2048, lane);
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&tmD, smem_u32(my_stg), n_blk * BN + c * 32, rowt);
+            if (two) tma_store_2d(&tmD, smem_u32(my_stg + 2048), n_blk * BN + (c + 1) * 32, rowt);
+            bulk_commit();
+          }
+          ++nst;
+        }
+      } else {
+#pragma unroll 1
+        for (int c = c0; c < c0 + CH; ++c) {
+          uint32_t r[32];
+          tmem_ld32(tbase + (uint32_t)(c * 32), r);
+          if (split >= 0) {
 #pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-          if constexpr (TMA_ST) {
-            epi_math<EPI>(v, n_blk * BN + c * 32, N, bias);
-            if (nst >= 2) {  // the store that used this buffer two chunks ago has read it
-              if (lane == 0) bulk_wait_read1();
-              __syncwarp();
-            }
-            epi_tma_store(v, my_stg + (nst & 1) * 2048, lane, &tmD, n_blk * BN + c * 32,
-                          m_blk * 256 + (int)rank * 128 + q * 32);
-            ++nst;
+            for (int j = 0; j < 32; j += 4)
+              __stcg(reinterpret_cast<float4*>(part + c * 32 + j),
+                     make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]), __uint_as_float(r[j + 2]),
+                                 __uint_as_float(r[j + 3])));
           } else {
+            float v[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
             epi_store<EPI>(v, row, n_blk * BN + c * 32, M, N, D, bias, qs);
           }
         }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(tempty_leader + (uint32_t)(acc * sizeof(uint64_t)));
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(tempty_leader + (uint32_t)(acc * sizeof(uint64_t)));
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
