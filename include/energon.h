@@ -107,6 +107,7 @@ typedef struct {
   int64_t last_rows;        /* rows the linears ran on in the last forward (T, or B*S with drce=0) */
   int64_t weight_bytes;     /* device bytes held for this rank's weights */
   int64_t workspace_bytes;  /* device bytes held for activations */
+  int64_t prefetch_bytes;   /* PMEP: bytes fetched from the memory pool, cumulative */
 } energon_stats;
 
 /*
@@ -133,6 +134,23 @@ typedef struct {
 } energon_shard;
 
 typedef struct energon_ctx energon_ctx;
+
+/*
+ * Peer memory pooling (PMEP, sec 4.4, fig:offload / fig:multistream).
+ * energon_pmep_plan (host only): the off-device layers when `resident` of `num_layers` layers stay on
+ *   the computing GPU, "distributed evenly among those to be held on device":
+ *   layer floor((g+1) L / m) - 1 for g = 0..m-1, m = L - resident; (24, 20) -> {5, 11, 17, 23}
+ *   (PAPER.md:601-602).  out_layers holds m ints, ascending.
+ * energon_offload_layers: move the listed (loaded) layers' weight matrices into the pool -- pool 0 =
+ *   pinned host memory, 1 = the memory of CUDA device `peer_device` (NVLink peer) -- and free them on
+ *   the computing GPU.  During a forward each off-device layer is copied into one of `slots` staging
+ *   buffers on a separate copy stream, issued as soon as the slot's previous layer finished computing
+ *   ("prefetch the next off-device layer immediately ..."); compute waits on an event.
+ *   Results are bit-identical to the all-resident run.  Call after every layer is loaded.
+ */
+ENERGON_API energon_status energon_pmep_plan(int32_t num_layers, int32_t resident, int32_t* out_layers);
+ENERGON_API energon_status energon_offload_layers(energon_ctx* ctx, const int32_t* layers, int32_t n, int32_t slots,
+                                                  int32_t pool, int32_t peer_device);
 
 /* Host-only: the shard of cfg->tp_rank (validates cfg like energon_init; touches no device). */
 ENERGON_API energon_status energon_shard_plan(const energon_config* cfg, energon_shard* out);

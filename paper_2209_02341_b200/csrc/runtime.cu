@@ -54,6 +54,19 @@ struct LayerDev {
   bool loaded = false;
 };
 
+// PMEP state of one context (energon_offload_layers)
+struct Pmep {
+  std::vector<int> layers;       // off-device layer ids, ascending
+  std::vector<int> index;        // layer -> position in `layers`, or -1 (resident)
+  std::vector<void*> pool;       // per off-device layer: [wqkv | wo | w1 | w2] in pinned host or peer memory
+  int pool_kind = 0, peer = -1;
+  size_t bytes = 0;              // matrix bytes of one layer
+  std::vector<LayerDev> slots;   // staging: matrices + tensor maps of one layer each
+  std::vector<void*> slot_buf;
+  std::vector<cudaEvent_t> fetched, freed;
+  cudaStream_t copy = nullptr;
+};
+
 }  // namespace
 
 struct energon_ctx {
@@ -79,6 +92,7 @@ struct energon_ctx {
   CUtensorMap tmA_A, tmA_Ctx, tmA_G;
   CUtensorMap tmD_P, tmD_G;  // TMA-store output maps of the out/down (P) and up (G) GEMMs
   int tm_rows = -1;
+  Pmep pm;
   int* err_host = nullptr;  // mapped pinned flag written by the embed kernel (bad token id)
   int* err_dev = nullptr;
   cudaStream_t load_stream = nullptr;
@@ -209,6 +223,18 @@ void release(energon_ctx* c) {
   cudaDeviceSynchronize();
   for (void* p : c->allocs) cudaFree(p);
   c->allocs.clear();
+  for (void* p : c->pm.pool) {
+    if (c->pm.pool_kind == 0) cudaFreeHost(p);
+    else {
+      cudaSetDevice(c->pm.peer);
+      cudaFree(p);
+      cudaSetDevice(c->cfg.device);
+    }
+  }
+  for (void* p : c->pm.slot_buf) cudaFree(p);
+  for (cudaEvent_t e : c->pm.fetched) cudaEventDestroy(e);
+  for (cudaEvent_t e : c->pm.freed) cudaEventDestroy(e);
+  if (c->pm.copy) cudaStreamDestroy(c->pm.copy);
   if (c->err_host) cudaFreeHost(c->err_host);
   if (c->load_stream) cudaStreamDestroy(c->load_stream);
   for (cudaEvent_t e : c->pool) cudaEventDestroy(e);
@@ -420,6 +446,22 @@ void gemm(energon_ctx* c, const CUtensorMap& tmA, const CUtensorMap* tmB, const 
   c->stats.kernel_launches++;
 }
 
+// ----------------------------------------------------------------------------- PMEP prefetch
+// Copy off-device layer `layer` (the j-th off-device layer of this forward) into staging slot
+// j % slots on the copy stream, after the slot's previous occupant finished computing.
+void pmep_fetch(energon_ctx* c, int j, int layer) {
+  Pmep& pm = c->pm;
+  const int s = j % (int)pm.slots.size();
+  const int i = pm.index[layer];
+  cudaStreamWaitEvent(pm.copy, pm.freed[s], 0);
+  if (pm.pool_kind == 0)
+    cudaMemcpyAsync(pm.slot_buf[s], pm.pool[i], pm.bytes, cudaMemcpyHostToDevice, pm.copy);
+  else
+    cudaMemcpyPeerAsync(pm.slot_buf[s], c->cfg.device, pm.pool[i], pm.peer, pm.bytes, pm.copy);
+  cudaEventRecord(pm.fetched[s], pm.copy);
+  c->stats.prefetch_bytes += (int64_t)pm.bytes;
+}
+
 template <typename Act>
 energon_status forward_t(energon_ctx** cs, int n, const Call& a, int64_t T) {
   cudaStream_t st = a.st;
@@ -439,6 +481,23 @@ energon_status forward_t(energon_ctx** cs, int n, const Call& a, int64_t T) {
   const int rpr = sp ? (rows + c0->k - 1) / c0->k : rows;
   auto shard0 = [&](const energon_ctx* c) { return sp ? std::min(rows, c->r * rpr) : 0; };
   auto shardn = [&](const energon_ctx* c) { return sp ? std::max(0, std::min(rows, (c->r + 1) * rpr) - c->r * rpr) : rows; };
+  // PMEP: the off-device layers of this forward in execution order, per context
+  std::vector<std::vector<int>> off_order(n);
+  std::vector<int> off_next(n, 0), off_slot(n, -1);
+  for (int i = 0; i < n; ++i) {
+    energon_ctx* c = cs[i];
+    if (c->pm.layers.empty()) continue;
+    for (int l : c->pm.layers)
+      if (l >= a.l0 && l < a.l1) off_order[i].push_back(l);
+    const int ns = (int)c->pm.slots.size();
+    for (int j = 0; j < (int)off_order[i].size() && j < ns; ++j) pmep_fetch(c, j, off_order[i][j]);
+  }
+  // the weights a layer computes with: its own, or the staging slot its off-device copy lands in
+  auto weights = [&](int i, int l) -> const LayerDev& {
+    energon_ctx* c = cs[i];
+    if (c->pm.layers.empty() || c->pm.index[l] < 0) return c->layers[l];
+    return c->pm.slots[off_slot[i]];
+  };
   LensParam lp;
   double allowed = 0.0;  // sum over sequences of visible (query, key) pairs
   for (int b = 0; b < a.B; ++b) {
@@ -490,15 +549,21 @@ energon_status forward_t(energon_ctx** cs, int n, const Call& a, int64_t T) {
     // ---- attention module: column-parallel QKV, local heads, row-parallel out-proj
     for (int i = 0; i < n; ++i) {
       energon_ctx* c = cs[i];
-      const LayerDev& L = c->layers[l];
+      if (!c->pm.layers.empty() && c->pm.index[l] >= 0) {  // off-device layer: wait for its prefetch
+        const int j = off_next[i]++;
+        off_slot[i] = j % (int)c->pm.slots.size();
+        cudaStreamWaitEvent(st, c->pm.fetched[off_slot[i]], 0);
+      }
+      const LayerDev& W = weights(i, l);  // matrices + tensor maps (resident or staged)
+      const LayerDev& L = c->layers[l];   // biases, LN vectors (always resident)
       const int* pidx = drce ? c->pack_idx : nullptr;
       if (fuse_a5) {
         // a4 + a5: the QKV epilogue scatters straight into the padded per-head Q, K, V
         QkvScatter qs{pidx, reinterpret_cast<bf16*>(c->Q), reinterpret_cast<bf16*>(c->K),
                       reinterpret_cast<bf16*>(c->Vb), a.S, c->hk, c->d};
-        gemm<Act>(c, c->tmA_A, L.tm_qkv, c->A, L.wqkv, L.bqkv, nullptr, rows, 3 * c->Hk, c->H, EPI_BIAS_QKV, st, &qs);
+        gemm<Act>(c, c->tmA_A, W.tm_qkv, c->A, W.wqkv, L.bqkv, nullptr, rows, 3 * c->Hk, c->H, EPI_BIAS_QKV, st, &qs);
       } else {
-        gemm<Act>(c, c->tmA_A, L.tm_qkv, c->A, L.wqkv, L.bqkv, c->QKV, rows, 3 * c->Hk, c->H, EPI_BIAS, st);
+        gemm<Act>(c, c->tmA_A, W.tm_qkv, c->A, W.wqkv, L.bqkv, c->QKV, rows, 3 * c->Hk, c->H, EPI_BIAS, st);
         Prof p(c, st, P_MEM, 2.0 * rows * 3 * Hk * act);
         launch_unpack_qkv<Act>(reinterpret_cast<const Act*>(c->QKV), pidx, rows, a.S, c->hk, c->d,
                                reinterpret_cast<Act*>(c->Q), reinterpret_cast<Act*>(c->K), reinterpret_cast<Act*>(c->Vb),
@@ -526,7 +591,7 @@ energon_status forward_t(energon_ctx** cs, int n, const Call& a, int64_t T) {
         }
         c->stats.kernel_launches += 2;
       }
-      gemm<Act>(c, c->tmA_Ctx, L.tm_o, c->Ctx, L.wo, nullptr, c->P, rows, c->H, c->Hk, EPI_NONE, st, nullptr, &c->tmD_P);
+      gemm<Act>(c, c->tmA_Ctx, W.tm_o, c->Ctx, W.wo, nullptr, c->P, rows, c->H, c->Hk, EPI_NONE, st, nullptr, &c->tmD_P);
     }
     energon_status s = tp_reduce<Act>(cs, n, rows, rpr, sp, st);
     if (s) return s;
@@ -545,9 +610,17 @@ energon_status forward_t(energon_ctx** cs, int n, const Call& a, int64_t T) {
     // ---- MLP module: column-parallel W1 (+GeLU), row-parallel W2
     for (int i = 0; i < n; ++i) {
       energon_ctx* c = cs[i];
+      const LayerDev& W = weights(i, l);
       const LayerDev& L = c->layers[l];
-      gemm<Act>(c, c->tmA_A, L.tm_1, c->A, L.w1, L.b1, c->G, rows, c->Fk, c->H, EPI_BIAS_GELU, st, nullptr, &c->tmD_G);
-      gemm<Act>(c, c->tmA_G, L.tm_2, c->G, L.w2, nullptr, c->P, rows, c->H, c->Fk, EPI_NONE, st, nullptr, &c->tmD_P);
+      gemm<Act>(c, c->tmA_A, W.tm_1, c->A, W.w1, L.b1, c->G, rows, c->Fk, c->H, EPI_BIAS_GELU, st, nullptr, &c->tmD_G);
+      gemm<Act>(c, c->tmA_G, W.tm_2, c->G, W.w2, nullptr, c->P, rows, c->H, c->Fk, EPI_NONE, st, nullptr, &c->tmD_P);
+      if (!c->pm.layers.empty() && c->pm.index[l] >= 0) {
+        // the slot is free once these GEMMs ran: record it and prefetch the off-device layer `slots` ahead
+        const int ns = (int)c->pm.slots.size();
+        cudaEventRecord(c->pm.freed[off_slot[i]], st);
+        const int jn = off_next[i] - 1 + ns;
+        if (jn < (int)off_order[i].size()) pmep_fetch(c, jn, off_order[i][jn]);
+      }
     }
     s = tp_reduce<Act>(cs, n, rows, rpr, sp, st);
     if (s) return s;
@@ -628,6 +701,105 @@ const char* energon_status_string(energon_status s) {
 }
 
 const char* energon_last_error(const energon_ctx* ctx) { return ctx ? ctx->err.c_str() : g_last_error.c_str(); }
+
+energon_status energon_pmep_plan(int32_t L, int32_t resident, int32_t* out) {
+  if (L < 1 || resident < 1 || resident > L) return fail(nullptr, ENERGON_ERR_ARG, "need 1 <= resident <= num_layers");
+  const int m = L - resident;
+  if (m > 0 && !out) return fail(nullptr, ENERGON_ERR_ARG, "out_layers is NULL");
+  // off-device layers "distributed evenly among those to be held on device"
+  for (int g = 0; g < m; ++g) out[g] = (int32_t)(((int64_t)(g + 1) * L) / m) - 1;
+  return ENERGON_OK;
+}
+
+energon_status energon_offload_layers(energon_ctx* c, const int32_t* layers, int32_t n, int32_t slots, int32_t pool,
+                                      int32_t peer) {
+  if (!c) return fail(nullptr, ENERGON_ERR_ARG, "ctx is NULL");
+  if (n < 0 || (n > 0 && !layers) || slots < 1 || (pool != 0 && pool != 1))
+    return fail(c, ENERGON_ERR_ARG, "bad offload arguments");
+  if (!c->pm.layers.empty()) return fail(c, ENERGON_ERR_ARG, "layers are already offloaded");
+  const int Lc = c->cfg.num_layers;
+  for (int i = 0; i < n; ++i) {
+    if (layers[i] < 0 || layers[i] >= Lc || (i > 0 && layers[i] <= layers[i - 1]))
+      return fail(c, ENERGON_ERR_ARG, "offloaded layers must be ascending ids in [0, num_layers)");
+    if (!c->layers[layers[i]].loaded) return fail(c, ENERGON_ERR_NOT_LOADED, "offload a layer after loading it");
+  }
+  if (n == 0) return ENERGON_OK;
+  CU(c, cudaSetDevice(c->cfg.device));
+  CU(c, cudaDeviceSynchronize());
+  Pmep& pm = c->pm;
+  const size_t a = c->act, H = c->H, Hk = c->Hk, Fk = c->Fk;
+  const size_t sz[4] = {a * 3 * Hk * H, a * H * Hk, a * Fk * H, a * H * Fk};
+  pm.bytes = sz[0] + sz[1] + sz[2] + sz[3];
+  pm.pool_kind = pool;
+  pm.peer = peer;
+  if (pool == 1) {
+    int ok = 0;
+    CU(c, cudaDeviceCanAccessPeer(&ok, c->cfg.device, peer));
+    if (!ok) return fail(c, ENERGON_ERR_ARG, "peer_device is not peer-accessible from this device");
+    cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+    if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) return cuda_fail(c, e, "cudaDeviceEnablePeerAccess");
+    cudaGetLastError();
+  }
+  pm.index.assign(Lc, -1);
+  for (int i = 0; i < n; ++i) {
+    LayerDev& L = c->layers[layers[i]];
+    void* buf = nullptr;
+    if (pool == 0) {
+      CU(c, cudaHostAlloc(&buf, pm.bytes, cudaHostAllocDefault));
+    } else {
+      CU(c, cudaSetDevice(peer));
+      cudaError_t e = cudaMalloc(&buf, pm.bytes);
+      cudaSetDevice(c->cfg.device);
+      if (e != cudaSuccess) return cuda_fail(c, e, "cudaMalloc on the peer device");
+    }
+    pm.pool.push_back(buf);
+    void* src[4] = {L.wqkv, L.wo, L.w1, L.w2};
+    size_t off = 0;
+    for (int k = 0; k < 4; ++k) {
+      if (pool == 0) CU(c, cudaMemcpy((char*)buf + off, src[k], sz[k], cudaMemcpyDeviceToHost));
+      else CU(c, cudaMemcpyPeer((char*)buf + off, peer, src[k], c->cfg.device, sz[k]));
+      off += sz[k];
+      for (size_t q = 0; q < c->allocs.size(); ++q)
+        if (c->allocs[q] == src[k]) {
+          c->allocs.erase(c->allocs.begin() + q);
+          break;
+        }
+      CU(c, cudaFree(src[k]));
+      c->stats.weight_bytes -= (int64_t)sz[k];
+    }
+    L.wqkv = L.wo = L.w1 = L.w2 = nullptr;
+    pm.layers.push_back(layers[i]);
+    pm.index[layers[i]] = i;
+  }
+  const int ns = std::min<int>(slots, n);
+  pm.slots.resize(ns);
+  CU(c, cudaStreamCreateWithFlags(&pm.copy, cudaStreamNonBlocking));
+  for (int s = 0; s < ns; ++s) {
+    void* buf = nullptr;
+    CU(c, cudaMalloc(&buf, pm.bytes));
+    pm.slot_buf.push_back(buf);
+    LayerDev& S = pm.slots[s];
+    S.wqkv = buf;
+    S.wo = (char*)buf + sz[0];
+    S.w1 = (char*)buf + sz[0] + sz[1];
+    S.w2 = (char*)buf + sz[0] + sz[1] + sz[2];
+    if (c->bf16)
+      for (int i = 0; i < 4; ++i)
+        if (!make_tmap_kmajor(&S.tm_qkv[i], S.wqkv, 3 * c->Hk, c->H, kBoxes[i]) ||
+            !make_tmap_kmajor(&S.tm_o[i], S.wo, c->H, c->Hk, kBoxes[i]) ||
+            !make_tmap_kmajor(&S.tm_1[i], S.w1, c->Fk, c->H, kBoxes[i]) ||
+            !make_tmap_kmajor(&S.tm_2[i], S.w2, c->H, c->Fk, kBoxes[i]))
+          return fail(c, ENERGON_ERR_CUDA, "cuTensorMapEncodeTiled failed for a staging slot");
+    cudaEvent_t ef, er;
+    CU(c, cudaEventCreateWithFlags(&ef, cudaEventDisableTiming));
+    CU(c, cudaEventCreateWithFlags(&er, cudaEventDisableTiming));
+    pm.fetched.push_back(ef);
+    pm.freed.push_back(er);
+    CU(c, cudaEventRecord(er, pm.copy));  // slots start free
+  }
+  CU(c, cudaDeviceSynchronize());
+  return ENERGON_OK;
+}
 
 energon_status energon_shard_plan(const energon_config* cfg, energon_shard* out) {
   if (!out) return fail(nullptr, ENERGON_ERR_ARG, "out is NULL");
@@ -751,6 +923,7 @@ energon_status energon_load_layer_weights(energon_ctx* c, int32_t layer, const e
                                           int32_t on_dev, int32_t layout) {
   if (!c || !w) return fail(c, ENERGON_ERR_ARG, "NULL argument");
   if (layer < 0 || layer >= c->cfg.num_layers) return fail(c, ENERGON_ERR_ARG, "layer index out of range");
+  if (!c->pm.index.empty() && c->pm.index[layer] >= 0) return fail(c, ENERGON_ERR_ARG, "layer is offloaded (PMEP)");
   if (sd < 0 || sd > 2) return fail(c, ENERGON_ERR_ARG, "src_dtype must be F32, BF16 or F64");
   if (layout != ENERGON_FULL && layout != ENERGON_RANK_SHARD) return fail(c, ENERGON_ERR_ARG, "bad src_layout");
   const void* ptrs[16] = {w->wq, w->wk, w->wv, w->wo, w->bq, w->bk, w->bv, w->bo,

@@ -29,7 +29,7 @@ EXPORTS = ("energon_get_unique_id", "energon_init", "energon_init_local_group", 
            "energon_load_layer_weights", "energon_forward", "energon_forward_group", "energon_forward_hidden",
            "energon_sync", "energon_get_stats", "energon_last_error", "energon_status_string", "energon_destroy",
            "energon_index_maps", "energon_gemm", "energon_attention", "energon_set_profiling", "energon_get_profile",
-           "energon_shard_plan", "energon_set_option")
+           "energon_shard_plan", "energon_set_option", "energon_pmep_plan", "energon_offload_layers")
 
 
 class EnergonError(RuntimeError):
@@ -54,7 +54,7 @@ class Shard(ctypes.Structure):
 
 class Stats(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int64) for n in ("forwards", "allreduce_calls", "kernel_launches", "last_tokens",
-                                              "last_rows", "weight_bytes", "workspace_bytes")]
+                                              "last_rows", "weight_bytes", "workspace_bytes", "prefetch_bytes")]
 
 
 class Profile(ctypes.Structure):
@@ -98,6 +98,8 @@ def load_library(path: str = SO_PATH):
     L.energon_shard_plan.argtypes = [ctypes.POINTER(Config), ctypes.POINTER(Shard)]
     L.energon_set_profiling.argtypes = [P, I32]
     L.energon_set_option.argtypes = [P, I32, I32]
+    L.energon_pmep_plan.argtypes = [I32, I32, ctypes.POINTER(ctypes.c_int32)]
+    L.energon_offload_layers.argtypes = [P, ctypes.POINTER(ctypes.c_int32), I32, I32, I32, I32]
     L.energon_get_profile.argtypes = [P, ctypes.POINTER(Profile)]
     for name in EXPORTS:
         fn = getattr(L, name)
@@ -210,6 +212,18 @@ def energon_get_stats(ctx) -> dict:
     s = Stats()
     _check(load_library().energon_get_stats(ctx, ctypes.byref(s)), ctx)
     return {n: getattr(s, n) for n, _ in Stats._fields_}
+
+
+def energon_pmep_plan(num_layers: int, resident: int) -> list:
+    m = num_layers - resident
+    out = (ctypes.c_int32 * max(m, 1))()
+    _check(load_library().energon_pmep_plan(num_layers, resident, out))
+    return [out[i] for i in range(m)]
+
+
+def energon_offload_layers(ctx, layers, slots: int = 1, pool: int = 0, peer_device: int = -1):
+    arr = (ctypes.c_int32 * max(len(layers), 1))(*layers)
+    _check(load_library().energon_offload_layers(ctx, arr, len(layers), slots, pool, peer_device), ctx)
 
 
 def energon_set_option(ctx, option: int, value: int):

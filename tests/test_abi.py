@@ -69,3 +69,29 @@ def test_index_maps_validates_lengths_on_host(lib):
     assert lib.energon_index_maps(lens, 2, 4, dummy, dummy, dummy, dummy, None) == -4
     lens = (ctypes.c_int32 * 2)(3, 5)
     assert lib.energon_index_maps(lens, 2, 4, dummy, dummy, dummy, dummy, None) == -4
+
+
+def test_pmep_plan_paper_example(lib):
+    """24 layers, 20 resident -> layers 5, 11, 17, 23 are offloaded."""
+    import json
+    g = json.load(open(os.path.join(ROOT, "tests", "golden", "spec_examples.json")))["pmep_placement"]
+    assert energon.energon_pmep_plan(g["num_layers"], g["resident"]) == g["offloaded"]
+
+
+@pytest.mark.parametrize("L,resident", [(24, 20), (30, 20), (40, 20), (40, 36), (12, 11), (7, 1), (5, 5)])
+def test_pmep_plan_is_even(lib, L, resident):
+    """'distributed evenly among those to be held on device': m ascending ids ending at
+    L-1, consecutive gaps differ by at most one layer."""
+    out = energon.energon_pmep_plan(L, resident)
+    m = L - resident
+    assert len(out) == m and out == sorted(set(out)) and all(0 <= x < L for x in out)
+    if m:
+        assert out[-1] == L - 1
+        gaps = [b - a for a, b in zip([-1] + out[:-1], out)]
+        assert max(gaps) - min(gaps) <= 1
+
+
+def test_pmep_plan_rejects_bad_arguments(lib):
+    n = (ctypes.c_int32 * 4)()
+    assert lib.energon_pmep_plan(4, 0, n) == -1
+    assert lib.energon_pmep_plan(4, 5, n) == -1

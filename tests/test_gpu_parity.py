@@ -462,3 +462,34 @@ def test_forward_edge_cases(dtype, case):
         assert max_abs_rel(y, ref, lens) <= TOL[dtype]
     for b, n in enumerate(lens):
         assert not y[b, n:].any()
+
+
+# ----------------------------------------------------------------------------- PMEP (next row N1)
+@pytest.mark.parametrize("slots", [1, 2])
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def test_pmep_offload_bitexact(slots, dtype):
+    """Peer memory pooling: off-device layers prefetched from pinned host memory
+    into staging slots on a copy stream give bit-identical output to the all-resident run, and the
+    fetched bytes match the placement."""
+    shape = dict(L=6, H=256, h=4, F=1024, V=500, max_seq=64)
+    B, S, seed = 5, 48, 21
+    lens = synth.random_lengths(B, S, seed)
+    tok = synth.tokens(B, S, shape["V"], lens, seed)
+    ctxs = make_engine(shape, seed, dtype, B * S)
+    try:
+        ref = run_forward(ctxs, tok, lens, dtype, shape["H"])
+    finally:
+        destroy(ctxs)
+    plan = E().energon_pmep_plan(shape["L"], 3)  # [1, 3, 5]
+    for layers in (plan, [0, 2, 4, 5]):
+        ctxs = make_engine(shape, seed, dtype, B * S)
+        try:
+            E().energon_offload_layers(ctxs[0], layers, slots=slots, pool=0)
+            y = run_forward(ctxs, tok, lens, dtype, shape["H"])
+            y2 = run_forward(ctxs, tok, lens, dtype, shape["H"])  # slots reused across forwards
+            st = E().energon_get_stats(ctxs[0])
+        finally:
+            destroy(ctxs)
+        assert np.array_equal(y, ref) and np.array_equal(y2, ref)
+        per_layer = (3 * 256 * 256 + 256 * 256 + 1024 * 256 * 2) * (2 if dtype == "bf16" else 4)
+        assert st["prefetch_bytes"] == 2 * len(layers) * per_layer
