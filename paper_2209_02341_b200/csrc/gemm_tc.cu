@@ -252,6 +252,27 @@ __device__ __forceinline__ void tma_load_2d_2sm(const CUtensorMap* map, uint32_t
       "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_leader), "r"(x), "r"(y)
       : "memory");
 }
+// same load with an L2 eviction-priority hint (createpolicy): weights are streamed once (evict_first),
+// activations are re-read by every N tile (evict_last)
+__device__ __forceinline__ void tma_load_2d_2sm_hint(const CUtensorMap* map, uint32_t dst, uint32_t bar_leader, int x,
+                                                     int y, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], "
+      "[%1, {%3, %4}], [%2], %5;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_leader), "r"(x), "r"(y), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
 __device__ __forceinline__ void umma_bf16_2sm(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
   asm volatile(
       "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
@@ -415,7 +436,7 @@ template <int BN, int EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     bf16* __restrict__ D, const float* __restrict__ bias, int M, int N, int K, int group_m,
-                    const QkvScatter qs, const TailPlan tp, const __grid_constant__ CUtensorMap tmD) {
+                    const QkvScatter qs, const TailPlan tp, const __grid_constant__ CUtensorMap tmD, int l2_hints) {
   pdl_trigger();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -467,6 +488,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
   if (warp == 0) {
     if (lane == 0) {
       pdl_wait();  // inputs of this GEMM are written by the previous kernel
+      const uint64_t pol_a = policy_evict_last(), pol_b = policy_evict_first();
       int stage = 0;
       uint32_t phase = 0;
       for (int u = cid; u < num_units; u += ncl) {
@@ -478,8 +500,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
           mbar_wait(&empty[stage], phase ^ 1);
           const uint32_t fb = smem_u32(&full[stage]) & PEER_MASK;
           if (leader) mbar_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
-          tma_load_2d_2sm(&tmA, smem_u32(sA + stage * C::A_BYTES), fb, kb * TC_BK, m_blk * 256 + (int)rank * 128);
-          tma_load_2d_2sm(&tmB, smem_u32(sB + stage * C::B_BYTES), fb, kb * TC_BK, n_blk * BN + (int)rank * (BN / 2));
+          if (l2_hints) {
+            tma_load_2d_2sm_hint(&tmA, smem_u32(sA + stage * C::A_BYTES), fb, kb * TC_BK, m_blk * 256 + (int)rank * 128,
+                                 pol_a);
+            tma_load_2d_2sm_hint(&tmB, smem_u32(sB + stage * C::B_BYTES), fb, kb * TC_BK,
+                                 n_blk * BN + (int)rank * (BN / 2), pol_b);
+          } else {
+            tma_load_2d_2sm(&tmA, smem_u32(sA + stage * C::A_BYTES), fb, kb * TC_BK, m_blk * 256 + (int)rank * 128);
+            tma_load_2d_2sm(&tmB, smem_u32(sB + stage * C::B_BYTES), fb, kb * TC_BK, n_blk * BN + (int)rank * (BN / 2));
+          }
           if (++stage == C::STAGES) {
             stage = 0;
             phase ^= 1;
@@ -786,8 +815,15 @@ static void launch_pair_epi(const CUtensorMap& tmA, const CUtensorMap& tmB, cons
     memset(&md, 0, sizeof(md));
     if (EPI != EPI_BIAS_QKV && !make_tmap_store(&md, D, M, N)) return;  // caller checks cudaGetLastError
   }
+  static int hints = -1;
+  if (hints < 0) {
+    // measured: evict_first(W) / evict_last(A) hints raise DRAM traffic (the 168 MB MLP-down panel
+    // thrashes) and cost ~2% of the step, so they are off unless ENERGON_L2_HINTS=1
+    const char* e = getenv("ENERGON_L2_HINTS");
+    hints = (e && e[0] == '1') ? 1 : 0;
+  }
   launch_k(gemm_tc2_kernel<BN, EPI>, dim3(grid), dim3(128 + 32 * C::EPI_WARPS), C::SMEM, st, tmA, tmB, D, bias, M, N, K,
-           group_m, qs, tp, md);
+           group_m, qs, tp, md, hints);
 }
 
 template <int BN, int EPI>
