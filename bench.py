@@ -47,6 +47,7 @@ def parse():
     ap.add_argument("--layers", type=int, default=None, help="override the layer count (debug only)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-ab", action="store_true", help="skip the DRCE-off (padded) A/B")
+    ap.add_argument("--graph", type=int, default=1, help="replay each forward as a CUDA graph (ENERGON_OPT_GRAPH)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-tokens", type=int, default=192)
     ap.add_argument("--local-tp", type=int, default=0,
@@ -180,7 +181,7 @@ def workload_config(args, shape, bcfg, lens, world):
                         f"max_len={S}, padding {1 - T / (B * S):.3f} (T={T}), bf16, TP={world}",
             "layers": shape["L"], "hidden": shape["H"], "heads": shape["h"], "batch": B, "max_len": S,
             "padding_ratio": round(1 - T / (B * S), 4), "valid_tokens_per_step": T, "tp": world,
-            "parallelism": f"tp{world}", "drce": bool(args.drce),
+            "parallelism": f"tp{world}", "drce": bool(args.drce), "cuda_graph": bool(getattr(args, "graph", 0)),
             "l2": "no flush: per-step working set (weights) > 126 MB L2"}
 
 
@@ -273,6 +274,7 @@ def energon_arm(args, world, rank, local):
         del w
     torch.cuda.synchronize()
     torch.cuda.empty_cache()
+    eng.set_option(energon.OPT_GRAPH, args.graph)
 
     stream = torch.cuda.current_stream()
     tok = torch.from_numpy(tok_np).cuda()

@@ -215,11 +215,14 @@ ENERGON_API energon_status energon_get_stats(const energon_ctx* ctx, energon_sta
  * Runtime options (take effect at the next forward; host-only, no device work):
  *   ENERGON_OPT_DRCE   1 = packed linears (the method), 0 = padded A/B ("pure EnergonAI",
  *                      PAPER.md:567-571); the workspace is sized for max_tokens padded rows either way.
+ *   ENERGON_OPT_GRAPH  1 = capture each distinct forward (shapes, lengths, buffers) into a CUDA graph
+ *                      on a private stream and replay it on the caller's stream (LRU cache of 8);
+ *                      ignored while profiling or with off-device (PMEP) layers.  Default 0.
  *   ENERGON_OPT_TP_SP  k > 1 only: 1 (default) = sequence-parallel schedule (reduce-scatter, bias +
  *                      residual + LN on this rank's 1/k of the rows, all-gather), 0 = allreduce and
  *                      the row-wise kernels replicated on every rank.
  */
-enum { ENERGON_OPT_DRCE = 1, ENERGON_OPT_TP_SP = 2 };
+enum { ENERGON_OPT_DRCE = 1, ENERGON_OPT_TP_SP = 2, ENERGON_OPT_GRAPH = 3 };
 ENERGON_API energon_status energon_set_option(energon_ctx* ctx, int32_t option, int32_t value);
 
 /* Enable (1) / disable (0) per-launch CUDA-event timing; enabling resets the accumulators. */

@@ -78,6 +78,17 @@ struct energon_ctx {
   bool local_group = false;
   bool fuse = true;  // fused a5 / a7 (ENERGON_NO_FUSE=1 disables, for A/B and tests)
   bool sp = true;    // k > 1: sequence-parallel schedule (reduce-scatter / LN on own rows / all-gather)
+  // CUDA-graph cache (ENERGON_OPT_GRAPH): whole forwards captured on cap_stream, replayed on the caller's
+  struct GraphEntry {
+    std::vector<int64_t> key;
+    cudaGraphExec_t exec = nullptr;
+    std::vector<energon_stats> delta;  // per context of the group: stats one forward adds
+    uint64_t last_use = 0;
+  };
+  bool graphs = false;
+  std::vector<GraphEntry> gcache;
+  uint64_t gclock = 0;
+  cudaStream_t cap_stream = nullptr;
   // replicated embeddings / final LN
   void* tok_emb = nullptr;
   void* pos_emb = nullptr;
@@ -237,6 +248,9 @@ void release(energon_ctx* c) {
   if (c->pm.copy) cudaStreamDestroy(c->pm.copy);
   if (c->err_host) cudaFreeHost(c->err_host);
   if (c->load_stream) cudaStreamDestroy(c->load_stream);
+  for (auto& g : c->gcache)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+  if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   for (cudaEvent_t e : c->pool) cudaEventDestroy(e);
   if (c->nccl) ncclCommDestroy(c->nccl);
   delete c;
@@ -664,6 +678,17 @@ energon_status forward_t(energon_ctx** cs, int n, const Call& a, int64_t T) {
   return ENERGON_OK;
 }
 
+energon_status run_eager(energon_ctx** cs, int n, const Call& a, int64_t T) {
+  return cs[0]->bf16 ? forward_t<bf16>(cs, n, a, T) : forward_t<float>(cs, n, a, T);
+}
+
+void stats_add(energon_stats& d, const energon_stats& x) {
+  d.forwards += x.forwards;
+  d.allreduce_calls += x.allreduce_calls;
+  d.kernel_launches += x.kernel_launches;
+  d.prefetch_bytes += x.prefetch_bytes;
+}
+
 energon_status run(energon_ctx** cs, int n, const Call& a) {
   energon_ctx* c0 = cs[0];
   cudaError_t e = cudaSetDevice(c0->cfg.device);
@@ -675,8 +700,72 @@ energon_status run(energon_ctx** cs, int n, const Call& a) {
   int64_t T = 0;
   energon_status s = validate_call(c0, a, &T);
   if (s) return s;
-  return c0->bf16 ? forward_t<bf16>(cs, n, a, T) : forward_t<float>(cs, n, a, T);
+  bool graph_ok = c0->graphs && c0->cap_stream;
+  for (int i = 0; i < n; ++i) graph_ok = graph_ok && !cs[i]->prof && cs[i]->pm.layers.empty();
+  if (!graph_ok) return run_eager(cs, n, a, T);
+
+  // ---- CUDA graph: key = everything the launch sequence depends on
+  std::vector<int64_t> key = {n, (int64_t)(uintptr_t)a.tokens, (int64_t)(uintptr_t)a.x_in, (int64_t)(uintptr_t)a.out,
+                              a.B, a.S, a.l0, a.l1, a.final_ln, a.out_f32, c0->cfg.drce, c0->sp, c0->fuse};
+  for (int i = 0; i < n; ++i) key.push_back((int64_t)(uintptr_t)cs[i]);
+  for (int b = 0; b < a.B; ++b) key.push_back(a.lens[b]);
+  for (auto& g : c0->gcache)
+    if (g.key == key) {
+      g.last_use = ++c0->gclock;
+      e = cudaGraphLaunch(g.exec, a.st);
+      if (e != cudaSuccess) return cuda_fail(c0, e, "cudaGraphLaunch");
+      for (int i = 0; i < n; ++i) {
+        stats_add(cs[i]->stats, g.delta[i]);
+        cs[i]->stats.last_tokens = T;
+        cs[i]->stats.last_rows = c0->cfg.drce ? T : (int64_t)a.B * a.S;
+      }
+      return ENERGON_OK;
+    }
+  // miss: run this forward eagerly on the caller's stream (first-use initialisation happens here),
+  // then record the same launch sequence on the private stream (nothing executes) for later replays
+  std::vector<energon_stats> before(n), after(n);
+  for (int i = 0; i < n; ++i) before[i] = cs[i]->stats;
+  s = run_eager(cs, n, a, T);
+  if (s) return s;
+  for (int i = 0; i < n; ++i) after[i] = cs[i]->stats;
+  Call ac = a;
+  ac.st = c0->cap_stream;
+  e = cudaStreamBeginCapture(c0->cap_stream, cudaStreamCaptureModeThreadLocal);
+  if (e != cudaSuccess) return cuda_fail(c0, e, "cudaStreamBeginCapture");
+  s = run_eager(cs, n, ac, T);
+  cudaGraph_t graph = nullptr;
+  e = cudaStreamEndCapture(c0->cap_stream, &graph);
+  for (int i = 0; i < n; ++i) cs[i]->stats = after[i];  // the recording pass did not execute anything
+  if (s || e != cudaSuccess) {
+    if (graph) cudaGraphDestroy(graph);
+    cudaGetLastError();
+    return s ? s : cuda_fail(c0, e, "cudaStreamEndCapture");
+  }
+  energon_ctx::GraphEntry ent;
+  ent.key = key;
+  e = cudaGraphInstantiate(&ent.exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (e != cudaSuccess) return cuda_fail(c0, e, "cudaGraphInstantiate");
+  for (int i = 0; i < n; ++i) {
+    energon_stats d = after[i];
+    d.forwards -= before[i].forwards;
+    d.allreduce_calls -= before[i].allreduce_calls;
+    d.kernel_launches -= before[i].kernel_launches;
+    d.prefetch_bytes -= before[i].prefetch_bytes;
+    ent.delta.push_back(d);
+  }
+  ent.last_use = ++c0->gclock;
+  if (c0->gcache.size() >= 8) {  // evict the least recently used graph
+    size_t v = 0;
+    for (size_t i = 1; i < c0->gcache.size(); ++i)
+      if (c0->gcache[i].last_use < c0->gcache[v].last_use) v = i;
+    cudaGraphExecDestroy(c0->gcache[v].exec);
+    c0->gcache.erase(c0->gcache.begin() + v);
+  }
+  c0->gcache.push_back(ent);
+  return ENERGON_OK;
 }
+
 
 }  // namespace
 
@@ -1046,6 +1135,12 @@ energon_status energon_set_option(energon_ctx* c, int32_t option, int32_t value)
     if (value != 0 && value != 1) return fail(c, ENERGON_ERR_ARG, "ENERGON_OPT_DRCE takes 0 or 1");
     c->cfg.drce = value;
     c->tm_rows = -1;  // activation tensor maps depend on the row count
+    return ENERGON_OK;
+  }
+  if (option == ENERGON_OPT_GRAPH) {
+    if (value != 0 && value != 1) return fail(c, ENERGON_ERR_ARG, "ENERGON_OPT_GRAPH takes 0 or 1");
+    c->graphs = value != 0;
+    if (c->graphs && !c->cap_stream) CU(c, cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
     return ENERGON_OK;
   }
   if (option == ENERGON_OPT_TP_SP) {

@@ -21,6 +21,7 @@ FULL, RANK_SHARD = 0, 1
 MAX_BATCH = 1024
 OPT_DRCE = 1
 OPT_TP_SP = 2
+OPT_GRAPH = 3
 LAYER_TENSORS = ("wq", "wk", "wv", "wo", "bq", "bk", "bv", "bo",
                  "w1", "b1", "w2", "b2", "ln1_g", "ln1_b", "ln2_g", "ln2_b")
 

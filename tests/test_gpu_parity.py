@@ -493,3 +493,41 @@ def test_pmep_offload_bitexact(slots, dtype):
         assert np.array_equal(y, ref) and np.array_equal(y2, ref)
         per_layer = (3 * 256 * 256 + 256 * 256 + 1024 * 256 * 2) * (2 if dtype == "bf16" else 4)
         assert st["prefetch_bytes"] == 2 * len(layers) * per_layer
+
+
+# ----------------------------------------------------------------------------- CUDA graphs
+@pytest.mark.parametrize("k", [1, 2])
+def test_cuda_graph_replay_bitexact(k):
+    """ENERGON_OPT_GRAPH: a replayed graph gives the eager bits, reads the current contents of the
+    token buffer, and a new length vector records a new graph."""
+    shape = dict(SHAPES["gpt2s"], L=2)
+    B, S, seed = 8, 96, 6
+    lens = synth.random_lengths(B, S, seed)
+    lens2 = synth.random_lengths(B, S, seed + 1)
+    tok1 = torch.from_numpy(synth.tokens(B, S, shape["V"], lens, seed)).cuda()
+    tok2 = torch.from_numpy(synth.tokens(B, S, shape["V"], lens, seed + 5)).cuda()
+    ctxs = make_engine(shape, seed, "bf16", B * S, k=k)
+    tok = torch.empty_like(tok1)
+    out = torch.empty(B, S, shape["H"], dtype=torch.bfloat16, device="cuda")
+
+    def fwd(t, ln):
+        tok.copy_(t)
+        if k == 1:
+            E().energon_forward(ctxs[0], tok, ln, out)
+        else:
+            E().energon_forward_group(ctxs, tok, ln, out)
+        torch.cuda.synchronize()
+        return out.clone()
+
+    try:
+        eager = [fwd(tok1, lens), fwd(tok2, lens), fwd(tok1, lens2)]
+        for c in ctxs:
+            E().energon_set_option(c, E().OPT_GRAPH, 1)
+        graphed = [fwd(tok1, lens), fwd(tok1, lens), fwd(tok2, lens), fwd(tok1, lens2), fwd(tok1, lens2)]
+        st = E().energon_get_stats(ctxs[0])
+    finally:
+        destroy(ctxs)
+    assert torch.equal(graphed[0], eager[0]) and torch.equal(graphed[1], eager[0])
+    assert torch.equal(graphed[2], eager[1])  # replay reads the new token contents
+    assert torch.equal(graphed[3], eager[2]) and torch.equal(graphed[4], eager[2])
+    assert st["forwards"] == 8
