@@ -47,7 +47,9 @@ def parse():
     ap.add_argument("--layers", type=int, default=None, help="override the layer count (debug only)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-ab", action="store_true", help="skip the DRCE-off (padded) A/B")
-    ap.add_argument("--graph", type=int, default=1, help="replay each forward as a CUDA graph (ENERGON_OPT_GRAPH)")
+    ap.add_argument("--graph", type=int, default=None,
+                    help="replay each forward as a CUDA graph (ENERGON_OPT_GRAPH); default on for one GPU, off "
+                         "under torchrun (NCCL collectives run eagerly)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-tokens", type=int, default=192)
     ap.add_argument("--local-tp", type=int, default=0,
@@ -274,6 +276,8 @@ def energon_arm(args, world, rank, local):
         del w
     torch.cuda.synchronize()
     torch.cuda.empty_cache()
+    if args.graph is None:
+        args.graph = 1 if world == 1 else 0
     eng.set_option(energon.OPT_GRAPH, args.graph)
 
     stream = torch.cuda.current_stream()

@@ -360,7 +360,7 @@ static bool launch_tc(const bf16* Q, const bf16* K, const bf16* V, bf16* Cp, con
                       const LensParam& lp, int B, int hk, int S, int causal, cudaStream_t st) {
   using C = AttnCfg<D>;
   // heaviest-first work list of (sequence, query tile) pairs, built from the host copy of the lengths
-  static AttnWork work;  // 8 KB kernel parameter; host-side staging only (copied at launch)
+  AttnWork work;  // 8 KB kernel parameter (copied into the launch)
   int n = 0;
   auto cost = [&](int b, int qt) {
     const int len = lp.lens[b];
