@@ -89,7 +89,6 @@ __global__ void __launch_bounds__(192, 2)
                         float scale_log2, const __grid_constant__ AttnWork work) {
   using C = AttnCfg<D>;
   constexpr int BM = C::BM, BN = C::BN, DH = C::DH;
-  pdl_trigger();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;
@@ -140,6 +139,10 @@ __global__ void __launch_bounds__(192, 2)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
+  // Dependents may launch only once this CTA HOLDS its TMEM: a CTA that triggered before allocating
+  // could find its columns taken by a co-resident dependent CTA that then waits (griddepcontrol.wait)
+  // on this grid -- a cycle.
+  pdl_trigger();
   const uint32_t tS = tmem_base, tO = tmem_base + BN;
 
   // decode item w -> (b, head, q0, number of key tiles)
@@ -242,6 +245,7 @@ __global__ void __launch_bounds__(192, 2)
         const uint32_t par = g & 1;
         const int k0 = j * BN;
         mbar_wait(s_full, par);
+        __syncwarp();  // reconverge the spin loop before the .sync.aligned tcgen05.ld
         tc_fence_after();
         uint32_t sr[2][32];
         tmem_ld32(tS + lane_off + 0, sr[0]);
@@ -269,20 +273,26 @@ __global__ void __launch_bounds__(192, 2)
         mt *= scale_log2;
         if (j > 0) {  // P_{g-1} . V_{g-1} done before P is overwritten or O rescaled
           mbar_wait(o_full, par ^ 1);
+          __syncwarp();
           tc_fence_after();
         }
-        if (mt > m_ref + 8.f) {  // first tile, or the max grew by more than 2^8: move the reference
-          const float alpha = (m_ref == -INFINITY) ? 0.f : ex2f(m_ref - mt);
-          if (j > 0) {
+        // first tile, or the max grew by more than 2^8: move the reference.  The decision is per row
+        // (per lane) but tcgen05.ld / st are .sync.aligned, so the O rescale runs warp-wide whenever
+        // any row needs it, with alpha = 1 (exact) for the others -- a per-lane branch around them
+        // is undefined and hung the warp under some schedules.
+        const bool grow = mt > m_ref + 8.f;
+        const float alpha = !grow ? 1.f : (m_ref == -INFINITY) ? 0.f : ex2f(m_ref - mt);
+        if (j > 0 && __any_sync(0xffffffffu, grow)) {
 #pragma unroll 1
-            for (int c = 0; c < D; c += 32) {
-              uint32_t o[32];
-              tmem_ld32(tO + lane_off + c, o);
+          for (int c = 0; c < D; c += 32) {
+            uint32_t o[32];
+            tmem_ld32(tO + lane_off + c, o);
 #pragma unroll
-              for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
-              tmem_st32(tO + lane_off + c, o);
-            }
+            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+            tmem_st32(tO + lane_off + c, o);
           }
+        }
+        if (grow) {
           l *= alpha;
           m_ref = mt;
         }
@@ -321,6 +331,7 @@ __global__ void __launch_bounds__(192, 2)
       }
       // ---------------- item epilogue: O / l -> packed context row (or padded O row)
       mbar_wait(o_full, (g - 1) & 1);
+      __syncwarp();
       tc_fence_after();
       const float inv = 1.f / l;
       const bool valid = srow < len;

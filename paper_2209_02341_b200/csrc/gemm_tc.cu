@@ -55,7 +55,6 @@ template <int BN, int EPI>
 __global__ void __launch_bounds__(256, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, bf16* __restrict__ D,
                    const float* __restrict__ bias, int M, int N, int K, const QkvScatter qs) {
-  pdl_trigger();
   using C = TcCfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -94,6 +93,10 @@ __global__ void __launch_bounds__(256, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
+  // Dependents may launch only once this CTA HOLDS its TMEM: a CTA that triggered before allocating
+  // could find its columns taken by a co-resident dependent CTA that then waits (griddepcontrol.wait)
+  // on this grid -- a cycle.
+  pdl_trigger();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -153,6 +156,7 @@ __global__ void __launch_bounds__(256, 1)
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
       const int m_blk = tile % num_m, n_blk = tile / num_m;
       mbar_wait(&tfull[acc], acc_phase);
+      __syncwarp();  // reconverge the spin loop before the .sync.aligned tcgen05.ld
       tc_fence_after();
       const int row = m_blk * TC_BM + q * 32 + lane;
       bf16* drow = D + (int64_t)row * N;
@@ -437,7 +441,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     bf16* __restrict__ D, const float* __restrict__ bias, int M, int N, int K, int group_m,
                     const QkvScatter qs, const TailPlan tp, const __grid_constant__ CUtensorMap tmD, int l2_hints) {
-  pdl_trigger();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   using C = Tc2Cfg<BN>;
@@ -484,6 +487,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
   __syncthreads();  // also a CTA barrier: orders the tcgen05.alloc write of tmem_holder for every checker
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
+  // Dependents may launch only once this CTA HOLDS its TMEM: a CTA that triggered before allocating
+  // could find its columns taken by a co-resident dependent CTA that then waits (griddepcontrol.wait)
+  // on this grid -- a cycle.
+  pdl_trigger();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -567,6 +574,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       int m_blk, n_blk;
       raster(tile, num_m, num_n, group_m, m_blk, n_blk);
       mbar_wait(&tfull[acc], acc_phase);
+      __syncwarp();  // reconverge the spin loop before the .sync.aligned tcgen05.ld
       tc_fence_after();
       const int row = m_blk * 256 + (int)rank * 128 + etid;
       // split unit: this CTA's 128 x BN partial goes to the workspace
@@ -747,38 +755,43 @@ int tc_pick_bn(int M, int N) {
   return N <= 128 ? 128 : 256;
 }
 
-// fp32 partial-tile workspace + self-resetting arrival counters of the stream-K tail, one per device
-// (GEMMs of one device are stream-ordered on the forward stream; concurrent GEMMs on other streams of
-// the same device would need their own workspace).
-struct TailWorkspace {
-  float* ws = nullptr;
-  int* counters = nullptr;
-};
-static TailWorkspace& tail_workspace(int pairs, int bn) {
-  static TailWorkspace per_dev[16];
+// fp32 partial-tile workspace + self-resetting arrival counters of the stream-K tail: rem * splits
+// <= pairs units of [2][128][256] fp32.  Contexts own one each (runtime.cu); launches without one
+// (the kernel-level ABI entry) share a per-device default.
+bool tail_ws_alloc(TailWs* w) {
+  const size_t units = (size_t)(num_sms() / 2);
+  if (cudaMalloc(&w->ws, units * 2 * 128 * 256 * sizeof(float)) != cudaSuccess ||
+      cudaMalloc(&w->counters, units * 2 * sizeof(int)) != cudaSuccess) {
+    cudaGetLastError();
+    tail_ws_free(w);
+    return false;
+  }
+  cudaMemset(w->counters, 0, units * 2 * sizeof(int));
+  cudaDeviceSynchronize();  // one-time: counters are zero before any stream uses them
+  return true;
+}
+
+void tail_ws_free(TailWs* w) {
+  if (w->ws) cudaFree(w->ws);
+  if (w->counters) cudaFree(w->counters);
+  w->ws = nullptr;
+  w->counters = nullptr;
+}
+
+static const TailWs* default_tail_ws() {
+  static TailWs per_dev[16];
   int dev = 0;
   cudaGetDevice(&dev);
-  TailWorkspace& w = per_dev[dev & 15];
-  if (!w.ws) {
-    const size_t units = (size_t)pairs;  // rem * splits <= pairs
-    if (cudaMalloc(&w.ws, units * 2 * 128 * 256 * sizeof(float)) != cudaSuccess ||
-        cudaMalloc(&w.counters, units * 2 * sizeof(int)) != cudaSuccess) {
-      cudaGetLastError();
-      w.ws = nullptr;
-      return w;
-    }
-    cudaMemset(w.counters, 0, units * 2 * sizeof(int));
-    cudaDeviceSynchronize();  // one-time: counters are zero before any stream uses them
-  }
-  (void)bn;
-  return w;
+  TailWs& w = per_dev[dev & 15];
+  if (!w.ws) tail_ws_alloc(&w);
+  return &w;
 }
 
 int tc_w_box(int code) { return code > 1000 ? (code - 1000) / 2 : code; }
 
 template <int BN, int EPI>
 static void launch_pair_epi(const CUtensorMap& tmA, const CUtensorMap& tmB, const float* bias, bf16* D, int M, int N,
-                            int K, cudaStream_t st, const QkvScatter& qs, const CUtensorMap* tmD) {
+                            int K, cudaStream_t st, const QkvScatter& qs, const CUtensorMap* tmD, const TailWs* tw) {
   using C = Tc2Cfg<BN>;
   static bool attr = false;
   if (!attr) {
@@ -799,8 +812,8 @@ static void launch_pair_epi(const CUtensorMap& tmA, const CUtensorMap& tmB, cons
     if (splits > nkb / 4) splits = nkb / 4;  // at least 4 K-blocks per split
     if (splits > 8) splits = 8;
     if (splits >= 2) {
-      TailWorkspace& w = tail_workspace(pairs, BN);
-      if (w.ws) tp = TailPlan{tiles - rem, splits, w.ws, w.counters};
+      const TailWs* w = tw ? tw : default_tail_ws();
+      if (w->ws) tp = TailPlan{tiles - rem, splits, w->ws, w->counters};
     }
   }
   // group of A panels kept L2-resident while the group sweeps N (about 48 MB of A per group)
@@ -828,7 +841,8 @@ static void launch_pair_epi(const CUtensorMap& tmA, const CUtensorMap& tmB, cons
 
 template <int BN, int EPI>
 static void launch_bn_epi(const CUtensorMap& tmA, const CUtensorMap& tmB, const float* bias, bf16* D, int M, int N,
-                          int K, cudaStream_t st, const QkvScatter& qs, const CUtensorMap* /*tmD*/) {
+                          int K, cudaStream_t st, const QkvScatter& qs, const CUtensorMap* /*tmD*/,
+                          const TailWs* /*tw*/) {
   using C = TcCfg<BN>;
   static bool attr = false;
   if (!attr) {
@@ -842,17 +856,17 @@ static void launch_bn_epi(const CUtensorMap& tmA, const CUtensorMap& tmB, const 
 
 #define DISPATCH_EPI(F, BNARGS)                                                  \
   switch (epi) {                                                                 \
-    case EPI_NONE: F<BNARGS EPI_NONE>(tmA, tmB, bias, D, M, N, K, st, qs, tmD); break; \
-    case EPI_BIAS: F<BNARGS EPI_BIAS>(tmA, tmB, bias, D, M, N, K, st, qs, tmD); break; \
-    case EPI_BIAS_GELU: F<BNARGS EPI_BIAS_GELU>(tmA, tmB, bias, D, M, N, K, st, qs, tmD); break; \
-    default: F<BNARGS EPI_BIAS_QKV>(tmA, tmB, bias, D, M, N, K, st, qs, tmD); break;   \
+    case EPI_NONE: F<BNARGS EPI_NONE>(tmA, tmB, bias, D, M, N, K, st, qs, tmD, tw); break; \
+    case EPI_BIAS: F<BNARGS EPI_BIAS>(tmA, tmB, bias, D, M, N, K, st, qs, tmD, tw); break; \
+    case EPI_BIAS_GELU: F<BNARGS EPI_BIAS_GELU>(tmA, tmB, bias, D, M, N, K, st, qs, tmD, tw); break; \
+    default: F<BNARGS EPI_BIAS_QKV>(tmA, tmB, bias, D, M, N, K, st, qs, tmD, tw); break;   \
   }
 #define BN256 256,
 #define BN192 192,
 #define BN128 128,
 
 void launch_gemm_tc(const CUtensorMap& tmA, const CUtensorMap& tmB, int bn, const float* bias, bf16* D, int M, int N,
-                    int K, int epi, cudaStream_t st, const QkvScatter* qkv, const CUtensorMap* tmD) {
+                    int K, int epi, cudaStream_t st, const QkvScatter* qkv, const CUtensorMap* tmD, const TailWs* tw) {
   if (M <= 0 || N <= 0) return;
   QkvScatter qs{};
   if (qkv) qs = *qkv;

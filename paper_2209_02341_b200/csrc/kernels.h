@@ -114,9 +114,19 @@ bool make_tmap_kmajor(CUtensorMap* map, const void* ptr, int rows, int K, int bo
 int tc_pick_bn(int M, int N);  // tile code (see gemm_tc.cu)
 int tc_w_box(int code);        // row box of the W tensor map the code needs (256, 128, 96 or 64)
 bool make_tmap_store(CUtensorMap* map, const void* ptr, int rows, int N);  // D map of the TMA-store epilogue
+// Scratch of the stream-K tail split: fp32 partial tiles + self-resetting arrival counters.  GEMMs that
+// share one are stream-ordered, so each context (one forward stream at a time) owns its own;
+// tail_ws_alloc sizes it for this device, nullptr in launch_gemm_tc = a per-device default.
+struct TailWs {
+  float* ws = nullptr;
+  int* counters = nullptr;
+};
+bool tail_ws_alloc(TailWs* w);  // cudaMalloc + zeroed counters (synchronous); false on OOM
+void tail_ws_free(TailWs* w);
 // tmD: the output map (make_tmap_store) or nullptr to build it per call.
 void launch_gemm_tc(const CUtensorMap& tmA, const CUtensorMap& tmB, int bn, const float* bias, bf16* D, int M, int N,
-                    int K, int epi, cudaStream_t st, const QkvScatter* qkv = nullptr, const CUtensorMap* tmD = nullptr);
+                    int K, int epi, cudaStream_t st, const QkvScatter* qkv = nullptr, const CUtensorMap* tmD = nullptr,
+                    const TailWs* tw = nullptr);
 int num_sms();
 
 }  // namespace energon
