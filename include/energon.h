@@ -208,6 +208,41 @@ ENERGON_API energon_status energon_forward_hidden(energon_ctx* ctx, const float*
                                       int32_t batch, int32_t max_len, int32_t layer_begin, int32_t layer_end,
                                       int32_t apply_final_ln, float* out_d, void* stream);
 
+/*
+ * Non-blocking pipeline parallelism (NBPP, sec 4.2 / fig:engine): the model is
+ * "partitioned by transformer layers" into pp_size stages; each stage is a context
+ * (or a TP group of contexts, "combine both pipeline parallelism and tensor parallelism",
+ * PAPER.md:345) that runs its contiguous layer range on every batch, and only the activations
+ * travel stage to stage -- with DRCE they travel PACKED ([T, H] rows), so the inter-stage transfer
+ * shrinks by the padding ratio too (an extension the paper does not state).
+ *
+ * energon_stage_plan (host only): out_begin[0..pp_size] with stage i = [out_begin[i], out_begin[i+1]);
+ *   contiguous, sizes differ by at most one, earlier stages take the remainder (L=12, pp=4 -> 3 each,
+ *   PAPER.md:548 "each device only executes 3 layers").  ENERGON_ERR_CONFIG unless 1 <= pp_size <= L.
+ * energon_forward_stage: run layers [layer_begin, layer_end) on one batch.
+ *   tokens_d  device int32 [batch, max_len] for the first stage (embed + remove padding), else NULL
+ *   x_d       device fp32 [rows, H] residual-stream rows from the previous stage, else NULL
+ *             (exactly one of tokens_d / x_d); rows = sum(seq_lens) with DRCE, batch*max_len without
+ *   out_kind  ENERGON_STAGE_PACKED: out_d device fp32 [rows, H] = the residual stream after layer_end-1
+ *             ENERGON_STAGE_FINAL:  out_d device [batch, max_len, H] cfg dtype = final LN (cfg.final_ln)
+ *                                   + rebuild padding, pad rows exactly 0 (as energon_forward)
+ *   Only layers [layer_begin, layer_end) must be loaded; the embeddings (energon_load_embeddings) only
+ *   when tokens_d is given or out_kind is FINAL.  A stage with x_d and PACKED output needs >= 1 layer.
+ *   Same SPMD / stream semantics and errors as energon_forward.  Chaining the stages of a plan gives
+ *   bit-identical results to one energon_forward over all layers (the same kernels on the same rows).
+ * energon_forward_stage_group: the same for a local TP group (energon_init_local_group).
+ */
+enum { ENERGON_STAGE_PACKED = 0, ENERGON_STAGE_FINAL = 1 };
+ENERGON_API energon_status energon_stage_plan(int32_t num_layers, int32_t pp_size, int32_t* out_begin);
+ENERGON_API energon_status energon_forward_stage(energon_ctx* ctx, const int32_t* tokens_d, const float* x_d,
+                                                 const int32_t* seq_lens, int32_t batch, int32_t max_len,
+                                                 int32_t layer_begin, int32_t layer_end, int32_t out_kind, void* out_d,
+                                                 void* stream);
+ENERGON_API energon_status energon_forward_stage_group(energon_ctx** ctxs, int32_t k, const int32_t* tokens_d,
+                                                       const float* x_d, const int32_t* seq_lens, int32_t batch,
+                                                       int32_t max_len, int32_t layer_begin, int32_t layer_end,
+                                                       int32_t out_kind, void* out_d, void* stream);
+
 /* Block until the context's work is done; surfaces sticky CUDA / NCCL / token errors. */
 ENERGON_API energon_status energon_sync(energon_ctx* ctx);
 ENERGON_API energon_status energon_get_stats(const energon_ctx* ctx, energon_stats* out);

@@ -18,6 +18,7 @@
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <string>
@@ -104,6 +105,7 @@ struct energon_ctx {
   CUtensorMap tmD_P, tmD_G;  // TMA-store output maps of the out/down (P) and up (G) GEMMs
   int tm_rows = -1;
   Pmep pm;
+  TailWs tail;              // stream-K scratch of this context's GEMMs (ordered on its forward stream)
   int* err_host = nullptr;  // mapped pinned flag written by the embed kernel (bad token id)
   int* err_dev = nullptr;
   cudaStream_t load_stream = nullptr;
@@ -219,6 +221,7 @@ energon_status setup(energon_ctx* c) {
     return s;
   // zero every activation buffer once: rows a schedule reads but never writes (sequence-parallel
   // padding rows, unwritten Ctx rows) stay finite
+  if (c->bf16 && !tail_ws_alloc(&c->tail)) return fail(c, ENERGON_ERR_OOM, "stream-K workspace allocation failed");
   for (void* p : c->allocs) CU(c, cudaMemset(p, 0, 16));
   CU(c, cudaMemset(c->X, 0, sizeof(float) * R * c->H));
   CU(c, cudaMemset(c->A, 0, a * R * c->H));
@@ -234,6 +237,7 @@ void release(energon_ctx* c) {
   cudaDeviceSynchronize();
   for (void* p : c->allocs) cudaFree(p);
   c->allocs.clear();
+  tail_ws_free(&c->tail);
   for (void* p : c->pm.pool) {
     if (c->pm.pool_kind == 0) cudaFreeHost(p);
     else {
@@ -330,6 +334,33 @@ cudaEvent_t next_event(energon_ctx* c) {
   return c->pool[c->pool_used++];
 }
 
+// ENERGON_DEBUG_SYNC=1 (diagnostics): wait for every launch to finish (eager runs only), and abort with
+// the launch class after 20 s -- names the kernel of a device-side hang
+bool debug_sync() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("ENERGON_DEBUG_SYNC");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
+void debug_wait(cudaStream_t st, int cls, double work) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return;
+  static long n = 0;
+  ++n;
+  for (int i = 0; i < 20000; ++i) {
+    const cudaError_t e = cudaStreamQuery(st);
+    if (e != cudaErrorNotReady) return;
+    usleep(1000);
+  }
+  fprintf(stderr, "[energon] device hang: launch #%ld class %d (0 gemm, 1 attn, 2 mem, 3 comm), work %.3g\n", n, cls,
+          work);
+  fflush(stderr);
+  abort();
+}
+
 struct Prof {
   energon_ctx* c;
   cudaStream_t st;
@@ -343,6 +374,7 @@ struct Prof {
     }
   }
   ~Prof() {
+    if (debug_sync()) debug_wait(st, cls, work);
     if (c->prof) {
       cudaEvent_t b = next_event(c);
       cudaEventRecord(b, st);
@@ -360,11 +392,15 @@ struct Call {
   void* out;
   bool out_f32;
   cudaStream_t st;
+  bool x_packed = false;    // x_in holds the linears' rows ([T,H] packed with DRCE) -- a pipeline stage input
+  bool out_packed = false;  // out receives the fp32 residual stream rows [rows,H] -- a pipeline stage output
 };
 
-energon_status check_ready(energon_ctx* c) {
-  if (!c->emb_loaded) return fail(c, ENERGON_ERR_NOT_LOADED, "embeddings not loaded");
-  for (size_t l = 0; l < c->layers.size(); ++l)
+energon_status check_ready(energon_ctx* c, const Call& a) {
+  // a pipeline stage needs only its own layers, and the embeddings only at the ends of the pipeline
+  if ((a.tokens || !a.out_packed) && !c->emb_loaded) return fail(c, ENERGON_ERR_NOT_LOADED, "embeddings not loaded");
+  if (a.l0 < 0 || a.l1 > (int)c->layers.size() || a.l0 > a.l1) return fail(c, ENERGON_ERR_ARG, "bad layer range");
+  for (int l = a.l0; l < a.l1; ++l)
     if (!c->layers[l].loaded) return fail(c, ENERGON_ERR_NOT_LOADED, "layer " + std::to_string(l) + " not loaded");
   if (*c->err_host) return fail(c, ENERGON_ERR_TOKEN, "a token id outside [0, vocab) was seen by a previous forward");
   return ENERGON_OK;
@@ -452,7 +488,7 @@ void gemm(energon_ctx* c, const CUtensorMap& tmA, const CUtensorMap* tmB, const 
   if constexpr (sizeof(Act) == 2) {
     const int code = tc_pick_bn(M, N);
     launch_gemm_tc(tmA, tmB[box_slot(tc_w_box(code))], code, bias, reinterpret_cast<bf16*>(D), M, N, K, epi, st, qs,
-                   tmD);
+                   tmD, &c->tail);
   } else {
     launch_gemm_f32(reinterpret_cast<const float*>(A), reinterpret_cast<const float*>(W), bias,
                     reinterpret_cast<float*>(D), M, N, K, epi, st);
@@ -550,7 +586,8 @@ energon_status forward_t(energon_ctx** cs, int n, const Call& a, int64_t T) {
                              reinterpret_cast<const Act*>(c->pos_emb), g1, b1, eps, c->X, reinterpret_cast<Act*>(c->A),
                              c->err_dev, st);
       else
-        launch_gather_ln<Act>(a.x_in, pidx, r0, sn, c->H, g1, b1, eps, c->X, reinterpret_cast<Act*>(c->A), st);
+        launch_gather_ln<Act>(a.x_in, a.x_packed ? nullptr : pidx, r0, sn, c->H, g1, b1, eps, c->X,
+                              reinterpret_cast<Act*>(c->A), st);
     }
     c->stats.kernel_launches++;
   }
@@ -659,8 +696,18 @@ energon_status forward_t(energon_ctx** cs, int n, const Call& a, int64_t T) {
     if (s) return s;
   }
 
-  // ---- a13: final LN + unpack (every rank holds the replicated result; a local group writes once)
   energon_ctx* c = cs[0];
+  if (a.out_packed) {
+    // pipeline stage output: the residual stream rows go to the next stage as they are
+    Prof p(c, st, P_MEM, 8.0 * rows * H);
+    cudaError_t e = cudaMemcpyAsync(a.out, c->X, sizeof(float) * (size_t)rows * c->H, cudaMemcpyDeviceToDevice, st);
+    if (e != cudaSuccess) return cuda_fail(c0, e, "stage output copy");
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(c0, e, "kernel launch");
+    for (int i = 0; i < n; ++i) cs[i]->stats.forwards++;
+    return ENERGON_OK;
+  }
+  // ---- a13: final LN + unpack (every rank holds the replicated result; a local group writes once)
   const int apply_ln = a.final_ln;
   {
     Prof p(c, st, P_MEM, 4.0 * a.B * a.S + 4.0 * T * H + (double)a.B * a.S * H * (a.out_f32 ? 4 : act));
@@ -694,7 +741,7 @@ energon_status run(energon_ctx** cs, int n, const Call& a) {
   cudaError_t e = cudaSetDevice(c0->cfg.device);
   if (e != cudaSuccess) return cuda_fail(c0, e, "cudaSetDevice");
   for (int i = 0; i < n; ++i) {
-    energon_status s = check_ready(cs[i]);
+    energon_status s = check_ready(cs[i], a);
     if (s) return s;
   }
   int64_t T = 0;
@@ -706,7 +753,8 @@ energon_status run(energon_ctx** cs, int n, const Call& a) {
 
   // ---- CUDA graph: key = everything the launch sequence depends on
   std::vector<int64_t> key = {n, (int64_t)(uintptr_t)a.tokens, (int64_t)(uintptr_t)a.x_in, (int64_t)(uintptr_t)a.out,
-                              a.B, a.S, a.l0, a.l1, a.final_ln, a.out_f32, c0->cfg.drce, c0->sp, c0->fuse};
+                              a.B, a.S, a.l0, a.l1, a.final_ln, a.out_f32, c0->cfg.drce, c0->sp, c0->fuse,
+                              a.x_packed, a.out_packed};
   for (int i = 0; i < n; ++i) key.push_back((int64_t)(uintptr_t)cs[i]);
   for (int b = 0; b < a.B; ++b) key.push_back(a.lens[b]);
   for (auto& g : c0->gcache)
@@ -1103,6 +1151,48 @@ energon_status energon_forward_hidden(energon_ctx* c, const float* x, const int3
   Call a{nullptr, x, lens, B, S, l0, l1, apply_final_ln, out, true, (cudaStream_t)stream};
   energon_ctx* cs[1] = {c};
   return run(cs, 1, a);
+}
+
+energon_status energon_stage_plan(int32_t L, int32_t pp, int32_t* out_begin) {
+  if (!out_begin) return fail(nullptr, ENERGON_ERR_ARG, "out_begin is NULL");
+  if (L < 1 || pp < 1 || pp > L) return fail(nullptr, ENERGON_ERR_CONFIG, "need 1 <= pp_size <= num_layers");
+  // contiguous ranges, sizes differ by at most one, the earlier stages take the remainder
+  out_begin[0] = 0;
+  for (int i = 0; i < pp; ++i) out_begin[i + 1] = out_begin[i] + L / pp + (i < L % pp ? 1 : 0);
+  return ENERGON_OK;
+}
+
+namespace {
+energon_status stage_call(energon_ctx** cs, int k, const int32_t* tokens, const float* x, const int32_t* lens,
+                          int32_t B, int32_t S, int32_t l0, int32_t l1, int32_t out_kind, void* out, void* stream) {
+  if ((tokens == nullptr) == (x == nullptr))
+    return fail(cs[0], ENERGON_ERR_ARG, "exactly one of tokens_d (first stage) and x_d (later stages) must be given");
+  if (out_kind != ENERGON_STAGE_PACKED && out_kind != ENERGON_STAGE_FINAL)
+    return fail(cs[0], ENERGON_ERR_ARG, "out_kind must be ENERGON_STAGE_PACKED or ENERGON_STAGE_FINAL");
+  Call a{tokens, x, lens, B, S, l0, l1, cs[0]->cfg.final_ln, out, false, (cudaStream_t)stream};
+  a.x_packed = x != nullptr;
+  a.out_packed = out_kind == ENERGON_STAGE_PACKED;
+  if (a.x_packed && a.out_packed && l0 >= l1) return fail(cs[0], ENERGON_ERR_ARG, "a middle stage needs >= 1 layer");
+  return run(cs, k, a);
+}
+}  // namespace
+
+energon_status energon_forward_stage(energon_ctx* c, const int32_t* tokens, const float* x, const int32_t* lens,
+                                     int32_t B, int32_t S, int32_t l0, int32_t l1, int32_t out_kind, void* out,
+                                     void* stream) {
+  if (!c) return fail(nullptr, ENERGON_ERR_ARG, "ctx is NULL");
+  energon_ctx* cs[1] = {c};
+  return stage_call(cs, 1, tokens, x, lens, B, S, l0, l1, out_kind, out, stream);
+}
+
+energon_status energon_forward_stage_group(energon_ctx** cs, int32_t k, const int32_t* tokens, const float* x,
+                                           const int32_t* lens, int32_t B, int32_t S, int32_t l0, int32_t l1,
+                                           int32_t out_kind, void* out, void* stream) {
+  if (!cs || k < 1 || k > 8) return fail(nullptr, ENERGON_ERR_ARG, "bad context list");
+  for (int i = 0; i < k; ++i)
+    if (!cs[i] || cs[i]->cfg.tp_size != k || cs[i]->cfg.tp_rank != i || (k > 1 && !cs[i]->local_group))
+      return fail(nullptr, ENERGON_ERR_ARG, "contexts must be ranks 0..k-1 of one local group");
+  return stage_call(cs, k, tokens, x, lens, B, S, l0, l1, out_kind, out, stream);
 }
 
 energon_status energon_sync(energon_ctx* c) {

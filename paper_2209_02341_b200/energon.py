@@ -22,6 +22,7 @@ MAX_BATCH = 1024
 OPT_DRCE = 1
 OPT_TP_SP = 2
 OPT_GRAPH = 3
+STAGE_PACKED, STAGE_FINAL = 0, 1
 LAYER_TENSORS = ("wq", "wk", "wv", "wo", "bq", "bk", "bv", "bo",
                  "w1", "b1", "w2", "b2", "ln1_g", "ln1_b", "ln2_g", "ln2_b")
 
@@ -30,7 +31,8 @@ EXPORTS = ("energon_get_unique_id", "energon_init", "energon_init_local_group", 
            "energon_load_layer_weights", "energon_forward", "energon_forward_group", "energon_forward_hidden",
            "energon_sync", "energon_get_stats", "energon_last_error", "energon_status_string", "energon_destroy",
            "energon_index_maps", "energon_gemm", "energon_attention", "energon_set_profiling", "energon_get_profile",
-           "energon_shard_plan", "energon_set_option", "energon_pmep_plan", "energon_offload_layers")
+           "energon_shard_plan", "energon_set_option", "energon_pmep_plan", "energon_offload_layers",
+           "energon_stage_plan", "energon_forward_stage", "energon_forward_stage_group")
 
 
 class EnergonError(RuntimeError):
@@ -102,6 +104,10 @@ def load_library(path: str = SO_PATH):
     L.energon_pmep_plan.argtypes = [I32, I32, ctypes.POINTER(ctypes.c_int32)]
     L.energon_offload_layers.argtypes = [P, ctypes.POINTER(ctypes.c_int32), I32, I32, I32, I32]
     L.energon_get_profile.argtypes = [P, ctypes.POINTER(Profile)]
+    L.energon_stage_plan.argtypes = [I32, I32, ctypes.POINTER(ctypes.c_int32)]
+    L.energon_forward_stage.argtypes = [P, P, P, ctypes.POINTER(ctypes.c_int32), I32, I32, I32, I32, I32, P, P]
+    L.energon_forward_stage_group.argtypes = [ctypes.POINTER(P), I32, P, P, ctypes.POINTER(ctypes.c_int32), I32, I32,
+                                              I32, I32, I32, P, P]
     for name in EXPORTS:
         fn = getattr(L, name)
         if fn.restype is ctypes.c_int:  # default restype: energon_status
@@ -203,6 +209,28 @@ def energon_forward_hidden(ctx, x, seq_lens, layer_begin, layer_end, apply_final
     B, S, _ = x.shape
     _check(load_library().energon_forward_hidden(ctx, _ptr(x), _lens(seq_lens), B, S, layer_begin, layer_end,
                                                  int(apply_final_ln), _ptr(out), _stream(stream)), ctx)
+
+
+def energon_stage_plan(num_layers: int, pp_size: int) -> list:
+    """Stage layer ranges [(begin, end), ...] (host only)."""
+    out = (ctypes.c_int32 * (max(pp_size, 0) + 1))()
+    _check(load_library().energon_stage_plan(num_layers, pp_size, out))
+    return [(out[i], out[i + 1]) for i in range(pp_size)]
+
+
+def energon_forward_stage(ctx, seq_lens, max_len, layer_begin, layer_end, out_kind, out, tokens=None, x=None,
+                          stream=None):
+    """One pipeline stage: tokens [B, S] (first stage) or x fp32 [rows, H] -> out (packed rows or final)."""
+    _check(load_library().energon_forward_stage(ctx, _ptr(tokens), _ptr(x), _lens(seq_lens), len(seq_lens), max_len,
+                                                layer_begin, layer_end, out_kind, _ptr(out), _stream(stream)), ctx)
+
+
+def energon_forward_stage_group(ctxs, seq_lens, max_len, layer_begin, layer_end, out_kind, out, tokens=None, x=None,
+                                stream=None):
+    arr = (ctypes.c_void_p * len(ctxs))(*[c.value for c in ctxs])
+    _check(load_library().energon_forward_stage_group(arr, len(ctxs), _ptr(tokens), _ptr(x), _lens(seq_lens),
+                                                      len(seq_lens), max_len, layer_begin, layer_end, out_kind,
+                                                      _ptr(out), _stream(stream)), ctxs[0])
 
 
 def energon_sync(ctx):

@@ -95,3 +95,27 @@ def test_pmep_plan_rejects_bad_arguments(lib):
     n = (ctypes.c_int32 * 4)()
     assert lib.energon_pmep_plan(4, 0, n) == -1
     assert lib.energon_pmep_plan(4, 5, n) == -1
+
+
+def test_stage_plan_paper_example(lib):
+    """12 layers on 4 devices -> 3 layers each; SPEC.md:362-367 remainder rule."""
+    import json
+    g = json.load(open(os.path.join(ROOT, "tests", "golden", "spec_examples.json")))["stage_plan"]
+    for ex in g["examples"]:
+        assert energon.energon_stage_plan(ex["num_layers"], ex["pp_size"]) == [tuple(r) for r in ex["ranges"]]
+
+
+@pytest.mark.parametrize("L,pp", [(40, 8), (40, 3), (48, 5), (64, 7), (2, 2), (1, 1)])
+def test_stage_plan_partitions(lib, L, pp):
+    """Contiguous ranges that partition [0, L), non-empty, sizes differ by at most one, earlier stages larger."""
+    r = energon.energon_stage_plan(L, pp)
+    assert r[0][0] == 0 and r[-1][1] == L and all(a[1] == b[0] for a, b in zip(r, r[1:]))
+    sizes = [e - b for b, e in r]
+    assert min(sizes) >= 1 and max(sizes) - min(sizes) <= 1 and sizes == sorted(sizes, reverse=True)
+
+
+def test_stage_plan_rejects_bad_arguments(lib):
+    out = (ctypes.c_int32 * 8)()
+    assert lib.energon_stage_plan(4, 5, out) == -2
+    assert lib.energon_stage_plan(4, 0, out) == -2
+    assert lib.energon_stage_plan(4, 2, None) == -1
