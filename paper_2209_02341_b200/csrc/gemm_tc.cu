@@ -303,36 +303,52 @@ __device__ __forceinline__ void raster(int tile, int num_m, int num_n, int group
   n_blk = r / gsize;
 }
 
-// Work decomposition of the pair kernel.  Tiles [0, full) are whole-K units (data parallel);
-// when the last wave would leave clusters idle, each of the `rem` tail tiles is split into
-// `splits` K-ranges that run concurrently on the otherwise idle clusters ("stream-K tail").  A
-// split unit writes its fp32 partial tile to `ws`; the last split to arrive (per tile and CTA,
-// counted in `counters`, which self-reset) sums the partials in split order 0..splits-1
-// (deterministic) and runs the epilogue.
+// Work decomposition of the pair kernel.  Tiles [0, full) are whole-K units handed out round-robin
+// (data parallel).  When the last wave would leave clusters idle, the k-iterations of the `rem` tail
+// tiles are spread evenly over the clusters instead ("stream-K tail"): cluster c runs the contiguous
+// iteration range [c L, (c + 1) L) of the tail's rem * nkb iterations, which may cover the end of one
+// tile and the start of the next.  A piece that is not a whole tile writes its fp32 partial to
+// workspace slot (c + tail) -- unique, at most clusters + rem slots -- in a coalesced [col/4][row][4]
+// layout; the last piece of a tile to arrive (per tile and CTA, counted in `counters`, which self-reset)
+// sums the tile's pieces in cluster order (deterministic) and runs the epilogue.
 struct TailPlan {
-  int full;    // whole tiles
-  int splits;  // K-splits per tail tile (0: no tail split)
-  float* ws;   // [rem * splits][2][128][BN] fp32 partials
+  int full;       // whole tiles (all tiles when L == 0)
+  int L;          // tail k-iterations per cluster (0: no stream-K tail)
+  int rem;        // tail tiles
+  float* ws;      // [slots][2][BN / 4][128][4] fp32 partials
   int* counters;  // [rem][2]
 };
 
-__device__ __forceinline__ void unit_decode(int u, const TailPlan& tp, int nkb, int& tile, int& kb0, int& kb1,
-                                            int& split, int& tail) {
-  if (tp.splits == 0 || u < tp.full) {
-    tile = u;
-    kb0 = 0;
-    kb1 = nkb;
-    split = -1;
-    tail = -1;
-    return;
+struct WorkIter {
+  int u, it, it_end;
+  __device__ __forceinline__ WorkIter(int cid, const TailPlan& tp, int nkb) : u(cid), it(0), it_end(0) {
+    if (tp.L > 0) {
+      it = cid * tp.L;
+      it_end = min(it + tp.L, tp.rem * nkb);
+    }
   }
-  const int j = u - tp.full;
-  tail = j / tp.splits;
-  split = j - tail * tp.splits;
-  tile = tp.full + tail;
-  kb0 = (int)(((long)nkb * split) / tp.splits);
-  kb1 = (int)(((long)nkb * (split + 1)) / tp.splits);
-}
+  // next unit of this cluster: tile, k-block range, split index within the tile (-1: whole tile), tail
+  __device__ __forceinline__ bool next(const TailPlan& tp, int nkb, int ncl, int& tile, int& kb0, int& kb1, int& split,
+                                       int& tail) {
+    if (u < tp.full) {
+      tile = u;
+      kb0 = 0;
+      kb1 = nkb;
+      split = -1;
+      tail = -1;
+      u += ncl;
+      return true;
+    }
+    if (it >= it_end) return false;
+    tail = it / nkb;
+    kb0 = it - tail * nkb;
+    kb1 = min(nkb, kb0 + (it_end - it));
+    tile = tp.full + tail;
+    split = (kb0 == 0 && kb1 == nkb) ? -1 : (it / tp.L) - (tail * nkb) / tp.L;
+    it += kb1 - kb0;
+    return true;
+  }
+};
 
 template <int EPI>
 __device__ __forceinline__ void epi_math(float (&v)[32], int n0, int N, const float* __restrict__ bias) {
@@ -358,6 +374,13 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t sr
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
                    reinterpret_cast<uint64_t>(map)),
                "r"(src), "r"(x), "r"(y)
+               : "memory");
+}
+// TMA store with an L2 eviction-priority hint (outputs streamed past the L2-resident A panels)
+__device__ __forceinline__ void tma_store_2d_hint(const CUtensorMap* map, uint32_t src, int x, int y, uint64_t pol) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%2, %3}], [%1], %4;" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(src), "r"(x), "r"(y), "l"(pol)
                : "memory");
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
@@ -460,9 +483,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
   const bool leader = rank == 0;
   const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
   const int num_m = (M + 255) / 256, num_n = (N + BN - 1) / BN;
-  const int num_tiles = num_m * num_n;
   const int nkb = (K + TC_BK - 1) / TC_BK;
-  const int num_units = tp.splits ? tp.full + (num_tiles - tp.full) * tp.splits : num_tiles;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -498,16 +519,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       const uint64_t pol_a = policy_evict_last(), pol_b = policy_evict_first();
       int stage = 0;
       uint32_t phase = 0;
-      for (int u = cid; u < num_units; u += ncl) {
-        int tile, kb0, kb1, split, tail;
-        unit_decode(u, tp, nkb, tile, kb0, kb1, split, tail);
+      WorkIter wi(cid, tp, nkb);
+      int tile, kb0, kb1, split, tail;
+      while (wi.next(tp, nkb, ncl, tile, kb0, kb1, split, tail)) {
         int m_blk, n_blk;
         raster(tile, num_m, num_n, group_m, m_blk, n_blk);
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           const uint32_t fb = smem_u32(&full[stage]) & PEER_MASK;
           if (leader) mbar_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
-          if (l2_hints) {
+          if (l2_hints & 1) {
             tma_load_2d_2sm_hint(&tmA, smem_u32(sA + stage * C::A_BYTES), fb, kb * TC_BK, m_blk * 256 + (int)rank * 128,
                                  pol_a);
             tma_load_2d_2sm_hint(&tmB, smem_u32(sB + stage * C::B_BYTES), fb, kb * TC_BK,
@@ -529,9 +550,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int u = cid; u < num_units; u += ncl) {
-        int tile, kb0, kb1, split, tail;
-        unit_decode(u, tp, nkb, tile, kb0, kb1, split, tail);
+      WorkIter wi(cid, tp, nkb);
+      int tile, kb0, kb1, split, tail;
+      while (wi.next(tp, nkb, ncl, tile, kb0, kb1, split, tail)) {
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
@@ -568,18 +589,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     uint32_t nst = 0;  // TMA stores issued by this warp (double-buffered staging)
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int u = cid; u < num_units; u += ncl) {
-      int tile, kb0, kb1, split, tail;
-      unit_decode(u, tp, nkb, tile, kb0, kb1, split, tail);
+    WorkIter wi(cid, tp, nkb);
+    int tile, kb0, kb1, split, tail;
+    while (wi.next(tp, nkb, ncl, tile, kb0, kb1, split, tail)) {
       int m_blk, n_blk;
       raster(tile, num_m, num_n, group_m, m_blk, n_blk);
       mbar_wait(&tfull[acc], acc_phase);
       __syncwarp();  // reconverge the spin loop before the .sync.aligned tcgen05.ld
       tc_fence_after();
       const int row = m_blk * 256 + (int)rank * 128 + etid;
-      // split unit: this CTA's 128 x BN partial goes to the workspace
-      float* part = (split >= 0) ? tp.ws + ((size_t)(tail * tp.splits + split) * 2 + rank) * 128 * BN + (size_t)etid * BN
-                                 : nullptr;
+      // split piece: this CTA's 128 x BN partial goes to workspace slot (cid + tail), [col/4][row][4]
+      float* part = (split >= 0) ? tp.ws + ((size_t)(cid + tail) * 2 + rank) * 128 * BN + (size_t)etid * 4 : nullptr;
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
       if (TMA_ST && split < 0) {
         // two 32-column chunks per step: both TMEM loads in flight, one proxy fence and one wait for the
@@ -614,8 +634,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
           if (lane == 0) {
-            tma_store_2d(&tmD, smem_u32(my_stg), n_blk * BN + c * 32, rowt);
-            if (two) tma_store_2d(&tmD, smem_u32(my_stg + 2048), n_blk * BN + (c + 1) * 32, rowt);
+            if (l2_hints & 2) {
+              const uint64_t pol_d = policy_evict_first();
+              tma_store_2d_hint(&tmD, smem_u32(my_stg), n_blk * BN + c * 32, rowt, pol_d);
+              if (two) tma_store_2d_hint(&tmD, smem_u32(my_stg + 2048), n_blk * BN + (c + 1) * 32, rowt, pol_d);
+            } else {
+              tma_store_2d(&tmD, smem_u32(my_stg), n_blk * BN + c * 32, rowt);
+              if (two) tma_store_2d(&tmD, smem_u32(my_stg + 2048), n_blk * BN + (c + 1) * 32, rowt);
+            }
             bulk_commit();
           }
           ++nst;
@@ -628,7 +654,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
           if (split >= 0) {
 #pragma unroll
             for (int j = 0; j < 32; j += 4)
-              __stcg(reinterpret_cast<float4*>(part + c * 32 + j),
+              __stcg(reinterpret_cast<float4*>(part + (size_t)((c * 32 + j) >> 2) * 512),
                      make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]), __uint_as_float(r[j + 2]),
                                  __uint_as_float(r[j + 3])));
           } else {
@@ -647,13 +673,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         acc_phase ^= 1;
       }
       if (split >= 0) {
-        // publish the partial; the last of the `splits` arrivals reduces (fixed order) + epilogue
+        // publish the partial; the last of the tile's pieces to arrive reduces (fixed order) + epilogue
+        const int cfirst = (tail * nkb) / tp.L, nsplit = ((tail + 1) * nkb - 1) / tp.L - cfirst + 1;
         __threadfence();
         epi_bar();
         if (warp == 4 && lane == 0) {
           const int old = atomicAdd(tp.counters + tail * 2 + rank, 1);
-          *fix_flag = (old == tp.splits - 1);
-          if (old == tp.splits - 1) tp.counters[tail * 2 + rank] = 0;  // self-reset for the next launch
+          *fix_flag = (old == nsplit - 1);
+          if (old == nsplit - 1) tp.counters[tail * 2 + rank] = 0;  // self-reset for the next launch
         }
         epi_bar();
         if (*fix_flag) {
@@ -663,11 +690,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
             float v[32];
 #pragma unroll
             for (int j = 0; j < 32; ++j) v[j] = 0.f;
-            for (int sp = 0; sp < tp.splits; ++sp) {
-              const float* ps = tp.ws + ((size_t)(tail * tp.splits + sp) * 2 + rank) * 128 * BN + (size_t)etid * BN + c * 32;
+            for (int sp = 0; sp < nsplit; ++sp) {  // pieces in cluster order: deterministic
+              const float* ps = tp.ws + ((size_t)(cfirst + sp + tail) * 2 + rank) * 128 * BN + (size_t)etid * 4;
 #pragma unroll
               for (int j = 0; j < 32; j += 4) {
-                const float4 x = __ldcg(reinterpret_cast<const float4*>(ps + j));
+                const float4 x = __ldcg(reinterpret_cast<const float4*>(ps + (size_t)((c * 32 + j) >> 2) * 512));
                 v[j] += x.x;
                 v[j + 1] += x.y;
                 v[j + 2] += x.z;
@@ -755,12 +782,12 @@ int tc_pick_bn(int M, int N) {
   return N <= 128 ? 128 : 256;
 }
 
-// fp32 partial-tile workspace + self-resetting arrival counters of the stream-K tail: rem * splits
-// <= pairs units of [2][128][256] fp32.  Contexts own one each (runtime.cu); launches without one
+// fp32 partial-tile workspace + self-resetting arrival counters of the stream-K tail: <= 2 * pairs slots
+// of [2][128][256] fp32 and rem < pairs counter pairs.  Contexts own one each (runtime.cu); launches without one
 // (the kernel-level ABI entry) share a per-device default.
 bool tail_ws_alloc(TailWs* w) {
-  const size_t units = (size_t)(num_sms() / 2);
-  if (cudaMalloc(&w->ws, units * 2 * 128 * 256 * sizeof(float)) != cudaSuccess ||
+  const size_t units = (size_t)(num_sms() / 2);  // slots <= clusters + tail tiles <= 2 * pairs
+  if (cudaMalloc(&w->ws, 2 * units * 2 * 128 * 256 * sizeof(float)) != cudaSuccess ||
       cudaMalloc(&w->counters, units * 2 * sizeof(int)) != cudaSuccess) {
     cudaGetLastError();
     tail_ws_free(w);
@@ -801,24 +828,37 @@ static void launch_pair_epi(const CUtensorMap& tmA, const CUtensorMap& tmB, cons
   const int num_m = (M + 255) / 256, num_n = (N + BN - 1) / BN;
   const int tiles = num_m * num_n;
   const int pairs = num_sms() / 2;
-  const int grid = 2 * (tiles < pairs ? tiles : pairs);
   const int nkb = (K + TC_BK - 1) / TC_BK;
-  TailPlan tp{tiles, 0, nullptr, nullptr};
+  // Stream-K tail (see TailPlan) when the last wave would leave >= 15% of the clusters idle and a tile
+  // is long (K >= 10240): splitting a tile costs ~7-12 us of partial-tile traffic and fix-up
+  // (measured: TP=4 out-proj 40 -> 48 us with 2 pieces per tail tile, qkv TP=8 60 -> 65 us), which
+  // only the long MLP-down tiles amortise.  ENERGON_NO_STREAMK=1 disables it (A/B, tests).
+  TailPlan tp{tiles, 0, 0, nullptr, nullptr};
   const int rem = tiles % pairs;
-  // Split the tail only when a tile is long (K >= 10240): the fp32 fix-up costs ~10-15 us, which
-  // outweighs the saved fraction of a wave for shorter K (profiles/r01_tile_sweep_streamk.log).
-  if (tiles > pairs && rem > 0 && nkb >= 160 && !getenv("ENERGON_NO_STREAMK")) {
-    int splits = pairs / rem;
-    if (splits > nkb / 4) splits = nkb / 4;  // at least 4 K-blocks per split
-    if (splits > 8) splits = 8;
-    if (splits >= 2) {
-      const TailWs* w = tw ? tw : default_tail_ws();
-      if (w->ws) tp = TailPlan{tiles - rem, splits, w->ws, w->counters};
+  int grid_cl = tiles < pairs ? tiles : pairs;
+  if (rem > 0 && (pairs - rem) * 100 >= 15 * pairs && nkb >= 160 && !getenv("ENERGON_NO_STREAMK")) {
+    const TailWs* w = tw ? tw : default_tail_ws();
+    if (w->ws) {
+      const int Lmin = (rem * nkb + pairs - 1) / pairs;  // every tail cluster index < pairs
+      int L = Lmin < 8 ? 8 : Lmin;
+      if (const char* f = getenv("ENERGON_SK_L")) L = atoi(f) > Lmin ? atoi(f) : L;  // experiment hook
+      tp = TailPlan{tiles - rem, L, rem, w->ws, w->counters};
+      const int used = (rem * nkb + L - 1) / L;  // clusters with tail work
+      if (grid_cl < used) grid_cl = used;
     }
   }
-  // group of A panels kept L2-resident while the group sweeps N (about 48 MB of A per group)
+  const int grid = 2 * grid_cl;
+  // group of A panels swept together along N: a wave of 74 concurrent tiles then spans group_m A panels
+  // and ~74/group_m W panels, each K-slice read from DRAM once per wave.  96 MB of A per group (group 8
+  // at K = 20480, all 16 m-blocks at K = 5120) measured ~1% faster in the step than 48 MB (group 4 at
+  // K = 20480 re-read the MLP-down weights ~4x: 1.46 GB of DRAM per launch for 420 MB algorithmic).
   const double panel = 256.0 * K * 2;
-  int group_m = (int)(48.0e6 / panel);
+  static double group_bytes = -1.0;
+  if (group_bytes < 0) {  // ENERGON_GROUP_MB: experiment hook for the A-panel group budget
+    const char* e = getenv("ENERGON_GROUP_MB");
+    group_bytes = (e ? atof(e) : 96.0) * 1e6;
+  }
+  int group_m = (int)(group_bytes / panel);
   if (group_m < 1) group_m = 1;
   if (group_m > num_m) group_m = num_m;
   CUtensorMap md;
@@ -832,8 +872,8 @@ static void launch_pair_epi(const CUtensorMap& tmA, const CUtensorMap& tmB, cons
   if (hints < 0) {
     // measured: evict_first(W) / evict_last(A) hints raise DRAM traffic (the 168 MB MLP-down panel
     // thrashes) and cost ~2% of the step, so they are off unless ENERGON_L2_HINTS=1
-    const char* e = getenv("ENERGON_L2_HINTS");
-    hints = (e && e[0] == '1') ? 1 : 0;
+    const char* e = getenv("ENERGON_L2_HINTS");  // bit 0: load hints, bit 1: evict_first on D stores
+    hints = e ? atoi(e) : 0;
   }
   launch_k(gemm_tc2_kernel<BN, EPI>, dim3(grid), dim3(128 + 32 * C::EPI_WARPS), C::SMEM, st, tmA, tmB, D, bias, M, N, K,
            group_m, qs, tp, md, hints);

@@ -370,10 +370,15 @@ def test_gemm_every_tile_shape(code, M, N, K, epi, monkeypatch):
     assert (np.abs(got - ref) <= 4e-3 * np.abs(ref) + 1e-4 * np.abs(ref).max()).all()
 
 
-@pytest.mark.parametrize("M,N,K,epi", [(2304, 2560, 10240, 2), (1200, 3800, 10240, 1)])
-def test_gemm_streamk_tail(M, N, K, epi, monkeypatch):
-    """Tail tiles split along K across idle clusters (90 tiles -> 16 tail tiles x 4 splits; 75 tiles ->
-    1 x 8): correct vs the oracle, deterministic run to run, close to the unsplit kernel."""
+@pytest.mark.parametrize("M,N,K,epi,L", [(2304, 2560, 10240, 2, 0), (1200, 3800, 10240, 1, 0),
+                                         (2304, 2560, 10240, 1, 50), (4096, 1920, 10240, 1, 0)])
+def test_gemm_streamk_tail(M, N, K, epi, L, monkeypatch):
+    """Stream-K tail: the tail tiles' k-iterations spread evenly over the clusters (90 tiles -> 16 tail
+    tiles in pieces of 35 k-blocks that straddle tile boundaries; 75 tiles -> 1 tile in 20 pieces of 8;
+    forced pieces of 50; 128 tiles -> 54 tail tiles): correct vs the oracle, deterministic run to run,
+    close to the unsplit kernel."""
+    if L:
+        monkeypatch.setenv("ENERGON_SK_L", str(L))
     tdt = torch.bfloat16
     g = torch.Generator(device="cpu").manual_seed(M + N)
     A = (torch.rand(M, K, generator=g) * 2 - 1).to(tdt)
