@@ -433,8 +433,8 @@ int attention_impl() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("ENERGON_ATTN");
-    v = e ? atoi(e) : 3;
-    if (v < 1 || v > 3) v = 3;
+    v = e ? atoi(e) : 4;
+    if (v < 1 || v > 4) v = 4;
   }
   return v;
 }
@@ -442,7 +442,9 @@ int attention_impl() {
 template <int D>
 static void launch_fa(const bf16* Q, const bf16* K, const bf16* V, bf16* O, bf16* Cp, const int* offsets,
                       const LensParam& lp, int B, int hk, int S, int causal, cudaStream_t st) {
-  if (attention_impl() == 3 && launch_attention_tc(Q, K, V, Cp, offsets, O, lp, B, hk, S, D, causal, st)) return;
+  if (attention_impl() >= 3 &&
+      launch_attention_tc(Q, K, V, Cp, offsets, O, lp, B, hk, S, D, causal, st, attention_impl() == 4))
+    return;
   const int gen = attention_impl() == 1 ? 1 : 2;
   dim3 grid((S + 63) / 64, hk, B);
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)D);

@@ -366,10 +366,331 @@ __global__ void __launch_bounds__(192, 2)
   }
 }
 
+// ============================================================================ v2: P in TMEM
+// Same work list, masks and numerics as attention_tc_kernel, restructured so that the softmax of key
+// tile j no longer waits for P_{j-1} V: S / P are double-buffered in TMEM (S_b at columns
+// [b BN, (b+1) BN), P_b written over the first BN/2 columns of S_b as packed bf16) and P V reads its A
+// operand straight from TMEM (tcgen05.mma ... [d], [a_tmem], b_desc), V is double-buffered in shared
+// memory, and the MMA thread issues S_{t+1} before P_t V_t across the CTA's whole tile sequence
+// (items included), so the tensor pipe works on the next scores while the softmax warps run.
+//   TMEM: S0 | S1 | O  (BN + BN + D <= 256 columns)      smem: Q | K[2] | V[2]
+// Ordering: S_t overwrites buffer t&1 only after P_{t-2} V (the last reader of that buffer) completed
+// (p_free); the O rescale waits for P_{t-1} V (o_full); P_t V is issued after p_full of tile t.
 template <int D>
+struct Attn2Cfg {
+  static constexpr int BM = 128, BN = 64, DH = D / 64;
+  static constexpr int Q_BYTES = BM * D * 2;
+  static constexpr int K_BYTES = BN * D * 2;
+  static constexpr int V_BYTES = BN * D * 2;
+  static constexpr int SMEM = Q_BYTES + 2 * K_BYTES + 2 * V_BYTES + 1024 + 256;
+  static constexpr int TMEM_COLS = 256;  // 2 * BN + D <= 256 for D <= 128
+  static constexpr uint32_t IDESC_S = AttnCfg<D>::IDESC_S;
+  static constexpr uint32_t IDESC_O = AttnCfg<D>::IDESC_O;
+};
+
+__device__ __forceinline__ void umma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc,
+                                             uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(
+          tmem_d),
+      "r"(tmem_a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+template <int D>
+__global__ void __launch_bounds__(192, 2)
+    attention_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                         const __grid_constant__ CUtensorMap tmV, bf16* __restrict__ Cp, const int* __restrict__ offsets,
+                         bf16* __restrict__ Opad, const __grid_constant__ LensParam lp, int hk, int S, int causal,
+                         float scale_log2, const __grid_constant__ AttnWork work) {
+  using C = Attn2Cfg<D>;
+  constexpr int BM = C::BM, BN = C::BN, DH = C::DH;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sK = sQ + C::Q_BYTES;
+  uint8_t* sV = sK + 2 * C::K_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + 2 * C::V_BYTES);
+  uint64_t* q_full = bars + 0;
+  uint64_t* q_empty = bars + 1;
+  uint64_t* o_empty = bars + 2;
+  uint64_t* o_full = bars + 3;    // [2]: P_t V_t done, one phase per two tiles (see the softmax waits)
+  uint64_t* k_full = bars + 5;    // [2]
+  uint64_t* k_empty = bars + 7;   // [2]
+  uint64_t* v_full = bars + 9;    // [2]
+  uint64_t* v_empty = bars + 11;  // [2]
+  uint64_t* s_full = bars + 13;   // [2]
+  uint64_t* p_full = bars + 15;   // [2]
+  uint64_t* p_free = bars + 17;   // [2]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 19);
+
+  const int items = work.npairs * hk;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmQ);
+    tma_prefetch_desc(&tmK);
+    tma_prefetch_desc(&tmV);
+    mbar_init(q_full, 1);
+    mbar_init(q_empty, 1);
+    mbar_init(o_empty, 4);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&o_full[i], 1);
+      mbar_init(&k_full[i], 1);
+      mbar_init(&k_empty[i], 1);
+      mbar_init(&v_full[i], 1);
+      mbar_init(&v_empty[i], 1);
+      mbar_init(&s_full[i], 1);
+      mbar_init(&p_full[i], 4);
+      mbar_init(&p_free[i], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                 "n"(C::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+  pdl_trigger();  // after the TMEM allocation (see attention_tc_kernel)
+  const uint32_t tO = tmem_base + 2 * BN;
+
+  auto decode = [&](int w, int& b, int& head, int& q0, int& nkv, int& len) {
+    const uint32_t pr = work.pair[w / hk];
+    head = w % hk;
+    b = (int)(pr >> 16);
+    q0 = (int)(pr & 0xFFFFu) * BM;
+    len = lp.lens[b];
+    const int kv_end = causal ? min(len, q0 + BM) : len;
+    nkv = (kv_end + BN - 1) / BN;
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer: per item Q once, then K_0, K_1, V_0, K_2, V_1, ... (t = CTA tile count)
+      pdl_wait();
+      int t = 0, qi = 0;
+      for (int w = blockIdx.x; w < items; w += gridDim.x, ++qi) {
+        int b, head, q0, nkv, len;
+        decode(w, b, head, q0, nkv, len);
+        const int row_base = (b * hk + head) * S;
+        mbar_wait(q_empty, (qi & 1) ^ 1);  // the previous item's last S has consumed Q
+        mbar_expect_tx(q_full, C::Q_BYTES);
+#pragma unroll
+        for (int h = 0; h < DH; ++h) tma_load_2d(&tmQ, smem_u32(sQ + h * BM * 128), q_full, h * 64, row_base + q0);
+        auto load_k = [&](int tt, int j) {
+          const int s2 = tt & 1;
+          mbar_wait(&k_empty[s2], ((tt >> 1) & 1) ^ 1);
+          mbar_expect_tx(&k_full[s2], C::K_BYTES);
+#pragma unroll
+          for (int h = 0; h < DH; ++h)
+            tma_load_2d(&tmK, smem_u32(sK + s2 * C::K_BYTES + h * BN * 128), &k_full[s2], h * 64, row_base + j * BN);
+        };
+        load_k(t, 0);
+        for (int j = 0; j < nkv; ++j) {
+          if (j + 1 < nkv) load_k(t + j + 1, j + 1);
+          const int tt = t + j, s2 = tt & 1;
+          mbar_wait(&v_empty[s2], ((tt >> 1) & 1) ^ 1);
+          mbar_expect_tx(&v_full[s2], C::V_BYTES);
+#pragma unroll
+          for (int h = 0; h < DH; ++h)
+            tma_load_2d(&tmV, smem_u32(sV + s2 * C::V_BYTES + h * BN * 128), &v_full[s2], h * 64, row_base + j * BN);
+        }
+        t += nkv;
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer: S_t, then P_{t-1} V_{t-1}, over the CTA's whole tile sequence
+      int w = blockIdx.x, qi = 0, j = 0, nkv = 0;
+      {
+        int b_, h_, q_, l_;
+        if (w < items) decode(w, b_, h_, q_, nkv, l_);
+      }
+      int t = 0;
+      int pv_j = -1, pv_qi = 0;  // the tile whose P V is pending (j within its item), -1: none
+      auto issue_pv = [&](int tt, int jj, int qq) {
+        const int b2 = tt & 1;
+        mbar_wait(&p_full[b2], (tt >> 1) & 1);
+        mbar_wait(&v_full[b2], (tt >> 1) & 1);
+        if (jj == 0) mbar_wait(o_empty, (qq & 1) ^ 1);  // the previous item's epilogue has read O
+        tc_fence_after();
+        const uint32_t tP = tmem_base + (uint32_t)(b2 * BN);
+#pragma unroll
+        for (int kk = 0; kk < BN / 16; ++kk) {
+          const uint64_t bb = umma_desc_sw128_mn(smem_u32(sV + b2 * C::V_BYTES + kk * 16 * 128), BN * 128);
+          umma_bf16_ts(tO, tP + (uint32_t)(kk * 8), bb, C::IDESC_O, (jj > 0 || kk > 0) ? 1u : 0u);
+        }
+        umma_commit(&v_empty[b2]);
+        umma_commit(&p_free[b2]);
+        umma_commit(&o_full[b2]);
+      };
+      while (w < items) {
+        const int b2 = t & 1;
+        if (j == 0) mbar_wait(q_full, qi & 1);
+        mbar_wait(&k_full[b2], (t >> 1) & 1);
+        mbar_wait(&p_free[b2], ((t >> 1) & 1) ^ 1);  // P_{t-2} V done: buffer b2 is free
+        tc_fence_after();
+        const uint32_t tS = tmem_base + (uint32_t)(b2 * BN);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t off = (kk & 3) * 32;
+          const uint64_t a = umma_desc_sw128(smem_u32(sQ + (kk >> 2) * BM * 128 + off));
+          const uint64_t bb = umma_desc_sw128(smem_u32(sK + b2 * C::K_BYTES + (kk >> 2) * BN * 128 + off));
+          umma_bf16(tS, a, bb, C::IDESC_S, kk > 0 ? 1u : 0u);
+        }
+        umma_commit(&k_empty[b2]);
+        if (j + 1 == nkv) umma_commit(q_empty);
+        umma_commit(&s_full[b2]);
+        if (pv_j >= 0) issue_pv(t - 1, pv_j, pv_qi);
+        pv_j = j;
+        pv_qi = qi;
+        ++t;
+        if (++j == nkv) {  // next item of this CTA
+          j = 0;
+          ++qi;
+          w += gridDim.x;
+          if (w < items) {
+            int b_, h_, q_, l_;
+            decode(w, b_, h_, q_, nkv, l_);
+          }
+        }
+      }
+      if (pv_j >= 0) issue_pv(t - 1, pv_j, pv_qi);
+    }
+  } else {
+    // ---------------- softmax warps: thread owns query row r (= TMEM lane r)
+    const int qd = warp & 3;
+    const int r = qd * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(qd * 32) << 16;
+    int t = 0;
+    for (int w = blockIdx.x; w < items; w += gridDim.x) {
+      int b, head, q0, nkv, len;
+      decode(w, b, head, q0, nkv, len);
+      const int srow = q0 + r;
+      float m_ref = -INFINITY, l = 0.f;
+      for (int j = 0; j < nkv; ++j, ++t) {
+        const int b2 = t & 1;
+        const uint32_t tS = tmem_base + (uint32_t)(b2 * BN) + lane_off;
+        const int k0 = j * BN;
+        mbar_wait(&s_full[b2], (t >> 1) & 1);
+        __syncwarp();
+        tc_fence_after();
+        uint32_t sr[2][32];
+        tmem_ld32_nowait(tS + 0, sr[0]);
+        tmem_ld32_nowait(tS + 32, sr[1]);
+        tmem_wait_ld();
+        float mt = -INFINITY;
+        const bool need_mask = (k0 + BN > len) || (causal && k0 + BN - 1 > q0 + qd * 32);
+        if (need_mask) {
+#pragma unroll
+          for (int c = 0; c < BN; ++c) {
+            const int tk = k0 + c;
+            float v = __uint_as_float(sr[c >> 5][c & 31]);
+            if (tk >= len || (causal && tk > srow)) v = -INFINITY;
+            sr[c >> 5][c & 31] = __float_as_uint(v);
+            mt = fmaxf(mt, v);
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < BN; ++c) mt = fmaxf(mt, __uint_as_float(sr[c >> 5][c & 31]));
+        }
+        mt *= scale_log2;
+        // lazy rescale, warp-wide (tcgen05.ld / st are .sync.aligned), alpha = 1 for rows keeping their max.
+        // Every tile's P V completion (o_full[t & 1], one phase per two tiles) is observed exactly once,
+        // in order: here when the rescale needs O, else right after this tile's P is handed over -- a
+        // parity wait must never fall two phases behind its barrier.
+        const bool grow = mt > m_ref + 8.f;
+        const float alpha = !grow ? 1.f : (m_ref == -INFINITY) ? 0.f : ex2f(m_ref - mt);
+        bool seen_prev = j == 0;  // the previous item's last P V was observed by its epilogue
+        if (j > 0 && __any_sync(0xffffffffu, grow)) {
+          mbar_wait(&o_full[(t - 1) & 1], ((t - 1) >> 1) & 1);  // P_{t-1} V_{t-1}: the last writer of O
+          seen_prev = true;
+          __syncwarp();
+          tc_fence_after();
+#pragma unroll 1
+          for (int c = 0; c < D; c += 32) {
+            uint32_t o[32];
+            tmem_ld32(tO + lane_off + c, o);
+#pragma unroll
+            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+            tmem_st32(tO + lane_off + c, o);
+          }
+        }
+        if (grow) {
+          l *= alpha;
+          m_ref = mt;
+        }
+        const float base = (m_ref == -INFINITY) ? 0.f : m_ref;
+        uint32_t pk[32];
+#pragma unroll
+        for (int c = 0; c < BN; c += 2) {
+          const float p0 = ex2f(fmaf(__uint_as_float(sr[c >> 5][c & 31]), scale_log2, -base));
+          const float p1 = ex2f(fmaf(__uint_as_float(sr[(c + 1) >> 5][(c + 1) & 31]), scale_log2, -base));
+          l += p0 + p1;
+          pk[c >> 1] = pack_bf16x2(p0, p1);
+        }
+        tmem_st32(tS, pk);  // P_t over the first BN/2 columns of S_t (S_t is in registers)
+        if (k0 + BN > len) {  // zero V rows of keys >= len (pad rows a5 never wrote may hold NaN)
+          mbar_wait(&v_full[b2], (t >> 1) & 1);
+          if (r < BN && k0 + r >= len) {
+#pragma unroll
+            for (int h = 0; h < DH; ++h) {
+              uint4* vr = reinterpret_cast<uint4*>(sV + b2 * C::V_BYTES + h * BN * 128 + r * 128);
+#pragma unroll
+              for (int c = 0; c < 8; ++c) vr[c] = make_uint4(0, 0, 0, 0);
+            }
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[b2]);
+        if (!seen_prev) mbar_wait(&o_full[(t - 1) & 1], ((t - 1) >> 1) & 1);
+      }
+      // ---------------- item epilogue: O / l -> packed context row (or padded O row)
+      mbar_wait(&o_full[(t - 1) & 1], ((t - 1) >> 1) & 1);
+      __syncwarp();
+      tc_fence_after();
+      const float inv = 1.f / l;
+      const bool valid = srow < len;
+      bf16* dst = Cp ? Cp + ((int64_t)__ldg(offsets + b) + srow) * (int64_t)(hk * D) + head * D
+                     : Opad + ((int64_t)(b * hk + head) * S + srow) * D;
+#pragma unroll 1
+      for (int c = 0; c < D; c += 32) {
+        uint32_t o[32];
+        tmem_ld32(tO + lane_off + c, o);
+        if (valid) {
+#pragma unroll
+          for (int e = 0; e < 32; e += 8) {
+            uint4 pq;
+            pq.x = pack_bf16x2(__uint_as_float(o[e]) * inv, __uint_as_float(o[e + 1]) * inv);
+            pq.y = pack_bf16x2(__uint_as_float(o[e + 2]) * inv, __uint_as_float(o[e + 3]) * inv);
+            pq.z = pack_bf16x2(__uint_as_float(o[e + 4]) * inv, __uint_as_float(o[e + 5]) * inv);
+            pq.w = pack_bf16x2(__uint_as_float(o[e + 6]) * inv, __uint_as_float(o[e + 7]) * inv);
+            *reinterpret_cast<uint4*>(dst + c + e) = pq;
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(o_empty);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(C::TMEM_COLS));
+  }
+}
+
+template <int D, bool V2>
 static bool launch_tc(const bf16* Q, const bf16* K, const bf16* V, bf16* Cp, const int* offsets, bf16* Opad,
                       const LensParam& lp, int B, int hk, int S, int causal, cudaStream_t st) {
   using C = AttnCfg<D>;
+  constexpr int SMEM = V2 ? Attn2Cfg<D>::SMEM : C::SMEM;
   // heaviest-first work list of (sequence, query tile) pairs, built from the host copy of the lengths
   AttnWork work;  // 8 KB kernel parameter (copied into the launch)
   int n = 0;
@@ -394,7 +715,8 @@ static bool launch_tc(const bf16* Q, const bf16* K, const bf16* V, bf16* Cp, con
     return false;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(attention_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    if (V2) cudaFuncSetAttribute(attention_tc2_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    else cudaFuncSetAttribute(attention_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
     attr = true;
   }
   const int items = n * hk;
@@ -402,15 +724,24 @@ static bool launch_tc(const bf16* Q, const bf16* K, const bf16* V, bf16* Cp, con
   const int grid = items < slots ? items : slots;
   if (grid <= 0) return true;
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)D);
-  launch_k(attention_tc_kernel<D>, dim3(grid), dim3(192), C::SMEM, st, mq, mk, mv, Cp, offsets, Opad, lp, hk, S,
-           causal, scale_log2, work);
+  if (V2)
+    launch_k(attention_tc2_kernel<D>, dim3(grid), dim3(192), SMEM, st, mq, mk, mv, Cp, offsets, Opad, lp, hk, S, causal,
+             scale_log2, work);
+  else
+    launch_k(attention_tc_kernel<D>, dim3(grid), dim3(192), SMEM, st, mq, mk, mv, Cp, offsets, Opad, lp, hk, S, causal,
+             scale_log2, work);
   return true;
 }
 
 bool launch_attention_tc(const bf16* Q, const bf16* K, const bf16* V, bf16* ctx_packed, const int* offsets,
-                         bf16* O_padded, const LensParam& lp, int B, int hk, int S, int d, int causal, cudaStream_t st) {
-  if (d == 128) return launch_tc<128>(Q, K, V, ctx_packed, offsets, O_padded, lp, B, hk, S, causal, st);
-  if (d == 64) return launch_tc<64>(Q, K, V, ctx_packed, offsets, O_padded, lp, B, hk, S, causal, st);
+                         bf16* O_padded, const LensParam& lp, int B, int hk, int S, int d, int causal, cudaStream_t st,
+                         bool v2) {
+  if (d == 128)
+    return v2 ? launch_tc<128, true>(Q, K, V, ctx_packed, offsets, O_padded, lp, B, hk, S, causal, st)
+              : launch_tc<128, false>(Q, K, V, ctx_packed, offsets, O_padded, lp, B, hk, S, causal, st);
+  if (d == 64)
+    return v2 ? launch_tc<64, true>(Q, K, V, ctx_packed, offsets, O_padded, lp, B, hk, S, causal, st)
+              : launch_tc<64, false>(Q, K, V, ctx_packed, offsets, O_padded, lp, B, hk, S, causal, st);
   return false;
 }
 

@@ -91,8 +91,9 @@ bool launch_attention_packed(const bf16* Q, const bf16* K, const bf16* V, bf16* 
                              const LensParam& lp, int B, int hk, int S, int d, int causal, cudaStream_t st);
 // tcgen05 / TMEM attention (d = 64 or 128): packed output (ctx_packed + offsets) or padded O.
 bool launch_attention_tc(const bf16* Q, const bf16* K, const bf16* V, bf16* ctx_packed, const int* offsets,
-                         bf16* O_padded, const LensParam& lp, int B, int hk, int S, int d, int causal, cudaStream_t st);
-int attention_impl();  // ENERGON_ATTN: 3 = tcgen05 (default), 2 = mma.sync v2, 1 = mma.sync v1
+                         bf16* O_padded, const LensParam& lp, int B, int hk, int S, int d, int causal, cudaStream_t st,
+                         bool v2);
+int attention_impl();  // ENERGON_ATTN: 4 = tcgen05, P in TMEM (default), 3 = tcgen05 v1, 2 / 1 = mma.sync
 
 // GEMM epilogues.  EPI_BIAS_QKV = bias, then a5 fused: the packed QKV row t / column block is
 // scattered straight into the padded per-head Q, K, V [B, hk, S, d] (needs d % 32 == 0).
