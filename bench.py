@@ -52,6 +52,8 @@ def parse():
                          "under torchrun (NCCL collectives run eagerly)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-tokens", type=int, default=192)
+    ap.add_argument("--comm", default="nccl", choices=["nccl", "p2p"],
+                    help="TP exchange under torchrun: NCCL, or the fused peer-memory kernels (CUDA IPC)")
     ap.add_argument("--local-tp", type=int, default=0,
                     help="emulate TP=k on ONE GPU with a local group (ranks serialised; per-rank kernel "
                          "shapes and ncu evidence of TP=k, not a TP=k latency)")
@@ -184,6 +186,7 @@ def workload_config(args, shape, bcfg, lens, world):
             "layers": shape["L"], "hidden": shape["H"], "heads": shape["h"], "batch": B, "max_len": S,
             "padding_ratio": round(1 - T / (B * S), 4), "valid_tokens_per_step": T, "tp": world,
             "parallelism": f"tp{world}", "drce": bool(args.drce), "cuda_graph": bool(getattr(args, "graph", 0)),
+            "tp_exchange": (getattr(args, "comm", "nccl") if world > 1 else "none"),
             "l2": "no flush: per-step working set (weights) > 126 MB L2"}
 
 
@@ -249,8 +252,9 @@ def energon_arm(args, world, rank, local):
     tok_np = synth.tokens(B, S, shape["V"], lens, args.seed)
     H = shape["H"]
 
+    comm = energon.COMM_P2P if (args.comm == "p2p" and world > 1) else energon.COMM_NCCL
     cfg = energon.make_config(shape["L"], H, shape["h"], shape["F"], shape["V"], shape["max_seq"], B * S,
-                              dtype="bf16", drce=args.drce, tp_size=world, tp_rank=rank, device=local)
+                              dtype="bf16", drce=args.drce, tp_size=world, tp_rank=rank, device=local, comm=comm)
     uid = None
     if world > 1:
         from paper_2209_02341_b200 import dist as edist
@@ -260,6 +264,10 @@ def energon_arm(args, world, rank, local):
         ctxs = energon.energon_init_local_group(cfg, args.local_tp)
     else:
         ctxs = [energon.energon_init(cfg, uid)]
+    if comm == energon.COMM_P2P:  # map every rank's exchange region (CUDA IPC handles, all-gathered)
+        handles = [None] * world
+        dist.all_gather_object(handles, energon.energon_p2p_handle(ctxs[0]))
+        energon.energon_p2p_connect(ctxs[0], handles)
     eng = Engine(energon, ctxs)
 
     # weights: generated on the device by the seeded counter-based generator, loaded unsharded

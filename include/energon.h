@@ -80,7 +80,9 @@ typedef struct {
   int32_t max_tokens;
   int32_t final_ln; /* 1 = apply the final LayerNorm */
   float ln_eps;     /* 1e-5 */
+  int32_t comm;     /* k > 1: ENERGON_COMM_NCCL (0, default) or ENERGON_COMM_P2P (1, see energon_p2p_connect) */
 } energon_config;
+enum { ENERGON_COMM_NCCL = 0, ENERGON_COMM_P2P = 1 };
 
 /*
  * One layer's weights, matrices [in, out] row-major (y = x W + b; SPEC.md:85,
@@ -154,6 +156,22 @@ ENERGON_API energon_status energon_offload_layers(energon_ctx* ctx, const int32_
 
 /* Host-only: the shard of cfg->tp_rank (validates cfg like energon_init; touches no device). */
 ENERGON_API energon_status energon_shard_plan(const energon_config* cfg, energon_shard* out);
+
+/*
+ * P2P TP exchange (cfg.comm = ENERGON_COMM_P2P, one process per GPU of one node): instead of NCCL the
+ * kernels reduce the row-parallel partials over peer memory ("accumulated by communications",
+ * PAPER.md:290) -- signal/wait flags, a reduce + bias + residual + LayerNorm kernel that reads every
+ * rank's partial rows of its own shard in rank order and stores the normalised rows straight into
+ * every rank's activation buffer (reduce-scatter, LN and all-gather in one pass over NVLink), and a
+ * completion flag.  Same results as the NCCL sequence-parallel schedule (bit-identical replicas).
+ *   energon_p2p_handle: 64-byte CUDA IPC handle of this rank's exchange region (after energon_init).
+ *   energon_p2p_connect: handles of all k ranks in rank order (the caller all-gathers them, e.g. with
+ *     torch.distributed); maps the peers' regions.  Required before the first forward.
+ * Errors: ENERGON_ERR_CONFIG unless cfg.comm == P2P and tp_size > 1; ENERGON_ERR_CUDA if a handle
+ * cannot be opened.  Forward calls are SPMD and must be issued by every rank (they wait for peers).
+ */
+ENERGON_API energon_status energon_p2p_handle(energon_ctx* ctx, void* out_64_bytes);
+ENERGON_API energon_status energon_p2p_connect(energon_ctx* ctx, const void* handles_k_x_64_bytes);
 
 /* 128-byte NCCL unique id for a TP group (call on one rank, broadcast the bytes). */
 ENERGON_API energon_status energon_get_unique_id(void* out_128_bytes);

@@ -42,6 +42,20 @@ struct PtrList {
   void* p[8];
 };
 
+// P2P TP exchange over CUDA-IPC-mapped peer regions (kernels_misc.cu; protocol described there)
+struct PeerSet {
+  void* base[8];  // exchange region of every rank of the TP group (own included)
+};
+enum { P2P_READY = 0, P2P_DELIVERED = 1 };
+constexpr int64_t P2P_FLAG_BYTES = 256;  // ready[8] | delivered[8] u64 | completion counter
+void launch_p2p_flag(const PeerSet& ps, int k, int me, int kind, uint64_t epoch, int do_signal, cudaStream_t st);
+template <typename Act>
+void launch_p2p_reduce_ln(const PeerSet& ps, int k, int me, int64_t off_X, int64_t off_A, int64_t off_P, int row0,
+                          int rows, int H, const float* bias, const float* g, const float* b, float eps, int write_A,
+                          uint64_t epoch, cudaStream_t st);
+void launch_p2p_push_rows(const PeerSet& ps, int k, int me, int64_t off, int row0, int rows, int64_t row_bytes,
+                          uint64_t epoch, cudaStream_t st);
+
 // a1
 void launch_index_maps(const LensParam& lp, int B, int S, int* offsets, int* pack_idx, int* pos, int* unpack_idx,
                        cudaStream_t st);

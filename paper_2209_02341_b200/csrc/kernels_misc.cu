@@ -584,6 +584,177 @@ void launch_convert_vec(const Src* src, int64_t off, int N, Dst* dst, cudaStream
 }
 
 // explicit instantiations
+
+// ============================================================================ P2P TP exchange
+// One process per GPU, peers' exchange regions mapped by CUDA IPC (energon_p2p_connect): the TP
+// reduction of the row-parallel partial is done by the kernels themselves over peer memory instead
+// of NCCL ("accumulated by communications").  Region of every rank (same offsets):
+//   [flags: ready[8] | delivered[8] u64, counter] [X fp32 R x H] [A act R x H] [P act R x H]
+// Protocol per exchange (epoch e, identical on every rank -- SPMD):
+//   p2p_flag(READY, signal+wait): after this rank's GEMM wrote P, publish ready[me] = e on every peer
+//     (release.sys) and wait until every peer published ready = e here;
+//   p2p_reduce_ln: rows of this rank's shard: sum_q P_q[t] in rank order (fp32, rounded to act like
+//     ncclReduceScatter), + bias + residual -> X (own rows), LN -> A row stored into EVERY rank's A
+//     (the all-gather as NVLink stores); the last block to finish publishes delivered[me] = e;
+//   p2p_flag(DELIVERED, wait): every peer's rows arrived here -- and every peer finished reading this
+//     rank's P, so the next GEMM may overwrite it.
+// The flag kernels are one block and never trigger their dependents early, so no kernel holds SMs
+// while a rank waits for its peers (a single GPU shared by several ranks stays deadlock-free).
+struct PeerSetK {
+  char* base[8];
+};
+
+__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__global__ void p2p_flag_kernel(PeerSetK ps, int k, int me, int kind, uint64_t epoch, int do_signal) {
+  pdl_wait();  // the kernel before (the GEMM writing P, or the pushing kernel) has completed
+  const int q = threadIdx.x;
+  if (q < k && do_signal) {
+    __threadfence_system();
+    st_release_sys(reinterpret_cast<uint64_t*>(ps.base[q]) + kind * 8 + me, epoch);
+  }
+  if (q < k) {
+    const uint64_t* f = reinterpret_cast<const uint64_t*>(ps.base[me]) + kind * 8 + q;
+    while (ld_acquire_sys(f) < epoch) __nanosleep(100);
+  }
+}
+
+// last block of a grid publishes delivered[me] = epoch on every peer (after all blocks' stores)
+__device__ __forceinline__ void p2p_grid_done(const PeerSetK& ps, int k, int me, uint64_t epoch) {
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned* counter = reinterpret_cast<unsigned*>(ps.base[me] + 16 * sizeof(uint64_t));
+    const unsigned prev = atomicAdd(counter, 1u);
+    if (prev == gridDim.x - 1) {
+      *counter = 0;  // self-reset for the next exchange (stream-ordered)
+      __threadfence_system();
+      for (int q = 0; q < k; ++q) st_release_sys(reinterpret_cast<uint64_t*>(ps.base[q]) + 8 + me, epoch);
+    }
+  }
+}
+
+template <typename Act, int LN_MAXV, int TPR>
+__global__ void __launch_bounds__(TPR) p2p_reduce_ln_kernel(PeerSetK ps, int k, int me, int64_t off_X, int64_t off_A,
+                                                            int64_t off_P, int row0, int rows, int H,
+                                                            const float* __restrict__ bias,
+                                                            const float* __restrict__ g, const float* __restrict__ b,
+                                                            float eps, int write_A, uint64_t epoch) {
+  pdl_trigger();
+  pdl_wait();
+  __shared__ float red[32];
+  if ((int)blockIdx.x < rows) {
+    const int t = row0 + blockIdx.x;
+    float* xrow = reinterpret_cast<float*>(ps.base[me] + off_X) + (int64_t)t * H;
+    float4 v[LN_MAXV], acc[LN_MAXV];
+    int nv = 0;
+#pragma unroll
+    for (int i = 0; i < LN_MAXV; ++i) {
+      const int c = threadIdx.x + i * TPR;
+      if (c < H / 4) {
+        v[i] = __ldcs(reinterpret_cast<const float4*>(xrow) + c);
+        acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        nv = i + 1;
+      }
+    }
+    for (int q = 0; q < k; ++q) {  // rank order: every rank sums the same way
+      const Act* prow = reinterpret_cast<const Act*>(ps.base[q] + off_P) + (int64_t)t * H;
+#pragma unroll
+      for (int i = 0; i < LN_MAXV; ++i)
+        if (i < nv) {
+          const float4 x = Row4<Act>::load(prow + 4 * (threadIdx.x + i * TPR));
+          acc[i].x += x.x;
+          acc[i].y += x.y;
+          acc[i].z += x.z;
+          acc[i].w += x.w;
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < LN_MAXV; ++i)
+      if (i < nv) {
+        const int c = threadIdx.x + i * TPR;
+        const float4 q = *reinterpret_cast<const float4*>(bias + 4 * c);
+        // the reduced partial is rounded to the activation type, as a reduce-scatter would store it
+        v[i].x += to_f32(from_f32<Act>(acc[i].x)) + q.x;
+        v[i].y += to_f32(from_f32<Act>(acc[i].y)) + q.y;
+        v[i].z += to_f32(from_f32<Act>(acc[i].z)) + q.z;
+        v[i].w += to_f32(from_f32<Act>(acc[i].w)) + q.w;
+        Row4<float>::store(xrow + 4 * c, v[i]);
+      }
+    if (write_A) {
+      float mean, rstd;
+      row_stats(v, nv, H, eps, red, mean, rstd);
+#pragma unroll
+      for (int i = 0; i < LN_MAXV; ++i)
+        if (i < nv) {
+          const int j = 4 * (threadIdx.x + i * TPR);
+          const float4 y = ln_apply(v[i], mean, rstd, g, b, j);
+          for (int q = 0; q < k; ++q)
+            Row4<Act>::store(reinterpret_cast<Act*>(ps.base[q] + off_A) + (int64_t)t * H + j, y);
+        }
+    }
+  }
+  p2p_grid_done(ps, k, me, epoch);
+}
+
+// all-gather by pushing: this rank's rows [row0, row0 + rows) of the buffer at `off` (row_bytes each)
+// are stored into the same rows of every peer's region
+__global__ void p2p_push_rows_kernel(PeerSetK ps, int k, int me, int64_t off, int row0, int rows, int64_t row_bytes,
+                                     uint64_t epoch) {
+  pdl_trigger();
+  pdl_wait();
+  const int64_t n16 = (int64_t)rows * row_bytes / 16;
+  const uint4* src = reinterpret_cast<const uint4*>(ps.base[me] + off + (int64_t)row0 * row_bytes);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n16; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint4 v = src[i];
+    for (int q = 0; q < k; ++q)
+      if (q != me) reinterpret_cast<uint4*>(ps.base[q] + off + (int64_t)row0 * row_bytes)[i] = v;
+  }
+  p2p_grid_done(ps, k, me, epoch);
+}
+
+void launch_p2p_flag(const PeerSet& ps, int k, int me, int kind, uint64_t epoch, int do_signal, cudaStream_t st) {
+  PeerSetK p;
+  for (int i = 0; i < 8; ++i) p.base[i] = reinterpret_cast<char*>(ps.base[i]);
+  launch_k(p2p_flag_kernel, dim3(1), dim3(32), 0, st, p, k, me, kind, epoch, do_signal);
+}
+
+template <typename Act>
+void launch_p2p_reduce_ln(const PeerSet& ps, int k, int me, int64_t off_X, int64_t off_A, int64_t off_P, int row0,
+                          int rows, int H, const float* bias, const float* g, const float* b, float eps, int write_A,
+                          uint64_t epoch, cudaStream_t st) {
+  PeerSetK p;
+  for (int i = 0; i < 8; ++i) p.base[i] = reinterpret_cast<char*>(ps.base[i]);
+  const int grid = rows > 0 ? rows : 1;  // an empty shard still takes part in the completion count
+  const int tpr = ln_tpr(H);
+  if (tpr == 512)
+    NV_DISPATCH_T(H, 512, (launch_k(p2p_reduce_ln_kernel<Act, NVX, 512>, dim3(grid), dim3(512), 0, st, p, k, me, off_X,
+                                    off_A, off_P, row0, rows, H, bias, g, b, eps, write_A, epoch)))
+  else
+    NV_DISPATCH_T(H, 256, (launch_k(p2p_reduce_ln_kernel<Act, NVX, 256>, dim3(grid), dim3(256), 0, st, p, k, me, off_X,
+                                    off_A, off_P, row0, rows, H, bias, g, b, eps, write_A, epoch)))
+}
+
+void launch_p2p_push_rows(const PeerSet& ps, int k, int me, int64_t off, int row0, int rows, int64_t row_bytes,
+                          uint64_t epoch, cudaStream_t st) {
+  PeerSetK p;
+  for (int i = 0; i < 8; ++i) p.base[i] = reinterpret_cast<char*>(ps.base[i]);
+  const int64_t n16 = (int64_t)rows * row_bytes / 16;
+  const int grid = n16 > 0 ? grid_for(n16, 256, 148 * 4) : 1;
+  launch_k(p2p_push_rows_kernel, dim3(grid), dim3(256), 0, st, p, k, me, off, row0, rows, row_bytes, epoch);
+}
+template void launch_p2p_reduce_ln<float>(const PeerSet&, int, int, int64_t, int64_t, int64_t, int, int, int,
+                                          const float*, const float*, const float*, float, int, uint64_t, cudaStream_t);
+template void launch_p2p_reduce_ln<bf16>(const PeerSet&, int, int, int64_t, int64_t, int64_t, int, int, int,
+                                         const float*, const float*, const float*, float, int, uint64_t, cudaStream_t);
+
 #define INST_ACT(Act)                                                                                                   \
   template void launch_embed_ln<Act>(const int*, const int*, int, int, int, int, int, const Act*, const Act*,            \
                                      const float*, const float*, float, float*, Act*, int*, cudaStream_t);              \

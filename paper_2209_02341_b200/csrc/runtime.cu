@@ -77,6 +77,13 @@ struct energon_ctx {
   size_t act = 4;  // bytes per activation element
   ncclComm_t nccl = nullptr;
   bool local_group = false;
+  // P2P TP exchange (cfg.comm == ENERGON_COMM_P2P): X | A | P live in one IPC-exportable region
+  bool p2p = false, p2p_connected = false;
+  void* region = nullptr;
+  int64_t off_X = 0, off_A = 0, off_P = 0;
+  PeerSet peers{};
+  std::vector<void*> ipc_opened;
+  uint64_t epoch = 0;
   bool fuse = true;  // fused a5 / a7 (ENERGON_NO_FUSE=1 disables, for A/B and tests)
   bool sp = true;    // k > 1: sequence-parallel schedule (reduce-scatter / LN on own rows / all-gather)
   // CUDA-graph cache (ENERGON_OPT_GRAPH): whole forwards captured on cap_stream, replayed on the caller's
@@ -175,6 +182,8 @@ energon_status validate_config(const energon_config* cfg) {
   if (cfg->causal != 0 && cfg->causal != 1) return fail(nullptr, ENERGON_ERR_CONFIG, "causal must be 0 or 1");
   if (cfg->drce != 0 && cfg->drce != 1) return fail(nullptr, ENERGON_ERR_CONFIG, "drce must be 0 or 1");
   if (!(cfg->ln_eps > 0.f)) return fail(nullptr, ENERGON_ERR_CONFIG, "ln_eps must be > 0");
+  if (cfg->comm != ENERGON_COMM_NCCL && cfg->comm != ENERGON_COMM_P2P)
+    return fail(nullptr, ENERGON_ERR_CONFIG, "comm must be ENERGON_COMM_NCCL or ENERGON_COMM_P2P");
   const int d = cfg->hidden / cfg->num_heads;
   if (cfg->hidden % 8 || d % 8 || (cfg->ffn / cfg->tp_size) % 8 || cfg->hidden > 12288)
     return fail(nullptr, ENERGON_ERR_SHAPE,
@@ -210,14 +219,29 @@ energon_status setup(energon_ctx* c) {
   const size_t R = (size_t)g.max_tokens + 8, a = c->act;
   int64_t* ws = &c->stats.workspace_bytes;
   energon_status s;
+  c->p2p = g.comm == ENERGON_COMM_P2P && c->k > 1 && !c->local_group;
+  if (c->p2p) {
+    // one region [flags | X | A | P] (same offsets on every rank) that peers map by CUDA IPC
+    auto al = [](int64_t x) { return (x + 255) & ~(int64_t)255; };
+    c->off_X = P2P_FLAG_BYTES;
+    c->off_A = al(c->off_X + (int64_t)sizeof(float) * R * c->H);
+    c->off_P = al(c->off_A + (int64_t)a * R * c->H);
+    const int64_t bytes = al(c->off_P + (int64_t)a * R * c->H);
+    if ((s = dalloc(c, reinterpret_cast<char**>(&c->region), (size_t)bytes, ws))) return s;
+    CU(c, cudaMemset(c->region, 0, (size_t)bytes));
+    c->X = reinterpret_cast<float*>(static_cast<char*>(c->region) + c->off_X);
+    c->A = static_cast<char*>(c->region) + c->off_A;
+    c->P = static_cast<char*>(c->region) + c->off_P;
+  } else if ((s = dalloc(c, &c->X, sizeof(float) * R * c->H, ws)) || (s = dalloc(c, &c->A, a * R * c->H, ws)) ||
+             (s = dalloc(c, &c->P, a * R * c->H, ws))) {
+    return s;
+  }
   if ((s = dalloc(c, &c->offsets, sizeof(int) * (ENERGON_MAX_BATCH + 1), ws)) ||
       (s = dalloc(c, &c->pack_idx, sizeof(int) * R, ws)) || (s = dalloc(c, &c->pos, sizeof(int) * R, ws)) ||
-      (s = dalloc(c, &c->unpack_idx, sizeof(int) * R, ws)) || (s = dalloc(c, &c->X, sizeof(float) * R * c->H, ws)) ||
-      (s = dalloc(c, &c->A, a * R * c->H, ws)) || (s = dalloc(c, &c->QKV, a * R * 3 * c->Hk, ws)) ||
+      (s = dalloc(c, &c->unpack_idx, sizeof(int) * R, ws)) || (s = dalloc(c, &c->QKV, a * R * 3 * c->Hk, ws)) ||
       (s = dalloc(c, &c->Q, a * R * c->Hk, ws)) || (s = dalloc(c, &c->K, a * R * c->Hk, ws)) ||
       (s = dalloc(c, &c->Vb, a * R * c->Hk, ws)) || (s = dalloc(c, &c->O, a * R * c->Hk, ws)) ||
-      (s = dalloc(c, &c->Ctx, a * R * c->Hk, ws)) || (s = dalloc(c, &c->P, a * R * c->H, ws)) ||
-      (s = dalloc(c, &c->G, a * R * c->Fk, ws)))
+      (s = dalloc(c, &c->Ctx, a * R * c->Hk, ws)) || (s = dalloc(c, &c->G, a * R * c->Fk, ws)))
     return s;
   // zero every activation buffer once: rows a schedule reads but never writes (sequence-parallel
   // padding rows, unwritten Ctx rows) stay finite
@@ -235,6 +259,8 @@ void release(energon_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->cfg.device);
   cudaDeviceSynchronize();
+  for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
+  c->ipc_opened.clear();
   for (void* p : c->allocs) cudaFree(p);
   c->allocs.clear();
   tail_ws_free(&c->tail);
@@ -403,6 +429,7 @@ energon_status check_ready(energon_ctx* c, const Call& a) {
   for (int l = a.l0; l < a.l1; ++l)
     if (!c->layers[l].loaded) return fail(c, ENERGON_ERR_NOT_LOADED, "layer " + std::to_string(l) + " not loaded");
   if (*c->err_host) return fail(c, ENERGON_ERR_TOKEN, "a token id outside [0, vocab) was seen by a previous forward");
+  if (c->p2p && !c->p2p_connected) return fail(c, ENERGON_ERR_NOT_LOADED, "P2P peers not connected (energon_p2p_connect)");
   return ENERGON_OK;
 }
 
@@ -480,6 +507,45 @@ energon_status tp_gather(energon_ctx** cs, int n, int rpr, bool x_buf, cudaStrea
   return ENERGON_OK;
 }
 
+// ---- P2P exchange (cfg.comm == ENERGON_COMM_P2P; kernels_misc.cu describes the protocol)
+template <typename Act>
+void p2p_exchange(energon_ctx* c, int rows, int rpr, const float* bias, const float* g, const float* b, bool write_A,
+                  cudaStream_t st) {
+  const int r0 = std::min(rows, c->r * rpr), sn = std::max(0, std::min(rows, (c->r + 1) * rpr) - c->r * rpr);
+  const uint64_t e = ++c->epoch;
+  {
+    Prof p(c, st, P_COMM, 0.0);
+    launch_p2p_flag(c->peers, c->k, c->r, P2P_READY, e, 1, st);
+  }
+  {
+    // bytes over NVLink + local: k partial rows read, (write_A ? k : 0) LN rows stored, X read + written
+    Prof p(c, st, P_COMM, (double)sn * c->H * (c->k * sizeof(Act) + (write_A ? c->k * sizeof(Act) : 0) + 8.0));
+    launch_p2p_reduce_ln<Act>(c->peers, c->k, c->r, c->off_X, c->off_A, c->off_P, r0, sn, c->H, bias, g, b,
+                              c->cfg.ln_eps, write_A ? 1 : 0, e, st);
+  }
+  {
+    Prof p(c, st, P_COMM, 0.0);
+    launch_p2p_flag(c->peers, c->k, c->r, P2P_DELIVERED, e, 0, st);
+  }
+  c->stats.kernel_launches += 3;
+  c->stats.allreduce_calls++;
+}
+
+// all-gather of this rank's row shard of the buffer at `off` (row_bytes per row) by pushing to peers
+void p2p_gather(energon_ctx* c, int rows, int rpr, int64_t off, int64_t row_bytes, cudaStream_t st) {
+  const int r0 = std::min(rows, c->r * rpr), sn = std::max(0, std::min(rows, (c->r + 1) * rpr) - c->r * rpr);
+  const uint64_t e = ++c->epoch;
+  {
+    Prof p(c, st, P_COMM, (double)sn * row_bytes * (c->k - 1));
+    launch_p2p_push_rows(c->peers, c->k, c->r, off, r0, sn, row_bytes, e, st);
+  }
+  {
+    Prof p(c, st, P_COMM, 0.0);
+    launch_p2p_flag(c->peers, c->k, c->r, P2P_DELIVERED, e, 0, st);
+  }
+  c->stats.kernel_launches += 2;
+}
+
 template <typename Act>
 void gemm(energon_ctx* c, const CUtensorMap& tmA, const CUtensorMap* tmB, const void* A, const void* W,
           const float* bias, void* D, int M, int N, int K, int epi, cudaStream_t st, const QkvScatter* qs = nullptr,
@@ -527,7 +593,8 @@ energon_status forward_t(energon_ctx** cs, int n, const Call& a, int64_t T) {
   const bool fuse_a5 = sizeof(Act) == 2 && c0->fuse && (c0->d == 64 || c0->d == 128);
   const bool fuse_a7 = fuse_a5 && drce;
   // TP schedule: row shard [r0, r0 + sn) of each rank (the whole range without sequence parallelism)
-  const bool sp = c0->k > 1 && c0->sp;
+  const bool p2p = c0->p2p;  // one context per process, peers over CUDA IPC (sequence-parallel schedule)
+  const bool sp = c0->k > 1 && (c0->sp || p2p);
   const int rpr = sp ? (rows + c0->k - 1) / c0->k : rows;
   auto shard0 = [&](const energon_ctx* c) { return sp ? std::min(rows, c->r * rpr) : 0; };
   auto shardn = [&](const energon_ctx* c) { return sp ? std::max(0, std::min(rows, (c->r + 1) * rpr) - c->r * rpr) : rows; };
@@ -591,7 +658,9 @@ energon_status forward_t(energon_ctx** cs, int n, const Call& a, int64_t T) {
     }
     c->stats.kernel_launches++;
   }
-  if (sp) {
+  if (p2p) {
+    p2p_gather(c0, rows, rpr, c0->off_A, (int64_t)sizeof(Act) * c0->H, st);
+  } else if (sp) {
     energon_status s = tp_gather<Act>(cs, n, rpr, false, st);
     if (s) return s;
   }
@@ -644,10 +713,14 @@ energon_status forward_t(energon_ctx** cs, int n, const Call& a, int64_t T) {
       }
       gemm<Act>(c, c->tmA_Ctx, W.tm_o, c->Ctx, W.wo, nullptr, c->P, rows, c->H, c->Hk, EPI_NONE, st, nullptr, &c->tmD_P);
     }
-    energon_status s = tp_reduce<Act>(cs, n, rows, rpr, sp, st);
-    if (s) return s;
+    energon_status s = ENERGON_OK;
+    if (p2p) {  // a9 fused: reduce over peer memory + bias + residual + LN2, LN rows pushed to every rank
+      const LayerDev& L = c0->layers[l];
+      p2p_exchange<Act>(c0, rows, rpr, L.bo, L.ln2g, L.ln2b, true, st);
+    }
+    if (!p2p && (s = tp_reduce<Act>(cs, n, rows, rpr, sp, st))) return s;
     // ---- a9: bias + residual + LN2 on this rank's rows, then (SP) all-gather of the LN output
-    for (int i = 0; i < n; ++i) {
+    for (int i = 0; i < n && !p2p; ++i) {
       energon_ctx* c = cs[i];
       const LayerDev& L = c->layers[l];
       const size_t o = (size_t)shard0(c) * c->H;
@@ -657,7 +730,7 @@ energon_status forward_t(energon_ctx** cs, int n, const Call& a, int64_t T) {
                               reinterpret_cast<Act*>(c->A) + o, st);
       c->stats.kernel_launches++;
     }
-    if (sp && (s = tp_gather<Act>(cs, n, rpr, false, st))) return s;
+    if (sp && !p2p && (s = tp_gather<Act>(cs, n, rpr, false, st))) return s;
     // ---- MLP module: column-parallel W1 (+GeLU), row-parallel W2
     for (int i = 0; i < n; ++i) {
       energon_ctx* c = cs[i];
@@ -673,11 +746,15 @@ energon_status forward_t(energon_ctx** cs, int n, const Call& a, int64_t T) {
         if (jn < (int)off_order[i].size()) pmep_fetch(c, jn, off_order[i][jn]);
       }
     }
-    s = tp_reduce<Act>(cs, n, rows, rpr, sp, st);
-    if (s) return s;
-    // ---- a12: bias + residual (+ LN1 of the next layer) on this rank's rows
     const bool last = (l + 1 == a.l1);
-    for (int i = 0; i < n; ++i) {
+    if (p2p) {  // a12 fused (LN1 of the next layer, none after the last layer)
+      const LayerDev& L = c0->layers[l];
+      const LayerDev& Ln = c0->layers[last ? l : l + 1];
+      p2p_exchange<Act>(c0, rows, rpr, L.b2, Ln.ln1g, Ln.ln1b, !last, st);
+    }
+    if (!p2p && (s = tp_reduce<Act>(cs, n, rows, rpr, sp, st))) return s;
+    // ---- a12: bias + residual (+ LN1 of the next layer) on this rank's rows
+    for (int i = 0; i < n && !p2p; ++i) {
       energon_ctx* c = cs[i];
       const LayerDev& L = c->layers[l];
       const LayerDev& Ln = c->layers[last ? l : l + 1];
@@ -688,9 +765,12 @@ energon_status forward_t(energon_ctx** cs, int n, const Call& a, int64_t T) {
                               last ? nullptr : reinterpret_cast<Act*>(c->A) + o, st);
       c->stats.kernel_launches++;
     }
-    if (sp && !last && (s = tp_gather<Act>(cs, n, rpr, false, st))) return s;
+    if (sp && !p2p && !last && (s = tp_gather<Act>(cs, n, rpr, false, st))) return s;
   }
-  if (sp) {
+  if (p2p) {
+    // the final LN / unpack (or the next pipeline stage) needs every row of the residual stream
+    p2p_gather(c0, rows, rpr, c0->off_X, (int64_t)sizeof(float) * c0->H, st);
+  } else if (sp) {
     // the final LN / unpack needs every row of the residual stream on every rank
     energon_status s = tp_gather<float>(cs, n, rpr, true, st);
     if (s) return s;
@@ -748,7 +828,7 @@ energon_status run(energon_ctx** cs, int n, const Call& a) {
   energon_status s = validate_call(c0, a, &T);
   if (s) return s;
   bool graph_ok = c0->graphs && c0->cap_stream;
-  for (int i = 0; i < n; ++i) graph_ok = graph_ok && !cs[i]->prof && cs[i]->pm.layers.empty();
+  for (int i = 0; i < n; ++i) graph_ok = graph_ok && !cs[i]->prof && cs[i]->pm.layers.empty() && !cs[i]->p2p;
   if (!graph_ok) return run_eager(cs, n, a, T);
 
   // ---- CUDA graph: key = everything the launch sequence depends on
@@ -952,6 +1032,45 @@ energon_status energon_shard_plan(const energon_config* cfg, energon_shard* out)
   return ENERGON_OK;
 }
 
+energon_status energon_p2p_handle(energon_ctx* c, void* out) {
+  if (!c || !out) return fail(c, ENERGON_ERR_ARG, "NULL argument");
+  if (!c->p2p) return fail(c, ENERGON_ERR_CONFIG, "context was not created with comm = ENERGON_COMM_P2P and tp_size > 1");
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+  CU(c, cudaSetDevice(c->cfg.device));
+  cudaIpcMemHandle_t h;
+  CU(c, cudaIpcGetMemHandle(&h, c->region));
+  memcpy(out, &h, sizeof(h));
+  return ENERGON_OK;
+}
+
+energon_status energon_p2p_connect(energon_ctx* c, const void* handles) {
+  if (!c || !handles) return fail(c, ENERGON_ERR_ARG, "NULL argument");
+  if (!c->p2p) return fail(c, ENERGON_ERR_CONFIG, "context was not created with comm = ENERGON_COMM_P2P and tp_size > 1");
+  if (c->p2p_connected) return fail(c, ENERGON_ERR_ARG, "already connected");
+  CU(c, cudaSetDevice(c->cfg.device));
+  const char* hs = static_cast<const char*>(handles);
+  for (int q = 0; q < c->k; ++q) {
+    if (q == c->r) {
+      c->peers.base[q] = c->region;
+      continue;
+    }
+    cudaIpcMemHandle_t h;
+    memcpy(&h, hs + 64 * q, 64);
+    void* p = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      for (void* o : c->ipc_opened) cudaIpcCloseMemHandle(o);
+      c->ipc_opened.clear();
+      return cuda_fail(c, e, ("cudaIpcOpenMemHandle(rank " + std::to_string(q) + ")").c_str());
+    }
+    c->ipc_opened.push_back(p);
+    c->peers.base[q] = p;
+  }
+  c->p2p_connected = true;
+  return ENERGON_OK;
+}
+
 energon_status energon_get_unique_id(void* out) {
   if (!out) return fail(nullptr, ENERGON_ERR_ARG, "out is NULL");
   ncclUniqueId id;
@@ -966,7 +1085,8 @@ energon_status energon_init(const energon_config* cfg, const void* uid, energon_
   *out = nullptr;
   energon_status s = validate_config(cfg);
   if (s) return s;
-  if (cfg->tp_size > 1 && !uid) return fail(nullptr, ENERGON_ERR_ARG, "nccl_unique_id required when tp_size > 1");
+  if (cfg->tp_size > 1 && cfg->comm == ENERGON_COMM_NCCL && !uid)
+    return fail(nullptr, ENERGON_ERR_ARG, "nccl_unique_id required when tp_size > 1 with NCCL");
   energon_ctx* c = new energon_ctx();
   c->cfg = *cfg;
   if ((s = setup(c))) {
@@ -974,7 +1094,7 @@ energon_status energon_init(const energon_config* cfg, const void* uid, energon_
     release(c);
     return s;
   }
-  if (cfg->tp_size > 1) {
+  if (cfg->tp_size > 1 && cfg->comm == ENERGON_COMM_NCCL) {
     ncclUniqueId id;
     memcpy(&id, uid, sizeof(id));
     ncclResult_t e = ncclCommInitRank(&c->nccl, cfg->tp_size, id, cfg->tp_rank);

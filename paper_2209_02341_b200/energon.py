@@ -23,6 +23,7 @@ OPT_DRCE = 1
 OPT_TP_SP = 2
 OPT_GRAPH = 3
 STAGE_PACKED, STAGE_FINAL = 0, 1
+COMM_NCCL, COMM_P2P = 0, 1
 LAYER_TENSORS = ("wq", "wk", "wv", "wo", "bq", "bk", "bv", "bo",
                  "w1", "b1", "w2", "b2", "ln1_g", "ln1_b", "ln2_g", "ln2_b")
 
@@ -32,7 +33,8 @@ EXPORTS = ("energon_get_unique_id", "energon_init", "energon_init_local_group", 
            "energon_sync", "energon_get_stats", "energon_last_error", "energon_status_string", "energon_destroy",
            "energon_index_maps", "energon_gemm", "energon_attention", "energon_set_profiling", "energon_get_profile",
            "energon_shard_plan", "energon_set_option", "energon_pmep_plan", "energon_offload_layers",
-           "energon_stage_plan", "energon_forward_stage", "energon_forward_stage_group")
+           "energon_stage_plan", "energon_forward_stage", "energon_forward_stage_group", "energon_p2p_handle",
+           "energon_p2p_connect")
 
 
 class EnergonError(RuntimeError):
@@ -44,7 +46,7 @@ class EnergonError(RuntimeError):
 class Config(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int32) for n in ("num_layers", "hidden", "num_heads", "ffn", "vocab", "max_seq",
                                               "causal", "dtype", "drce", "tp_size", "tp_rank", "device",
-                                              "max_tokens", "final_ln")] + [("ln_eps", ctypes.c_float)]
+                                              "max_tokens", "final_ln")] + [("ln_eps", ctypes.c_float), ("comm", ctypes.c_int32)]
 
 
 class LayerWeights(ctypes.Structure):
@@ -105,6 +107,8 @@ def load_library(path: str = SO_PATH):
     L.energon_offload_layers.argtypes = [P, ctypes.POINTER(ctypes.c_int32), I32, I32, I32, I32]
     L.energon_get_profile.argtypes = [P, ctypes.POINTER(Profile)]
     L.energon_stage_plan.argtypes = [I32, I32, ctypes.POINTER(ctypes.c_int32)]
+    L.energon_p2p_handle.argtypes = [P, P]
+    L.energon_p2p_connect.argtypes = [P, P]
     L.energon_forward_stage.argtypes = [P, P, P, ctypes.POINTER(ctypes.c_int32), I32, I32, I32, I32, I32, P, P]
     L.energon_forward_stage_group.argtypes = [ctypes.POINTER(P), I32, P, P, ctypes.POINTER(ctypes.c_int32), I32, I32,
                                               I32, I32, I32, P, P]
@@ -146,10 +150,10 @@ def _src_dtype(t):
 
 
 def make_config(num_layers, hidden, num_heads, ffn, vocab, max_seq, max_tokens, dtype="bf16", causal=1, drce=1,
-                tp_size=1, tp_rank=0, device=0, final_ln=1, ln_eps=1e-5) -> Config:
+                tp_size=1, tp_rank=0, device=0, final_ln=1, ln_eps=1e-5, comm=0) -> Config:
     return Config(num_layers, hidden, num_heads, ffn, vocab, max_seq, causal,
                   DTYPE_BF16 if dtype == "bf16" else DTYPE_F32, drce, tp_size, tp_rank, device, max_tokens,
-                  final_ln, ln_eps)
+                  final_ln, ln_eps, comm)
 
 
 # ----------------------------------------------------------------------------- ABI wrappers (same names)
@@ -231,6 +235,20 @@ def energon_forward_stage_group(ctxs, seq_lens, max_len, layer_begin, layer_end,
     _check(load_library().energon_forward_stage_group(arr, len(ctxs), _ptr(tokens), _ptr(x), _lens(seq_lens),
                                                       len(seq_lens), max_len, layer_begin, layer_end, out_kind,
                                                       _ptr(out), _stream(stream)), ctxs[0])
+
+
+def energon_p2p_handle(ctx) -> bytes:
+    """64-byte CUDA IPC handle of this rank's exchange region (cfg.comm = COMM_P2P)."""
+    buf = ctypes.create_string_buffer(64)
+    _check(load_library().energon_p2p_handle(ctx, buf), ctx)
+    return buf.raw
+
+
+def energon_p2p_connect(ctx, handles):
+    """handles: the k ranks' 64-byte handles in rank order."""
+    blob = b"".join(handles)
+    buf = ctypes.create_string_buffer(blob, len(blob))
+    _check(load_library().energon_p2p_connect(ctx, buf), ctx)
 
 
 def energon_sync(ctx):

@@ -41,6 +41,7 @@ def test_status_strings(lib):
     ("tp_size", 3, -2),        # 4 heads % 3
     ("tp_rank", 2, -2),        # rank >= tp_size
     ("dtype", 7, -2),
+    ("comm", 2, -2),           # neither ENERGON_COMM_NCCL nor ENERGON_COMM_P2P
     ("num_layers", 0, -2),
     ("hidden", 12, -2),        # 12 % 4 == 0 but hidden=12/h=4 -> d=3: shape check
 ])
