@@ -26,4 +26,4 @@ for name, (B, S, lens) in cases.items():
         energon.energon_attention(Q, K, V, O, lens, 1)
     e1.record(); torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / 20
-    print(f"{name:24s} impl={os.environ.get('ENERGON_ATTN','3')} {ms*1e3:8.1f} us  {flops/ms/1e9:7.1f} TFLOP/s", flush=True)
+    print(f"{name:24s} impl={os.environ.get('ENERGON_ATTN','4')} {ms*1e3:8.1f} us  {flops/ms/1e9:7.1f} TFLOP/s", flush=True)

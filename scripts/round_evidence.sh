@@ -1,0 +1,15 @@
+# Round evidence with the current code: full GPU suite, smoke, default bench (JSON line), ncu launch
+# list of one step, ncu --set full of one layer's kernels (GEMM DRAM traffic), attention microbench.
+mkdir -p gpurun_out
+timeout 1500 python -m pytest tests -m gpu -x -q -p no:cacheprovider > gpurun_out/pytest_gpu_full.log 2>&1; echo "pytest rc=$?"; tail -1 gpurun_out/pytest_gpu_full.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2
+timeout 900 python bench.py > gpurun_out/bench.json 2>gpurun_out/bench.err; python -c "
+import json; d=json.load(open('gpurun_out/bench.json')); print(d['value'], d['ms_per_step'], d['e2e']['value'], d['phases'], d['roofline'], d['clocks'])"
+export ENERGON_PROFILE_RANGE=1
+timeout 900 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-ab --graph 0 > gpurun_out/ncu_launch_run.log 2>&1
+timeout 900 ncu --profile-from-start off --set full --clock-control none --import-source on -c 9 -o gpurun_out/prof_full -f python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-ab --layers 2 --graph 0 > gpurun_out/ncu_full_run.log 2>&1
+python scripts/ncu_summary.py launches gpurun_out/launches.csv > gpurun_out/launches_summary.md
+python scripts/ncu_summary.py full gpurun_out/prof_full.ncu-rep > gpurun_out/full_summary.md
+cat gpurun_out/launches_summary.md
+unset ENERGON_PROFILE_RANGE
+timeout 300 python scripts/bench_attn.py 2>&1 | tail -4 > gpurun_out/attn_bench.txt; cat gpurun_out/attn_bench.txt
