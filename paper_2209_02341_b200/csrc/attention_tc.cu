@@ -528,7 +528,12 @@ __global__ void __launch_bounds__(192, 2)
       };
       while (w < items) {
         const int b2 = t & 1;
-        if (j == 0) mbar_wait(q_full, qi & 1);
+        if (j == 0) {
+          // finish the previous item before waiting for this item's Q: its epilogue overlaps the Q load
+          if (pv_j >= 0) issue_pv(t - 1, pv_j, pv_qi);
+          pv_j = -1;
+          mbar_wait(q_full, qi & 1);
+        }
         mbar_wait(&k_full[b2], (t >> 1) & 1);
         mbar_wait(&p_free[b2], ((t >> 1) & 1) ^ 1);  // P_{t-2} V done: buffer b2 is free
         tc_fence_after();
@@ -581,21 +586,25 @@ __global__ void __launch_bounds__(192, 2)
         tmem_ld32_nowait(tS + 0, sr[0]);
         tmem_ld32_nowait(tS + 32, sr[1]);
         tmem_wait_ld();
-        float mt = -INFINITY;
+        // row max with 8 independent partial maxima (a 64-long fmax chain would serialise on latency)
+        float mx[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) mx[e] = -INFINITY;
         const bool need_mask = (k0 + BN > len) || (causal && k0 + BN - 1 > q0 + qd * 32);
         if (need_mask) {
+          const int lim = min(len, causal ? srow + 1 : len) - k0;  // keys c < lim are allowed
 #pragma unroll
           for (int c = 0; c < BN; ++c) {
-            const int tk = k0 + c;
             float v = __uint_as_float(sr[c >> 5][c & 31]);
-            if (tk >= len || (causal && tk > srow)) v = -INFINITY;
+            if (c >= lim) v = -INFINITY;
             sr[c >> 5][c & 31] = __float_as_uint(v);
-            mt = fmaxf(mt, v);
+            mx[c & 7] = fmaxf(mx[c & 7], v);
           }
         } else {
 #pragma unroll
-          for (int c = 0; c < BN; ++c) mt = fmaxf(mt, __uint_as_float(sr[c >> 5][c & 31]));
+          for (int c = 0; c < BN; ++c) mx[c & 7] = fmaxf(mx[c & 7], __uint_as_float(sr[c >> 5][c & 31]));
         }
+        float mt = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])), fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
         mt *= scale_log2;
         // lazy rescale, warp-wide (tcgen05.ld / st are .sync.aligned), alpha = 1 for rows keeping their max.
         // Every tile's P V completion (o_full[t & 1], one phase per two tiles) is observed exactly once,
@@ -624,13 +633,15 @@ __global__ void __launch_bounds__(192, 2)
         }
         const float base = (m_ref == -INFINITY) ? 0.f : m_ref;
         uint32_t pk[32];
+        float ls[4] = {0.f, 0.f, 0.f, 0.f};  // independent partial row sums (latency, as for the max)
 #pragma unroll
         for (int c = 0; c < BN; c += 2) {
           const float p0 = ex2f(fmaf(__uint_as_float(sr[c >> 5][c & 31]), scale_log2, -base));
           const float p1 = ex2f(fmaf(__uint_as_float(sr[(c + 1) >> 5][(c + 1) & 31]), scale_log2, -base));
-          l += p0 + p1;
+          ls[(c >> 1) & 3] += p0 + p1;
           pk[c >> 1] = pack_bf16x2(p0, p1);
         }
+        l += (ls[0] + ls[1]) + (ls[2] + ls[3]);
         tmem_st32(tS, pk);  // P_t over the first BN/2 columns of S_t (S_t is in registers)
         if (k0 + BN > len) {  // zero V rows of keys >= len (pad rows a5 never wrote may hold NaN)
           mbar_wait(&v_full[b2], (t >> 1) & 1);
@@ -658,17 +669,20 @@ __global__ void __launch_bounds__(192, 2)
       bf16* dst = Cp ? Cp + ((int64_t)__ldg(offsets + b) + srow) * (int64_t)(hk * D) + head * D
                      : Opad + ((int64_t)(b * hk + head) * S + srow) * D;
 #pragma unroll 1
-      for (int c = 0; c < D; c += 32) {
-        uint32_t o[32];
-        tmem_ld32(tO + lane_off + c, o);
+      for (int c = 0; c < D; c += 64) {  // two 32-column TMEM loads in flight per step
+        uint32_t o[2][32];
+        tmem_ld32_nowait(tO + lane_off + c, o[0]);
+        tmem_ld32_nowait(tO + lane_off + c + 32, o[1]);
+        tmem_wait_ld();
         if (valid) {
 #pragma unroll
-          for (int e = 0; e < 32; e += 8) {
+          for (int e = 0; e < 64; e += 8) {
+            const uint32_t* oe = &o[e >> 5][e & 31];
             uint4 pq;
-            pq.x = pack_bf16x2(__uint_as_float(o[e]) * inv, __uint_as_float(o[e + 1]) * inv);
-            pq.y = pack_bf16x2(__uint_as_float(o[e + 2]) * inv, __uint_as_float(o[e + 3]) * inv);
-            pq.z = pack_bf16x2(__uint_as_float(o[e + 4]) * inv, __uint_as_float(o[e + 5]) * inv);
-            pq.w = pack_bf16x2(__uint_as_float(o[e + 6]) * inv, __uint_as_float(o[e + 7]) * inv);
+            pq.x = pack_bf16x2(__uint_as_float(oe[0]) * inv, __uint_as_float(oe[1]) * inv);
+            pq.y = pack_bf16x2(__uint_as_float(oe[2]) * inv, __uint_as_float(oe[3]) * inv);
+            pq.z = pack_bf16x2(__uint_as_float(oe[4]) * inv, __uint_as_float(oe[5]) * inv);
+            pq.w = pack_bf16x2(__uint_as_float(oe[6]) * inv, __uint_as_float(oe[7]) * inv);
             *reinterpret_cast<uint4*>(dst + c + e) = pq;
           }
         }
