@@ -427,7 +427,10 @@ class DistLink:
 
     HDR = 8  # fixed preamble: [n_header_words, n_token_words]
 
-    def __init__(self, pp: int, tp: int, act_spec, out_spec, *, cmd_group=None, act_group=None, res_group=None):
+    def __init__(self, pp: int, tp: int, act_spec, out_spec, *, cmd_group=None, act_group=None, res_group=None,
+                 stage_via_host: bool = False):
+        """stage_via_host: move CUDA activations through host memory (for a gloo `act_group`,
+        e.g. several stages sharing one GPU in a test; NCCL sends device memory directly)."""
         import torch.distributed as dist
         self.dist = dist
         self.pp, self.tp = pp, tp
@@ -445,6 +448,7 @@ class DistLink:
         self._send_lock = threading.Lock()
         self._res_thread = None
         self.result_src = (pp - 1) * tp
+        self.via_host = stage_via_host
 
     # -- engine side (rank 0)
     def broadcast_command(self, cmd: Command) -> None:
@@ -485,7 +489,7 @@ class DistLink:
                     continue
                 shape, dtype, device = self.out_spec(cmd)
                 import torch
-                out = torch.empty(shape, dtype=dtype, device=device)
+                out = torch.empty(shape, dtype=dtype, device="cpu" if self.via_host else device)
                 self.dist.recv(out, self.result_src, group=self.res_group)
                 self.engine.complete(key, out)
                 key += 1
@@ -515,14 +519,23 @@ class DistLink:
             tok = t.reshape(B, S).numpy()
         return Command(key, bid, h[5:5 + B], S, tok)
 
+    def _host(self, x):
+        if self.via_host and getattr(x, "is_cuda", False):
+            return x.to("cpu")  # synchronous copy: the stream's work on x is complete
+        return x.contiguous()
+
     def send_act(self, stage: int, cmd: Command, x) -> None:
         if isinstance(x, _Poison):
             raise x.err
-        self.dist.send(x.contiguous(), self.rank + self.tp, group=self.act_group)
+        self.dist.send(self._host(x), self.rank + self.tp, group=self.act_group)
 
     def recv_act(self, stage: int, cmd: Command):
         import torch
         shape, dtype, device = self.act_spec(cmd)
+        if self.via_host and str(device).startswith("cuda"):
+            h = torch.empty(shape, dtype=dtype)
+            self.dist.recv(h, self.rank - self.tp, group=self.act_group)
+            return h.to(device)
         x = torch.empty(shape, dtype=dtype, device=device)
         self.dist.recv(x, self.rank - self.tp, group=self.act_group)
         return x
@@ -538,7 +551,7 @@ class DistLink:
             return
         if isinstance(out, _Poison):
             raise out.err
-        self.dist.send(out.contiguous(), 0, group=self.res_group)
+        self.dist.send(self._host(out), 0, group=self.res_group)
 
 
 # ----------------------------------------------------------------------------- the GPU stage runner

@@ -184,3 +184,103 @@ def test_local_pipeline_gpu(dtype, pp):
         assert np.array_equal(y, ys)
         ref = reference(shape, seed, dtype, tok, lens)
         assert max_abs_rel(y, ref, lens) <= TOL[dtype]
+
+
+def _dist_stage(rank, world, port, dtype, q):
+    import os
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    sys.path.insert(0, os.path.join(root, "tests"))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    try:
+        import random as rnd
+
+        import torch.distributed as dist
+
+        import synth
+        from gpu_helpers import SHAPES, load_engine, torch_dtype
+        from paper_2209_02341_b200 import energon
+        from paper_2209_02341_b200 import pipeline as pl
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        cmd_group, res_group = dist.new_group(backend="gloo"), dist.new_group(backend="gloo")
+        energon.load_library()
+        shape = dict(SHAPES["tiny"], L=4, V=300, max_seq=40)
+        H, seed = shape["H"], 9
+        a, b = energon.energon_stage_plan(shape["L"], world)[rank]
+        cfg = energon.make_config(shape["L"], H, shape["h"], shape["F"], shape["V"], shape["max_seq"], 8 * 40,
+                                  dtype=dtype)
+        ctx = energon.energon_init(cfg)
+        load_engine([ctx], shape, seed, dtype, layers=range(a, b))
+        link = pl.DistLink(world, 1, act_spec=lambda c: ((c.rows(), H), torch.float32, "cuda:0"),
+                           out_spec=lambda c: ((c.batch, c.max_len, H), torch_dtype(dtype), "cuda:0"),
+                           cmd_group=cmd_group, act_group=None, res_group=res_group, stage_via_host=True)
+        trace = pl.Trace()
+        runner = pl.EnergonStageRunner(ctx, a, b, first=rank == 0, last=rank == world - 1, hidden=H,
+                                       out_dtype=torch_dtype(dtype))
+        worker = pl.StageWorker(rank, world, runner, link, admit_delay=0.002, trace=trace, seed=rank).start()
+        res = {"rank": rank}
+        if rank == 0:
+            engine = pl.Engine(link, 2 * world, lane_delay=0.002, seed=3)
+            link.engine = engine
+            link.start_results()
+            r = rnd.Random(5)
+            batches = []
+            for i in range(10):
+                B, S = r.randint(1, 8), r.choice([8, 16, 33])
+                lens = [r.randint(1, S) for _ in range(B)]
+                batches.append((synth.tokens(B, S, shape["V"], lens, 70 + i), lens))
+            futs = [engine.submit(*bt) for bt in batches]
+            res["outs"] = [f.result(timeout=120).float().cpu().numpy() for f in futs]
+            res["batches"] = batches
+            engine.shutdown()
+            link.join_results(30)
+        worker.join(60)
+        res.update(keys=trace.keys(rank), transfers=worker.transfers,
+                   error=repr(worker.error) if worker.error else None)
+        dist.barrier()
+        energon.energon_destroy(ctx)
+        dist.destroy_process_group()
+        q.put(res)
+    except Exception as e:  # noqa: BLE001
+        import traceback
+        q.put({"rank": rank, "exc": repr(e), "tb": traceback.format_exc()})
+
+
+@pytest.mark.parametrize("dtype", ["bf16"])
+def test_dist_pipeline_two_processes_one_gpu(dtype):
+    """NBPP across processes with GPU stages: stage 0 and stage 1 in two processes (both on cuda:0),
+    commands from the engine on rank 0 over gloo, packed activations between the processes (through
+    host memory, since both share the GPU), results back to rank 0; every result equals the
+    sequential chain of the same stages bit for bit, keys in order on both stages, 1 transfer per
+    batch."""
+    import socket
+
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    world = 2
+    ctx_mp = mp.get_context("spawn")
+    q = ctx_mp.Queue()
+    procs = [ctx_mp.Process(target=_dist_stage, args=(r, world, port, dtype, q)) for r in range(world)]
+    [p.start() for p in procs]
+    res = [q.get(timeout=300) for _ in range(world)]
+    [p.join(60) for p in procs]
+    res = {r["rank"]: r for r in res}
+    for r in range(world):
+        assert "exc" not in res[r], res[r].get("tb")
+        assert res[r]["error"] is None
+        assert res[r]["keys"] == list(range(10))
+    assert res[0]["transfers"] == 10 and res[1]["transfers"] == 0
+    shape = dict(SHAPES["tiny"], L=4, V=300, max_seq=40)
+    stages = make_stages(shape, 9, dtype, 8 * 40, world)
+    try:
+        for (tok, lens), y in zip(res[0]["batches"], res[0]["outs"]):
+            ys = as_np(run_chain(stages, tok, lens, dtype, shape["H"]))
+            assert np.array_equal(y.astype(np.float64), ys)
+    finally:
+        for ctxs, _, _ in stages:
+            destroy(ctxs)
