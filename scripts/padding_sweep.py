@@ -1,5 +1,6 @@
-"""Padding-ratio sweep of the DRCE A/B on one B200 (BASELINE config 5 style sweep p in {0,.25,.5,.75},
-run at the config-3 GPT-3-13B shape that fits one GPU): DRCE on vs off latency and valid tok/s."""
+"""Padding-ratio sweep of the DRCE A/B on one B200 (BASELINE config 5's sweep p in {0,.25,.5,.75}):
+DRCE on vs off latency and valid tok/s.  CFG=gpt3_13b (default) or opt30b / opt66b (the whole model at
+TP=1 fits the 180 GB of one B200: 130 GB of bf16 weights for OPT-66B); ITERS timed forwards per point."""
 import json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -27,7 +28,7 @@ for p in (0.0, 0.25, 0.5, 0.75):
     lens = synth.exact_p_lengths(B, S, p, 0)
     T = sum(lens)
     tok = torch.from_numpy(synth.tokens(B, S, shape["V"], lens, 0)).cuda()
-    res = {"p": p, "T": T}
+    res = {"config": cfgname, "layers": shape["L"], "p": p, "T": T}
     for drce in (1, 0):
         energon.energon_set_option(ctx, energon.OPT_DRCE, drce)
         for _ in range(2):
@@ -35,10 +36,11 @@ for p in (0.0, 0.25, 0.5, 0.75):
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        for _ in range(5):
+        iters = int(os.environ.get("ITERS", "5"))
+        for _ in range(iters):
             energon.energon_forward(ctx, tok, lens, out)
         e1.record(); torch.cuda.synchronize()
-        ms = e0.elapsed_time(e1) / 5
+        ms = e0.elapsed_time(e1) / iters
         res["on_ms" if drce else "off_ms"] = ms
         res["on_tok_s" if drce else "off_tok_s"] = T / ms * 1e3
     res["latency_reduction"] = 1 - res["on_ms"] / res["off_ms"]
