@@ -236,11 +236,22 @@ def energon_arm(args, world, rank, local):
     import synth
     from paper_2209_02341_b200 import energon
 
+    # ENERGON_BENCH_SHARE_GPU=1 (test hook): every rank on cuda:0 with gloo plumbing and the P2P exchange
+    # (NCCL refuses two ranks on one GPU) -- exercises the N > 1 bench path on a single-GPU box; its
+    # timings mean nothing (the ranks time-slice one GPU)
+    share = os.environ.get("ENERGON_BENCH_SHARE_GPU") == "1" and world > 1
+    if share:
+        local = 0
+        args.comm = "p2p"
     torch.cuda.set_device(local)
+    plumb = "cpu" if share else "cuda"
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     energon.load_library()
     shape = dict(synth.SHAPES[args.config])
     if args.layers:
@@ -258,8 +269,8 @@ def energon_arm(args, world, rank, local):
     uid = None
     if world > 1:
         from paper_2209_02341_b200 import dist as edist
-        uid = edist.broadcast_bytes(energon.energon_get_unique_id() if rank == 0 else None, 128, device="cuda")
-        lens = edist.broadcast_lengths(lens, device="cuda")  # the engine command's seq_lens
+        uid = edist.broadcast_bytes(energon.energon_get_unique_id() if rank == 0 else None, 128, device=plumb)
+        lens = edist.broadcast_lengths(lens, device=plumb)  # the engine command's seq_lens
     if args.local_tp > 1:
         ctxs = energon.energon_init_local_group(cfg, args.local_tp)
     else:
@@ -300,7 +311,7 @@ def energon_arm(args, world, rank, local):
         if dist is None:
             return x
         from paper_2209_02341_b200 import dist as edist
-        return edist.max_over_ranks(x, device="cuda")
+        return edist.max_over_ranks(x, device=plumb)
 
     for _ in range(args.warmup):
         eng.forward(tok, lens, out, stream)
