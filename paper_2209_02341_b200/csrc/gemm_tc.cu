@@ -836,7 +836,12 @@ static void launch_pair_epi(const CUtensorMap& tmA, const CUtensorMap& tmB, cons
   TailPlan tp{tiles, 0, 0, nullptr, nullptr};
   const int rem = tiles % pairs;
   int grid_cl = tiles < pairs ? tiles : pairs;
-  if (rem > 0 && (pairs - rem) * 100 >= 15 * pairs && nkb >= 160 && !getenv("ENERGON_NO_STREAMK")) {
+  static int min_nkb = -1;
+  if (min_nkb < 0) {  // ENERGON_SK_MIN_NKB: experiment hook for the K threshold (k-blocks of 64)
+    const char* e = getenv("ENERGON_SK_MIN_NKB");
+    min_nkb = e ? atoi(e) : 160;
+  }
+  if (rem > 0 && (pairs - rem) * 100 >= 15 * pairs && nkb >= min_nkb && !getenv("ENERGON_NO_STREAMK")) {
     const TailWs* w = tw ? tw : default_tail_ws();
     if (w->ws) {
       const int Lmin = (rem * nkb + pairs - 1) / pairs;  // every tail cluster index < pairs
