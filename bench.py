@@ -52,6 +52,9 @@ def parse():
                          "under torchrun (NCCL collectives run eagerly)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-tokens", type=int, default=192)
+    ap.add_argument("--pp", type=int, default=1,
+                    help="NBPP: one pipeline stage per rank (torchrun, world == pp), --pp-batches batches in flight")
+    ap.add_argument("--pp-batches", type=int, default=8)
     ap.add_argument("--comm", default="nccl", choices=["nccl", "p2p"],
                     help="TP exchange under torchrun: NCCL, or the fused peer-memory kernels (CUDA IPC)")
     ap.add_argument("--local-tp", type=int, default=0,
@@ -472,6 +475,114 @@ def energon_arm(args, world, rank, local):
         dist.destroy_process_group()
 
 
+# ============================================================================= NBPP pipeline arm
+def pipeline_arm(args, world, rank, local):
+    """Non-blocking pipeline parallelism: rank i runs stage i (a contiguous layer
+    range, energon_forward_stage), the engine on rank 0 submits --pp-batches batches of the workload at
+    once; value = valid tokens of all batches / device-clock time from the first submit to the last
+    result (max over ranks).  One process per GPU, activations rank to rank over NCCL (or through host
+    memory with ENERGON_BENCH_SHARE_GPU=1, where the timing is meaningless)."""
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    from paper_2209_02341_b200 import energon
+    from paper_2209_02341_b200 import pipeline as pl
+
+    share = os.environ.get("ENERGON_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
+    torch.cuda.set_device(local)
+    if share:
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    cmd_group = dist.new_group(backend="gloo")
+    res_group = dist.new_group(backend="gloo" if share else "nccl")
+    energon.load_library()
+    shape = dict(synth.SHAPES[args.config])
+    if args.layers:
+        shape["L"] = args.layers
+    bcfg = synth.BATCHES[args.config]
+    B, S = bcfg["B"], bcfg["S"]
+    H = shape["H"]
+    lens = synth.batch_lengths(args.config, args.seed, p=args.p, regime=args.regime)
+    T = sum(lens)
+    tok_np = synth.tokens(B, S, shape["V"], lens, args.seed)
+    l0, l1 = energon.energon_stage_plan(shape["L"], world)[rank]
+    cfg = energon.make_config(shape["L"], H, shape["h"], shape["F"], shape["V"], shape["max_seq"], B * S,
+                              dtype="bf16", drce=args.drce, device=local)
+    ctx = energon.energon_init(cfg)
+    if rank == 0 or rank == world - 1:
+        emb = {n: synth.emb_tensor_device(n, H, shape["V"], shape["max_seq"], args.seed, True, torch.bfloat16)
+               for n in synth.EMB_TENSORS}
+        energon.energon_load_embeddings(ctx, emb["tok_emb"], emb["pos_emb"], emb["lnf_g"], emb["lnf_b"])
+        del emb
+    for l in range(l0, l1):
+        w = {n: synth.layer_tensor_device(n, l, H, shape["F"], args.seed, True, torch.bfloat16)
+             for n in synth.LAYER_TENSORS}
+        energon.energon_load_layer_weights(ctx, l, w)
+        del w
+    torch.cuda.synchronize()
+    dev = f"cuda:{local}"
+    link = pl.DistLink(world, 1, act_spec=lambda c: ((c.rows(bool(args.drce)), H), torch.float32, dev),
+                       out_spec=lambda c: ((c.batch, c.max_len, H), torch.bfloat16, dev),
+                       cmd_group=cmd_group, act_group=None, res_group=res_group, stage_via_host=share)
+    runner = pl.EnergonStageRunner(ctx, l0, l1, first=rank == 0, last=rank == world - 1, hidden=H,
+                                   out_dtype=torch.bfloat16, device=local, drce=bool(args.drce))
+    worker = pl.StageWorker(rank, world, runner, link).start()
+    engine = None
+    if rank == 0:
+        engine = pl.Engine(link, 2 * world)
+        link.engine = engine
+        link.start_results()
+
+    def run_round(n):
+        futs = [engine.submit(tok_np, lens) for _ in range(n)]
+        for f in futs:
+            f.result(timeout=600)
+
+    # warm-up: every stage compiles its launch path; then the timed round (rank 0 drives)
+    if rank == 0:
+        run_round(max(args.warmup, 1))
+    dist.barrier(group=cmd_group)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    if rank == 0:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        run_round(args.pp_batches)
+        e1.record()
+        torch.cuda.synchronize()
+        dev_ms = e0.elapsed_time(e1)
+    dist.barrier(group=cmd_group)
+    wall_ms = (time.perf_counter() - t0) * 1e3
+    if rank == 0:
+        engine.shutdown()
+        link.join_results(60)
+    worker.join(120)
+    t = torch.tensor([wall_ms], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=cmd_group)
+    if rank == 0:
+        ms = max(dev_ms, 0.0)
+        tokens = T * args.pp_batches
+        print(json.dumps({
+            "metric": METRIC, "value": tokens / ms * 1e3, "unit": "tokens/s", "n_gpus": world,
+            "steps": args.pp_batches, "warmup": max(args.warmup, 1), "ms_per_step": ms / args.pp_batches,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (seeded counter-based generator; random-init weights)",
+            "config": dict(workload_config(args, shape, bcfg, lens, 1), parallelism=f"pp{world}",
+                           pipeline={"stages": world, "batches_in_flight": args.pp_batches,
+                                     "stage_layers": energon.energon_stage_plan(shape["L"], world),
+                                     "transfers_per_batch": world - 1,
+                                     "activation_transport": "host (shared GPU)" if share else "nccl p2p"}),
+            "wall_ms_max_over_ranks": float(t.item()),
+            "note": "NBPP: engine + distributed consistency queue (pipeline.py); value = valid tokens of all "
+                    "batches / time from the first submit to the last result on rank 0's clock"}))
+    energon.energon_destroy(ctx)
+    dist.destroy_process_group()
+
+
 def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -482,6 +593,11 @@ def main():
         sys.exit(2)
     if args.impl == "reference":
         reference_arm(args, world, rank)
+    elif args.pp > 1:
+        if args.pp != world:
+            print(json.dumps({"error": "--pp P needs exactly P ranks (one stage per GPU)"}))
+            sys.exit(2)
+        pipeline_arm(args, world, rank, local)
     else:
         energon_arm(args, world, rank, local)
 
