@@ -20,6 +20,8 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include <cstdio>
+#include <vector>
 #include "tc_ptx.cuh"
 
 namespace energon {
@@ -319,6 +321,17 @@ struct TailPlan {
   int* counters;  // [rem][2]
 };
 
+// Diagnostics (ENERGON_GEMM_TRACE=<file>): per-unit timestamps of the pair kernel (leader CTA) -- MMA
+// issuer: accumulator acquired, first stage full, last MMA issued; epilogue: accumulator full, unit
+// done (stores / fix-up issued) -- in %globaltimer ns, appended to the file after every launch (the
+// launch is then synchronous; scripts/gemm_trace_report.py).  Off (null pointer) in normal runs.
+__device__ uint64_t* g_gemm_trace = nullptr;
+__device__ __forceinline__ uint64_t gtimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 struct WorkIter {
   int u, it, it_end;
   __device__ __forceinline__ WorkIter(int cid, const TailPlan& tp, int nkb) : u(cid), it(0), it_end(0) {
@@ -552,12 +565,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       uint32_t acc_phase = 0;
       WorkIter wi(cid, tp, nkb);
       int tile, kb0, kb1, split, tail;
+      uint64_t* trace = g_gemm_trace;
+      int nu = 0;
       while (wi.next(tp, nkb, ncl, tile, kb0, kb1, split, tail)) {
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
+        uint64_t* rec = (trace && nu < 30) ? trace + ((size_t)cid * 32 + nu) * 6 : nullptr;
+        if (rec) rec[0] = gtimer();
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);
+          if (rec && kb == kb0) rec[1] = gtimer();
           tc_fence_after();
           const uint64_t a0 = umma_desc_sw128(smem_u32(sA + stage * C::A_BYTES));
           const uint64_t b0 = umma_desc_sw128(smem_u32(sB + stage * C::B_BYTES));
@@ -571,6 +589,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
           }
         }
         umma_commit_2sm_mc(&tfull[acc]);
+        if (rec) {
+          rec[2] = gtimer();
+          rec[3] = (uint64_t)tile | ((uint64_t)(kb1 - kb0) << 32);
+        }
+        ++nu;
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
@@ -591,10 +614,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     uint32_t acc_phase = 0;
     WorkIter wi(cid, tp, nkb);
     int tile, kb0, kb1, split, tail;
+    uint64_t* etrace = (leader && warp == 4 && lane == 0) ? g_gemm_trace : nullptr;
+    int enu = 0;
     while (wi.next(tp, nkb, ncl, tile, kb0, kb1, split, tail)) {
       int m_blk, n_blk;
       raster(tile, num_m, num_n, group_m, m_blk, n_blk);
       mbar_wait(&tfull[acc], acc_phase);
+      uint64_t* erec = (etrace && enu < 30) ? etrace + ((size_t)cid * 32 + enu) * 6 : nullptr;
+      ++enu;
+      if (erec) erec[4] = gtimer();
       __syncwarp();  // reconverge the spin loop before the .sync.aligned tcgen05.ld
       tc_fence_after();
       const int row = m_blk * 256 + (int)rank * 128 + etid;
@@ -706,6 +734,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         }
         epi_bar();  // fix_flag is reused by the next split unit
       }
+      if (erec) erec[5] = gtimer();
     }
     if (TMA_ST && lane == 0) bulk_wait_all();  // stores complete before the CTA's smem goes away
   }
@@ -880,8 +909,31 @@ static void launch_pair_epi(const CUtensorMap& tmA, const CUtensorMap& tmB, cons
     const char* e = getenv("ENERGON_L2_HINTS");  // bit 0: load hints, bit 1: evict_first on D stores
     hints = e ? atoi(e) : 0;
   }
+  static const char* trace_file = getenv("ENERGON_GEMM_TRACE");
+  static uint64_t* trace_buf = nullptr;
+  const size_t trace_n = (size_t)(grid / 2) * 32 * 6;
+  if (trace_file && !trace_buf) {
+    cudaMalloc(&trace_buf, (size_t)(num_sms() / 2) * 32 * 6 * sizeof(uint64_t));
+    cudaMemcpyToSymbol(g_gemm_trace, &trace_buf, sizeof(trace_buf));
+  }
+  if (trace_buf) cudaMemsetAsync(trace_buf, 0, trace_n * sizeof(uint64_t), st);
   launch_k(gemm_tc2_kernel<BN, EPI>, dim3(grid), dim3(128 + 32 * C::EPI_WARPS), C::SMEM, st, tmA, tmB, D, bias, M, N, K,
            group_m, qs, tp, md, hints);
+  if (trace_buf) {  // diagnostics only: synchronous dump of this launch's unit timestamps
+    std::vector<uint64_t> h(trace_n);
+    cudaMemcpy(h.data(), trace_buf, trace_n * sizeof(uint64_t), cudaMemcpyDeviceToHost);
+    if (FILE* f = fopen(trace_file, "a")) {
+      fprintf(f, "launch M=%d N=%d K=%d clusters=%d\n", M, N, K, grid / 2);
+      for (int c = 0; c < grid / 2; ++c)
+        for (int u = 0; u < 32; ++u) {
+          const uint64_t* r = &h[((size_t)c * 32 + u) * 6];
+          if (r[0]) fprintf(f, "%d %d %llu %llu %llu %llu %llu %llu %llu\n", c, u, (unsigned long long)(r[3] & 0xffffffffu),
+                            (unsigned long long)(r[3] >> 32), (unsigned long long)r[0], (unsigned long long)r[1],
+                            (unsigned long long)r[2], (unsigned long long)r[4], (unsigned long long)r[5]);
+        }
+      fclose(f);
+    }
+  }
 }
 
 template <int BN, int EPI>
