@@ -703,6 +703,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       if (split >= 0) {
         // publish the partial; the last of the tile's pieces to arrive reduces (fixed order) + epilogue
         const int cfirst = (tail * nkb) / tp.L, nsplit = ((tail + 1) * nkb - 1) / tp.L - cfirst + 1;
+        uint64_t* srec = erec ? etrace + ((size_t)cid * 32 + 31) * 6 : nullptr;  // last split piece's phases
+        if (srec) srec[0] = gtimer();
         __threadfence();
         epi_bar();
         if (warp == 4 && lane == 0) {
@@ -711,6 +713,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
           if (old == nsplit - 1) tp.counters[tail * 2 + rank] = 0;  // self-reset for the next launch
         }
         epi_bar();
+        if (srec) srec[1] = gtimer();
         if (*fix_flag) {
           __threadfence();
 #pragma unroll 1
@@ -732,7 +735,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
             epi_store<EPI>(v, row, n_blk * BN + c * 32, M, N, D, bias, qs);
           }
         }
+        if (srec) srec[2] = gtimer();
         epi_bar();  // fix_flag is reused by the next split unit
+        if (srec) {
+          srec[3] = gtimer();
+          srec[4] = (uint64_t)nsplit | ((uint64_t)(*fix_flag) << 32);
+        }
       }
       if (erec) erec[5] = gtimer();
     }
@@ -924,8 +932,14 @@ static void launch_pair_epi(const CUtensorMap& tmA, const CUtensorMap& tmB, cons
     cudaMemcpy(h.data(), trace_buf, trace_n * sizeof(uint64_t), cudaMemcpyDeviceToHost);
     if (FILE* f = fopen(trace_file, "a")) {
       fprintf(f, "launch M=%d N=%d K=%d clusters=%d\n", M, N, K, grid / 2);
+      for (int c = 0; c < grid / 2; ++c) {
+        const uint64_t* q = &h[((size_t)c * 32 + 31) * 6];
+        if (q[0])
+          fprintf(f, "split %d %llu %llu %llu %llu %llu\n", c, (unsigned long long)q[0], (unsigned long long)q[1],
+                  (unsigned long long)q[2], (unsigned long long)q[3], (unsigned long long)q[4]);
+      }
       for (int c = 0; c < grid / 2; ++c)
-        for (int u = 0; u < 32; ++u) {
+        for (int u = 0; u < 30; ++u) {
           const uint64_t* r = &h[((size_t)c * 32 + u) * 6];
           if (r[0]) fprintf(f, "%d %d %llu %llu %llu %llu %llu %llu %llu\n", c, u, (unsigned long long)(r[3] & 0xffffffffu),
                             (unsigned long long)(r[3] >> 32), (unsigned long long)r[0], (unsigned long long)r[1],

@@ -7,6 +7,13 @@ launches = []
 for line in open(sys.argv[1]):
     if line.startswith("launch"):
         launches.append((line.strip(), []))
+        splits = []
+    elif line.startswith("split"):
+        _, c, a, b, cc, d, flag = line.split()
+        a, b, cc, d, flag = int(a), int(b), int(cc), int(d), int(flag)
+        print(f"  split piece (cluster {c}): fence+barrier+atomic {(b - a) / 1e3:.2f} us, "
+              f"{'reduce+store' if flag >> 32 else 'wait'} {(cc - b) / 1e3:.2f} us, final barrier {(d - cc) / 1e3:.2f} us,"
+              f" nsplit {flag & 0xffffffff}") if (flag >> 32) else None
     elif launches:
         c, u, tile, nkb, t0, t1, t2, e0, e1 = map(int, line.split())
         launches[-1][1].append((c, u, tile, nkb, t0, t1, t2, e0, e1))
