@@ -7,6 +7,10 @@ down GEMM, [allreduce], residual+LN), final LN + unpack) over one synthetic batc
 shape (B=16, max_len=512, exact padding ratio 0.5 -> T=4096 valid tokens), bf16, random-init weights.
 
   python bench.py [--gpus N --steps K --warmup W]       energon arm (N>1: under torchrun, TP=N)
+      --comm nccl|p2p     TP exchange: NCCL, or the fused peer-memory kernels (CUDA IPC)
+      --pp P              NBPP: one pipeline stage per rank (world == P), --pp-batches in flight
+      --local-tp k        TP=k per-rank shapes emulated on ONE GPU (in-device reductions)
+      --config / --p / --regime / --layers / --graph / --drce    workload and option overrides
   python bench.py --impl reference ...                  the fp64 CPU oracle arm (rank 0 only)
 
 Timing: W untimed warm-up steps, then K steps bracketed by barrier + cuda.synchronize, CUDA events

@@ -26,7 +26,7 @@ def _free_port():
     return p
 
 
-def _rank(rank, world, port, dtype, q):
+def _rank(rank, world, port, dtype, q, case="random"):
     import sys
     sys.path.insert(0, ROOT)
     sys.path.insert(0, os.path.join(ROOT, "tests"))
@@ -41,8 +41,7 @@ def _rank(rank, world, port, dtype, q):
         dist.init_process_group("gloo", rank=rank, world_size=world)
         energon.load_library()
         shape = dict(SHAPES["tiny"], L=2, V=300, max_seq=40)
-        B, S, seed = 5, 33, 4
-        lens = synth.random_lengths(B, S, seed)
+        B, S, seed, lens = _case(case)
         tok = torch.from_numpy(synth.tokens(B, S, shape["V"], lens, seed)).cuda()
         cfg = energon.make_config(shape["L"], shape["H"], shape["h"], shape["F"], shape["V"], shape["max_seq"], B * S,
                                   dtype=dtype, tp_size=world, tp_rank=rank, comm=energon.COMM_P2P)
@@ -74,8 +73,17 @@ def _rank(rank, world, port, dtype, q):
         q.put({"rank": rank, "exc": repr(e), "tb": traceback.format_exc()})
 
 
-@pytest.mark.parametrize("dtype", ["bf16", "f32"])
-def test_p2p_two_processes_one_gpu(dtype):
+def _case(case):
+    """(B, S, seed, lens): random lengths, or a single 1-token sequence (T = 1 < k: rank 1's shard is
+    empty, its kernels still take part in the completion protocol)."""
+    import synth
+    if case == "one_token":
+        return 1, 4, 4, [1]
+    return 5, 33, 4, synth.random_lengths(5, 33, 4)
+
+
+@pytest.mark.parametrize("dtype,case", [("bf16", "random"), ("f32", "random"), ("bf16", "one_token")])
+def test_p2p_two_processes_one_gpu(dtype, case):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     import torch.multiprocessing as mp
@@ -90,7 +98,7 @@ def test_p2p_two_processes_one_gpu(dtype):
     ctx_mp = mp.get_context("spawn")
     q = ctx_mp.Queue()
     port = _free_port()
-    procs = [ctx_mp.Process(target=_rank, args=(r, world, port, dtype, q)) for r in range(world)]
+    procs = [ctx_mp.Process(target=_rank, args=(r, world, port, dtype, q, case)) for r in range(world)]
     [p.start() for p in procs]
     res = [q.get(timeout=300) for _ in range(world)]
     [p.join(60) for p in procs]
@@ -105,8 +113,7 @@ def test_p2p_two_processes_one_gpu(dtype):
     # same schedule in one process (local group, in-device rank-order reduce-scatter / all-gather)
     energon.load_library()
     shape = dict(SHAPES["tiny"], L=2, V=300, max_seq=40)
-    B, S, seed = 5, 33, 4
-    lens = synth.random_lengths(B, S, seed)
+    B, S, seed, lens = _case(case)
     tok = synth.tokens(B, S, shape["V"], lens, seed)
     ctxs = make_engine(shape, seed, dtype, B * S, k=2)
     try:
