@@ -1,0 +1,82 @@
+"""The benchmark's own workload at full size, in the launch configuration bench.py times (BASELINE
+config 3: GPT-3-13B shape, 40 layers, B=16, S=512, exact p=0.5, bf16, TP=1, CUDA-graph replay), checked
+through properties that hold at any size -- the fp64 oracle cannot run the
+40-layer stack, and its per-layer teacher-forced check at this shape lives in test_gpu_parity.py:
+
+* graph replay gives the eager bits;
+* sequence independence (P12): changing every token of sequence 0 leaves the other 15 sequences'
+  outputs bit-identical (the linears are row-wise with a fixed K order, attention is per sequence);
+* causal prefix invariance (P13): changing the second half of sequence 3's tokens leaves its first
+  half (and every other sequence) bit-identical;
+* pad rows are exactly 0 and every valid output is finite; 283 kernel launches per forward.
+"""
+import numpy as np
+import pytest
+
+import synth
+from gpu_helpers import SHAPES, destroy, make_engine
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2209_02341_b200 import build, energon
+    build()
+    energon.load_library()
+    synth.build(device=True)
+
+
+def test_bench_workload_properties_full_size():
+    from paper_2209_02341_b200 import energon
+    shape = SHAPES["gpt3_13b"]
+    bcfg = synth.BATCHES["gpt3_13b"]
+    B, S, seed = bcfg["B"], bcfg["S"], 0
+    lens = synth.batch_lengths("gpt3_13b", seed)
+    assert sum(lens) == 4096
+    H = shape["H"]
+    tok_np = synth.tokens(B, S, shape["V"], lens, seed)
+    ctxs = make_engine(shape, seed, "bf16", B * S)
+    ctx = ctxs[0]
+    try:
+        energon.energon_set_option(ctx, energon.OPT_GRAPH, 1)
+        tok = torch.from_numpy(tok_np).cuda()
+        out = torch.empty(B, S, H, dtype=torch.bfloat16, device="cuda")
+
+        def fwd(t):
+            tok.copy_(t)
+            energon.energon_forward(ctx, tok, lens, out)
+            energon.energon_sync(ctx)
+            return out.clone()
+
+        base = torch.from_numpy(tok_np)
+        s0 = energon.energon_get_stats(ctx)["kernel_launches"]
+        y_eager = fwd(base)  # first call: eager + graph recording
+        s1 = energon.energon_get_stats(ctx)["kernel_launches"]
+        y = fwd(base)        # replay
+        assert torch.equal(y, y_eager)
+        assert s1 - s0 == 283
+        # P12: sequence 0 gets entirely different tokens
+        t2 = base.clone()
+        rng = np.random.default_rng(1)
+        t2[0, :lens[0]] = torch.from_numpy(rng.integers(1, shape["V"], lens[0]).astype(np.int32))
+        y2 = fwd(t2)
+        # P13: the second half of sequence 3's tokens change
+        t3 = base.clone()
+        h3 = lens[3] // 2
+        t3[3, h3:lens[3]] = torch.from_numpy(rng.integers(1, shape["V"], lens[3] - h3).astype(np.int32))
+        y3 = fwd(t3)
+    finally:
+        destroy(ctxs)
+    yf = y.float()
+    for b, n in enumerate(lens):
+        assert torch.isfinite(yf[b, :n]).all()
+        assert not yf[b, n:].any()  # pad rows exactly 0
+    assert not torch.equal(y2[0, :lens[0]], y[0, :lens[0]])
+    assert torch.equal(y2[1:], y[1:])
+    assert torch.equal(y3[3, :h3], y[3, :h3])
+    assert not torch.equal(y3[3, h3:lens[3]], y[3, h3:lens[3]])
+    assert torch.equal(y3[:3], y[:3]) and torch.equal(y3[4:], y[4:])
