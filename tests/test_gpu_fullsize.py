@@ -30,18 +30,22 @@ def _lib():
     synth.build(device=True)
 
 
-def test_bench_workload_properties_full_size():
+@pytest.mark.parametrize("name", ["gpt3_13b", "opt30b"])
+def test_bench_workload_properties_full_size(name):
+    """config 3 (the bench workload) and config 4 (OPT-30B shape, 48 layers, H=7168, B=32, S=1024,
+    p=0.5 -- 59 GB of bf16 weights, the whole model on one B200)."""
     from paper_2209_02341_b200 import energon
-    shape = SHAPES["gpt3_13b"]
-    bcfg = synth.BATCHES["gpt3_13b"]
+    shape = SHAPES[name]
+    bcfg = synth.BATCHES[name]
     B, S, seed = bcfg["B"], bcfg["S"], 0
-    lens = synth.batch_lengths("gpt3_13b", seed)
-    assert sum(lens) == 4096
+    lens = synth.batch_lengths(name, seed)
+    assert sum(lens) == round(0.5 * B * S)
     H = shape["H"]
     tok_np = synth.tokens(B, S, shape["V"], lens, seed)
     ctxs = make_engine(shape, seed, "bf16", B * S)
     ctx = ctxs[0]
     try:
+        torch.cuda.empty_cache()
         energon.energon_set_option(ctx, energon.OPT_GRAPH, 1)
         tok = torch.from_numpy(tok_np).cuda()
         out = torch.empty(B, S, H, dtype=torch.bfloat16, device="cuda")
@@ -58,7 +62,7 @@ def test_bench_workload_properties_full_size():
         s1 = energon.energon_get_stats(ctx)["kernel_launches"]
         y = fwd(base)        # replay
         assert torch.equal(y, y_eager)
-        assert s1 - s0 == 283
+        assert s1 - s0 == 3 + 7 * shape["L"]  # index maps, embed, final LN + 7 per layer (283 at 40 layers)
         # P12: sequence 0 gets entirely different tokens
         t2 = base.clone()
         rng = np.random.default_rng(1)
@@ -71,6 +75,7 @@ def test_bench_workload_properties_full_size():
         y3 = fwd(t3)
     finally:
         destroy(ctxs)
+        torch.cuda.empty_cache()
     yf = y.float()
     for b, n in enumerate(lens):
         assert torch.isfinite(yf[b, :n]).all()
