@@ -110,6 +110,8 @@ typedef struct {
   int64_t weight_bytes;     /* device bytes held for this rank's weights */
   int64_t workspace_bytes;  /* device bytes held for activations */
   int64_t prefetch_bytes;   /* PMEP: bytes fetched from the memory pool, cumulative */
+  int64_t fused_exchanges;  /* P2P: TP reductions whose partials the row-parallel GEMM stored straight into the
+                               owners' slots (GEMM -> reduce-scatter fused), cumulative */
 } energon_stats;
 
 /*

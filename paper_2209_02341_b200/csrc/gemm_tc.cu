@@ -476,7 +476,8 @@ template <int BN, int EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     bf16* __restrict__ D, const float* __restrict__ bias, int M, int N, int K, int group_m,
-                    const QkvScatter qs, const TailPlan tp, const __grid_constant__ CUtensorMap tmD, int l2_hints) {
+                    const QkvScatter qs, const TailPlan tp, const __grid_constant__ CUtensorMap tmD, int l2_hints,
+                    const __grid_constant__ ShardStore shard) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   using C = Tc2Cfg<BN>;
@@ -656,19 +657,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
             if (lane == 0) bulk_wait_read0();
             __syncwarp();
           }
-          const int rowt = m_blk * 256 + (int)rank * 128 + q * 32;
+          int rowt = m_blk * 256 + (int)rank * 128 + q * 32;
           epi_stage(v0, my_stg, lane);
           if (two) epi_stage(v1, my_stg + 2048, lane);
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
           if (lane == 0) {
+            const CUtensorMap* dm = &tmD;
+            if (shard.k > 0) {  // GEMM -> reduce-scatter: these 32 rows go straight to their owner's slot
+              const int s = min(rowt / shard.rpr, shard.k - 1);
+              dm = &shard.maps[s];
+              rowt -= s * shard.rpr;
+            }
             if (l2_hints & 2) {
               const uint64_t pol_d = policy_evict_first();
-              tma_store_2d_hint(&tmD, smem_u32(my_stg), n_blk * BN + c * 32, rowt, pol_d);
-              if (two) tma_store_2d_hint(&tmD, smem_u32(my_stg + 2048), n_blk * BN + (c + 1) * 32, rowt, pol_d);
+              tma_store_2d_hint(dm, smem_u32(my_stg), n_blk * BN + c * 32, rowt, pol_d);
+              if (two) tma_store_2d_hint(dm, smem_u32(my_stg + 2048), n_blk * BN + (c + 1) * 32, rowt, pol_d);
             } else {
-              tma_store_2d(&tmD, smem_u32(my_stg), n_blk * BN + c * 32, rowt);
-              if (two) tma_store_2d(&tmD, smem_u32(my_stg + 2048), n_blk * BN + (c + 1) * 32, rowt);
+              tma_store_2d(dm, smem_u32(my_stg), n_blk * BN + c * 32, rowt);
+              if (two) tma_store_2d(dm, smem_u32(my_stg + 2048), n_blk * BN + (c + 1) * 32, rowt);
             }
             bulk_commit();
           }
@@ -855,7 +862,8 @@ int tc_w_box(int code) { return code > 1000 ? (code - 1000) / 2 : code; }
 
 template <int BN, int EPI>
 static void launch_pair_epi(const CUtensorMap& tmA, const CUtensorMap& tmB, const float* bias, bf16* D, int M, int N,
-                            int K, cudaStream_t st, const QkvScatter& qs, const CUtensorMap* tmD, const TailWs* tw) {
+                            int K, cudaStream_t st, const QkvScatter& qs, const CUtensorMap* tmD, const TailWs* tw,
+                            const ShardStore* shard) {
   using C = Tc2Cfg<BN>;
   static bool attr = false;
   if (!attr) {
@@ -878,7 +886,7 @@ static void launch_pair_epi(const CUtensorMap& tmA, const CUtensorMap& tmB, cons
     const char* e = getenv("ENERGON_SK_MIN_NKB");
     min_nkb = e ? atoi(e) : 160;
   }
-  if (rem > 0 && (pairs - rem) * 100 >= 15 * pairs && nkb >= min_nkb && !getenv("ENERGON_NO_STREAMK")) {
+  if (!(shard && EPI == EPI_NONE) && rem > 0 && (pairs - rem) * 100 >= 15 * pairs && nkb >= min_nkb && !getenv("ENERGON_NO_STREAMK")) {
     const TailWs* w = tw ? tw : default_tail_ws();
     if (w->ws) {
       const int Lmin = (rem * nkb + pairs - 1) / pairs;  // every tail cluster index < pairs
@@ -927,8 +935,14 @@ static void launch_pair_epi(const CUtensorMap& tmA, const CUtensorMap& tmB, cons
     cudaMemcpyToSymbol(g_gemm_trace, &trace_buf, sizeof(trace_buf));
   }
   if (trace_buf) cudaMemsetAsync(trace_buf, 0, trace_n * sizeof(uint64_t), st);
+  ShardStore sh;
+  if (shard && EPI == EPI_NONE) {  // (the stream-K tail is off for shard-routed GEMMs)
+    sh = *shard;
+  } else {
+    memset(&sh, 0, sizeof(sh));  // k = 0: the output map tmD
+  }
   launch_k(gemm_tc2_kernel<BN, EPI>, dim3(grid), dim3(128 + 32 * C::EPI_WARPS), C::SMEM, st, tmA, tmB, D, bias, M, N, K,
-           group_m, qs, tp, md, hints);
+           group_m, qs, tp, md, hints, sh);
   if (trace_buf) {  // diagnostics only: synchronous dump of this launch's unit timestamps
     std::vector<uint64_t> h(trace_n);
     cudaMemcpy(h.data(), trace_buf, trace_n * sizeof(uint64_t), cudaMemcpyDeviceToHost);
@@ -955,7 +969,7 @@ static void launch_pair_epi(const CUtensorMap& tmA, const CUtensorMap& tmB, cons
 template <int BN, int EPI>
 static void launch_bn_epi(const CUtensorMap& tmA, const CUtensorMap& tmB, const float* bias, bf16* D, int M, int N,
                           int K, cudaStream_t st, const QkvScatter& qs, const CUtensorMap* /*tmD*/,
-                          const TailWs* /*tw*/) {
+                          const TailWs* /*tw*/, const ShardStore* /*shard*/) {
   using C = TcCfg<BN>;
   static bool attr = false;
   if (!attr) {
@@ -969,17 +983,18 @@ static void launch_bn_epi(const CUtensorMap& tmA, const CUtensorMap& tmB, const 
 
 #define DISPATCH_EPI(F, BNARGS)                                                  \
   switch (epi) {                                                                 \
-    case EPI_NONE: F<BNARGS EPI_NONE>(tmA, tmB, bias, D, M, N, K, st, qs, tmD, tw); break; \
-    case EPI_BIAS: F<BNARGS EPI_BIAS>(tmA, tmB, bias, D, M, N, K, st, qs, tmD, tw); break; \
-    case EPI_BIAS_GELU: F<BNARGS EPI_BIAS_GELU>(tmA, tmB, bias, D, M, N, K, st, qs, tmD, tw); break; \
-    default: F<BNARGS EPI_BIAS_QKV>(tmA, tmB, bias, D, M, N, K, st, qs, tmD, tw); break;   \
+    case EPI_NONE: F<BNARGS EPI_NONE>(tmA, tmB, bias, D, M, N, K, st, qs, tmD, tw, shard); break; \
+    case EPI_BIAS: F<BNARGS EPI_BIAS>(tmA, tmB, bias, D, M, N, K, st, qs, tmD, tw, shard); break; \
+    case EPI_BIAS_GELU: F<BNARGS EPI_BIAS_GELU>(tmA, tmB, bias, D, M, N, K, st, qs, tmD, tw, shard); break; \
+    default: F<BNARGS EPI_BIAS_QKV>(tmA, tmB, bias, D, M, N, K, st, qs, tmD, tw, shard); break;   \
   }
 #define BN256 256,
 #define BN192 192,
 #define BN128 128,
 
 void launch_gemm_tc(const CUtensorMap& tmA, const CUtensorMap& tmB, int bn, const float* bias, bf16* D, int M, int N,
-                    int K, int epi, cudaStream_t st, const QkvScatter* qkv, const CUtensorMap* tmD, const TailWs* tw) {
+                    int K, int epi, cudaStream_t st, const QkvScatter* qkv, const CUtensorMap* tmD, const TailWs* tw,
+                    const ShardStore* shard) {
   if (M <= 0 || N <= 0) return;
   QkvScatter qs{};
   if (qkv) qs = *qkv;

@@ -52,7 +52,7 @@ void launch_p2p_flag(const PeerSet& ps, int k, int me, int kind, uint64_t epoch,
 template <typename Act>
 void launch_p2p_reduce_ln(const PeerSet& ps, int k, int me, int64_t off_X, int64_t off_A, int64_t off_P, int row0,
                           int rows, int H, const float* bias, const float* g, const float* b, float eps, int write_A,
-                          uint64_t epoch, cudaStream_t st);
+                          uint64_t epoch, cudaStream_t st, int slot_rows = 0);
 void launch_p2p_push_rows(const PeerSet& ps, int k, int me, int64_t off, int row0, int rows, int64_t row_bytes,
                           uint64_t epoch, cudaStream_t st);
 
@@ -138,10 +138,18 @@ struct TailWs {
 };
 bool tail_ws_alloc(TailWs* w);  // cudaMalloc + zeroed counters (synchronous); false on OOM
 void tail_ws_free(TailWs* w);
+// GEMM -> reduce-scatter fused (P2P exchange): output row t goes to rank s = t / rpr, which owns rows
+// [s rpr, (s+1) rpr), at local row t - s rpr of the store map maps[s] (that rank's slot for this rank's
+// partial, in its IPC-mapped region).  rpr is a multiple of 32 so no 32-row store box straddles ranks.
+struct ShardStore {
+  CUtensorMap maps[8];
+  int rpr;
+  int k;
+};
 // tmD: the output map (make_tmap_store) or nullptr to build it per call.
 void launch_gemm_tc(const CUtensorMap& tmA, const CUtensorMap& tmB, int bn, const float* bias, bf16* D, int M, int N,
                     int K, int epi, cudaStream_t st, const QkvScatter* qkv = nullptr, const CUtensorMap* tmD = nullptr,
-                    const TailWs* tw = nullptr);
+                    const TailWs* tw = nullptr, const ShardStore* shard = nullptr);
 int num_sms();
 
 }  // namespace energon

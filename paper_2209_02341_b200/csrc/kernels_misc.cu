@@ -641,12 +641,15 @@ __device__ __forceinline__ void p2p_grid_done(const PeerSetK& ps, int k, int me,
   }
 }
 
+// slot_rows > 0: the partials were pushed here by the peers' GEMM epilogues (GEMM -> reduce-scatter
+// fused, see launch_gemm_tc's ShardStore): rank q's partial of local row i is at
+// off_P + (q * slot_rows + i) * H of THIS rank's region; slot_rows == 0: read each peer's own P.
 template <typename Act, int LN_MAXV, int TPR>
 __global__ void __launch_bounds__(TPR) p2p_reduce_ln_kernel(PeerSetK ps, int k, int me, int64_t off_X, int64_t off_A,
                                                             int64_t off_P, int row0, int rows, int H,
                                                             const float* __restrict__ bias,
                                                             const float* __restrict__ g, const float* __restrict__ b,
-                                                            float eps, int write_A, uint64_t epoch) {
+                                                            float eps, int write_A, uint64_t epoch, int slot_rows) {
   pdl_trigger();
   pdl_wait();
   __shared__ float red[32];
@@ -665,7 +668,9 @@ __global__ void __launch_bounds__(TPR) p2p_reduce_ln_kernel(PeerSetK ps, int k, 
       }
     }
     for (int q = 0; q < k; ++q) {  // rank order: every rank sums the same way
-      const Act* prow = reinterpret_cast<const Act*>(ps.base[q] + off_P) + (int64_t)t * H;
+      const Act* prow = slot_rows ? reinterpret_cast<const Act*>(ps.base[me] + off_P) +
+                                        ((int64_t)q * slot_rows + blockIdx.x) * H
+                                  : reinterpret_cast<const Act*>(ps.base[q] + off_P) + (int64_t)t * H;
 #pragma unroll
       for (int i = 0; i < LN_MAXV; ++i)
         if (i < nv) {
@@ -729,17 +734,17 @@ void launch_p2p_flag(const PeerSet& ps, int k, int me, int kind, uint64_t epoch,
 template <typename Act>
 void launch_p2p_reduce_ln(const PeerSet& ps, int k, int me, int64_t off_X, int64_t off_A, int64_t off_P, int row0,
                           int rows, int H, const float* bias, const float* g, const float* b, float eps, int write_A,
-                          uint64_t epoch, cudaStream_t st) {
+                          uint64_t epoch, cudaStream_t st, int slot_rows) {
   PeerSetK p;
   for (int i = 0; i < 8; ++i) p.base[i] = reinterpret_cast<char*>(ps.base[i]);
   const int grid = rows > 0 ? rows : 1;  // an empty shard still takes part in the completion count
   const int tpr = ln_tpr(H);
   if (tpr == 512)
     NV_DISPATCH_T(H, 512, (launch_k(p2p_reduce_ln_kernel<Act, NVX, 512>, dim3(grid), dim3(512), 0, st, p, k, me, off_X,
-                                    off_A, off_P, row0, rows, H, bias, g, b, eps, write_A, epoch)))
+                                    off_A, off_P, row0, rows, H, bias, g, b, eps, write_A, epoch, slot_rows)))
   else
     NV_DISPATCH_T(H, 256, (launch_k(p2p_reduce_ln_kernel<Act, NVX, 256>, dim3(grid), dim3(256), 0, st, p, k, me, off_X,
-                                    off_A, off_P, row0, rows, H, bias, g, b, eps, write_A, epoch)))
+                                    off_A, off_P, row0, rows, H, bias, g, b, eps, write_A, epoch, slot_rows)))
 }
 
 void launch_p2p_push_rows(const PeerSet& ps, int k, int me, int64_t off, int row0, int rows, int64_t row_bytes,
@@ -751,9 +756,11 @@ void launch_p2p_push_rows(const PeerSet& ps, int k, int me, int64_t off, int row
   launch_k(p2p_push_rows_kernel, dim3(grid), dim3(256), 0, st, p, k, me, off, row0, rows, row_bytes, epoch);
 }
 template void launch_p2p_reduce_ln<float>(const PeerSet&, int, int, int64_t, int64_t, int64_t, int, int, int,
-                                          const float*, const float*, const float*, float, int, uint64_t, cudaStream_t);
+                                          const float*, const float*, const float*, float, int, uint64_t, cudaStream_t,
+                                          int);
 template void launch_p2p_reduce_ln<bf16>(const PeerSet&, int, int, int64_t, int64_t, int64_t, int, int, int,
-                                         const float*, const float*, const float*, float, int, uint64_t, cudaStream_t);
+                                         const float*, const float*, const float*, float, int, uint64_t, cudaStream_t,
+                                         int);
 
 #define INST_ACT(Act)                                                                                                   \
   template void launch_embed_ln<Act>(const int*, const int*, int, int, int, int, int, const Act*, const Act*,            \

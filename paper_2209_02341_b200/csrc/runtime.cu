@@ -84,6 +84,11 @@ struct energon_ctx {
   PeerSet peers{};
   std::vector<void*> ipc_opened;
   uint64_t epoch = 0;
+  // GEMM -> reduce-scatter fused: slots [k][slot_rows][H] in every region receive the peers' partials
+  int64_t off_S = 0;
+  int slot_rows = 0;
+  ShardStore shard{};
+  ShardStore shard_rpr{};  // `shard` with this forward's rows per rank
   bool fuse = true;  // fused a5 / a7 (ENERGON_NO_FUSE=1 disables, for A/B and tests)
   bool sp = true;    // k > 1: sequence-parallel schedule (reduce-scatter / LN on own rows / all-gather)
   // CUDA-graph cache (ENERGON_OPT_GRAPH): whole forwards captured on cap_stream, replayed on the caller's
@@ -226,7 +231,9 @@ energon_status setup(energon_ctx* c) {
     c->off_X = P2P_FLAG_BYTES;
     c->off_A = al(c->off_X + (int64_t)sizeof(float) * R * c->H);
     c->off_P = al(c->off_A + (int64_t)a * R * c->H);
-    const int64_t bytes = al(c->off_P + (int64_t)a * R * c->H);
+    c->slot_rows = (int)((((int64_t)R + c->k - 1) / c->k + 31) / 32 * 32);  // rows per rank, multiple of 32
+    c->off_S = al(c->off_P + (int64_t)a * R * c->H);
+    const int64_t bytes = al(c->off_S + (int64_t)a * c->k * c->slot_rows * c->H);
     if ((s = dalloc(c, reinterpret_cast<char**>(&c->region), (size_t)bytes, ws))) return s;
     CU(c, cudaMemset(c->region, 0, (size_t)bytes));
     c->X = reinterpret_cast<float*>(static_cast<char*>(c->region) + c->off_X);
@@ -510,7 +517,7 @@ energon_status tp_gather(energon_ctx** cs, int n, int rpr, bool x_buf, cudaStrea
 // ---- P2P exchange (cfg.comm == ENERGON_COMM_P2P; kernels_misc.cu describes the protocol)
 template <typename Act>
 void p2p_exchange(energon_ctx* c, int rows, int rpr, const float* bias, const float* g, const float* b, bool write_A,
-                  cudaStream_t st) {
+                  cudaStream_t st, bool fused_rs) {
   const int r0 = std::min(rows, c->r * rpr), sn = std::max(0, std::min(rows, (c->r + 1) * rpr) - c->r * rpr);
   const uint64_t e = ++c->epoch;
   {
@@ -520,8 +527,9 @@ void p2p_exchange(energon_ctx* c, int rows, int rpr, const float* bias, const fl
   {
     // bytes over NVLink + local: k partial rows read, (write_A ? k : 0) LN rows stored, X read + written
     Prof p(c, st, P_COMM, (double)sn * c->H * (c->k * sizeof(Act) + (write_A ? c->k * sizeof(Act) : 0) + 8.0));
-    launch_p2p_reduce_ln<Act>(c->peers, c->k, c->r, c->off_X, c->off_A, c->off_P, r0, sn, c->H, bias, g, b,
-                              c->cfg.ln_eps, write_A ? 1 : 0, e, st);
+    // fused: the partials of this rank's rows are already in its own slots (local reads only)
+    launch_p2p_reduce_ln<Act>(c->peers, c->k, c->r, c->off_X, c->off_A, fused_rs ? c->off_S : c->off_P, r0, sn, c->H,
+                              bias, g, b, c->cfg.ln_eps, write_A ? 1 : 0, e, st, fused_rs ? c->slot_rows : 0);
   }
   {
     Prof p(c, st, P_COMM, 0.0);
@@ -529,6 +537,7 @@ void p2p_exchange(energon_ctx* c, int rows, int rpr, const float* bias, const fl
   }
   c->stats.kernel_launches += 3;
   c->stats.allreduce_calls++;
+  if (fused_rs) c->stats.fused_exchanges++;
 }
 
 // all-gather of this rank's row shard of the buffer at `off` (row_bytes per row) by pushing to peers
@@ -549,12 +558,12 @@ void p2p_gather(energon_ctx* c, int rows, int rpr, int64_t off, int64_t row_byte
 template <typename Act>
 void gemm(energon_ctx* c, const CUtensorMap& tmA, const CUtensorMap* tmB, const void* A, const void* W,
           const float* bias, void* D, int M, int N, int K, int epi, cudaStream_t st, const QkvScatter* qs = nullptr,
-          const CUtensorMap* tmD = nullptr) {
+          const CUtensorMap* tmD = nullptr, const ShardStore* shard = nullptr) {
   Prof p(c, st, P_GEMM, 2.0 * M * N * K);
   if constexpr (sizeof(Act) == 2) {
     const int code = tc_pick_bn(M, N);
     launch_gemm_tc(tmA, tmB[box_slot(tc_w_box(code))], code, bias, reinterpret_cast<bf16*>(D), M, N, K, epi, st, qs,
-                   tmD, &c->tail);
+                   tmD, &c->tail, shard);
   } else {
     launch_gemm_f32(reinterpret_cast<const float*>(A), reinterpret_cast<const float*>(W), bias,
                     reinterpret_cast<float*>(D), M, N, K, epi, st);
@@ -595,7 +604,15 @@ energon_status forward_t(energon_ctx** cs, int n, const Call& a, int64_t T) {
   // TP schedule: row shard [r0, r0 + sn) of each rank (the whole range without sequence parallelism)
   const bool p2p = c0->p2p;  // one context per process, peers over CUDA IPC (sequence-parallel schedule)
   const bool sp = c0->k > 1 && (c0->sp || p2p);
-  const int rpr = sp ? (rows + c0->k - 1) / c0->k : rows;
+  // P2P: shards of a multiple of 32 rows, so the fused GEMM -> reduce-scatter's 32-row store boxes never
+  // straddle two owners (the trailing ranks may own fewer rows, or none)
+  const int rpr = !sp ? rows : p2p ? ((rows + c0->k - 1) / c0->k + 31) / 32 * 32 : (rows + c0->k - 1) / c0->k;
+  // the row-parallel GEMMs route their rows to the owners' slots when the 2-CTA tcgen05 kernel runs them
+  const bool fused_rs = p2p && sizeof(Act) == 2 && c0->shard.k > 0 && tc_pick_bn(rows, c0->H) > 1000;
+  if (fused_rs) {
+    c0->shard_rpr = c0->shard;
+    c0->shard_rpr.rpr = rpr;
+  }
   auto shard0 = [&](const energon_ctx* c) { return sp ? std::min(rows, c->r * rpr) : 0; };
   auto shardn = [&](const energon_ctx* c) { return sp ? std::max(0, std::min(rows, (c->r + 1) * rpr) - c->r * rpr) : rows; };
   // PMEP: the off-device layers of this forward in execution order, per context
@@ -711,12 +728,13 @@ energon_status forward_t(energon_ctx** cs, int n, const Call& a, int64_t T) {
         }
         c->stats.kernel_launches += 2;
       }
-      gemm<Act>(c, c->tmA_Ctx, W.tm_o, c->Ctx, W.wo, nullptr, c->P, rows, c->H, c->Hk, EPI_NONE, st, nullptr, &c->tmD_P);
+      gemm<Act>(c, c->tmA_Ctx, W.tm_o, c->Ctx, W.wo, nullptr, c->P, rows, c->H, c->Hk, EPI_NONE, st, nullptr, &c->tmD_P,
+                fused_rs ? &c->shard_rpr : nullptr);
     }
     energon_status s = ENERGON_OK;
     if (p2p) {  // a9 fused: reduce over peer memory + bias + residual + LN2, LN rows pushed to every rank
       const LayerDev& L = c0->layers[l];
-      p2p_exchange<Act>(c0, rows, rpr, L.bo, L.ln2g, L.ln2b, true, st);
+      p2p_exchange<Act>(c0, rows, rpr, L.bo, L.ln2g, L.ln2b, true, st, fused_rs);
     }
     if (!p2p && (s = tp_reduce<Act>(cs, n, rows, rpr, sp, st))) return s;
     // ---- a9: bias + residual + LN2 on this rank's rows, then (SP) all-gather of the LN output
@@ -737,7 +755,8 @@ energon_status forward_t(energon_ctx** cs, int n, const Call& a, int64_t T) {
       const LayerDev& W = weights(i, l);
       const LayerDev& L = c->layers[l];
       gemm<Act>(c, c->tmA_A, W.tm_1, c->A, W.w1, L.b1, c->G, rows, c->Fk, c->H, EPI_BIAS_GELU, st, nullptr, &c->tmD_G);
-      gemm<Act>(c, c->tmA_G, W.tm_2, c->G, W.w2, nullptr, c->P, rows, c->H, c->Fk, EPI_NONE, st, nullptr, &c->tmD_P);
+      gemm<Act>(c, c->tmA_G, W.tm_2, c->G, W.w2, nullptr, c->P, rows, c->H, c->Fk, EPI_NONE, st, nullptr, &c->tmD_P,
+                fused_rs ? &c->shard_rpr : nullptr);
       if (!c->pm.layers.empty() && c->pm.index[l] >= 0) {
         // the slot is free once these GEMMs ran: record it and prefetch the off-device layer `slots` ahead
         const int ns = (int)c->pm.slots.size();
@@ -750,7 +769,7 @@ energon_status forward_t(energon_ctx** cs, int n, const Call& a, int64_t T) {
     if (p2p) {  // a12 fused (LN1 of the next layer, none after the last layer)
       const LayerDev& L = c0->layers[l];
       const LayerDev& Ln = c0->layers[last ? l : l + 1];
-      p2p_exchange<Act>(c0, rows, rpr, L.b2, Ln.ln1g, Ln.ln1b, !last, st);
+      p2p_exchange<Act>(c0, rows, rpr, L.b2, Ln.ln1g, Ln.ln1b, !last, st, fused_rs);
     }
     if (!p2p && (s = tp_reduce<Act>(cs, n, rows, rpr, sp, st))) return s;
     // ---- a12: bias + residual (+ LN1 of the next layer) on this rank's rows
@@ -810,6 +829,7 @@ energon_status run_eager(energon_ctx** cs, int n, const Call& a, int64_t T) {
 }
 
 void stats_add(energon_stats& d, const energon_stats& x) {
+  d.fused_exchanges += x.fused_exchanges;
   d.forwards += x.forwards;
   d.allreduce_calls += x.allreduce_calls;
   d.kernel_launches += x.kernel_launches;
@@ -880,6 +900,7 @@ energon_status run(energon_ctx** cs, int n, const Call& a) {
     d.allreduce_calls -= before[i].allreduce_calls;
     d.kernel_launches -= before[i].kernel_launches;
     d.prefetch_bytes -= before[i].prefetch_bytes;
+    d.fused_exchanges -= before[i].fused_exchanges;
     ent.delta.push_back(d);
   }
   ent.last_use = ++c0->gclock;
@@ -1066,6 +1087,17 @@ energon_status energon_p2p_connect(energon_ctx* c, const void* handles) {
     }
     c->ipc_opened.push_back(p);
     c->peers.base[q] = p;
+  }
+  if (c->bf16) {
+    // the row-parallel GEMMs store the rows rank s owns into rank s's slot for this rank (GEMM ->
+    // reduce-scatter fused): one TMA store map per destination rank over [slot_rows, H] bf16
+    memset(&c->shard, 0, sizeof(c->shard));
+    for (int q = 0; q < c->k; ++q) {
+      char* slot = static_cast<char*>(c->peers.base[q]) + c->off_S + (int64_t)c->r * c->slot_rows * c->H * 2;
+      if (!make_tmap_store(&c->shard.maps[q], slot, c->slot_rows, c->H))
+        return fail(c, ENERGON_ERR_CUDA, "cuTensorMapEncodeTiled failed for a peer slot");
+    }
+    c->shard.k = c->k;
   }
   c->p2p_connected = true;
   return ENERGON_OK;

@@ -40,7 +40,7 @@ def _rank(rank, world, port, dtype, q, case="random"):
         torch.cuda.set_device(0)
         dist.init_process_group("gloo", rank=rank, world_size=world)
         energon.load_library()
-        shape = dict(SHAPES["tiny"], L=2, V=300, max_seq=40)
+        shape = _shape(case)
         B, S, seed, lens = _case(case)
         tok = torch.from_numpy(synth.tokens(B, S, shape["V"], lens, seed)).cuda()
         cfg = energon.make_config(shape["L"], shape["H"], shape["h"], shape["F"], shape["V"], shape["max_seq"], B * S,
@@ -75,14 +75,25 @@ def _rank(rank, world, port, dtype, q, case="random"):
 
 def _case(case):
     """(B, S, seed, lens): random lengths, or a single 1-token sequence (T = 1 < k: rank 1's shard is
-    empty, its kernels still take part in the completion protocol)."""
+    empty, its kernels still take part in the completion protocol), or a wider model whose row-parallel
+    GEMMs run on the 2-CTA tcgen05 kernel and so store their rows straight into the owners' slots (the
+    fused GEMM -> reduce-scatter)."""
     import synth
     if case == "one_token":
         return 1, 4, 4, [1]
+    if case == "wide":
+        return 8, 64, 5, synth.random_lengths(8, 64, 5)
     return 5, 33, 4, synth.random_lengths(5, 33, 4)
 
 
-@pytest.mark.parametrize("dtype,case", [("bf16", "random"), ("f32", "random"), ("bf16", "one_token")])
+def _shape(case):
+    from gpu_helpers import SHAPES
+    if case == "wide":
+        return dict(SHAPES["tiny"], L=2, H=256, h=4, F=1024, V=300, max_seq=64)
+    return dict(SHAPES["tiny"], L=2, V=300, max_seq=40)
+
+
+@pytest.mark.parametrize("dtype,case", [("bf16", "random"), ("f32", "random"), ("bf16", "one_token"), ("bf16", "wide")])
 def test_p2p_two_processes_one_gpu(dtype, case):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
@@ -107,12 +118,14 @@ def test_p2p_two_processes_one_gpu(dtype, case):
         assert "exc" not in res[r], res[r].get("tb")
         assert res[r]["not_connected_status"] == -7
         assert res[r]["stats"]["allreduce_calls"] == 2 * 2 * 2  # 2 per layer, 2 layers, 2 forwards
+        # the wide model's row-parallel GEMMs run on the 2-CTA kernel: every exchange is GEMM -> RS fused
+        assert res[r]["stats"]["fused_exchanges"] == (8 if case == "wide" else 0)
     y0, y1 = res[0]["y"], res[1]["y"]
     assert np.array_equal(y0[0], y1[0]) and np.array_equal(y0[1], y1[1])  # bit-identical replicas
     assert np.array_equal(y0[0], y0[1])                                    # run to run
     # same schedule in one process (local group, in-device rank-order reduce-scatter / all-gather)
     energon.load_library()
-    shape = dict(SHAPES["tiny"], L=2, V=300, max_seq=40)
+    shape = _shape(case)
     B, S, seed, lens = _case(case)
     tok = synth.tokens(B, S, shape["V"], lens, seed)
     ctxs = make_engine(shape, seed, dtype, B * S, k=2)
