@@ -8,3 +8,6 @@ done
 timeout 1200 compute-sanitizer --tool memcheck --error-exitcode 9 --print-limit 20 python -m pytest tests/test_gpu_pipeline.py -q -x -m gpu \
   -k "stage_chain or validation" -p no:cacheprovider > gpurun_out/sanitize_memcheck_pipeline.log 2>&1
 echo "memcheck pipeline exit $?"; tail -3 gpurun_out/sanitize_memcheck_pipeline.log
+# memcheck on the two-process P2P exchange (incl. the fused GEMM -> reduce-scatter peer TMA stores)
+timeout 1200 compute-sanitizer --tool memcheck --target-processes all --error-exitcode 9 --print-limit 20 python -m pytest tests/test_gpu_p2p.py -q -x -p no:cacheprovider > gpurun_out/sanitize_memcheck_p2p.log 2>&1
+echo "memcheck p2p exit $?"; tail -4 gpurun_out/sanitize_memcheck_p2p.log
