@@ -146,7 +146,8 @@ typedef struct energon_ctx energon_ctx;
  *   layer floor((g+1) L / m) - 1 for g = 0..m-1, m = L - resident; (24, 20) -> {5, 11, 17, 23}
  *   (PAPER.md:601-602).  out_layers holds m ints, ascending.
  * energon_offload_layers: move the listed (loaded) layers' weight matrices into the pool -- pool 0 =
- *   pinned host memory, 1 = the memory of CUDA device `peer_device` (NVLink peer) -- and free them on
+ *   pinned host memory, 1 = the memory of CUDA device `peer_device` (NVLink peer; the computing device
+ *   itself is accepted, a same-device pool for single-GPU tests) -- and free them on
  *   the computing GPU.  During a forward each off-device layer is copied into one of `slots` staging
  *   buffers on a separate copy stream, issued as soon as the slot's previous layer finished computing
  *   ("prefetch the next off-device layer immediately ..."); compute waits on an event.

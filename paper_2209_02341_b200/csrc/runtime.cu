@@ -970,7 +970,7 @@ energon_status energon_offload_layers(energon_ctx* c, const int32_t* layers, int
   pm.bytes = sz[0] + sz[1] + sz[2] + sz[3];
   pm.pool_kind = pool;
   pm.peer = peer;
-  if (pool == 1) {
+  if (pool == 1 && peer != c->cfg.device) {  // (peer == device: a same-device pool, for single-GPU tests)
     int ok = 0;
     CU(c, cudaDeviceCanAccessPeer(&ok, c->cfg.device, peer));
     if (!ok) return fail(c, ENERGON_ERR_ARG, "peer_device is not peer-accessible from this device");

@@ -470,12 +470,13 @@ def test_forward_edge_cases(dtype, case):
 
 
 # ----------------------------------------------------------------------------- PMEP (next row N1)
-@pytest.mark.parametrize("slots", [1, 2])
+@pytest.mark.parametrize("slots,pool", [(1, 0), (2, 0), (2, 1)])
 @pytest.mark.parametrize("dtype", ["bf16", "f32"])
-def test_pmep_offload_bitexact(slots, dtype):
+def test_pmep_offload_bitexact(slots, pool, dtype):
     """Peer memory pooling: off-device layers prefetched from pinned host memory
-    into staging slots on a copy stream give bit-identical output to the all-resident run, and the
-    fetched bytes match the placement."""
+    (pool 0) or a peer device's memory (pool 1 -- on the single-GPU pool the 'peer' is device 0 itself,
+    which runs the same cudaMemcpyPeerAsync path) into staging slots on a copy stream give bit-identical
+    output to the all-resident run, and the fetched bytes match the placement."""
     shape = dict(L=6, H=256, h=4, F=1024, V=500, max_seq=64)
     B, S, seed = 5, 48, 21
     lens = synth.random_lengths(B, S, seed)
@@ -489,7 +490,7 @@ def test_pmep_offload_bitexact(slots, dtype):
     for layers in (plan, [0, 2, 4, 5]):
         ctxs = make_engine(shape, seed, dtype, B * S)
         try:
-            E().energon_offload_layers(ctxs[0], layers, slots=slots, pool=0)
+            E().energon_offload_layers(ctxs[0], layers, slots=slots, pool=pool, peer_device=0 if pool else -1)
             y = run_forward(ctxs, tok, lens, dtype, shape["H"])
             y2 = run_forward(ctxs, tok, lens, dtype, shape["H"])  # slots reused across forwards
             st = E().energon_get_stats(ctxs[0])
