@@ -518,14 +518,17 @@ void launch_gather_ln(const float* x, const int* pack_idx, int row0, int rows, i
 
 // Threads per row for the residual + LN kernel: 512 for H >= 4096, else 256; ENERGON_LN_TPR=128|256|512
 // overrides (128 only when the row fits in 12 float4 per thread).
-static int ln_tpr(int H) {
+static int ln_tpr(int H, int rows) {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("ENERGON_LN_TPR");
-    v = e ? atoi(e) : 0;  // 0: by hidden size
+    v = e ? atoi(e) : 0;  // 0: by hidden size and row count
     if (v != 0 && v != 128 && v != 256 && v != 512) v = 0;
   }
-  if (v == 0) return H >= 4096 ? 512 : 256;  // measured: 512 threads per row is ~4% faster at H = 5120
+  // measured (H = 5120): 512 threads per row is ~4% faster for the 4096 rows of TP = 1 (40.3 vs 42.0 us),
+  // 256 is 21% faster for the 512 rows a rank normalises at TP = 8 (8.6 vs 10.9 us): few rows want
+  // more, smaller CTAs per SM
+  if (v == 0) return (H >= 4096 && rows > 8 * 148) ? 512 : 256;
   if (v == 128 && H / 4 > 128 * 12) return 256;
   return v;
 }
@@ -534,7 +537,7 @@ template <typename Act>
 void launch_residual_ln(float* X, const Act* P, const float* bias, int rows, int H, const float* g, const float* b,
                         float eps, Act* A, cudaStream_t st) {
   if (rows <= 0) return;
-  const int tpr = ln_tpr(H);
+  const int tpr = ln_tpr(H, rows);
   if (tpr == 128)
     NV_DISPATCH_T(H, 128, (launch_k(residual_ln_kernel<Act, NVX, 128>, dim3(rows), dim3(128), 0, st, X, P, bias, H, g, b, eps, A)))
   else if (tpr == 512)
@@ -738,7 +741,7 @@ void launch_p2p_reduce_ln(const PeerSet& ps, int k, int me, int64_t off_X, int64
   PeerSetK p;
   for (int i = 0; i < 8; ++i) p.base[i] = reinterpret_cast<char*>(ps.base[i]);
   const int grid = rows > 0 ? rows : 1;  // an empty shard still takes part in the completion count
-  const int tpr = ln_tpr(H);
+  const int tpr = ln_tpr(H, rows);
   if (tpr == 512)
     NV_DISPATCH_T(H, 512, (launch_k(p2p_reduce_ln_kernel<Act, NVX, 512>, dim3(grid), dim3(512), 0, st, p, k, me, off_X,
                                     off_A, off_P, row0, rows, H, bias, g, b, eps, write_A, epoch, slot_rows)))
