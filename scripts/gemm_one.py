@@ -3,7 +3,7 @@ import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2209_02341_b200 import energon
-energon.load_library()
+energon.load_library(os.environ.get("AB_LIB", energon.SO_PATH))
 M, N, K, epi = (int(x) for x in sys.argv[1:5])
 A = (torch.randn(M, K, device="cuda") * 0.5).bfloat16()
 W = (torch.randn(N, K, device="cuda") * 0.02).bfloat16()
