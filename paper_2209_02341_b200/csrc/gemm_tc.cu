@@ -538,11 +538,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       while (wi.next(tp, nkb, ncl, tile, kb0, kb1, split, tail)) {
         int m_blk, n_blk;
         raster(tile, num_m, num_n, group_m, m_blk, n_blk);
-        // serpentine K order (hints bit 2): whole tiles of odd rounds walk K backwards, so a round
-        // starts on the k-slices of its A panels the previous round read last (still in L2)
-        const bool rev = (l2_hints & 4) && tail < 0 && ((tile / ncl) & 1);
-        for (int i = kb0; i < kb1; ++i) {
-          const int kb = rev ? kb0 + kb1 - 1 - i : i;
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           const uint32_t fb = smem_u32(&full[stage]) & PEER_MASK;
           if (leader) mbar_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
@@ -931,9 +927,6 @@ static void launch_pair_epi(const CUtensorMap& tmA, const CUtensorMap& tmB, cons
     const char* e = getenv("ENERGON_L2_HINTS");
     hints = e ? atoi(e) : 2;
   }
-  // bit 2, serpentine K order, where a round's A panels overflow L2 (K >= 10240: MLP-down at TP <= 2)
-  static const bool serp = getenv("ENERGON_NO_SERPENTINE") == nullptr;
-  const int hints_l = hints | ((serp && nkb >= 160) ? 4 : 0);
   static const char* trace_file = getenv("ENERGON_GEMM_TRACE");
   static uint64_t* trace_buf = nullptr;
   const size_t trace_n = (size_t)(grid / 2) * 32 * 6;
@@ -949,7 +942,7 @@ static void launch_pair_epi(const CUtensorMap& tmA, const CUtensorMap& tmB, cons
     memset(&sh, 0, sizeof(sh));  // k = 0: the output map tmD
   }
   launch_k(gemm_tc2_kernel<BN, EPI>, dim3(grid), dim3(128 + 32 * C::EPI_WARPS), C::SMEM, st, tmA, tmB, D, bias, M, N, K,
-           group_m, qs, tp, md, hints_l, sh);
+           group_m, qs, tp, md, hints, sh);
   if (trace_buf) {  // diagnostics only: synchronous dump of this launch's unit timestamps
     std::vector<uint64_t> h(trace_n);
     cudaMemcpy(h.data(), trace_buf, trace_n * sizeof(uint64_t), cudaMemcpyDeviceToHost);
