@@ -1,4 +1,4 @@
-"""GPU test of the P2P TP exchange (cfg.comm = ENERGON_COMM_P2P): two processes, one context each,
+"""GPU test of the P2P TP exchange (cfg.comm = ENERGON_COMM_P2P): two or eight processes, one context each,
 peers' exchange regions mapped by CUDA IPC, handles all-gathered over torch.distributed (gloo).  The
 single-GPU pool runs both ranks on cuda:0 (IPC works between processes of one device; the GPU
 time-slices the two contexts), which exercises the same signal / reduce / push / wait protocol an
@@ -81,7 +81,7 @@ def _case(case):
     import synth
     if case == "one_token":
         return 1, 4, 4, [1]
-    if case == "wide":
+    if case in ("wide", "wide8"):
         return 8, 64, 5, synth.random_lengths(8, 64, 5)
     return 5, 33, 4, synth.random_lengths(5, 33, 4)
 
@@ -90,11 +90,16 @@ def _shape(case):
     from gpu_helpers import SHAPES
     if case == "wide":
         return dict(SHAPES["tiny"], L=2, H=256, h=4, F=1024, V=300, max_seq=64)
+    if case == "wide8":  # 8 heads of d = 64: one head and 256 FFN columns per rank at k = 8
+        return dict(SHAPES["tiny"], L=2, H=512, h=8, F=2048, V=300, max_seq=64)
     return dict(SHAPES["tiny"], L=2, V=300, max_seq=40)
 
 
-@pytest.mark.parametrize("dtype,case", [("bf16", "random"), ("f32", "random"), ("bf16", "one_token"), ("bf16", "wide")])
-def test_p2p_two_processes_one_gpu(dtype, case):
+@pytest.mark.parametrize("dtype,case,world", [("bf16", "random", 2), ("f32", "random", 2), ("bf16", "one_token", 2),
+                                              ("bf16", "wide", 2), ("bf16", "wide8", 8), ("f32", "wide8", 8)])
+def test_p2p_processes_one_gpu(dtype, case, world):
+    """world = 2, and world = 8 (the north-star TP degree: 8 peers' regions mapped, 8 per-destination
+    store maps in the fused GEMM -> reduce-scatter, 8-way flags) -- all processes on cuda:0."""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     import torch.multiprocessing as mp
@@ -105,7 +110,6 @@ def test_p2p_two_processes_one_gpu(dtype, case):
     from paper_2209_02341_b200 import build, energon
     build()
     synth.build(device=True)
-    world = 2
     ctx_mp = mp.get_context("spawn")
     q = ctx_mp.Queue()
     port = _free_port()
@@ -119,16 +123,17 @@ def test_p2p_two_processes_one_gpu(dtype, case):
         assert res[r]["not_connected_status"] == -7
         assert res[r]["stats"]["allreduce_calls"] == 2 * 2 * 2  # 2 per layer, 2 layers, 2 forwards
         # the wide model's row-parallel GEMMs run on the 2-CTA kernel: every exchange is GEMM -> RS fused
-        assert res[r]["stats"]["fused_exchanges"] == (8 if case == "wide" else 0)
-    y0, y1 = res[0]["y"], res[1]["y"]
-    assert np.array_equal(y0[0], y1[0]) and np.array_equal(y0[1], y1[1])  # bit-identical replicas
+        assert res[r]["stats"]["fused_exchanges"] == (8 if case.startswith("wide") and dtype == "bf16" else 0)
+    y0 = res[0]["y"]
+    for r in range(1, world):  # bit-identical replicas
+        assert np.array_equal(y0[0], res[r]["y"][0]) and np.array_equal(y0[1], res[r]["y"][1])
     assert np.array_equal(y0[0], y0[1])                                    # run to run
     # same schedule in one process (local group, in-device rank-order reduce-scatter / all-gather)
     energon.load_library()
     shape = _shape(case)
     B, S, seed, lens = _case(case)
     tok = synth.tokens(B, S, shape["V"], lens, seed)
-    ctxs = make_engine(shape, seed, dtype, B * S, k=2)
+    ctxs = make_engine(shape, seed, dtype, B * S, k=world)
     try:
         for c in ctxs:
             energon.energon_set_option(c, energon.OPT_TP_SP, 1)
