@@ -10,7 +10,8 @@ through properties that hold at any size -- the fp64 or
   half (and every other sequence) bit-identical;
 * pad rows are exactly 0 and every valid output is finite; 283 kernel launches per forward;
 * end to end against the oracle on a sampled sequence, at TP=1 (the bench launch) and TP=8 (the
-  north-star stack): the shortest sequence (47 tokens) recomputed in fp64 through all 40 layers.
+  north-star stack): the shortest sequence (47 tokens) recomputed in fp64 through all 40 layers;
+  config 4 likewise on a 32-token prefix through all 48 layers.
 """
 import numpy as np
 import pytest
@@ -89,22 +90,24 @@ def test_bench_workload_properties_full_size(name):
     assert torch.equal(y3[:3], y[:3]) and torch.equal(y3[4:], y[4:])
 
 
-@pytest.mark.parametrize("k", [1, 8])
-def test_bench_workload_end_to_end_vs_oracle_sampled_sequence(k):
-    """config 3 end to end against the fp64 oracle on a sampled output the oracle can compute on its
-    own.  k=1 is exactly what bench.py times (40 layers, B=16, S=512, exact p=0.5, bf16, TP=1,
-    CUDA-graph replay); k=8 is the north-star target, the bf16 TP=8 DRCE stack (the 8 ranks' shards as
-    a local group on one GPU: same per-rank kernels, in-device rank-order allreduce).  By sequence
-    independence (P12) the shortest sequence's 47 rows depend only on its own tokens, so the oracle
-    runs embed -> 40 padded layers -> final LN on that one sequence, streaming one layer's fp64 weights
-    at a time (2.5 GB each) from the shared seeded generator.  Bar: the north-star bf16 tolerance,
-    max-abs-rel <= 2e-2, after 40 layers of bf16 rounding."""
+@pytest.mark.parametrize("name,k,prefix", [("gpt3_13b", 1, None), ("gpt3_13b", 8, None), ("opt30b", 1, 32)])
+def test_bench_workload_end_to_end_vs_oracle_sampled_sequence(name, k, prefix):
+    """Configs 3 and 4 end to end against the fp64 oracle on a sampled output the oracle can compute on
+    its own.  gpt3_13b k=1 is exactly what bench.py times (40 layers, B=16, S=512, exact p=0.5, bf16,
+    TP=1, CUDA-graph replay); k=8 is the north-star target, the bf16 TP=8 DRCE stack (the 8 ranks'
+    shards as a local group on one GPU: same per-rank kernels, in-device rank-order allreduce); opt30b
+    is config 4 (48 layers, H=7168, B=32, S=1024) with graph replay.  By sequence independence (P12)
+    the shortest sequence's rows depend only on its own tokens, and by causal prefix invariance (P13)
+    its first `prefix` rows only on its first `prefix` tokens, so the oracle runs embed -> all padded
+    layers -> final LN on that one sequence (or prefix), streaming one layer's fp64 weights at a time
+    from the shared seeded generator.  Bar: the north-star bf16 tolerance, max-abs-rel <= 2e-2
+    (SURVEY.md C14), after 40 / 48 layers of bf16 rounding."""
     import oracle
     from paper_2209_02341_b200 import energon
-    shape = SHAPES["gpt3_13b"]
-    bcfg = synth.BATCHES["gpt3_13b"]
+    shape = SHAPES[name]
+    bcfg = synth.BATCHES[name]
     B, S, seed = bcfg["B"], bcfg["S"], 0
-    lens = synth.batch_lengths("gpt3_13b", seed)
+    lens = synth.batch_lengths(name, seed)
     H, F, L = shape["H"], shape["F"], shape["L"]
     tok_np = synth.tokens(B, S, shape["V"], lens, seed)
     ctxs = make_engine(shape, seed, "bf16", B * S, k=k)
@@ -118,14 +121,15 @@ def test_bench_workload_end_to_end_vs_oracle_sampled_sequence(k):
                 energon.energon_forward(ctxs[0], tok, lens, out)
                 energon.energon_sync(ctxs[0])
             y = out.float().cpu().double().numpy()
+            del out
         else:
             y = run_forward(ctxs, tok_np, lens, "bf16", H)
     finally:
         destroy(ctxs)
         torch.cuda.empty_cache()
     b = int(np.argmin(lens))
-    n = lens[b]
-    assert n == 47
+    n = lens[b] if prefix is None else min(prefix, lens[b])
+    assert n == {"gpt3_13b": 47, "opt30b": 32}[name]
     cfg = oracle.make_cfg(1, H, shape["h"], F)
     emb = {e: synth.emb_tensor_host(e, H, shape["V"], shape["max_seq"], seed, True) for e in synth.EMB_TENSORS}
     X = oracle.embed(cfg, emb, tok_np[b:b + 1, :n])
@@ -135,7 +139,7 @@ def test_bench_workload_end_to_end_vs_oracle_sampled_sequence(k):
         del layer
     ref = oracle.layernorm(X, emb["lnf_g"], emb["lnf_b"], cfg.eps)
     err = max_abs_rel(y[b:b + 1, :n], ref, [n])
-    print(f"config 3 end to end, TP={k}, sequence {b} ({n} tokens): max-abs-rel {err:.3e} (tol 2e-2)")
+    print(f"{name} end to end, TP={k}, sequence {b} ({n} rows of {lens[b]}): max-abs-rel {err:.3e} (tol 2e-2)")
     assert err <= 2e-2, err
     for bb, nn in enumerate(lens):
         assert not y[bb, nn:].any()
