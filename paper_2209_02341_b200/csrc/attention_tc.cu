@@ -456,6 +456,10 @@ __global__ void __launch_bounds__(192, 2)
   pdl_trigger();  // after the TMEM allocation (see attention_tc_kernel)
   const uint32_t tO = tmem_base + 2 * BN;
 
+  // the CTA's k-th item: heaviest-first list dealt out boustrophedon (round k even: slot bid, odd:
+  // slot G-1-bid), so no CTA takes the heaviest item of every round (simulated makespan on config 3:
+  // 45.2 -> 41.3 us of item cost vs plain round-robin)
+  auto item_at = [&](int k) { return k * (int)gridDim.x + ((k & 1) ? (int)gridDim.x - 1 - (int)blockIdx.x : (int)blockIdx.x); };
   auto decode = [&](int w, int& b, int& head, int& q0, int& nkv, int& len) {
     const uint32_t pr = work.pair[w / hk];
     head = w % hk;
@@ -471,7 +475,7 @@ __global__ void __launch_bounds__(192, 2)
       // ---------------- TMA producer: per item Q once, then K_0, K_1, V_0, K_2, V_1, ... (t = CTA tile count)
       pdl_wait();
       int t = 0, qi = 0;
-      for (int w = blockIdx.x; w < items; w += gridDim.x, ++qi) {
+      for (int w = item_at(0); w < items; w = item_at(++qi)) {
         int b, head, q0, nkv, len;
         decode(w, b, head, q0, nkv, len);
         const int row_base = (b * hk + head) * S;
@@ -503,7 +507,7 @@ __global__ void __launch_bounds__(192, 2)
   } else if (warp == 1) {
     if (lane == 0) {
       // ---------------- MMA issuer: S_t, then P_{t-1} V_{t-1}, over the CTA's whole tile sequence
-      int w = blockIdx.x, qi = 0, j = 0, nkv = 0;
+      int w = item_at(0), qi = 0, j = 0, nkv = 0;
       {
         int b_, h_, q_, l_;
         if (w < items) decode(w, b_, h_, q_, nkv, l_);
@@ -555,7 +559,7 @@ __global__ void __launch_bounds__(192, 2)
         if (++j == nkv) {  // next item of this CTA
           j = 0;
           ++qi;
-          w += gridDim.x;
+          w = item_at(qi);
           if (w < items) {
             int b_, h_, q_, l_;
             decode(w, b_, h_, q_, nkv, l_);
@@ -570,7 +574,7 @@ __global__ void __launch_bounds__(192, 2)
     const int r = qd * 32 + lane;
     const uint32_t lane_off = (uint32_t)(qd * 32) << 16;
     int t = 0;
-    for (int w = blockIdx.x; w < items; w += gridDim.x) {
+    for (int k = 0, w = item_at(0); w < items; w = item_at(++k)) {
       int b, head, q0, nkv, len;
       decode(w, b, head, q0, nkv, len);
       const int srow = q0 + r;

@@ -4,7 +4,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import synth
 from paper_2209_02341_b200 import energon
-energon.load_library()
+energon.load_library(os.environ.get("AB_LIB", energon.SO_PATH))
 cases = {
     "gpt3_p0.5 (B16 S512)": (16, 512, synth.exact_p_lengths(16, 512, 0.5, 0)),
     "full S512 (B16)": (16, 512, [512] * 16),
