@@ -11,7 +11,9 @@ cases = {
     "full S2048 (B4)": (4, 2048, [2048] * 4),
     "full S128 (B64)": (64, 128, [128] * 64),
 }
-hk, d = 40, 128
+if os.environ.get("ATTN_CASES") == "gpt3":  # only the config-3 mix (e.g. under ncu)
+    cases = {k: v for k, v in cases.items() if k.startswith("gpt3")}
+hk, d = int(os.environ.get("ATTN_HK", "40")), 128  # ATTN_HK: heads per rank (TP=8: 5)
 for name, (B, S, lens) in cases.items():
     Q, K, V = (torch.randn(B, hk, S, d, device="cuda").bfloat16() for _ in range(3))
     O = torch.empty_like(Q)
