@@ -64,8 +64,6 @@ def lib():
         L.oracle_forward_drce.argtypes = fwd
         L.oracle_forward_tp.argtypes = [ctypes.POINTER(Cfg), ctypes.c_int] + fwd[1:] + [
             ctypes.POINTER(ctypes.c_int64)]
-        L.oracle_tp_partial.argtypes = [ctypes.POINTER(Cfg), ctypes.c_int, ctypes.c_int, ctypes.c_int, PP, _D,
-                                        _I, ctypes.c_int, ctypes.c_int, _D]
         L.oracle_embed.argtypes = [ctypes.POINTER(Cfg), _D, _D, _I, ctypes.c_int, ctypes.c_int, _D]
         L.oracle_num_threads.restype = ctypes.c_int
         _lib = L
@@ -206,15 +204,6 @@ def forward_tp(cfg: Cfg, k: int, layers: list, emb: dict, tok, lens, final_ln=Tr
     Y = _fwd(lib().oracle_forward_tp, cfg, layers, emb, tok, lens, final_ln, extra_pre=(ctypes.c_int(k),),
              extra_post=(ctypes.byref(cnt),))
     return Y, cnt.value
-
-
-def tp_partial(cfg: Cfg, k: int, r: int, which: int, layer: dict, A, lens) -> np.ndarray:
-    A = f64(A)
-    B, S, H = A.shape
-    w = _Weights([layer])
-    part = np.empty((B, S, H))
-    lib().oracle_tp_partial(ctypes.byref(cfg), k, r, which, w.table, _d(A), _i(i32(lens)), B, S, _d(part))
-    return part
 
 
 def num_threads() -> int:

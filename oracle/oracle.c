@@ -376,38 +376,6 @@ void oracle_forward_tp(const oracle_cfg* cfg, int k, const double* const* layer_
   free(X); free(A); free(Q); free(K); free(V); free(C); free(G); free(part);
 }
 
-/*
- * One rank's share of a TP layer, for multi-process (gloo) tests of the N>1
- * host path: computes this rank's attention partial (or MLP partial) for the
- * given LN output A [M,H].  which = 0: attention module; 1: MLP module.
- */
-void oracle_tp_partial(const oracle_cfg* cfg, int k, int r, int which, const double* const* w, const double* A,
-                       const int* lens, int B, int S, double* part) {
-  const int64_t M = (int64_t)B * S, H = cfg->H, F = cfg->F, Hk = H / k, Fk = F / k, hk = cfg->h / k;
-  if (which == 0) {
-    double* Q = (double*)malloc(sizeof(double) * M * Hk);
-    double* K = (double*)malloc(sizeof(double) * M * Hk);
-    double* V = (double*)malloc(sizeof(double) * M * Hk);
-    double* C = (double*)malloc(sizeof(double) * M * Hk);
-    double* wq = col_slice(w[W_Q], H, H, r * Hk, Hk);
-    double* wk = col_slice(w[W_K], H, H, r * Hk, Hk);
-    double* wv = col_slice(w[W_V], H, H, r * Hk, Hk);
-    linear(A, wq, w[B_Q] + r * Hk, M, H, Hk, Q);
-    linear(A, wk, w[B_K] + r * Hk, M, H, Hk, K);
-    linear(A, wv, w[B_V] + r * Hk, M, H, Hk, V);
-    oracle_attention(Q, K, V, B, S, (int)Hk, (int)hk, lens, cfg->causal, C);
-    linear(C, w[W_O] + r * Hk * H, NULL, M, Hk, H, part);
-    free(Q); free(K); free(V); free(C); free(wq); free(wk); free(wv);
-  } else {
-    double* G = (double*)malloc(sizeof(double) * M * Fk);
-    double* w1 = col_slice(w[W_1], H, F, r * Fk, Fk);
-    linear(A, w1, w[B_1] + r * Fk, M, H, Fk, G);
-    for (int64_t i = 0; i < M * Fk; ++i) G[i] = oracle_gelu(G[i]);
-    linear(G, w[W_2] + r * Fk * H, NULL, M, Fk, H, part);
-    free(G); free(w1);
-  }
-}
-
 /* Number of threads OpenMP will use (reported as cpu_baseline.cores). */
 int oracle_num_threads(void) {
 #ifdef _OPENMP

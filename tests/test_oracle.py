@@ -255,6 +255,42 @@ def test_layer_single_token_reduces_to_matmuls():
     np.testing.assert_allclose(Y[0, 0], x2, rtol=0, atol=1e-12)
 
 
+def test_layer_two_token_qk_wiring_closed_form():
+    """S=2, causal, one head, distinct Wq/Wk/Wv and bq/bk: the second query sees two keys, so its
+    attention weight on key 1 is the two-key sigmoid p = 1/(1+exp(-(q1.k1 - q1.k0)/sqrt(d)))
+    (SPEC.md:65-83).  Everything else is closed form: LN of a zero-mean row x with
+    gamma=1, beta=0 is x/sqrt(var+eps); Wv = Wo = I, MLP weights 0.  Pins which weight feeds Q, K and V
+    in oracle_layer_padded -- a swap of wq/wk, bq/bk or wk/wv moves the result by > 1e-2 (checked)."""
+    H, F, eps = 4, 8, 1e-5
+    d = H
+    X = np.array([[[2.0, -2.0, 2.0, -2.0], [3.0, 1.0, -1.0, -3.0]]])
+    a0 = X[0, 0] / math.sqrt(4.0 + eps)      # var([2,-2,2,-2]) = 4
+    a1 = X[0, 1] / math.sqrt(5.0 + eps)      # var([3,1,-1,-3]) = 5
+    w = zero_layer(H, F)
+    w["wq"] = np.diag([0.5, 1.0, 1.5, 2.0])
+    w["bq"] = np.array([0.6, 0.0, 0.0, 0.0])
+    w["wk"] = np.array([[0.0, 1.0, 0.0, 0.0], [1.0, 0.0, 0.0, 0.0], [0.0, 0.0, 0.0, -1.0], [0.0, 0.0, 1.0, 0.0]])
+    w["bk"] = np.array([0.0, 0.9, 0.0, 0.0])
+    w["wv"] = np.eye(H)
+    w["wo"] = np.eye(H)
+
+    def expected(wq, bq, wk, bk, wv):
+        q1 = a1 @ wq + bq
+        k0, k1 = a0 @ wk + bk, a1 @ wk + bk
+        v0, v1 = a0 @ wv, a1 @ wv
+        p = 1.0 / (1.0 + math.exp(-(q1 @ k1 - q1 @ k0) / math.sqrt(d)))
+        return np.stack([X[0, 0] + v0, X[0, 1] + (1 - p) * v0 + p * v1])
+
+    Y = oracle.layer_padded(oracle.make_cfg(1, H, 1, F), w, X, [2])
+    ref = expected(w["wq"], w["bq"], w["wk"], w["bk"], w["wv"])
+    np.testing.assert_allclose(Y[0], ref, rtol=0, atol=1e-13)
+    # the pin discriminates: each plausible miswiring gives a visibly different layer output
+    for alt in (expected(w["wk"], w["bk"], w["wq"], w["bq"], w["wv"]),   # Q <-> K
+                expected(w["wq"], w["bk"], w["wk"], w["bq"], w["wv"]),   # bq <-> bk
+                expected(w["wq"], w["bq"], w["wv"], w["bk"], w["wk"])):  # K <-> V
+        assert np.abs(alt - ref).max() > 1e-2
+
+
 def test_param_count_gpt3_layer():
     """P14 / PAPER.md:397: one GPT-3 layer = 12H^2+13H = 1.812e9 parameters, 3.375 GiB in FP16."""
     g = GOLD["gpt3_layer_params"]
