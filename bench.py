@@ -46,7 +46,10 @@ def parse():
     ap.add_argument("--config", default="gpt3_13b")
     ap.add_argument("--p", type=float, default=None, help="padding ratio (exact-p configs)")
     ap.add_argument("--regime", default=None, choices=[None, "exact_p", "paper", "random"])
-    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--seed", type=int, default=0, help="first seed of the rotated batches")
+    ap.add_argument("--seeds", type=int, default=5,
+                    help="SURVEY.md 8(d): the timed steps rotate over the batches of seeds seed..seed+seeds-1 "
+                         "(new lengths and tokens every step); per-seed medians are reported")
     ap.add_argument("--drce", type=int, default=1)
     ap.add_argument("--layers", type=int, default=None, help="override the layer count (debug only)")
     ap.add_argument("--no-e2e", action="store_true")
@@ -55,12 +58,12 @@ def parse():
                     help="replay each forward as a CUDA graph (ENERGON_OPT_GRAPH); default on for one GPU, off "
                          "under torchrun (NCCL collectives run eagerly)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-sample-tokens", type=int, default=192)
     ap.add_argument("--pp", type=int, default=1,
                     help="NBPP: one pipeline stage per rank (torchrun, world == pp), --pp-batches batches in flight")
     ap.add_argument("--pp-batches", type=int, default=8)
-    ap.add_argument("--comm", default="nccl", choices=["nccl", "p2p"],
-                    help="TP exchange under torchrun: NCCL, or the fused peer-memory kernels (CUDA IPC)")
+    ap.add_argument("--comm", default="p2p", choices=["nccl", "p2p"],
+                    help="TP exchange for N > 1: the fused peer-memory kernels over CUDA IPC (default; the exchange "
+                         "the multi-process GPU tests check against the oracle) or NCCL")
     ap.add_argument("--local-tp", type=int, default=0,
                     help="emulate TP=k on ONE GPU with a local group (ranks serialised; per-rank kernel "
                          "shapes and ncu evidence of TP=k, not a TP=k latency)")
@@ -130,25 +133,55 @@ class ClockSampler:
 
 
 # ============================================================================= oracle (CPU) arm
-def oracle_sample(args, shape, lens, tok, sample_tokens):
-    """Bounded sample of the workload for the fp64 oracle: layer 0 of the stack over the first
-    `sample_tokens` tokens of the longest sequence (an exact sub-problem: causal prefix, P13 and
-    sequence independence, P12).  Returns (fn, tokens_per_call, layers_extrapolated)."""
+def cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def step_flops(H, L, lens) -> float:
+    """Algorithmic FLOPs of one DRCE forward: per sequence of n valid tokens and per layer,
+    linears 24 H^2 n and causal attention 2 H n (n + 1) (QK^T and PV over the n(n+1)/2 allowed pairs)."""
+    return float(L) * sum(24.0 * H * H * n + 2.0 * H * n * (n + 1) for n in lens)
+
+
+def oracle_sample(args, shape, lens, tok):
+    """SURVEY.md 8(d) "Oracle timing": one layer (layer 0) of the fp64 oracle over the LONGEST and the
+    SHORTEST sequence of the batch, each at its full length (exact sub-problems by sequence independence,
+    P12), measured, then extrapolated to the whole step (all sequences, all layers) by the FLOP ratio of
+    step_flops.  Returns (run, describe): run() -> sample seconds; describe(t) -> (tokens/s, note)."""
     import numpy as np
 
     import oracle
     import synth
-    b = int(np.argmax(lens))
-    n = min(sample_tokens, lens[b])
-    layers, emb = synth.model_host(1, shape["H"], shape["F"], shape["V"], shape["max_seq"], args.seed, True,
-                                   layer_ids=[0])
-    cfg = oracle.make_cfg(1, shape["H"], shape["h"], shape["F"])
-    X = oracle.embed(cfg, emb, tok[b:b + 1, :n])
+    H, L = shape["H"], shape["L"]
+    picks = sorted({int(np.argmax(lens)), int(np.argmin(lens))})
+    layers, emb = synth.model_host(1, H, shape["F"], shape["V"], shape["max_seq"], args.seed, True, layer_ids=[0])
+    cfg = oracle.make_cfg(1, H, shape["h"], shape["F"])
+    xs = [(oracle.embed(cfg, emb, tok[b:b + 1, :lens[b]]), lens[b]) for b in picks]
+    f_sample = step_flops(H, 1, [n for _, n in xs])
+    f_step = step_flops(H, L, lens)
+    T = sum(lens)
 
     def run():
-        oracle.layers_padded(cfg, layers, 0, 1, X, [n])
+        t0 = time.perf_counter()
+        for X, n in xs:
+            oracle.layers_padded(cfg, layers, 0, 1, X, [n])
+        return time.perf_counter() - t0
 
-    return run, n, shape["L"]
+    def describe(t):
+        est = t * f_step / f_sample
+        note = (f"fp64 oracle (oracle/oracle.c, OpenMP), layer 0 of {L} over the longest ({max(lens)}) and the "
+                f"shortest ({min(lens)}) sequence at full length ({t:.1f} s for {f_sample / 1e9:.0f} GFLOP), "
+                f"extrapolated by the FLOP ratio {f_step / f_sample:.0f}x to the whole step (T={T}, {L} layers): "
+                f"{est:.0f} s per step, extrapolated; CPU: {cpu_model()}, {oracle.num_threads()} OpenMP threads")
+        return T / est, note
+
+    return run, describe
 
 
 def reference_arm(args, world, rank):
@@ -162,25 +195,19 @@ def reference_arm(args, world, rank):
     bcfg = synth.BATCHES[args.config]
     lens = synth.batch_lengths(args.config, args.seed, p=args.p, regime=args.regime)
     tok = synth.tokens(bcfg["B"], bcfg["S"], shape["V"], lens, args.seed)
-    ntok = max(8, args.cpu_sample_tokens // 6)
-    run, n, L = oracle_sample(args, shape, lens, tok, ntok)
+    run, describe = oracle_sample(args, shape, lens, tok)
     for _ in range(args.warmup):
         run()
-    times = []
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        run()
-        times.append(time.perf_counter() - t0)
-    tot = sum(times)
-    value = n * args.steps / (tot * L)
-    cores = oracle.num_threads()
-    sample = (f"oracle fp64: layer 0 of {L} over the first {n} tokens of the longest sequence per step, "
-              f"tokens/s extrapolated by the layer count ({L}x)")
+    times = [run() for _ in range(args.steps)]
+    t = sum(times) / len(times)
+    value, note = describe(t)
+    step_s = sum(lens) / value
     out = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
-           "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * step_s, "sample_s_per_step": t,
            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
            "data": "synthetic", "config": workload_config(args, shape, bcfg, lens, world),
-           "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+                            "sample": note, "cpu_model": cpu_model()},
            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 
@@ -265,10 +292,15 @@ def energon_arm(args, world, rank, local):
         shape["L"] = args.layers
     bcfg = synth.BATCHES[args.config]
     B, S = bcfg["B"], bcfg["S"]
-    lens = synth.batch_lengths(args.config, args.seed, p=args.p, regime=args.regime)
-    T = sum(lens)
-    tok_np = synth.tokens(B, S, shape["V"], lens, args.seed)
     H = shape["H"]
+    # the rotated batches (SURVEY.md 8(d) "Seeds 0-4"): lengths + tokens of seeds seed .. seed+seeds-1;
+    # with exact-p lengths every batch has the same T but a different length mix
+    seeds = [args.seed + i for i in range(max(1, args.seeds))]
+    batches = []
+    for sd in seeds:
+        lens = synth.batch_lengths(args.config, sd, p=args.p, regime=args.regime)
+        batches.append({"seed": sd, "lens": lens, "T": sum(lens), "tok": synth.tokens(B, S, shape["V"], lens, sd)})
+    lens0 = batches[0]["lens"]
 
     comm = energon.COMM_P2P if (args.comm == "p2p" and world > 1) else energon.COMM_NCCL
     cfg = energon.make_config(shape["L"], H, shape["h"], shape["F"], shape["V"], shape["max_seq"], B * S,
@@ -276,13 +308,15 @@ def energon_arm(args, world, rank, local):
     uid = None
     if world > 1:
         from paper_2209_02341_b200 import dist as edist
-        uid = edist.broadcast_bytes(energon.energon_get_unique_id() if rank == 0 else None, 128, device=plumb)
-        lens = edist.broadcast_lengths(lens, device=plumb)  # the engine command's seq_lens
+        if comm == energon.COMM_NCCL:
+            uid = edist.broadcast_bytes(energon.energon_get_unique_id() if rank == 0 else None, 128, device=plumb)
+        for bt in batches:  # the engine command's seq_lens: rank 0's list on every rank
+            bt["lens"] = edist.broadcast_lengths(bt["lens"], device=plumb)
     if args.local_tp > 1:
         ctxs = energon.energon_init_local_group(cfg, args.local_tp)
     else:
         ctxs = [energon.energon_init(cfg, uid)]
-    if comm == energon.COMM_P2P:  # map every rank's exchange region (CUDA IPC handles, all-gathered)
+    if comm == energon.COMM_P2P and world > 1:  # map every rank's exchange region (CUDA IPC handles, all-gathered)
         handles = [None] * world
         dist.all_gather_object(handles, energon.energon_p2p_handle(ctxs[0]))
         energon.energon_p2p_connect(ctxs[0], handles)
@@ -307,8 +341,10 @@ def energon_arm(args, world, rank, local):
     eng.set_option(energon.OPT_GRAPH, args.graph)
 
     stream = torch.cuda.current_stream()
-    tok = torch.from_numpy(tok_np).cuda()
+    for bt in batches:
+        bt["tok_d"] = torch.from_numpy(bt["tok"]).cuda()
     out = torch.empty(B, S, H, dtype=torch.bfloat16, device="cuda")
+    nb = len(batches)
 
     def barrier():
         if dist is not None:
@@ -320,8 +356,14 @@ def energon_arm(args, world, rank, local):
         from paper_2209_02341_b200 import dist as edist
         return edist.max_over_ranks(x, device=plumb)
 
-    for _ in range(args.warmup):
-        eng.forward(tok, lens, out, stream)
+    def fwd(i, tok=None, o=None):
+        bt = batches[i % nb]
+        eng.forward(bt["tok_d"] if tok is None else tok, bt["lens"], out if o is None else o, stream)
+
+    # warm-up: W steps, and at least one per rotated batch (each batch's first forward records its graph)
+    warm = max(args.warmup, nb)
+    for i in range(warm):
+        fwd(i)
     eng.sync()
 
     # ---------------- device-timed region: inputs resident in HBM (no per-launch instrumentation)
@@ -336,7 +378,7 @@ def energon_arm(args, world, rank, local):
         torch.cuda.cudart().cudaProfilerStart()
     evs[0].record(stream)
     for i in range(args.steps):
-        eng.forward(tok, lens, out, stream)
+        fwd(i)
         evs[i + 1].record(stream)
     torch.cuda.synchronize()
     if prof_range:
@@ -347,6 +389,13 @@ def energon_arm(args, world, rank, local):
     step_ms = [evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)]
     total_ms = max_over_ranks(evs[0].elapsed_time(evs[-1]))
     launches = eng.launches() - launches0
+    tokens_timed = sum(batches[i % nb]["T"] for i in range(args.steps))
+    value = tokens_timed / (total_ms * 1e-3)
+    per_seed = {}
+    for i, ms in enumerate(step_ms):
+        per_seed.setdefault(batches[i % nb]["seed"], []).append(ms)
+    seed_ms = {sd: statistics.median(v) for sd, v in per_seed.items()}
+    seed_tok_s = {sd: batches[[b["seed"] for b in batches].index(sd)]["T"] / (ms * 1e-3) for sd, ms in seed_ms.items()}
 
     # ---------------- instrumented pass: the same K steps with CUDA events around every launch on
     # the forward stream (energon_set_profiling) -> per-kernel-class device time for the roofline
@@ -356,24 +405,22 @@ def energon_arm(args, world, rank, local):
     p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     p0.record(stream)
     for i in range(args.steps):
-        eng.forward(tok, lens, out, stream)
+        fwd(i)
     p1.record(stream)
     torch.cuda.synchronize()
     barrier()
     prof = eng.profile()
     prof_ms = p0.elapsed_time(p1) / args.steps
     eng.set_profiling(False)
-    value = T * args.steps / (total_ms * 1e-3)
 
     # ---------------- end-to-end: host tokens -> device, forward, result -> host, every step.  The
     # device->host copy of step i's result runs on a copy stream while step i+1 computes (two device
     # output buffers, two pinned host buffers); the timed region ends after the last copy has landed.
     e2e = None
     if not args.no_e2e:
-        tok_h = torch.from_numpy(tok_np).pin_memory()
+        toks_h = [torch.from_numpy(bt["tok"]).pin_memory() for bt in batches]
         outs = [out, torch.empty_like(out)]
         outs_h = [torch.empty(B, S, H, dtype=torch.bfloat16).pin_memory() for _ in range(2)]
-        tok_d = torch.empty_like(tok)
         copy_st = torch.cuda.Stream()
         done = [torch.cuda.Event(), torch.cuda.Event()]  # buffer i's D2H finished
         ready = [torch.cuda.Event(), torch.cuda.Event()]  # buffer i's forward finished
@@ -381,8 +428,9 @@ def energon_arm(args, world, rank, local):
         def e2e_step(i):
             k = i & 1
             stream.wait_event(done[k])  # the D2H of step i-2 has read outs[k]
-            tok_d.copy_(tok_h, non_blocking=True)
-            eng.forward(tok_d, lens, outs[k], stream)
+            tok_d = batches[i % nb]["tok_d"]
+            tok_d.copy_(toks_h[i % nb], non_blocking=True)  # this step's tokens, host -> device
+            fwd(i, tok_d, outs[k])
             ready[k].record(stream)
             copy_st.wait_event(ready[k])
             with torch.cuda.stream(copy_st):
@@ -391,8 +439,8 @@ def energon_arm(args, world, rank, local):
 
         for k in range(2):
             done[k].record(copy_st)
-        e2e_step(0)
-        e2e_step(1)
+        for i in range(nb if nb % 2 == 0 else 2 * nb):  # every (batch, output buffer) pair records its graph
+            e2e_step(i)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         barrier()
@@ -405,16 +453,17 @@ def energon_arm(args, world, rank, local):
         torch.cuda.synchronize()
         barrier()
         e2e_ms = max_over_ranks(e0.elapsed_time(e1))
-        e2e = {"value": T * args.steps / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": tok_h.numel() * 4,
+        e2e = {"value": tokens_timed / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": toks_h[0].numel() * 4,
                "d2h_bytes_per_step": outs_h[0].numel() * 2, "ms_per_step": e2e_ms / args.steps,
                "overlap": "step i's device->host copy overlaps step i+1 (copy stream, double-buffered output)"}
     eng.sync()
 
-    # ---------------- DRCE A/B: the same batch with the linears on all B*S padded rows
+    # ---------------- DRCE A/B: the first batch with the linears on all B*S padded rows
     drce_ab = None
+    T0 = batches[0]["T"]
     if not args.no_ab and args.drce:
         eng.set_option(energon.OPT_DRCE, 0)
-        eng.forward(tok, lens, out, stream)
+        fwd(0)
         torch.cuda.synchronize()
         a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         nab = max(2, args.steps // 2)
@@ -422,16 +471,27 @@ def energon_arm(args, world, rank, local):
         torch.cuda.synchronize()
         a0.record(stream)
         for _ in range(nab):
-            eng.forward(tok, lens, out, stream)
+            fwd(0)
         a1.record(stream)
         torch.cuda.synchronize()
         barrier()
         off_ms = max_over_ranks(a0.elapsed_time(a1)) / nab
         eng.set_option(energon.OPT_DRCE, 1)
-        on_ms = total_ms / args.steps
-        drce_ab = {"drce_on_ms": on_ms, "drce_off_ms": off_ms, "latency_reduction": 1 - on_ms / off_ms,
-                   "valid_tok_s_off": T / (off_ms * 1e-3), "padding_ratio": 1 - T / (B * S),
-                   "ideal_reduction": 1 - T / (B * S),
+        fwd(0)
+        torch.cuda.synchronize()
+        b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        torch.cuda.synchronize()
+        b0.record(stream)
+        for _ in range(nab):
+            fwd(0)
+        b1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        on_ms = max_over_ranks(b0.elapsed_time(b1)) / nab
+        drce_ab = {"batch_seed": batches[0]["seed"], "drce_on_ms": on_ms, "drce_off_ms": off_ms,
+                   "latency_reduction": 1 - on_ms / off_ms, "valid_tok_s_off": T0 / (off_ms * 1e-3),
+                   "padding_ratio": 1 - T0 / (B * S), "ideal_reduction": 1 - T0 / (B * S),
                    "note": "paper: up to 46.8% latency reduction at p=0.5 on A100 (PAPER.md:567-579)"}
     eng.sync()
 
@@ -444,7 +504,7 @@ def energon_arm(args, world, rank, local):
         traffic = tr.get(args.config, {}).get(f"tp{world}")
     except Exception:
         pass
-    roofline = {"bound": "tensor", "kernel": "gemm_tc_kernel (a4/a8/a10/a11, tcgen05 bf16)",
+    roofline = {"bound": "tensor", "kernel": "gemm_tc2_kernel (a4/a8/a10/a11, tcgen05 bf16)",
                 "achieved": achieved, "peak": pk["bf16_tflops_sustained"], "unit": "TFLOP/s",
                 "frac": (achieved / pk["bf16_tflops_sustained"]) if achieved else None, "traffic": traffic,
                 "peak_source": f"{pk['source']} bf16_tflops_sustained (kernel timed inside a long step)",
@@ -453,6 +513,21 @@ def energon_arm(args, world, rank, local):
                 "avg_launch_ms": gemm_ms_avg, "flops_per_step": prof["gemm_flops"] / args.steps,
                 "share_of_step": prof["gemm_ms"] / args.steps / prof_ms,
                 "measured_in": "instrumented pass of the same K steps (CUDA events around every launch)"}
+    k_tp = world if args.local_tp <= 1 else args.local_tp
+    exch_calls = prof["comm_calls"] / args.steps
+    exchange = None
+    if k_tp > 1:
+        # allreduce-equivalent bus bandwidth of the 2 L exchanges per step (nccl-tests convention:
+        # busbw = payload * 2 (k-1) / k / time), payload = the packed [T, H] bf16 partial
+        payload = tokens_timed / args.steps * H * 2
+        n_ex = 2 * shape["L"]
+        ms = prof["comm_ms"] / args.steps
+        exchange = {"kind": "local group (in-device)" if args.local_tp > 1 else args.comm, "exchanges_per_step": n_ex,
+                    "payload_bytes": payload, "ms_per_step": ms,
+                    "bus_gbs": (n_ex * payload * 2 * (k_tp - 1) / k_tp / (ms * 1e-3) / 1e9) if ms else None,
+                    "launch_records_per_step": exch_calls,
+                    "note": "time of the exchange launches (P2P: flag + reduce/LN + flag kernels, which also do the "
+                            "bias + residual + LN2 work; NCCL: reduce-scatter + all-gather); nvlink peak 900 GB/s"}
     phases = {
         "gemm": {"ms_per_step": prof["gemm_ms"] / args.steps, "launches": prof["gemm_launches"] // args.steps,
                  "tflops": achieved},
@@ -462,36 +537,40 @@ def energon_arm(args, world, rank, local):
                          "gbs": prof["mem_bytes"] / (prof["mem_ms"] * 1e-3) / 1e9 if prof["mem_ms"] else None,
                          "frac_of_hbm": (prof["mem_bytes"] / (prof["mem_ms"] * 1e-3) / 1e9 / pk["hbm_gbs"])
                          if prof["mem_ms"] else None},
-        "allreduce": {"ms_per_step": prof["comm_ms"] / args.steps, "calls": prof["comm_calls"] // args.steps,
-                      "bus_gbs": (prof["comm_bytes"] * 2 * (world - 1) / world / (prof["comm_ms"] * 1e-3) / 1e9)
-                      if prof["comm_ms"] else None},
+        "exchange": {"ms_per_step": prof["comm_ms"] / args.steps, "calls": prof["comm_calls"] // args.steps},
         "note": "per-launch CUDA events (instrumented pass) add a few us to every launch and break the "
                 "programmatic-launch overlap, which inflates the short memory-bound kernels most: the ncu "
                 "launch list (profiles/) times residual+LN at ~42.5 us = ~5.9 TB/s of algorithmic traffic",
     }
+    gpus_active = world if not share else 1
+    config = workload_config(args, shape, bcfg, lens0, k_tp)
+    config["seeds"] = seeds
+    config["valid_tokens_per_step"] = tokens_timed / args.steps
     result = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-              "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+              "warmup": args.warmup, "warmup_steps_run": warm, "ms_per_step": total_ms / args.steps,
               "latency_ms_p50": statistics.median(step_ms), "latency_ms_p95": sorted(step_ms)[
                   min(len(step_ms) - 1, int(round(0.95 * (len(step_ms) - 1))))],
+              "per_seed": {"ms_median": {str(k): v for k, v in seed_ms.items()},
+                           "tok_s": {str(k): v for k, v in seed_tok_s.items()},
+                           "median_tok_s": statistics.median(seed_tok_s.values())},
               "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
-              "data": "synthetic (seeded counter-based generator; random-init weights of the GPT-3-13B shape)",
-              "config": workload_config(args, shape, bcfg, lens, world if args.local_tp <= 1 else args.local_tp),
-              "clocks": clk, "e2e": e2e,
-              "gpu_launches": int(launches), "roofline": roofline, "phases": phases, "drce_ab": drce_ab}
+              "data": "synthetic (seeded counter-based generator; random-init weights of the GPT-3-13B shape; "
+                      f"batches of seeds {seeds[0]}..{seeds[-1]} rotated step by step)",
+              "config": config, "clocks": clk, "e2e": e2e, "gpus_active": gpus_active,
+              "gpu_launches": int(launches), "roofline": roofline, "phases": phases, "exchange": exchange,
+              "drce_ab": drce_ab}
 
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and args.local_tp <= 1 and not args.no_cpu_baseline:
         import oracle
-        run, n, L = oracle_sample(args, shape, lens, tok_np, args.cpu_sample_tokens)
-        t0 = time.perf_counter()
-        run()
-        dt = time.perf_counter() - t0
-        result["cpu_baseline"] = {"value": n / (dt * L), "unit": UNIT, "cores": oracle.num_threads(),
-                                  "kind": "oracle",
-                                  "sample": f"fp64 oracle, layer 0 of {L} over the first {n} tokens of the longest "
-                                            f"sequence ({dt:.1f} s), tokens/s extrapolated by the layer count"}
+        run, describe = oracle_sample(args, shape, batches[0]["lens"], batches[0]["tok"])
+        v, note = describe(run())
+        result["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+                                  "sample": note, "cpu_model": cpu_model()}
     if args.local_tp > 1:
         result["local_tp_emulation"] = (f"TP={args.local_tp} ranks run serially on ONE GPU (in-device reductions): "
                                         "per-rank kernel shapes of TP=k, not a TP=k latency")
+    if share:
+        result["shared_gpu"] = "ENERGON_BENCH_SHARE_GPU=1: all ranks time-slice cuda:0 -- the timings mean nothing"
     if rank == 0:
         print(json.dumps(result), flush=True)
     eng.destroy()
@@ -607,14 +686,44 @@ def pipeline_arm(args, world, rank, local):
     dist.destroy_process_group()
 
 
+def self_launch(args) -> int:
+    """`bench.py --gpus N` (N > 1) outside torchrun: relaunch this script under torch.distributed.run, one
+    rank per GPU on this node (rendezvous on 127.0.0.1), with the same arguments; rank 0 prints the line."""
+    import socket
+    if os.environ.get("ENERGON_BENCH_SHARE_GPU") != "1" and args.impl != "reference":
+        try:
+            import torch
+            n = torch.cuda.device_count()
+        except Exception:
+            n = 0
+        if n < args.gpus:
+            print(json.dumps({"metric": METRIC, "error": f"--gpus {args.gpus} needs {args.gpus} visible GPUs, found {n} "
+                                                         "(ENERGON_BENCH_SHARE_GPU=1 runs every rank on cuda:0)"}),
+                  flush=True)
+            return 2
+    so = socket.socket()
+    so.bind(("127.0.0.1", 0))
+    port = so.getsockname()[1]
+    so.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ, ENERGON_BENCH_SELF_LAUNCHED="1")
+    return subprocess.run(cmd, env=env).returncode
+
+
 def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world == 1 and args.gpus > 1:
-        print(json.dumps({"error": "--gpus > 1 must be launched under torchrun"}))
+    if world == 1 and args.gpus > 1 and "RANK" not in os.environ:
+        sys.exit(self_launch(args))
+    if args.gpus > 1 and world != args.gpus:
+        print(json.dumps({"metric": METRIC, "error": f"--gpus {args.gpus} but WORLD_SIZE={world}"}), flush=True)
         sys.exit(2)
+    if world > 1:
+        # the driver reads NCCL's own log (comm_nranks) to confirm the group spans every GPU
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
     if args.impl == "reference":
         reference_arm(args, world, rank)
     elif args.pp > 1:

@@ -48,7 +48,7 @@ typedef enum {
   ENERGON_ERR_CONFIG = -2,     /* H != h*d, h % k, F % k, tp_rank out of range  */
   ENERGON_ERR_SHAPE = -3,      /* unsupported shape (e.g. hidden not a multiple of 64 in bf16 mode)    */
   ENERGON_ERR_LENGTH = -4,     /* seq_lens[b] not in [1, max_len], or max_len > max_seq */
-  ENERGON_ERR_TOKEN = -5,      /* a token id outside [0, vocab) was seen on the device   */
+  ENERGON_ERR_TOKEN = -5,      /* a token id outside [0, vocab) was seen on the device; energon_sync */
   ENERGON_ERR_CAPACITY = -6,   /* batch * max_len > max_tokens, or batch > ENERGON_MAX_BATCH          */
   ENERGON_ERR_NOT_LOADED = -7, /* forward before every weight was loaded                               */
   ENERGON_ERR_CUDA = -8,       /* a CUDA runtime error (sticky errors surface on energon_sync)         */
@@ -206,7 +206,11 @@ ENERGON_API energon_status energon_load_layer_weights(energon_ctx* ctx, int32_t 
  * group: every rank calls it with identical arguments in the same order
  * (PAPER.md:251, 300).  seq_lens is the engine command's length list
  * (PAPER.md:368-370), host memory, copied during the call.
- *   tokens_d  device int32 [batch, max_len]; ids in [0, vocab); pad positions ignored
+ *   tokens_d  device int32 [batch, max_len]; ids of valid positions in [0, vocab); pad positions are
+ *             ignored (read as id 0).  A valid position holding an id outside [0, vocab) does not stop
+ *             the forward (the row gathers embedding row 0); it sets a device flag that the next
+ *             energon_sync returns as ENERGON_ERR_TOKEN -- on EVERY rank of a TP group, since every rank
+ *             checks the whole batch (the flag never gates an enqueue, so ranks cannot diverge)
  *   seq_lens  host int32 [batch], each in [1, max_len]
  *   out_d     device [batch, max_len, hidden], dtype = cfg->dtype; rows s >= seq_lens[b] are 0
  *   stream    cudaStream_t (NULL = legacy default stream); the call returns after enqueue
@@ -272,13 +276,18 @@ ENERGON_API energon_status energon_get_stats(const energon_ctx* ctx, energon_sta
  *   ENERGON_OPT_DRCE   1 = packed linears (the method), 0 = padded A/B ("pure EnergonAI",
  *                      PAPER.md:567-571); the workspace is sized for max_tokens padded rows either way.
  *   ENERGON_OPT_GRAPH  1 = capture each distinct forward (shapes, lengths, buffers) into a CUDA graph
- *                      on a private stream and replay it on the caller's stream (LRU cache of 8);
+ *                      on a private stream and replay it on the caller's stream (LRU cache of 32);
  *                      ignored while profiling or with off-device (PMEP) layers.  Default 0.
  *   ENERGON_OPT_TP_SP  k > 1 only: 1 (default) = sequence-parallel schedule (reduce-scatter, bias +
  *                      residual + LN on this rank's 1/k of the rows, all-gather), 0 = allreduce and
  *                      the row-wise kernels replicated on every rank.
+ *   ENERGON_OPT_RING_NUMERICS  local group only (energon_init_local_group; set it on every context): 1 = the
+ *                      in-device reductions reproduce the numerics of NCCL's ring algorithm on a bf16
+ *                      payload -- each chunk's running sum travels rank s+1 -> ... -> s and is rounded to
+ *                      the activation type after every hop -- instead of the fp32 rank-order sum (0,
+ *                      default).  Lets one GPU check the parity of the NCCL exchange.
  */
-enum { ENERGON_OPT_DRCE = 1, ENERGON_OPT_TP_SP = 2, ENERGON_OPT_GRAPH = 3 };
+enum { ENERGON_OPT_DRCE = 1, ENERGON_OPT_TP_SP = 2, ENERGON_OPT_GRAPH = 3, ENERGON_OPT_RING_NUMERICS = 4 };
 ENERGON_API energon_status energon_set_option(energon_ctx* ctx, int32_t option, int32_t value);
 
 /* Enable (1) / disable (0) per-launch CUDA-event timing; enabling resets the accumulators. */
@@ -300,11 +309,36 @@ ENERGON_API void energon_destroy(energon_ctx* ctx);
 ENERGON_API energon_status energon_index_maps(const int32_t* lens, int32_t batch, int32_t max_len, int32_t* offsets_d,
                                   int32_t* pack_idx_d, int32_t* pos_d, int32_t* unpack_idx_d, void* stream);
 /*   energon_attention: a6 on the padded per-head layout Q, K, V, O [batch, heads, max_len, head_dim]
- *     (dtype F32: SIMT fp32; BF16: mma.sync tensor-core kernel for head_dim 64 / 128); rows
- *     s >= lens[b] of O are not written. */
+ *     (dtype F32: SIMT fp32; BF16: the tcgen05 / TMEM kernel for head_dim 64 / 128, SIMT otherwise);
+ *     rows s >= lens[b] of O are not written. */
 ENERGON_API energon_status energon_attention(int32_t dtype, const void* Q_d, const void* K_d, const void* V_d, void* O_d,
                                              const int32_t* lens, int32_t batch, int32_t heads, int32_t max_len,
                                              int32_t head_dim, int32_t causal, void* stream);
+/*
+ * Standalone layout kernels of the paper's two fused transpose + pad kernels (sec 4.3)
+ * and of the final rebuild of padding.  Pure index + copy work: results are bit-exact
+ * (a byte permutation; fp32 -> bf16 output rounds to nearest even).  Device pointers; dtype F32 or
+ * BF16 is the element type of every activation argument; index maps as energon_index_maps writes them.
+ *   energon_unpack_qkv (a5, "rebuild padding"): QKV [T, 3*hk*d] packed rows, columns q | k | v, each
+ *     head-major then d -> Q, K, V [B, hk, S, d] at cell pack_idx[t] = b*S + s
+ *     (pack_idx NULL: identity, row t is cell t).  Pad rows of Q / K / V are not written.
+ *   energon_repack (a7, "remove padding"): O [B, hk, S, d] -> C [T, hk*d], row t from cell pack_idx[t];
+ *     with pack_idx NULL (padded A/B mode, T = B*S) row t is cell t and cells with unpack_idx[t] < 0
+ *     are written as 0.
+ *   energon_final_unpack (a13): out [cells, H] (cells = B*S, out_dtype) = LN(X[unpack_idx[cell]]) with
+ *     gamma / beta and eps when apply_ln, else the fp32 row itself; cells with unpack_idx < 0 are
+ *     exactly 0.  X is fp32 [T, H], H a multiple of 4 and <= 12288.
+ * Errors: ENERGON_ERR_ARG for NULL pointers / bad sizes / dtype, ENERGON_ERR_CUDA on a launch error.
+ */
+ENERGON_API energon_status energon_unpack_qkv(int32_t dtype, const void* QKV_d, const int32_t* pack_idx_d, int32_t T,
+                                              int32_t max_len, int32_t heads, int32_t head_dim, void* Q_d, void* K_d,
+                                              void* V_d, void* stream);
+ENERGON_API energon_status energon_repack(int32_t dtype, const void* O_d, const int32_t* pack_idx_d,
+                                          const int32_t* unpack_idx_d, int32_t T, int32_t max_len, int32_t heads,
+                                          int32_t head_dim, void* C_d, void* stream);
+ENERGON_API energon_status energon_final_unpack(int32_t out_dtype, const float* X_d, const int32_t* unpack_idx_d,
+                                                int32_t cells, int32_t hidden, const float* ln_g_d, const float* ln_b_d,
+                                                float ln_eps, int32_t apply_ln, void* out_d, void* stream);
 ENERGON_API energon_status energon_gemm(int32_t dtype, const void* A_d, const void* W_d, const float* bias_d, void* D_d,
                             int32_t M, int32_t N, int32_t K, int32_t epilogue, void* stream);
 

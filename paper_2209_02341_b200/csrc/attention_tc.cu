@@ -731,12 +731,9 @@ static bool launch_tc(const bf16* Q, const bf16* K, const bf16* V, bf16* Cp, con
   if (!make_tmap_kmajor(&mq, Q, rows, D, C::BM) || !make_tmap_kmajor(&mk, K, rows, D, C::BN) ||
       !make_tmap_kmajor(&mv, V, rows, D, C::BN))
     return false;
-  static bool attr = false;
-  if (!attr) {
-    if (V2) cudaFuncSetAttribute(attention_tc2_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-    else cudaFuncSetAttribute(attention_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr{0};
+  if (V2) smem_attr_once(attention_tc2_kernel<D>, SMEM, attr);
+  else smem_attr_once(attention_tc_kernel<D>, SMEM, attr);
   const int items = n * hk;
   const int slots = 2 * num_sms();  // 2 CTAs per SM (shared memory and 256 TMEM columns each)
   const int grid = items < slots ? items : slots;

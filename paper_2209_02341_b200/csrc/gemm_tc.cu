@@ -802,12 +802,14 @@ bool make_tmap_store(CUtensorMap* map, const void* ptr, int rows, int N) {
 }
 
 int num_sms() {
-  static int n = 0;
+  static std::atomic<int> per_dev[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int n = per_dev[dev & 63].load(std::memory_order_relaxed);
   if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
     if (n <= 0) n = 148;
+    per_dev[dev & 63].store(n, std::memory_order_relaxed);
   }
   return n;
 }
@@ -861,15 +863,12 @@ static const TailWs* default_tail_ws() {
 int tc_w_box(int code) { return code > 1000 ? (code - 1000) / 2 : code; }
 
 template <int BN, int EPI>
-static void launch_pair_epi(const CUtensorMap& tmA, const CUtensorMap& tmB, const float* bias, bf16* D, int M, int N,
+static bool launch_pair_epi(const CUtensorMap& tmA, const CUtensorMap& tmB, const float* bias, bf16* D, int M, int N,
                             int K, cudaStream_t st, const QkvScatter& qs, const CUtensorMap* tmD, const TailWs* tw,
                             const ShardStore* shard) {
   using C = Tc2Cfg<BN>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(gemm_tc2_kernel<BN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr{0};
+  smem_attr_once(gemm_tc2_kernel<BN, EPI>, C::SMEM, attr);
   const int num_m = (M + 255) / 256, num_n = (N + BN - 1) / BN;
   const int tiles = num_m * num_n;
   const int pairs = num_sms() / 2;
@@ -916,7 +915,7 @@ static void launch_pair_epi(const CUtensorMap& tmA, const CUtensorMap& tmB, cons
     md = *tmD;
   } else {
     memset(&md, 0, sizeof(md));
-    if (EPI != EPI_BIAS_QKV && !make_tmap_store(&md, D, M, N)) return;  // caller checks cudaGetLastError
+    if (EPI != EPI_BIAS_QKV && !make_tmap_store(&md, D, M, N)) return false;
   }
   static int hints = -1;
   if (hints < 0) {
@@ -964,38 +963,37 @@ static void launch_pair_epi(const CUtensorMap& tmA, const CUtensorMap& tmB, cons
       fclose(f);
     }
   }
+  return true;
 }
 
 template <int BN, int EPI>
-static void launch_bn_epi(const CUtensorMap& tmA, const CUtensorMap& tmB, const float* bias, bf16* D, int M, int N,
+static bool launch_bn_epi(const CUtensorMap& tmA, const CUtensorMap& tmB, const float* bias, bf16* D, int M, int N,
                           int K, cudaStream_t st, const QkvScatter& qs, const CUtensorMap* /*tmD*/,
                           const TailWs* /*tw*/, const ShardStore* /*shard*/) {
   using C = TcCfg<BN>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(gemm_tc_kernel<BN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr{0};
+  smem_attr_once(gemm_tc_kernel<BN, EPI>, C::SMEM, attr);
   const int tiles = ((M + TC_BM - 1) / TC_BM) * ((N + BN - 1) / BN);
   const int grid = tiles < num_sms() ? tiles : num_sms();
   launch_k(gemm_tc_kernel<BN, EPI>, dim3(grid), dim3(256), C::SMEM, st, tmA, tmB, D, bias, M, N, K, qs);
+  return true;
 }
 
 #define DISPATCH_EPI(F, BNARGS)                                                  \
   switch (epi) {                                                                 \
-    case EPI_NONE: F<BNARGS EPI_NONE>(tmA, tmB, bias, D, M, N, K, st, qs, tmD, tw, shard); break; \
-    case EPI_BIAS: F<BNARGS EPI_BIAS>(tmA, tmB, bias, D, M, N, K, st, qs, tmD, tw, shard); break; \
-    case EPI_BIAS_GELU: F<BNARGS EPI_BIAS_GELU>(tmA, tmB, bias, D, M, N, K, st, qs, tmD, tw, shard); break; \
-    default: F<BNARGS EPI_BIAS_QKV>(tmA, tmB, bias, D, M, N, K, st, qs, tmD, tw, shard); break;   \
+    case EPI_NONE: return F<BNARGS EPI_NONE>(tmA, tmB, bias, D, M, N, K, st, qs, tmD, tw, shard); \
+    case EPI_BIAS: return F<BNARGS EPI_BIAS>(tmA, tmB, bias, D, M, N, K, st, qs, tmD, tw, shard); \
+    case EPI_BIAS_GELU: return F<BNARGS EPI_BIAS_GELU>(tmA, tmB, bias, D, M, N, K, st, qs, tmD, tw, shard); \
+    default: return F<BNARGS EPI_BIAS_QKV>(tmA, tmB, bias, D, M, N, K, st, qs, tmD, tw, shard);   \
   }
 #define BN256 256,
 #define BN192 192,
 #define BN128 128,
 
-void launch_gemm_tc(const CUtensorMap& tmA, const CUtensorMap& tmB, int bn, const float* bias, bf16* D, int M, int N,
+bool launch_gemm_tc(const CUtensorMap& tmA, const CUtensorMap& tmB, int bn, const float* bias, bf16* D, int M, int N,
                     int K, int epi, cudaStream_t st, const QkvScatter* qkv, const CUtensorMap* tmD, const TailWs* tw,
                     const ShardStore* shard) {
-  if (M <= 0 || N <= 0) return;
+  if (M <= 0 || N <= 0) return true;
   QkvScatter qs{};
   if (qkv) qs = *qkv;
   if (bn == 1256) {

@@ -7,6 +7,7 @@
 
 #define ENERGON_MAX_B 1024
 
+#include <atomic>
 #include <utility>
 
 namespace energon {
@@ -33,6 +34,18 @@ inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, siz
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) applies to the CURRENT device only: raise the limit
+// once per (kernel, device) -- `done` is the kernel's own bit set of devices already configured.
+template <typename... KArgs>
+inline void smem_attr_once(void (*kernel)(KArgs...), int smem, std::atomic<uint64_t>& done) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return;
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  done.fetch_or(bit, std::memory_order_acq_rel);
+}
+
 // seq_lens passed by value as a kernel parameter (4 KB): no host->device copy, no sync.
 struct LensParam {
   int lens[ENERGON_MAX_B];
@@ -57,13 +70,14 @@ void launch_p2p_push_rows(const PeerSet& ps, int k, int me, int64_t off, int row
                           uint64_t epoch, cudaStream_t st);
 
 // a1
+// tok != nullptr: range-check the ids of the valid cells, raise *err on a bad one
 void launch_index_maps(const LensParam& lp, int B, int S, int* offsets, int* pack_idx, int* pos, int* unpack_idx,
-                       cudaStream_t st);
+                       const int* tok, int V, int* err, cudaStream_t st);
 // a2 + a3
 // rows [row0, row0 + rows) of the packed layout
 template <typename Act>
-void launch_embed_ln(const int* tok, const int* pack_idx, int row0, int rows, int S, int V, int H, const Act* tok_emb,
-                     const Act* pos_emb, const float* g, const float* b, float eps, float* X, Act* A, int* err,
+void launch_embed_ln(const int* tok, const int* pack_idx, const int* unpack_idx, int row0, int rows, int S, int V, int H,
+                     const Act* tok_emb, const Act* pos_emb, const float* g, const float* b, float eps, float* X, Act* A,
                      cudaStream_t st);
 template <typename Act>
 void launch_gather_ln(const float* x, const int* pack_idx, int row0, int rows, int H, const float* g, const float* b,
@@ -83,10 +97,11 @@ void launch_unpack_qkv(const Act* QKV, const int* pack_idx, int T, int S, int hk
 template <typename Act>
 void launch_repack(const Act* O, const int* pack_idx, const int* unpack_idx, int T, int S, int hk, int d, Act* C,
                    cudaStream_t st);
+// ring != 0: NCCL ring numerics (one rounding to Act per hop) instead of the fp32 rank-order sum
 template <typename Act>
-void launch_local_allreduce(const PtrList& parts, int k, int64_t n, cudaStream_t st);
+void launch_local_allreduce(const PtrList& parts, int k, int64_t n, int ring, cudaStream_t st);
 template <typename Act>
-void launch_local_reduce_scatter(const PtrList& parts, int k, int64_t shard, cudaStream_t st);
+void launch_local_reduce_scatter(const PtrList& parts, int k, int64_t shard, int ring, cudaStream_t st);
 void launch_local_all_gather(const PtrList& parts, int k, int64_t shard_bytes, cudaStream_t st);
 // load-time relayout
 template <typename Src, typename Dst>
@@ -147,9 +162,10 @@ struct ShardStore {
   int k;
 };
 // tmD: the output map (make_tmap_store) or nullptr to build it per call.
-void launch_gemm_tc(const CUtensorMap& tmA, const CUtensorMap& tmB, int bn, const float* bias, bf16* D, int M, int N,
+// returns false (nothing launched) if the output tensor map cannot be built (D not 16-byte aligned)
+bool launch_gemm_tc(const CUtensorMap& tmA, const CUtensorMap& tmB, int bn, const float* bias, bf16* D, int M, int N,
                     int K, int epi, cudaStream_t st, const QkvScatter* qkv = nullptr, const CUtensorMap* tmD = nullptr,
                     const TailWs* tw = nullptr, const ShardStore* shard = nullptr);
-int num_sms();
+int num_sms();  // SM count of the current device
 
 }  // namespace energon

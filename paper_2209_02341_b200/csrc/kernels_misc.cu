@@ -24,9 +24,14 @@ static inline int grid_for(int64_t work, int threads, int max_blocks) {
 //   s < lens[b] : t = offsets[b] + s, unpack_idx[cell] = t, pack_idx[t] = cell, pos[t] = s
 //   otherwise   : unpack_idx[cell] = -1
 // Every CTA recomputes the (tiny, B <= 1024) scan in shared memory, so the whole step is one launch.
+// tok != nullptr: the token id of every VALID cell is range-checked here (pad cells are ignored,
+// energon.h); an id outside [0, V) raises the device error flag.  Every rank of a TP group runs this
+// kernel over the whole batch, so every rank raises the same flag (the embedding gathers only its own
+// rows and never checks).
 __global__ void __launch_bounds__(256) index_maps_kernel(LensParam lp, int B, int S, int* __restrict__ offsets,
                                                          int* __restrict__ pack_idx, int* __restrict__ pos,
-                                                         int* __restrict__ unpack_idx) {
+                                                         int* __restrict__ unpack_idx, const int* __restrict__ tok,
+                                                         int V, int* err_flag) {
   pdl_trigger();
   pdl_wait();
   __shared__ int s_off[ENERGON_MAX_B + 1];
@@ -64,6 +69,10 @@ __global__ void __launch_bounds__(256) index_maps_kernel(LensParam lp, int B, in
       unpack_idx[c] = t;
       pack_idx[t] = c;
       pos[t] = s;
+      if (tok) {
+        const int id = tok[c];
+        if (id < 0 || id >= V) *err_flag = 1;
+      }
     } else {
       unpack_idx[c] = -1;
     }
@@ -126,25 +135,24 @@ __device__ __forceinline__ float4 ln_apply(float4 x, float mean, float rstd, con
 // ============================================================================ a2 + a3: embed, pack, LN1
 // PAPER.md:138 embedding layer; padding is removed at the entry: only the T valid
 // rows are gathered.  X[t] = E[tok[cell]] + P[pos] (fp32 residual stream), A[t] = LN1_0(X[t]).
-// pack_idx == nullptr means the padded A/B mode (row t is cell t).  An id outside [0, V) gathers
-// row 0 and raises the device error flag (checked by energon_sync), so the kernel never faults.
+// pack_idx == nullptr means the padded A/B mode (row t is cell t; unpack_idx[cell] < 0 marks a pad
+// cell, whose id is ignored and read as 0 -- energon.h "pad positions ignored").  An id outside
+// [0, V) gathers row 0 so the kernel never faults (index_maps_kernel raised the error flag).
 template <typename Act, int LN_MAXV>
 __global__ void __launch_bounds__(LN_THREADS) embed_ln_kernel(const int* __restrict__ tok, const int* __restrict__ pack_idx,
-                                                              int row0, int S, int V, int H, const Act* __restrict__ tok_emb,
+                                                              const int* __restrict__ unpack_idx, int row0, int S, int V,
+                                                              int H, const Act* __restrict__ tok_emb,
                                                               const Act* __restrict__ pos_emb, const float* __restrict__ g,
                                                               const float* __restrict__ b, float eps, float* __restrict__ X,
-                                                              Act* __restrict__ A, int* err_flag) {
+                                                              Act* __restrict__ A) {
   pdl_trigger();
   pdl_wait();
   __shared__ float red[32];
   const int t = row0 + blockIdx.x;
   const int cell = pack_idx ? pack_idx[t] : t;
   const int s = cell % S;
-  int id = tok[cell];
-  if (id < 0 || id >= V) {
-    if (threadIdx.x == 0) *err_flag = 1;
-    id = 0;
-  }
+  int id = (pack_idx || unpack_idx[cell] >= 0) ? tok[cell] : 0;
+  if (id < 0 || id >= V) id = 0;
   const Act* e = tok_emb + (int64_t)id * H;
   const Act* p = pos_emb + (int64_t)s * H;
   float4 v[LN_MAXV];
@@ -346,22 +354,38 @@ __global__ void repack_kernel(const Act* __restrict__ O, const int* __restrict__
 // ============================================================================ local TP reduction
 // In-device allreduce for a local group (energon_init_local_group): sum the k partials in rank
 // order 0..k-1 in fp32 (every rank gets bit-identical data), write back to all k.
+// ring != 0 (ENERGON_OPT_RING_NUMERICS, tests): reproduce the numerics of NCCL's ring algorithm on a
+// bf16 payload instead -- the element of chunk s starts at rank s+1 and travels s+1 -> s+2 -> ... -> s,
+// every hop adding its own partial in fp32 and storing the running sum in the payload type (one
+// rounding per hop, SURVEY.md 8(c) "bf16 per hop").
 template <typename Act>
-__global__ void local_allreduce_kernel(PtrList parts, int k, int64_t n) {
+__device__ __forceinline__ void reduce_parts(const PtrList& parts, int k, int64_t off, int owner, int ring,
+                                             float (&acc)[16 / sizeof(Act)]) {
+  constexpr int E = 16 / sizeof(Act);
+#pragma unroll
+  for (int e = 0; e < E; ++e) acc[e] = 0.f;
+  for (int j = 0; j < k; ++j) {
+    const int r = ring ? (owner + 1 + j) % k : j;
+    Vec16<Act> v;
+    v.u = reinterpret_cast<const uint4*>(parts.p[r])[off];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      acc[e] += to_f32(v.e[e]);
+      if (ring) acc[e] = to_f32(from_f32<Act>(acc[e]));
+    }
+  }
+}
+
+template <typename Act>
+__global__ void local_allreduce_kernel(PtrList parts, int k, int64_t n, int ring) {
   pdl_trigger();
   pdl_wait();
   constexpr int E = 16 / sizeof(Act);
   const int64_t nv = n / E;
+  const int64_t chunk = (nv + k - 1) / k;  // ring chunks: chunk s is owned by rank s
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nv; i += (int64_t)gridDim.x * blockDim.x) {
     float acc[E];
-#pragma unroll
-    for (int e = 0; e < E; ++e) acc[e] = 0.f;
-    for (int r = 0; r < k; ++r) {
-      Vec16<Act> v;
-      v.u = reinterpret_cast<const uint4*>(parts.p[r])[i];
-#pragma unroll
-      for (int e = 0; e < E; ++e) acc[e] += to_f32(v.e[e]);
-    }
+    reduce_parts<Act>(parts, k, i, (int)(i / chunk), ring, acc);
     Vec16<Act> o;
 #pragma unroll
     for (int e = 0; e < E; ++e) o.e[e] = from_f32<Act>(acc[e]);
@@ -371,9 +395,9 @@ __global__ void local_allreduce_kernel(PtrList parts, int k, int64_t n) {
 
 // Local-group reduce-scatter (sequence-parallel schedule): shard s (= rank s) of every partial,
 // `shard` elements starting at s * shard, is summed over the k ranks in rank order (fp32) and
-// written to rank s's buffer only -- the semantics of ncclReduceScatter in place.
+// written to rank s's buffer only -- the semantics of ncclReduceScatter in place (ring: see above).
 template <typename Act>
-__global__ void local_reduce_scatter_kernel(PtrList parts, int k, int64_t shard) {
+__global__ void local_reduce_scatter_kernel(PtrList parts, int k, int64_t shard, int ring) {
   pdl_trigger();
   pdl_wait();
   constexpr int E = 16 / sizeof(Act);
@@ -382,14 +406,7 @@ __global__ void local_reduce_scatter_kernel(PtrList parts, int k, int64_t shard)
     const int s = (int)(i / nv);
     const int64_t off = (int64_t)s * nv + (i - (int64_t)s * nv);
     float acc[E];
-#pragma unroll
-    for (int e = 0; e < E; ++e) acc[e] = 0.f;
-    for (int r = 0; r < k; ++r) {
-      Vec16<Act> v;
-      v.u = reinterpret_cast<const uint4*>(parts.p[r])[off];
-#pragma unroll
-      for (int e = 0; e < E; ++e) acc[e] += to_f32(v.e[e]);
-    }
+    reduce_parts<Act>(parts, k, off, s, ring, acc);
     Vec16<Act> o;
 #pragma unroll
     for (int e = 0; e < E; ++e) o.e[e] = from_f32<Act>(acc[e]);
@@ -413,9 +430,10 @@ __global__ void local_all_gather_kernel(PtrList parts, int k, int64_t shard_byte
 }
 
 template <typename Act>
-void launch_local_reduce_scatter(const PtrList& parts, int k, int64_t shard, cudaStream_t st) {
+void launch_local_reduce_scatter(const PtrList& parts, int k, int64_t shard, int ring, cudaStream_t st) {
   const int64_t work = shard / (16 / sizeof(Act)) * k;
-  if (work > 0) launch_k(local_reduce_scatter_kernel<Act>, dim3(grid_for(work, 256, 148 * 8)), dim3(256), 0, st, parts, k, shard);
+  if (work > 0)
+    launch_k(local_reduce_scatter_kernel<Act>, dim3(grid_for(work, 256, 148 * 8)), dim3(256), 0, st, parts, k, shard, ring);
 }
 
 void launch_local_all_gather(const PtrList& parts, int k, int64_t shard_bytes, cudaStream_t st) {
@@ -463,9 +481,10 @@ __global__ void convert_vec_kernel(const Src* __restrict__ src, int64_t off, int
 // ============================================================================ host launchers
 
 void launch_index_maps(const LensParam& lp, int B, int S, int* offsets, int* pack_idx, int* pos, int* unpack_idx,
-                       cudaStream_t st) {
+                       const int* tok, int V, int* err, cudaStream_t st) {
   const int cells = B * S;
-  launch_k(index_maps_kernel, dim3(grid_for(cells, 256, 148 * 4)), dim3(256), 0, st, lp, B, S, offsets, pack_idx, pos, unpack_idx);
+  launch_k(index_maps_kernel, dim3(grid_for(cells, 256, 148 * 4)), dim3(256), 0, st, lp, B, S, offsets, pack_idx, pos,
+           unpack_idx, tok, V, err);
 }
 
 #define NV_DISPATCH(H, KERNEL_CALL)                                         \
@@ -485,12 +504,12 @@ void launch_index_maps(const LensParam& lp, int B, int S, int* offsets, int* pac
   }
 
 template <typename Act>
-void launch_embed_ln(const int* tok, const int* pack_idx, int row0, int rows, int S, int V, int H, const Act* tok_emb,
-                     const Act* pos_emb, const float* g, const float* b, float eps, float* X, Act* A, int* err,
+void launch_embed_ln(const int* tok, const int* pack_idx, const int* unpack_idx, int row0, int rows, int S, int V, int H,
+                     const Act* tok_emb, const Act* pos_emb, const float* g, const float* b, float eps, float* X, Act* A,
                      cudaStream_t st) {
   if (rows > 0)
-    NV_DISPATCH(H, (launch_k(embed_ln_kernel<Act, NVX>, dim3(rows), dim3(LN_THREADS), 0, st, tok, pack_idx, row0, S, V, H, tok_emb, pos_emb,
-                                                                           g, b, eps, X, A, err)))
+    NV_DISPATCH(H, (launch_k(embed_ln_kernel<Act, NVX>, dim3(rows), dim3(LN_THREADS), 0, st, tok, pack_idx, unpack_idx,
+                             row0, S, V, H, tok_emb, pos_emb, g, b, eps, X, A)))
 }
 
 template <typename Act>
@@ -569,9 +588,10 @@ void launch_repack(const Act* O, const int* pack_idx, const int* unpack_idx, int
 }
 
 template <typename Act>
-void launch_local_allreduce(const PtrList& parts, int k, int64_t n, cudaStream_t st) {
+void launch_local_allreduce(const PtrList& parts, int k, int64_t n, int ring, cudaStream_t st) {
   const int64_t work = n / (16 / sizeof(Act));
-  if (work > 0) launch_k(local_allreduce_kernel<Act>, dim3(grid_for(work, 256, 148 * 8)), dim3(256), 0, st, parts, k, n);
+  if (work > 0)
+    launch_k(local_allreduce_kernel<Act>, dim3(grid_for(work, 256, 148 * 8)), dim3(256), 0, st, parts, k, n, ring);
 }
 
 template <typename Src, typename Dst>
@@ -766,18 +786,18 @@ template void launch_p2p_reduce_ln<bf16>(const PeerSet&, int, int, int64_t, int6
                                          int);
 
 #define INST_ACT(Act)                                                                                                   \
-  template void launch_embed_ln<Act>(const int*, const int*, int, int, int, int, int, const Act*, const Act*,            \
-                                     const float*, const float*, float, float*, Act*, int*, cudaStream_t);              \
+  template void launch_embed_ln<Act>(const int*, const int*, const int*, int, int, int, int, int, const Act*,           \
+                                     const Act*, const float*, const float*, float, float*, Act*, cudaStream_t);        \
   template void launch_gather_ln<Act>(const float*, const int*, int, int, int, const float*, const float*, float,        \
                                       float*, Act*, cudaStream_t);                                                      \
-  template void launch_local_reduce_scatter<Act>(const PtrList&, int, int64_t, cudaStream_t);                          \
+  template void launch_local_reduce_scatter<Act>(const PtrList&, int, int64_t, int, cudaStream_t);                     \
   template void launch_residual_ln<Act>(float*, const Act*, const float*, int, int, const float*, const float*, float,   \
                                         Act*, cudaStream_t);                                                            \
   template void launch_final_ln_unpack<Act>(const float*, const int*, int, int, int, const float*, const float*, float,  \
                                             int, Act*, cudaStream_t);                                                   \
   template void launch_unpack_qkv<Act>(const Act*, const int*, int, int, int, int, Act*, Act*, Act*, cudaStream_t);    \
   template void launch_repack<Act>(const Act*, const int*, const int*, int, int, int, int, Act*, cudaStream_t);        \
-  template void launch_local_allreduce<Act>(const PtrList&, int, int64_t, cudaStream_t);
+  template void launch_local_allreduce<Act>(const PtrList&, int, int64_t, int, cudaStream_t);
 INST_ACT(float)
 INST_ACT(bf16)
 

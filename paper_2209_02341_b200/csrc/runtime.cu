@@ -91,6 +91,7 @@ struct energon_ctx {
   ShardStore shard_rpr{};  // `shard` with this forward's rows per rank
   bool fuse = true;  // fused a5 / a7 (ENERGON_NO_FUSE=1 disables, for A/B and tests)
   bool sp = true;    // k > 1: sequence-parallel schedule (reduce-scatter / LN on own rows / all-gather)
+  bool ring = false; // local group: NCCL ring numerics in the in-device reductions (ENERGON_OPT_RING_NUMERICS)
   // CUDA-graph cache (ENERGON_OPT_GRAPH): whole forwards captured on cap_stream, replayed on the caller's
   struct GraphEntry {
     std::vector<int64_t> key;
@@ -118,11 +119,12 @@ struct energon_ctx {
   int tm_rows = -1;
   Pmep pm;
   TailWs tail;              // stream-K scratch of this context's GEMMs (ordered on its forward stream)
-  int* err_host = nullptr;  // mapped pinned flag written by the embed kernel (bad token id)
+  int* err_host = nullptr;  // mapped pinned flag written by the index-maps kernel (bad token id)
   int* err_dev = nullptr;
   cudaStream_t load_stream = nullptr;
   std::vector<void*> allocs;
   std::string err;
+  std::string launch_err;  // a launcher refused (e.g. a tensor map could not be built): the forward fails
   energon_stats stats;
   // profiling (energon_set_profiling): CUDA events around every launch on the forward stream
   struct ProfRec {
@@ -435,7 +437,9 @@ energon_status check_ready(energon_ctx* c, const Call& a) {
   if (a.l0 < 0 || a.l1 > (int)c->layers.size() || a.l0 > a.l1) return fail(c, ENERGON_ERR_ARG, "bad layer range");
   for (int l = a.l0; l < a.l1; ++l)
     if (!c->layers[l].loaded) return fail(c, ENERGON_ERR_NOT_LOADED, "layer " + std::to_string(l) + " not loaded");
-  if (*c->err_host) return fail(c, ENERGON_ERR_TOKEN, "a token id outside [0, vocab) was seen by a previous forward");
+  // (a bad token id raised on the device is NOT checked here: the flag is written asynchronously, so
+  // gating the SPMD enqueue on it could let one rank skip a forward its peers run -- a distributed hang;
+  // it surfaces on energon_sync, where every rank of the group sees the same flag)
   if (c->p2p && !c->p2p_connected) return fail(c, ENERGON_ERR_NOT_LOADED, "P2P peers not connected (energon_p2p_connect)");
   return ENERGON_OK;
 }
@@ -477,8 +481,8 @@ energon_status tp_reduce(energon_ctx** cs, int n, int rows, int rpr, bool sp, cu
   if (c0->local_group) {
     PtrList pl;
     for (int i = 0; i < n; ++i) pl.p[i] = cs[i]->P;
-    if (sp) launch_local_reduce_scatter<Act>(pl, n, (int64_t)rpr * c0->H, st);
-    else launch_local_allreduce<Act>(pl, n, (int64_t)count, st);
+    if (sp) launch_local_reduce_scatter<Act>(pl, n, (int64_t)rpr * c0->H, c0->ring ? 1 : 0, st);
+    else launch_local_allreduce<Act>(pl, n, (int64_t)count, c0->ring ? 1 : 0, st);
     c0->stats.kernel_launches++;
   } else {
     ncclResult_t e;
@@ -562,8 +566,9 @@ void gemm(energon_ctx* c, const CUtensorMap& tmA, const CUtensorMap* tmB, const 
   Prof p(c, st, P_GEMM, 2.0 * M * N * K);
   if constexpr (sizeof(Act) == 2) {
     const int code = tc_pick_bn(M, N);
-    launch_gemm_tc(tmA, tmB[box_slot(tc_w_box(code))], code, bias, reinterpret_cast<bf16*>(D), M, N, K, epi, st, qs,
-                   tmD, &c->tail, shard);
+    if (!launch_gemm_tc(tmA, tmB[box_slot(tc_w_box(code))], code, bias, reinterpret_cast<bf16*>(D), M, N, K, epi, st,
+                        qs, tmD, &c->tail, shard))
+      c->launch_err = "GEMM launch refused: output tensor map could not be built";
   } else {
     launch_gemm_f32(reinterpret_cast<const float*>(A), reinterpret_cast<const float*>(W), bias,
                     reinterpret_cast<float*>(D), M, N, K, epi, st);
@@ -646,7 +651,7 @@ energon_status forward_t(energon_ctx** cs, int n, const Call& a, int64_t T) {
     c->stats.last_rows = rows;
     {
       Prof p(c, st, P_MEM, 4.0 * (a.B + 1) + 8.0 * T + 4.0 * a.B * a.S);
-      launch_index_maps(lp, a.B, a.S, c->offsets, c->pack_idx, c->pos, c->unpack_idx, st);
+      launch_index_maps(lp, a.B, a.S, c->offsets, c->pack_idx, c->pos, c->unpack_idx, a.tokens, c->V, c->err_dev, st);
     }
     c->stats.kernel_launches++;
     if (sizeof(Act) == 2 && c->tm_rows != rows) {
@@ -666,9 +671,9 @@ energon_status forward_t(energon_ctx** cs, int n, const Call& a, int64_t T) {
       const int r0 = shard0(c), sn = shardn(c);
       Prof p(c, st, P_MEM, a.tokens ? sn * (4.0 + H * (2 * act + 4 + act)) : sn * H * (4 + 4 + act));
       if (a.tokens)
-        launch_embed_ln<Act>(a.tokens, pidx, r0, sn, a.S, c->V, c->H, reinterpret_cast<const Act*>(c->tok_emb),
-                             reinterpret_cast<const Act*>(c->pos_emb), g1, b1, eps, c->X, reinterpret_cast<Act*>(c->A),
-                             c->err_dev, st);
+        launch_embed_ln<Act>(a.tokens, pidx, c->unpack_idx, r0, sn, a.S, c->V, c->H,
+                             reinterpret_cast<const Act*>(c->tok_emb), reinterpret_cast<const Act*>(c->pos_emb), g1, b1,
+                             eps, c->X, reinterpret_cast<Act*>(c->A), st);
       else
         launch_gather_ln<Act>(a.x_in, a.x_packed ? nullptr : pidx, r0, sn, c->H, g1, b1, eps, c->X,
                               reinterpret_cast<Act*>(c->A), st);
@@ -710,9 +715,10 @@ energon_status forward_t(energon_ctx** cs, int n, const Call& a, int64_t T) {
       if (fuse_a7) {
         // a6 + a7: attention writes its rows straight into the packed context [T, Hk]
         Prof p(c, st, P_ATTN, 4.0 * c->d * allowed * c->hk);
-        launch_attention_packed(reinterpret_cast<const bf16*>(c->Q), reinterpret_cast<const bf16*>(c->K),
-                                reinterpret_cast<const bf16*>(c->Vb), reinterpret_cast<bf16*>(c->Ctx), c->offsets, lp,
-                                a.B, c->hk, a.S, c->d, g.causal, st);
+        if (!launch_attention_packed(reinterpret_cast<const bf16*>(c->Q), reinterpret_cast<const bf16*>(c->K),
+                                     reinterpret_cast<const bf16*>(c->Vb), reinterpret_cast<bf16*>(c->Ctx), c->offsets,
+                                     lp, a.B, c->hk, a.S, c->d, g.causal, st))
+          c->launch_err = "attention launch refused: tensor maps could not be built";
         c->stats.kernel_launches++;
       } else {
         {
@@ -795,6 +801,12 @@ energon_status forward_t(energon_ctx** cs, int n, const Call& a, int64_t T) {
     if (s) return s;
   }
 
+  for (int i = 0; i < n; ++i)
+    if (!cs[i]->launch_err.empty()) {
+      const std::string m = cs[i]->launch_err;
+      cs[i]->launch_err.clear();
+      return fail(c0, ENERGON_ERR_CUDA, m);
+    }
   energon_ctx* c = cs[0];
   if (a.out_packed) {
     // pipeline stage output: the residual stream rows go to the next stage as they are
@@ -853,7 +865,7 @@ energon_status run(energon_ctx** cs, int n, const Call& a) {
 
   // ---- CUDA graph: key = everything the launch sequence depends on
   std::vector<int64_t> key = {n, (int64_t)(uintptr_t)a.tokens, (int64_t)(uintptr_t)a.x_in, (int64_t)(uintptr_t)a.out,
-                              a.B, a.S, a.l0, a.l1, a.final_ln, a.out_f32, c0->cfg.drce, c0->sp, c0->fuse,
+                              a.B, a.S, a.l0, a.l1, a.final_ln, a.out_f32, c0->cfg.drce, c0->sp, c0->fuse, c0->ring,
                               a.x_packed, a.out_packed};
   for (int i = 0; i < n; ++i) key.push_back((int64_t)(uintptr_t)cs[i]);
   for (int b = 0; b < a.B; ++b) key.push_back(a.lens[b]);
@@ -904,7 +916,7 @@ energon_status run(energon_ctx** cs, int n, const Call& a) {
     ent.delta.push_back(d);
   }
   ent.last_use = ++c0->gclock;
-  if (c0->gcache.size() >= 8) {  // evict the least recently used graph
+  if (c0->gcache.size() >= 32) {  // evict the least recently used graph
     size_t v = 0;
     for (size_t i = 1; i < c0->gcache.size(); ++i)
       if (c0->gcache[i].last_use < c0->gcache[v].last_use) v = i;
@@ -964,12 +976,9 @@ energon_status energon_offload_layers(energon_ctx* c, const int32_t* layers, int
   if (n == 0) return ENERGON_OK;
   CU(c, cudaSetDevice(c->cfg.device));
   CU(c, cudaDeviceSynchronize());
-  Pmep& pm = c->pm;
   const size_t a = c->act, H = c->H, Hk = c->Hk, Fk = c->Fk;
   const size_t sz[4] = {a * 3 * Hk * H, a * H * Hk, a * Fk * H, a * H * Fk};
-  pm.bytes = sz[0] + sz[1] + sz[2] + sz[3];
-  pm.pool_kind = pool;
-  pm.peer = peer;
+  const size_t bytes = sz[0] + sz[1] + sz[2] + sz[3];
   if (pool == 1 && peer != c->cfg.device) {  // (peer == device: a same-device pool, for single-GPU tests)
     int ok = 0;
     CU(c, cudaDeviceCanAccessPeer(&ok, c->cfg.device, peer));
@@ -978,45 +987,66 @@ energon_status energon_offload_layers(energon_ctx* c, const int32_t* layers, int
     if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) return cuda_fail(c, e, "cudaDeviceEnablePeerAccess");
     cudaGetLastError();
   }
-  pm.index.assign(Lc, -1);
-  for (int i = 0; i < n; ++i) {
-    LayerDev& L = c->layers[layers[i]];
-    void* buf = nullptr;
-    if (pool == 0) {
-      CU(c, cudaHostAlloc(&buf, pm.bytes, cudaHostAllocDefault));
-    } else {
-      CU(c, cudaSetDevice(peer));
-      cudaError_t e = cudaMalloc(&buf, pm.bytes);
-      cudaSetDevice(c->cfg.device);
-      if (e != cudaSuccess) return cuda_fail(c, e, "cudaMalloc on the peer device");
+  // Two phases so that a failure leaves the context exactly as it was (every layer resident): first
+  // allocate the whole pool, the staging slots, their events and tensor maps and copy the weights into
+  // the pool; only then free the device copies and switch the layers to the pool.
+  const int ns = std::min<int>(slots, n);
+  Pmep np;
+  np.bytes = bytes;
+  np.pool_kind = pool;
+  np.peer = peer;
+  auto rollback = [&](energon_status st, const std::string& msg) {
+    cudaSetDevice(peer >= 0 && pool == 1 ? peer : c->cfg.device);
+    for (void* p : np.pool) {
+      if (pool == 0) cudaFreeHost(p);
+      else cudaFree(p);
     }
-    pm.pool.push_back(buf);
-    void* src[4] = {L.wqkv, L.wo, L.w1, L.w2};
+    cudaSetDevice(c->cfg.device);
+    for (void* p : np.slot_buf) cudaFree(p);
+    for (cudaEvent_t e : np.fetched) cudaEventDestroy(e);
+    for (cudaEvent_t e : np.freed) cudaEventDestroy(e);
+    if (np.copy) cudaStreamDestroy(np.copy);
+    cudaGetLastError();
+    return fail(c, st, msg);
+  };
+  auto cu_ok = [&](cudaError_t e, const char* what, energon_status* st, std::string* msg) {
+    if (e == cudaSuccess) return true;
+    *st = e == cudaErrorMemoryAllocation ? ENERGON_ERR_OOM : ENERGON_ERR_CUDA;
+    *msg = std::string(what) + ": " + cudaGetErrorString(e);
+    return false;
+  };
+  energon_status est = ENERGON_OK;
+  std::string emsg;
+  for (int i = 0; i < n; ++i) {
+    const LayerDev& L = c->layers[layers[i]];
+    void* buf = nullptr;
+    cudaError_t e;
+    if (pool == 0) {
+      e = cudaHostAlloc(&buf, bytes, cudaHostAllocDefault);
+    } else {
+      cudaSetDevice(peer);
+      e = cudaMalloc(&buf, bytes);
+      cudaSetDevice(c->cfg.device);
+    }
+    if (!cu_ok(e, "pool allocation", &est, &emsg)) return rollback(est, emsg);
+    np.pool.push_back(buf);
+    const void* src[4] = {L.wqkv, L.wo, L.w1, L.w2};
     size_t off = 0;
     for (int k = 0; k < 4; ++k) {
-      if (pool == 0) CU(c, cudaMemcpy((char*)buf + off, src[k], sz[k], cudaMemcpyDeviceToHost));
-      else CU(c, cudaMemcpyPeer((char*)buf + off, peer, src[k], c->cfg.device, sz[k]));
+      e = pool == 0 ? cudaMemcpy((char*)buf + off, src[k], sz[k], cudaMemcpyDeviceToHost)
+                    : cudaMemcpyPeer((char*)buf + off, peer, src[k], c->cfg.device, sz[k]);
+      if (!cu_ok(e, "copy into the pool", &est, &emsg)) return rollback(est, emsg);
       off += sz[k];
-      for (size_t q = 0; q < c->allocs.size(); ++q)
-        if (c->allocs[q] == src[k]) {
-          c->allocs.erase(c->allocs.begin() + q);
-          break;
-        }
-      CU(c, cudaFree(src[k]));
-      c->stats.weight_bytes -= (int64_t)sz[k];
     }
-    L.wqkv = L.wo = L.w1 = L.w2 = nullptr;
-    pm.layers.push_back(layers[i]);
-    pm.index[layers[i]] = i;
   }
-  const int ns = std::min<int>(slots, n);
-  pm.slots.resize(ns);
-  CU(c, cudaStreamCreateWithFlags(&pm.copy, cudaStreamNonBlocking));
-  for (int s = 0; s < ns; ++s) {
+  if (!cu_ok(cudaStreamCreateWithFlags(&np.copy, cudaStreamNonBlocking), "copy stream", &est, &emsg))
+    return rollback(est, emsg);
+  np.slots.resize(ns);
+  for (int q = 0; q < ns; ++q) {
     void* buf = nullptr;
-    CU(c, cudaMalloc(&buf, pm.bytes));
-    pm.slot_buf.push_back(buf);
-    LayerDev& S = pm.slots[s];
+    if (!cu_ok(cudaMalloc(&buf, bytes), "staging slot", &est, &emsg)) return rollback(est, emsg);
+    np.slot_buf.push_back(buf);
+    LayerDev& S = np.slots[q];
     S.wqkv = buf;
     S.wo = (char*)buf + sz[0];
     S.w1 = (char*)buf + sz[0] + sz[1];
@@ -1027,15 +1057,34 @@ energon_status energon_offload_layers(energon_ctx* c, const int32_t* layers, int
             !make_tmap_kmajor(&S.tm_o[i], S.wo, c->H, c->Hk, kBoxes[i]) ||
             !make_tmap_kmajor(&S.tm_1[i], S.w1, c->Fk, c->H, kBoxes[i]) ||
             !make_tmap_kmajor(&S.tm_2[i], S.w2, c->H, c->Fk, kBoxes[i]))
-          return fail(c, ENERGON_ERR_CUDA, "cuTensorMapEncodeTiled failed for a staging slot");
-    cudaEvent_t ef, er;
-    CU(c, cudaEventCreateWithFlags(&ef, cudaEventDisableTiming));
-    CU(c, cudaEventCreateWithFlags(&er, cudaEventDisableTiming));
-    pm.fetched.push_back(ef);
-    pm.freed.push_back(er);
-    CU(c, cudaEventRecord(er, pm.copy));  // slots start free
+          return rollback(ENERGON_ERR_CUDA, "cuTensorMapEncodeTiled failed for a staging slot");
+    cudaEvent_t ef = nullptr, er = nullptr;
+    if (!cu_ok(cudaEventCreateWithFlags(&ef, cudaEventDisableTiming), "event", &est, &emsg)) return rollback(est, emsg);
+    np.fetched.push_back(ef);
+    if (!cu_ok(cudaEventCreateWithFlags(&er, cudaEventDisableTiming), "event", &est, &emsg)) return rollback(est, emsg);
+    np.freed.push_back(er);
+    if (!cu_ok(cudaEventRecord(er, np.copy), "event record", &est, &emsg)) return rollback(est, emsg);  // slots start free
   }
-  CU(c, cudaDeviceSynchronize());
+  if (!cu_ok(cudaDeviceSynchronize(), "cudaDeviceSynchronize", &est, &emsg)) return rollback(est, emsg);
+  // ---- commit: nothing below can fail
+  np.index.assign(Lc, -1);
+  for (int i = 0; i < n; ++i) {
+    LayerDev& L = c->layers[layers[i]];
+    void* src[4] = {L.wqkv, L.wo, L.w1, L.w2};
+    for (int k = 0; k < 4; ++k) {
+      for (size_t q = 0; q < c->allocs.size(); ++q)
+        if (c->allocs[q] == src[k]) {
+          c->allocs.erase(c->allocs.begin() + q);
+          break;
+        }
+      cudaFree(src[k]);
+      c->stats.weight_bytes -= (int64_t)sz[k];
+    }
+    L.wqkv = L.wo = L.w1 = L.w2 = nullptr;
+    np.layers.push_back(layers[i]);
+    np.index[layers[i]] = i;
+  }
+  c->pm = np;
   return ENERGON_OK;
 }
 
@@ -1385,6 +1434,12 @@ energon_status energon_set_option(energon_ctx* c, int32_t option, int32_t value)
     if (c->graphs && !c->cap_stream) CU(c, cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
     return ENERGON_OK;
   }
+  if (option == ENERGON_OPT_RING_NUMERICS) {
+    if (value != 0 && value != 1) return fail(c, ENERGON_ERR_ARG, "ENERGON_OPT_RING_NUMERICS takes 0 or 1");
+    if (!c->local_group && value) return fail(c, ENERGON_ERR_CONFIG, "ENERGON_OPT_RING_NUMERICS needs a local group");
+    c->ring = value != 0;
+    return ENERGON_OK;
+  }
   if (option == ENERGON_OPT_TP_SP) {
     if (value != 0 && value != 1) return fail(c, ENERGON_ERR_ARG, "ENERGON_OPT_TP_SP takes 0 or 1");
     c->sp = value != 0;
@@ -1436,7 +1491,7 @@ energon_status energon_index_maps(const int32_t* lens, int32_t B, int32_t S, int
     if (lens[b] < 1 || lens[b] > S) return fail(nullptr, ENERGON_ERR_LENGTH, "seq_lens not in [1, max_len]");
     lp.lens[b] = lens[b];
   }
-  launch_index_maps(lp, B, S, offsets, pack_idx, pos, unpack_idx, (cudaStream_t)stream);
+  launch_index_maps(lp, B, S, offsets, pack_idx, pos, unpack_idx, nullptr, 0, nullptr, (cudaStream_t)stream);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(nullptr, e, "index_maps");
   return ENERGON_OK;
@@ -1478,17 +1533,70 @@ energon_status energon_gemm(int32_t dtype, const void* A, const void* W, const f
                     reinterpret_cast<float*>(D), M, N, K, epi, (cudaStream_t)stream);
   } else if (dtype == ENERGON_DTYPE_BF16) {
     if (K % 8 || N % 8) return fail(nullptr, ENERGON_ERR_SHAPE, "bf16 GEMM needs K and N multiples of 8");
+    if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(W) | reinterpret_cast<uintptr_t>(D)) & 15)
+      return fail(nullptr, ENERGON_ERR_SHAPE, "bf16 GEMM needs 16-byte aligned A, W and D");
     const int code = tc_pick_bn(M, N);
     CUtensorMap ta, tb;
     if (!make_tmap_kmajor(&ta, A, M, K, 128) || !make_tmap_kmajor(&tb, W, N, K, tc_w_box(code)))
       return fail(nullptr, ENERGON_ERR_CUDA, "cuTensorMapEncodeTiled failed");
-    launch_gemm_tc(ta, tb, code, bias, reinterpret_cast<bf16*>(D), M, N, K, epi, (cudaStream_t)stream);
+    if (!launch_gemm_tc(ta, tb, code, bias, reinterpret_cast<bf16*>(D), M, N, K, epi, (cudaStream_t)stream))
+      return fail(nullptr, ENERGON_ERR_CUDA, "GEMM output tensor map could not be built");
   } else {
     return fail(nullptr, ENERGON_ERR_ARG, "dtype must be F32 or BF16");
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(nullptr, e, "gemm");
   return ENERGON_OK;
+}
+
+// ---- a5 / a7 / a13 standalone layout kernels (the same kernels the forward path runs when the fused
+// epilogues are off: fp32 mode, head sizes other than 64 / 128, ENERGON_NO_FUSE, padded A/B)
+namespace {
+energon_status layout_args(int32_t dtype, int32_t T, int32_t S, int32_t hk, int32_t d) {
+  if (dtype != ENERGON_DTYPE_F32 && dtype != ENERGON_DTYPE_BF16) return fail(nullptr, ENERGON_ERR_ARG, "dtype must be F32 or BF16");
+  if (T < 0 || S < 1 || hk < 1 || d < 1 || d % 8) return fail(nullptr, ENERGON_ERR_ARG, "bad layout arguments");
+  return ENERGON_OK;
+}
+energon_status launched(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? ENERGON_OK : cuda_fail(nullptr, e, what);
+}
+}  // namespace
+
+energon_status energon_unpack_qkv(int32_t dtype, const void* QKV, const int32_t* pack_idx, int32_t T, int32_t S,
+                                  int32_t hk, int32_t d, void* Q, void* K, void* V, void* stream) {
+  if (!QKV || !Q || !K || !V) return fail(nullptr, ENERGON_ERR_ARG, "NULL argument");
+  if (energon_status s = layout_args(dtype, T, S, hk, d)) return s;
+  if (dtype == ENERGON_DTYPE_F32)
+    launch_unpack_qkv<float>((const float*)QKV, pack_idx, T, S, hk, d, (float*)Q, (float*)K, (float*)V, (cudaStream_t)stream);
+  else
+    launch_unpack_qkv<bf16>((const bf16*)QKV, pack_idx, T, S, hk, d, (bf16*)Q, (bf16*)K, (bf16*)V, (cudaStream_t)stream);
+  return launched("unpack_qkv");
+}
+
+energon_status energon_repack(int32_t dtype, const void* O, const int32_t* pack_idx, const int32_t* unpack_idx, int32_t T,
+                              int32_t S, int32_t hk, int32_t d, void* C, void* stream) {
+  if (!O || !C || (!pack_idx && !unpack_idx)) return fail(nullptr, ENERGON_ERR_ARG, "NULL argument");
+  if (energon_status s = layout_args(dtype, T, S, hk, d)) return s;
+  if (dtype == ENERGON_DTYPE_F32)
+    launch_repack<float>((const float*)O, pack_idx, unpack_idx, T, S, hk, d, (float*)C, (cudaStream_t)stream);
+  else
+    launch_repack<bf16>((const bf16*)O, pack_idx, unpack_idx, T, S, hk, d, (bf16*)C, (cudaStream_t)stream);
+  return launched("repack");
+}
+
+energon_status energon_final_unpack(int32_t out_dtype, const float* X, const int32_t* unpack_idx, int32_t cells,
+                                    int32_t H, const float* ln_g, const float* ln_b, float eps, int32_t apply_ln,
+                                    void* out, void* stream) {
+  if (!X || !unpack_idx || !out || (apply_ln && (!ln_g || !ln_b))) return fail(nullptr, ENERGON_ERR_ARG, "NULL argument");
+  if (out_dtype != ENERGON_DTYPE_F32 && out_dtype != ENERGON_DTYPE_BF16)
+    return fail(nullptr, ENERGON_ERR_ARG, "out_dtype must be F32 or BF16");
+  if (cells < 0 || H < 4 || H % 4 || H > 12288 || !(eps > 0.f)) return fail(nullptr, ENERGON_ERR_ARG, "bad arguments");
+  if (out_dtype == ENERGON_DTYPE_F32)
+    launch_final_ln_unpack<float>(X, unpack_idx, 0, cells, H, ln_g, ln_b, eps, apply_ln, (float*)out, (cudaStream_t)stream);
+  else
+    launch_final_ln_unpack<bf16>(X, unpack_idx, 0, cells, H, ln_g, ln_b, eps, apply_ln, (bf16*)out, (cudaStream_t)stream);
+  return launched("final_unpack");
 }
 
 }  // extern "C"

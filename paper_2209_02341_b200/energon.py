@@ -22,6 +22,7 @@ MAX_BATCH = 1024
 OPT_DRCE = 1
 OPT_TP_SP = 2
 OPT_GRAPH = 3
+OPT_RING_NUMERICS = 4
 STAGE_PACKED, STAGE_FINAL = 0, 1
 COMM_NCCL, COMM_P2P = 0, 1
 LAYER_TENSORS = ("wq", "wk", "wv", "wo", "bq", "bk", "bv", "bo",
@@ -34,7 +35,7 @@ EXPORTS = ("energon_get_unique_id", "energon_init", "energon_init_local_group", 
            "energon_index_maps", "energon_gemm", "energon_attention", "energon_set_profiling", "energon_get_profile",
            "energon_shard_plan", "energon_set_option", "energon_pmep_plan", "energon_offload_layers",
            "energon_stage_plan", "energon_forward_stage", "energon_forward_stage_group", "energon_p2p_handle",
-           "energon_p2p_connect")
+           "energon_p2p_connect", "energon_unpack_qkv", "energon_repack", "energon_final_unpack")
 
 
 class EnergonError(RuntimeError):
@@ -101,6 +102,9 @@ def load_library(path: str = SO_PATH):
     L.energon_index_maps.argtypes = [ctypes.POINTER(ctypes.c_int32), I32, I32, P, P, P, P, P]
     L.energon_gemm.argtypes = [I32, P, P, P, P, I32, I32, I32, I32, P]
     L.energon_attention.argtypes = [I32, P, P, P, P, ctypes.POINTER(ctypes.c_int32), I32, I32, I32, I32, I32, P]
+    L.energon_unpack_qkv.argtypes = [I32, P, P, I32, I32, I32, I32, P, P, P, P]
+    L.energon_repack.argtypes = [I32, P, P, P, I32, I32, I32, I32, P, P]
+    L.energon_final_unpack.argtypes = [I32, P, P, I32, I32, P, P, ctypes.c_float, I32, P, P]
     L.energon_shard_plan.argtypes = [ctypes.POINTER(Config), ctypes.POINTER(Shard)]
     L.energon_set_profiling.argtypes = [P, I32]
     L.energon_set_option.argtypes = [P, I32, I32]
@@ -318,3 +322,29 @@ def energon_attention(Q, K, V, O, seq_lens, causal=1, stream=None):
     dt = DTYPE_BF16 if Q.dtype == torch.bfloat16 else DTYPE_F32
     _check(load_library().energon_attention(dt, _ptr(Q), _ptr(K), _ptr(V), _ptr(O), _lens(seq_lens), B, hk, S, d,
                                             causal, _stream(stream)))
+
+
+def _act_dtype(t):
+    import torch
+    return DTYPE_BF16 if t.dtype == torch.bfloat16 else DTYPE_F32
+
+
+def energon_unpack_qkv(QKV, pack_idx, max_len, heads, head_dim, Q, K, V, stream=None):
+    """a5: packed QKV [T, 3*heads*head_dim] -> Q, K, V [B, heads, max_len, head_dim] (pack_idx None: identity)."""
+    T = QKV.shape[0]
+    _check(load_library().energon_unpack_qkv(_act_dtype(QKV), _ptr(QKV), _ptr(pack_idx), T, max_len, heads, head_dim,
+                                             _ptr(Q), _ptr(K), _ptr(V), _stream(stream)))
+
+
+def energon_repack(O, pack_idx, unpack_idx, T, C, stream=None):
+    """a7: O [B, heads, max_len, head_dim] -> packed C [T, heads*head_dim]."""
+    B, hk, S, d = O.shape
+    _check(load_library().energon_repack(_act_dtype(O), _ptr(O), _ptr(pack_idx), _ptr(unpack_idx), T, S, hk, d, _ptr(C),
+                                         _stream(stream)))
+
+
+def energon_final_unpack(X, unpack_idx, out, ln_g=None, ln_b=None, eps=1e-5, apply_ln=False, stream=None):
+    """a13: out [cells, H] = (LN of) X[unpack_idx[cell]], pad cells exactly 0."""
+    cells, H = out.shape[0] * (out.shape[1] if out.dim() == 3 else 1), X.shape[-1]
+    _check(load_library().energon_final_unpack(_act_dtype(out), _ptr(X), _ptr(unpack_idx), cells, H, _ptr(ln_g),
+                                               _ptr(ln_b), float(eps), int(apply_ln), _ptr(out), _stream(stream)))

@@ -13,6 +13,8 @@ through properties that hold at any size -- the fp64 or
   north-star stack): the shortest sequence (47 tokens) recomputed in fp64 through all 40 layers;
   config 4 likewise on a 32-token prefix through all 48 layers.
 """
+import functools
+
 import numpy as np
 import pytest
 
@@ -102,13 +104,12 @@ def test_bench_workload_end_to_end_vs_oracle_sampled_sequence(name, k, prefix):
     layers -> final LN on that one sequence (or prefix), streaming one layer's fp64 weights at a time
     from the shared seeded generator.  Bar: the north-star bf16 tolerance, max-abs-rel <= 2e-2
     (SURVEY.md C14), after 40 / 48 layers of bf16 rounding."""
-    import oracle
     from paper_2209_02341_b200 import energon
     shape = SHAPES[name]
     bcfg = synth.BATCHES[name]
     B, S, seed = bcfg["B"], bcfg["S"], 0
     lens = synth.batch_lengths(name, seed)
-    H, F, L = shape["H"], shape["F"], shape["L"]
+    H = shape["H"]
     tok_np = synth.tokens(B, S, shape["V"], lens, seed)
     ctxs = make_engine(shape, seed, "bf16", B * S, k=k)
     try:
@@ -127,9 +128,28 @@ def test_bench_workload_end_to_end_vs_oracle_sampled_sequence(name, k, prefix):
     finally:
         destroy(ctxs)
         torch.cuda.empty_cache()
+    b, n, ref = _oracle_sampled(name, prefix)
+    assert n == {"gpt3_13b": 47, "opt30b": 32}[name]
+    err = max_abs_rel(y[b:b + 1, :n], ref, [n])
+    print(f"{name} end to end, TP={k}, sequence {b} ({n} rows of {lens[b]}): max-abs-rel {err:.3e} (tol 2e-2)")
+    assert err <= 2e-2, err
+    for bb, nn in enumerate(lens):
+        assert not y[bb, nn:].any()
+
+
+@functools.lru_cache(maxsize=None)
+def _oracle_sampled(name, prefix):
+    """fp64 oracle of the shortest sequence of the config's seed-0 batch (its first `prefix` rows, exact
+    by P12 + P13): embed -> every padded layer -> final LN, one layer's weights at a time."""
+    import oracle
+    shape = SHAPES[name]
+    bcfg = synth.BATCHES[name]
+    B, S, seed = bcfg["B"], bcfg["S"], 0
+    lens = synth.batch_lengths(name, seed)
+    H, F, L = shape["H"], shape["F"], shape["L"]
+    tok_np = synth.tokens(B, S, shape["V"], lens, seed)
     b = int(np.argmin(lens))
     n = lens[b] if prefix is None else min(prefix, lens[b])
-    assert n == {"gpt3_13b": 47, "opt30b": 32}[name]
     cfg = oracle.make_cfg(1, H, shape["h"], F)
     emb = {e: synth.emb_tensor_host(e, H, shape["V"], shape["max_seq"], seed, True) for e in synth.EMB_TENSORS}
     X = oracle.embed(cfg, emb, tok_np[b:b + 1, :n])
@@ -137,9 +157,53 @@ def test_bench_workload_end_to_end_vs_oracle_sampled_sequence(name, k, prefix):
         layer = {t: synth.layer_tensor_host(t, layer_id, H, F, seed, True) for t in oracle.LAYER_TENSORS}
         X = oracle.layers_padded(cfg, [layer], 0, 1, X, [n])
         del layer
-    ref = oracle.layernorm(X, emb["lnf_g"], emb["lnf_b"], cfg.eps)
+    return b, n, oracle.layernorm(X, emb["lnf_g"], emb["lnf_b"], cfg.eps)
+
+
+@pytest.mark.parametrize("k,ring", [(1, 0), (8, 0), (8, 1)])
+def test_opt66b_end_to_end_vs_oracle_sampled_sequence(k, ring):
+    """Config 5 (OPT-66B shape: 64 layers, H=9216, 72 heads, B=32, S=1024, exact p=0.5, bf16) -- the
+    deepest stack and the tightest bf16 margin (SURVEY.md 8(c) projects 7e-3 with an fp32 reduce,
+    1.1-1.3e-2 with NCCL's bf16-per-hop ring) -- end to end against the fp64 oracle on the first 16 rows
+    of the shortest sequence (P12 + P13).  k=1: the whole model on one B200 (130 GB of bf16 weights),
+    CUDA-graph replay; k=8: the north-star TP=8 stack as a local group (8 shards on one GPU, per-rank
+    kernels of TP=8), reductions in fp32 rank order (ring=0, the P2P / local exchange) or with NCCL's
+    ring numerics (ring=1: every hop rounds the running sum to bf16, ENERGON_OPT_RING_NUMERICS) -- the
+    exchange the NCCL path runs.  Bar: max-abs-rel <= 2e-2 (north star)."""
+    from paper_2209_02341_b200 import energon
+    name, prefix = "opt66b", 16
+    shape = SHAPES[name]
+    bcfg = synth.BATCHES[name]
+    B, S, seed = bcfg["B"], bcfg["S"], 0
+    lens = synth.batch_lengths(name, seed)
+    H = shape["H"]
+    tok_np = synth.tokens(B, S, shape["V"], lens, seed)
+    ctxs = make_engine(shape, seed, "bf16", B * S, k=k)
+    try:
+        torch.cuda.empty_cache()
+        for c in ctxs:
+            if ring:
+                energon.energon_set_option(c, energon.OPT_RING_NUMERICS, 1)
+            energon.energon_set_option(c, energon.OPT_GRAPH, 1)
+        tok = torch.from_numpy(tok_np).cuda()
+        out = torch.empty(B, S, H, dtype=torch.bfloat16, device="cuda")
+        for _ in range(2):  # eager + recording, then a replay
+            if k == 1:
+                energon.energon_forward(ctxs[0], tok, lens, out)
+            else:
+                energon.energon_forward_group(ctxs, tok, lens, out)
+            energon.energon_sync(ctxs[0])
+        y = out.float().cpu().double().numpy()
+        st = energon.energon_get_stats(ctxs[0])
+        del out
+    finally:
+        destroy(ctxs)
+        torch.cuda.empty_cache()
+    assert st["allreduce_calls"] == (0 if k == 1 else 2 * 2 * shape["L"])
+    b, n, ref = _oracle_sampled(name, prefix)
     err = max_abs_rel(y[b:b + 1, :n], ref, [n])
-    print(f"{name} end to end, TP={k}, sequence {b} ({n} rows of {lens[b]}): max-abs-rel {err:.3e} (tol 2e-2)")
+    print(f"{name} end to end, TP={k}, ring numerics {ring}, sequence {b} ({n} rows of {lens[b]}): "
+          f"max-abs-rel {err:.3e} (tol 2e-2)")
     assert err <= 2e-2, err
     for bb, nn in enumerate(lens):
         assert not y[bb, nn:].any()

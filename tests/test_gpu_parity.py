@@ -321,6 +321,77 @@ def test_attention_kernel_vs_oracle(dtype, d, causal):
         assert (got[b, :, n:] == 7.0).all()  # pad query rows untouched
 
 
+# ----------------------------------------------------------------------------- a5 / a7 / a13 vs the oracle's maps
+def _bits(t):
+    import torch as _t
+    return t.view(_t.int16 if t.dtype == _t.bfloat16 else _t.int32).cpu().numpy()
+
+
+LAYOUT_CASES = [([2, 3], 4, 2, 16), ([1, 7, 64, 3], 64, 3, 64), (synth.exact_p_lengths(16, 512, 0.5, 0), 512, 5, 128),
+                (synth.random_lengths(33, 40, 9), 40, 2, 32), ([1], 1, 1, 8)]
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+@pytest.mark.parametrize("lens,S,hk,d", LAYOUT_CASES)
+def test_layout_kernels_bitexact_vs_oracle_maps(dtype, lens, S, hk, d):
+    """a5 / a7 / a13 are index + copy work: each standalone kernel must equal, bit for bit, the scatter /
+    gather that oracle_index_maps (the fp64 oracle's closed-form maps) drives on the
+    host.  Pad rows a5 must not write keep their NaN sentinel; pad cells a13 writes are exactly 0."""
+    tdt = torch_dtype(dtype)
+    B = len(lens)
+    off, pack, pos, unpack = oracle.index_maps(lens, S)
+    T = int(off[-1])
+    Hk = hk * d
+    pack_d = torch.from_numpy(pack.astype(np.int32)).cuda()
+    unpack_d = torch.from_numpy(unpack.astype(np.int32)).cuda()
+    g = torch.Generator().manual_seed(T * 7 + d)
+    # a5: packed QKV -> padded Q, K, V
+    qkv = torch.randn(T, 3 * Hk, generator=g).to(tdt).cuda()
+    outs = [torch.full((B, hk, S, d), float("nan"), dtype=tdt, device="cuda") for _ in range(3)]
+    E().energon_unpack_qkv(qkv, pack_d, S, hk, d, *outs)
+    torch.cuda.synchronize()
+    qkv_h = qkv.cpu()
+    for w, o in enumerate(outs):
+        exp = torch.full((B, hk, S, d), float("nan"), dtype=tdt)
+        for t in range(T):
+            b, s = divmod(int(pack[t]), S)
+            exp[b, :, s, :] = qkv_h[t, w * Hk:(w + 1) * Hk].view(hk, d)
+        assert np.array_equal(_bits(o), _bits(exp))
+    # a7: padded O -> packed C (DRCE), and the padded A/B form (identity rows, pad cells zeroed)
+    O = torch.randn(B, hk, S, d, generator=g).to(tdt).cuda()
+    C = torch.full((T, Hk), 3.0, dtype=tdt, device="cuda")
+    E().energon_repack(O, pack_d, unpack_d, T, C)
+    Cp = torch.full((B * S, Hk), 3.0, dtype=tdt, device="cuda")
+    E().energon_repack(O, None, unpack_d, B * S, Cp)
+    torch.cuda.synchronize()
+    Oh = O.cpu()
+    expC = torch.stack([Oh[int(c) // S, :, int(c) % S, :].reshape(Hk) for c in pack])
+    assert np.array_equal(_bits(C), _bits(expC))
+    expP = Oh.permute(0, 2, 1, 3).reshape(B * S, Hk).clone()
+    expP[torch.from_numpy(unpack < 0)] = 0
+    assert np.array_equal(_bits(Cp), _bits(expP))
+    # a13 without LN: out[cell] = X[unpack[cell]] (fp32 -> out dtype, RNE) or exactly 0
+    H = 4 * max(2, Hk // 8)
+    X = torch.randn(T, H, generator=g).cuda()
+    out = torch.full((B, S, H), float("nan"), dtype=tdt, device="cuda")
+    E().energon_final_unpack(X, unpack_d, out)
+    torch.cuda.synchronize()
+    exp = torch.zeros(B * S, H, dtype=tdt)
+    valid = torch.from_numpy(unpack >= 0)
+    exp[valid] = X.cpu()[torch.from_numpy(unpack[unpack >= 0].astype(np.int64))].to(tdt)
+    assert np.array_equal(_bits(out.view(B * S, H)), _bits(exp))
+    # a13 with the final LN: the unpack is exact, the LN within fp32 rounding of the oracle's fp64 LN
+    gam = (1 + 0.1 * torch.randn(H, generator=g)).cuda()
+    bet = (0.1 * torch.randn(H, generator=g)).cuda()
+    E().energon_final_unpack(X, unpack_d, out, gam, bet, 1e-5, True)
+    torch.cuda.synchronize()
+    y = out.view(B * S, H).float().cpu().numpy()
+    ref = oracle.layernorm(X.cpu().double().numpy(), gam.cpu().double().numpy(), bet.cpu().double().numpy())
+    assert not y[unpack < 0].any()
+    tol = 1e-5 if dtype == "f32" else 8e-3
+    assert np.abs(y[unpack >= 0] - ref[unpack[unpack >= 0]]).max() <= tol * max(1.0, np.abs(ref).max())
+
+
 # ----------------------------------------------------------------------------- fused a5 / a7
 @pytest.mark.parametrize("drce", [1, 0])
 def test_fused_layout_kernels_bitexact(drce, monkeypatch):
@@ -486,6 +557,9 @@ def test_pmep_offload_bitexact(slots, pool, dtype):
         ref = run_forward(ctxs, tok, lens, dtype, shape["H"])
     finally:
         destroy(ctxs)
+    layers_h, emb_h = oracle_model(shape, seed, dtype)
+    oref = oracle.forward_drce(oracle.make_cfg(shape["L"], shape["H"], shape["h"], shape["F"]), layers_h, emb_h, tok,
+                               lens)
     plan = E().energon_pmep_plan(shape["L"], 3)  # [1, 3, 5]
     for layers in (plan, [0, 2, 4, 5]):
         ctxs = make_engine(shape, seed, dtype, B * S)
@@ -497,6 +571,8 @@ def test_pmep_offload_bitexact(slots, pool, dtype):
         finally:
             destroy(ctxs)
         assert np.array_equal(y, ref) and np.array_equal(y2, ref)
+        # and directly against the fp64 oracle (PMEP changes where the weights live, not the math)
+        assert max_abs_rel(y, oref, lens) <= TOL[dtype]
         per_layer = (3 * 256 * 256 + 256 * 256 + 1024 * 256 * 2) * (2 if dtype == "bf16" else 4)
         assert st["prefetch_bytes"] == 2 * len(layers) * per_layer
 
