@@ -106,12 +106,14 @@ typedef struct {
   int64_t allreduce_calls;  /* TP reductions issued (2 per layer per forward when k > 1) */
   int64_t kernel_launches;  /* kernels this library launched, cumulative */
   int64_t last_tokens;      /* T = sum(seq_lens) of the last forward */
-  int64_t last_rows;        /* rows the linears ran on in the last forward (T, or B*S with drce=0) */
+  int64_t last_rows;        /* rows the linears ran on in the last forward: T rounded up to a bucket of 128
+                               (<= max_tokens) with DRCE, B*S with drce=0 */
   int64_t weight_bytes;     /* device bytes held for this rank's weights */
   int64_t workspace_bytes;  /* device bytes held for activations */
   int64_t prefetch_bytes;   /* PMEP: bytes fetched from the memory pool, cumulative */
   int64_t fused_exchanges;  /* P2P: TP reductions whose partials the row-parallel GEMM stored straight into the
                                owners' slots (GEMM -> reduce-scatter fused), cumulative */
+  int64_t graphs_recorded;  /* ENERGON_OPT_GRAPH: CUDA graphs recorded (cache misses), cumulative */
 } energon_stats;
 
 /*
@@ -275,8 +277,10 @@ ENERGON_API energon_status energon_get_stats(const energon_ctx* ctx, energon_sta
  * Runtime options (take effect at the next forward; host-only, no device work):
  *   ENERGON_OPT_DRCE   1 = packed linears (the method), 0 = padded A/B ("pure EnergonAI",
  *                      PAPER.md:567-571); the workspace is sized for max_tokens padded rows either way.
- *   ENERGON_OPT_GRAPH  1 = capture each distinct forward (shapes, lengths, buffers) into a CUDA graph
- *                      on a private stream and replay it on the caller's stream (LRU cache of 32);
+ *   ENERGON_OPT_GRAPH  1 = capture each distinct forward (shapes, buffers, and the row bucket: T rounded
+ *                      up to 128) into a CUDA graph on a private stream and replay it on the caller's
+ *                      stream (LRU cache of 32); a new batch of the same bucket replays the recorded
+ *                      graph with its lengths written into the graph's one index-maps node;
  *                      ignored while profiling or with off-device (PMEP) layers.  Default 0.
  *   ENERGON_OPT_TP_SP  k > 1 only: 1 (default) = sequence-parallel schedule (reduce-scatter, bias +
  *                      residual + LN on this rank's 1/k of the rows, all-gather), 0 = allreduce and

@@ -19,7 +19,8 @@ namespace energon {
 // (attention_tc.cu).
 template <typename Act>
 __global__ void __launch_bounds__(128) attention_simt_kernel(const Act* __restrict__ Q, const Act* __restrict__ K,
-                                                             const Act* __restrict__ V, Act* __restrict__ O, LensParam lp,
+                                                             const Act* __restrict__ V, Act* __restrict__ O,
+                                                             const int* __restrict__ lens,
                                                              int hk, int S, int d, int causal, float scale) {
   pdl_trigger();
   pdl_wait();
@@ -28,7 +29,7 @@ __global__ void __launch_bounds__(128) attention_simt_kernel(const Act* __restri
   float* sc = sm + d;   // [S]
   __shared__ float red[32];
   const int s = blockIdx.x, head = blockIdx.y, b = blockIdx.z;
-  const int len = lp.lens[b];
+  const int len = lens[b];
   if (s >= len) return;
   const int nk = causal ? min(s + 1, len) : len;
   const int64_t base = ((int64_t)b * hk + head) * S * d;
@@ -67,12 +68,13 @@ __global__ void __launch_bounds__(128) attention_simt_kernel(const Act* __restri
 }
 
 template <typename Act>
-void launch_attention_simt(const Act* Q, const Act* K, const Act* V, Act* O, const LensParam& lp, int B, int hk, int S,
+void launch_attention_simt(const Act* Q, const Act* K, const Act* V, Act* O, const int* lens, int B, int hk, int S,
                            int d, int causal, cudaStream_t st) {
   if (B <= 0) return;
   dim3 grid(S, hk, B);
   const size_t smem = sizeof(float) * (size_t)(d + S);
-  launch_k(attention_simt_kernel<Act>, dim3(grid), dim3(128), smem, st, Q, K, V, O, lp, hk, S, d, causal, 1.f / sqrtf((float)d));
+  launch_k(attention_simt_kernel<Act>, dim3(grid), dim3(128), smem, st, Q, K, V, O, lens, hk, S, d, causal,
+           1.f / sqrtf((float)d));
 }
 
 int attention_impl() {
@@ -80,32 +82,33 @@ int attention_impl() {
   if (v < 0) {
     const char* e = getenv("ENERGON_ATTN");
     v = e ? atoi(e) : 4;
-    if (v < 3 || v > 4) v = 4;
+    if (v != 4) v = 4;
   }
   return v;
 }
 
 template <typename Act>
-void launch_attention(const Act* Q, const Act* K, const Act* V, Act* O, const LensParam& lp, int B, int hk, int S, int d,
-                      int causal, cudaStream_t st) {
+void launch_attention(const Act* Q, const Act* K, const Act* V, Act* O, const int* lens_d, const uint32_t* work_d,
+                      int B, int hk, int S, int d, int causal, cudaStream_t st, AttnMaps* maps) {
   // bf16, d = 64 / 128: the tcgen05 kernel; everything else (fp32 parity mode, other head sizes): SIMT
   if constexpr (sizeof(Act) == 2) {
-    if ((d == 128 || d == 64) &&
-        launch_attention_tc(Q, K, V, nullptr, nullptr, O, lp, B, hk, S, d, causal, st, attention_impl() == 4))
+    if ((d == 128 || d == 64) && work_d &&
+        launch_attention_tc(Q, K, V, nullptr, nullptr, O, lens_d, work_d, B, hk, S, d, causal, st, maps))
       return;
   }
-  launch_attention_simt<Act>(Q, K, V, O, lp, B, hk, S, d, causal, st);
+  launch_attention_simt<Act>(Q, K, V, O, lens_d, B, hk, S, d, causal, st);
 }
 
 bool launch_attention_packed(const bf16* Q, const bf16* K, const bf16* V, bf16* ctx_packed, const int* offsets,
-                             const LensParam& lp, int B, int hk, int S, int d, int causal, cudaStream_t st) {
+                             const int* lens_d, const uint32_t* work_d, int B, int hk, int S, int d, int causal,
+                             cudaStream_t st, AttnMaps* maps) {
   if (d != 128 && d != 64) return false;
-  return launch_attention_tc(Q, K, V, ctx_packed, offsets, nullptr, lp, B, hk, S, d, causal, st, attention_impl() == 4);
+  return launch_attention_tc(Q, K, V, ctx_packed, offsets, nullptr, lens_d, work_d, B, hk, S, d, causal, st, maps);
 }
 
-template void launch_attention<float>(const float*, const float*, const float*, float*, const LensParam&, int, int, int,
-                                      int, int, cudaStream_t);
-template void launch_attention<bf16>(const bf16*, const bf16*, const bf16*, bf16*, const LensParam&, int, int, int, int,
-                                     int, cudaStream_t);
+template void launch_attention<float>(const float*, const float*, const float*, float*, const int*, const uint32_t*,
+                                      int, int, int, int, int, cudaStream_t, AttnMaps*);
+template void launch_attention<bf16>(const bf16*, const bf16*, const bf16*, bf16*, const int*, const uint32_t*, int,
+                                     int, int, int, int, cudaStream_t, AttnMaps*);
 
 }  // namespace energon

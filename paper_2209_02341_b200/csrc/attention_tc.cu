@@ -3,18 +3,17 @@
 // attention module still requires the padding area"), writing the packed context
 // rows [T, hk*d] at offsets[b] + s (PAPER.md:373 kernel #2 fused).
 //
-// Persistent: each CTA (2 per SM) loops over a heaviest-first list of work items, one item = 128 query
-// rows of one (sequence, head), so the next item's Q / K loads overlap the current item's tail; 6 warps:
-//   warp 0    TMA producer: the Q tile once, then K and V tiles of 64 keys (single-buffered each;
-//             the next K tile streams in while the current tile's softmax and P.V run)
-//   warp 1    MMA issuer (one thread): S = Q K^T  (M=128, N=64, K=d; K-major A and B)
-//                                      O += P V    (M=128, N=d, K=64; A = P from shared memory,
-//                                                   B = V, MN-major)  -- accumulators in TMEM
+// Persistent: each CTA (2 per SM) loops over a heaviest-first list of work items built on the device by
+// the index-maps kernel (build_attn_work: one item = 128 query rows of one sequence; item w = pair
+// w / hk, head w % hk), so the next item's Q / K loads overlap the current item's tail.  6 warps:
+//   warp 0    TMA producer: the Q tile once, then K and V tiles of 64 keys (double-buffered)
+//   warp 1    MMA issuer (one thread): S = Q K^T (M=128, N=64, K=d; K-major A and B) into TMEM, and
+//             O += P V with P read straight from TMEM (M=128, N=d, K=64; B = V, MN-major)
 //   warps 2-5 softmax: thread i owns query row i (TMEM lane i): tcgen05.ld its 64 scores, masks
 //             (t >= len, causal t > s), runs the online softmax in fp32 / exp2 and writes its P row
-//             (bf16, 128B-swizzled) to shared memory; O stays in TMEM and is rescaled only when the
-//             row maximum grew by more than 2^8 (exact: P values are bounded by 256).
-// Key tiles stop at min(len, q0 + 128) (causal) or len; query tiles with q0 >= len exit at once.
+//             (bf16) back over its scores in TMEM; O stays in TMEM and is rescaled only when the row
+//             maximum grew by more than 2^8 (exact: P values are bounded by 256).
+// Key tiles stop at min(len, q0 + 128) (causal) or len; query tiles with q0 >= len are not items.
 // Rows t >= len of the last V tile are zeroed in shared memory before P.V, so pad rows of V that a5
 // never wrote (possibly NaN) cannot reach the output even as 0 * NaN.
 #include <algorithm>
@@ -23,9 +22,11 @@
 #include "kernels.h"
 #include "tc_ptx.cuh"
 
-#define ATTN_MAX_PAIRS 2048
-
 namespace energon {
+
+constexpr int ATTN_BM = 128, ATTN_BN = 64;  // query rows per item, keys per tile (the work list's costs)
+int attention_tile_bm() { return ATTN_BM; }
+int attention_tile_bn() { return ATTN_BN; }
 
 __device__ __forceinline__ float ex2f(float x) {
   float y;
@@ -56,319 +57,8 @@ __device__ __forceinline__ uint64_t umma_desc_sw128_mn(uint32_t saddr, uint32_t 
   return d;
 }
 
-template <int D>
-struct AttnCfg {
-  static constexpr int BM = 128, BN = 64, DH = D / 64;
-  static constexpr int Q_BYTES = BM * D * 2;  // DH blocks of [128 rows x 64] (16 KB each)
-  static constexpr int K_BYTES = BN * D * 2;  // DH blocks of [64 keys x 64]
-  static constexpr int V_BYTES = BN * D * 2;
-  static constexpr int P_BYTES = BM * BN * 2;  // [128 rows x 64 keys], one swizzle block
-  static constexpr int K_STAGES = 2;  // K double-buffered: K_{j+1} streams in while S_j runs
-  static constexpr int SMEM = Q_BYTES + K_STAGES * K_BYTES + V_BYTES + P_BYTES + 1024 + 256;
-  static constexpr int TMEM_COLS = (BN + D) <= 128 ? 128 : 256;  // S at col 0, O at col BN
-  // S = Q K^T: M=128, N=BN, both K-major
-  static constexpr uint32_t IDESC_S = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
-                                      ((uint32_t)(BM >> 4) << 24);
-  // O += P V: M=128, N=D, A K-major, B MN-major (bit 16)
-  static constexpr uint32_t IDESC_O = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | ((uint32_t)(D >> 3) << 17) |
-                                      ((uint32_t)(BM >> 4) << 24);
-};
-
-// Work list of the persistent kernel: (sequence b, query tile qt) pairs with qt * 128 < len_b, sorted
-// heaviest first (most key tiles) on the host; item w = (pair w / hk, head w % hk).
-struct AttnWork {
-  int npairs;
-  uint32_t pair[ATTN_MAX_PAIRS];  // (b << 16) | qt
-};
-
-template <int D>
-__global__ void __launch_bounds__(192, 2)
-    attention_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                        const __grid_constant__ CUtensorMap tmV, bf16* __restrict__ Cp, const int* __restrict__ offsets,
-                        bf16* __restrict__ Opad, const __grid_constant__ LensParam lp, int hk, int S, int causal,
-                        float scale_log2, const __grid_constant__ AttnWork work) {
-  using C = AttnCfg<D>;
-  constexpr int BM = C::BM, BN = C::BN, DH = C::DH;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = smem;
-  uint8_t* sK = sQ + C::Q_BYTES;
-  uint8_t* sV = sK + C::K_STAGES * C::K_BYTES;
-  uint8_t* sP = sV + C::V_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + C::P_BYTES);
-  uint64_t* q_full = bars + 0;
-  uint64_t* q_empty = bars + 1;
-  uint64_t* v_full = bars + 2;
-  uint64_t* v_empty = bars + 3;
-  uint64_t* s_full = bars + 4;
-  uint64_t* s_empty = bars + 5;
-  uint64_t* p_full = bars + 6;
-  uint64_t* o_full = bars + 7;
-  uint64_t* o_empty = bars + 8;
-  uint64_t* k_full = bars + 9;    // [K_STAGES]
-  uint64_t* k_empty = bars + 11;  // [K_STAGES]
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 13);
-
-  const int items = work.npairs * hk;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (warp == 0 && lane == 0) {
-    tma_prefetch_desc(&tmQ);
-    tma_prefetch_desc(&tmK);
-    tma_prefetch_desc(&tmV);
-    mbar_init(q_full, 1);
-    mbar_init(q_empty, 1);
-    for (int i = 0; i < C::K_STAGES; ++i) {
-      mbar_init(&k_full[i], 1);
-      mbar_init(&k_empty[i], 1);
-    }
-    mbar_init(v_full, 1);
-    mbar_init(v_empty, 1);
-    mbar_init(s_full, 1);
-    mbar_init(s_empty, 4);
-    mbar_init(p_full, 4);
-    mbar_init(o_full, 1);
-    mbar_init(o_empty, 4);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
-                 "n"(C::TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem_base = *tmem_holder;
-  // Dependents may launch only once this CTA HOLDS its TMEM: a CTA that triggered before allocating
-  // could find its columns taken by a co-resident dependent CTA that then waits (griddepcontrol.wait)
-  // on this grid -- a cycle.
-  pdl_trigger();
-  const uint32_t tS = tmem_base, tO = tmem_base + BN;
-
-  // decode item w -> (b, head, q0, number of key tiles)
-  auto decode = [&](int w, int& b, int& head, int& q0, int& nkv, int& len) {
-    const uint32_t pr = work.pair[w / hk];
-    head = w % hk;
-    b = (int)(pr >> 16);
-    q0 = (int)(pr & 0xFFFFu) * BM;
-    len = lp.lens[b];
-    const int kv_end = causal ? min(len, q0 + BM) : len;
-    nkv = (kv_end + BN - 1) / BN;
-  };
-
-  if (warp == 0) {
-    if (lane == 0) {
-      // ---------------- TMA producer: per item Q once, then K_0, K_1, V_0, K_2, V_1, ... (g = global tile)
-      pdl_wait();
-      int g = 0, qi = 0;
-      for (int w = blockIdx.x; w < items; w += gridDim.x, ++qi) {
-        int b, head, q0, nkv, len;
-        decode(w, b, head, q0, nkv, len);
-        const int row_base = (b * hk + head) * S;
-        mbar_wait(q_empty, (qi & 1) ^ 1);  // the previous item's last S has consumed Q
-        mbar_expect_tx(q_full, C::Q_BYTES);
-#pragma unroll
-        for (int h = 0; h < DH; ++h) tma_load_2d(&tmQ, smem_u32(sQ + h * BM * 128), q_full, h * 64, row_base + q0);
-        auto load_k = [&](int gt, int j) {
-          const int ks = gt & 1;
-          mbar_wait(&k_empty[ks], ((gt >> 1) & 1) ^ 1);
-          mbar_expect_tx(&k_full[ks], C::K_BYTES);
-#pragma unroll
-          for (int h = 0; h < DH; ++h)
-            tma_load_2d(&tmK, smem_u32(sK + ks * C::K_BYTES + h * BN * 128), &k_full[ks], h * 64, row_base + j * BN);
-        };
-        load_k(g, 0);
-        for (int j = 0; j < nkv; ++j) {
-          if (j + 1 < nkv) load_k(g + j + 1, j + 1);
-          mbar_wait(v_empty, ((g + j) & 1) ^ 1);
-          mbar_expect_tx(v_full, C::V_BYTES);
-#pragma unroll
-          for (int h = 0; h < DH; ++h)
-            tma_load_2d(&tmV, smem_u32(sV + h * BN * 128), v_full, h * 64, row_base + j * BN);
-        }
-        g += nkv;
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      // ---------------- MMA issuer
-      int g = 0, qi = 0;
-      for (int w = blockIdx.x; w < items; w += gridDim.x, ++qi) {
-        int b, head, q0, nkv, len;
-        decode(w, b, head, q0, nkv, len);
-        mbar_wait(q_full, qi & 1);
-        for (int j = 0; j < nkv; ++j, ++g) {
-          const uint32_t par = g & 1;
-          const int ks = g & 1;
-          // ---- S = Q K^T
-          mbar_wait(&k_full[ks], (g >> 1) & 1);
-          mbar_wait(s_empty, par ^ 1);
-          tc_fence_after();
-#pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk) {
-            const uint32_t off = (kk & 3) * 32;
-            const uint64_t a = umma_desc_sw128(smem_u32(sQ + (kk >> 2) * BM * 128 + off));
-            const uint64_t bb = umma_desc_sw128(smem_u32(sK + ks * C::K_BYTES + (kk >> 2) * BN * 128 + off));
-            umma_bf16(tS, a, bb, C::IDESC_S, kk > 0 ? 1u : 0u);
-          }
-          umma_commit(&k_empty[ks]);
-          if (j + 1 == nkv) umma_commit(q_empty);
-          umma_commit(s_full);
-          // ---- O += P V
-          mbar_wait(p_full, par);
-          mbar_wait(v_full, par);
-          if (j == 0) mbar_wait(o_empty, (qi & 1) ^ 1);  // the previous item's epilogue has read O
-          tc_fence_after();
-#pragma unroll
-          for (int kk = 0; kk < BN / 16; ++kk) {
-            const uint64_t a = umma_desc_sw128(smem_u32(sP + kk * 32));
-            const uint64_t bb = umma_desc_sw128_mn(smem_u32(sV + kk * 16 * 128), BN * 128);
-            umma_bf16(tO, a, bb, C::IDESC_O, (j > 0 || kk > 0) ? 1u : 0u);
-          }
-          umma_commit(v_empty);
-          umma_commit(o_full);
-        }
-      }
-    }
-  } else {
-    // ---------------- softmax warps: thread owns query row r (= TMEM lane r)
-    const int qd = warp & 3;
-    const int r = qd * 32 + lane;
-    const uint32_t lane_off = (uint32_t)(qd * 32) << 16;
-    int g = 0;
-    for (int w = blockIdx.x; w < items; w += gridDim.x) {
-      int b, head, q0, nkv, len;
-      decode(w, b, head, q0, nkv, len);
-      const int srow = q0 + r;
-      float m_ref = -INFINITY, l = 0.f;
-      for (int j = 0; j < nkv; ++j, ++g) {
-        const uint32_t par = g & 1;
-        const int k0 = j * BN;
-        mbar_wait(s_full, par);
-        __syncwarp();  // reconverge the spin loop before the .sync.aligned tcgen05.ld
-        tc_fence_after();
-        uint32_t sr[2][32];
-        tmem_ld32(tS + lane_off + 0, sr[0]);
-        tmem_ld32(tS + lane_off + 32, sr[1]);
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(s_empty);
-        // tile max over the raw scores (scale > 0 commutes with max); mask only on tiles that cross
-        // len or the causal diagonal of this warp's rows (warp-uniform test)
-        float mt = -INFINITY;
-        const bool need_mask = (k0 + BN > len) || (causal && k0 + BN - 1 > q0 + qd * 32);
-        if (need_mask) {
-#pragma unroll
-          for (int c = 0; c < BN; ++c) {
-            const int t = k0 + c;
-            float v = __uint_as_float(sr[c >> 5][c & 31]);
-            if (t >= len || (causal && t > srow)) v = -INFINITY;
-            sr[c >> 5][c & 31] = __float_as_uint(v);
-            mt = fmaxf(mt, v);
-          }
-        } else {
-#pragma unroll
-          for (int c = 0; c < BN; ++c) mt = fmaxf(mt, __uint_as_float(sr[c >> 5][c & 31]));
-        }
-        mt *= scale_log2;
-        if (j > 0) {  // P_{g-1} . V_{g-1} done before P is overwritten or O rescaled
-          mbar_wait(o_full, par ^ 1);
-          __syncwarp();
-          tc_fence_after();
-        }
-        // first tile, or the max grew by more than 2^8: move the reference.  The decision is per row
-        // (per lane) but tcgen05.ld / st are .sync.aligned, so the O rescale runs warp-wide whenever
-        // any row needs it, with alpha = 1 (exact) for the others -- a per-lane branch around them
-        // is undefined and hung the warp under some schedules.
-        const bool grow = mt > m_ref + 8.f;
-        const float alpha = !grow ? 1.f : (m_ref == -INFINITY) ? 0.f : ex2f(m_ref - mt);
-        if (j > 0 && __any_sync(0xffffffffu, grow)) {
-#pragma unroll 1
-          for (int c = 0; c < D; c += 32) {
-            uint32_t o[32];
-            tmem_ld32(tO + lane_off + c, o);
-#pragma unroll
-            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
-            tmem_st32(tO + lane_off + c, o);
-          }
-        }
-        if (grow) {
-          l *= alpha;
-          m_ref = mt;
-        }
-        const float base = (m_ref == -INFINITY) ? 0.f : m_ref;
-        uint8_t* prow = sP + r * 128;  // 128B swizzle: chunk c of row r at c ^ (r & 7)
-#pragma unroll
-        for (int c8 = 0; c8 < BN / 8; ++c8) {
-          float p[8];
-#pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            p[e] = ex2f(fmaf(__uint_as_float(sr[(c8 * 8 + e) >> 5][(c8 * 8 + e) & 31]), scale_log2, -base));
-            l += p[e];
-          }
-          uint4 pk;
-          pk.x = pack_bf16x2(p[0], p[1]);
-          pk.y = pack_bf16x2(p[2], p[3]);
-          pk.z = pack_bf16x2(p[4], p[5]);
-          pk.w = pack_bf16x2(p[6], p[7]);
-          *reinterpret_cast<uint4*>(prow + ((c8 ^ (r & 7)) << 4)) = pk;
-        }
-        if (k0 + BN > len) {  // zero V rows of keys >= len (pad rows a5 never wrote may hold NaN)
-          mbar_wait(v_full, par);
-          if (r < BN && k0 + r >= len) {
-#pragma unroll
-            for (int h = 0; h < DH; ++h) {
-              uint4* vr = reinterpret_cast<uint4*>(sV + h * BN * 128 + r * 128);
-#pragma unroll
-              for (int c = 0; c < 8; ++c) vr[c] = make_uint4(0, 0, 0, 0);
-            }
-          }
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(p_full);
-      }
-      // ---------------- item epilogue: O / l -> packed context row (or padded O row)
-      mbar_wait(o_full, (g - 1) & 1);
-      __syncwarp();
-      tc_fence_after();
-      const float inv = 1.f / l;
-      const bool valid = srow < len;
-      bf16* dst = Cp ? Cp + ((int64_t)__ldg(offsets + b) + srow) * (int64_t)(hk * D) + head * D
-                     : Opad + ((int64_t)(b * hk + head) * S + srow) * D;
-#pragma unroll 1
-      for (int c = 0; c < D; c += 32) {
-        uint32_t o[32];
-        tmem_ld32(tO + lane_off + c, o);
-        if (valid) {
-#pragma unroll
-          for (int e = 0; e < 32; e += 8) {
-            uint4 pk;
-            pk.x = pack_bf16x2(__uint_as_float(o[e]) * inv, __uint_as_float(o[e + 1]) * inv);
-            pk.y = pack_bf16x2(__uint_as_float(o[e + 2]) * inv, __uint_as_float(o[e + 3]) * inv);
-            pk.z = pack_bf16x2(__uint_as_float(o[e + 4]) * inv, __uint_as_float(o[e + 5]) * inv);
-            pk.w = pack_bf16x2(__uint_as_float(o[e + 6]) * inv, __uint_as_float(o[e + 7]) * inv);
-            *reinterpret_cast<uint4*>(dst + c + e) = pk;
-          }
-        }
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(o_empty);
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 1) {
-    tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(C::TMEM_COLS));
-  }
-}
-
-// ============================================================================ v2: P in TMEM
-// Same work list, masks and numerics as attention_tc_kernel, restructured so that the softmax of key
-// tile j no longer waits for P_{j-1} V: S / P are double-buffered in TMEM (S_b at columns
+// ============================================================================ the kernel
+// The softmax of key tile j never waits for P_{j-1} V: S / P are double-buffered in TMEM (S_b at columns
 // [b BN, (b+1) BN), P_b written over the first BN/2 columns of S_b as packed bf16) and P V reads its A
 // operand straight from TMEM (tcgen05.mma ... [d], [a_tmem], b_desc), V is double-buffered in shared
 // memory, and the MMA thread issues S_{t+1} before P_t V_t across the CTA's whole tile sequence
@@ -378,14 +68,18 @@ __global__ void __launch_bounds__(192, 2)
 // (p_free); the O rescale waits for P_{t-1} V (o_full); P_t V is issued after p_full of tile t.
 template <int D>
 struct Attn2Cfg {
-  static constexpr int BM = 128, BN = 64, DH = D / 64;
+  static constexpr int BM = ATTN_BM, BN = ATTN_BN, DH = D / 64;
   static constexpr int Q_BYTES = BM * D * 2;
   static constexpr int K_BYTES = BN * D * 2;
   static constexpr int V_BYTES = BN * D * 2;
   static constexpr int SMEM = Q_BYTES + 2 * K_BYTES + 2 * V_BYTES + 1024 + 256;
   static constexpr int TMEM_COLS = 256;  // 2 * BN + D <= 256 for D <= 128
-  static constexpr uint32_t IDESC_S = AttnCfg<D>::IDESC_S;
-  static constexpr uint32_t IDESC_O = AttnCfg<D>::IDESC_O;
+  // S = Q K^T: M=128, N=BN, both K-major
+  static constexpr uint32_t IDESC_S = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                                      ((uint32_t)(BM >> 4) << 24);
+  // O += P V: M=128, N=D, A K-major, B MN-major (bit 16)
+  static constexpr uint32_t IDESC_O = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | ((uint32_t)(D >> 3) << 17) |
+                                      ((uint32_t)(BM >> 4) << 24);
 };
 
 __device__ __forceinline__ void umma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc,
@@ -400,8 +94,8 @@ template <int D>
 __global__ void __launch_bounds__(192, 2)
     attention_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                          const __grid_constant__ CUtensorMap tmV, bf16* __restrict__ Cp, const int* __restrict__ offsets,
-                         bf16* __restrict__ Opad, const __grid_constant__ LensParam lp, int hk, int S, int causal,
-                         float scale_log2, const __grid_constant__ AttnWork work) {
+                         bf16* __restrict__ Opad, const int* __restrict__ lens, const uint32_t* __restrict__ work,
+                         int hk, int S, int causal, float scale_log2) {
   using C = Attn2Cfg<D>;
   constexpr int BM = C::BM, BN = C::BN, DH = C::DH;
   extern __shared__ uint8_t smem_raw[];
@@ -423,7 +117,6 @@ __global__ void __launch_bounds__(192, 2)
   uint64_t* p_free = bars + 17;   // [2]
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 19);
 
-  const int items = work.npairs * hk;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmQ);
@@ -453,7 +146,12 @@ __global__ void __launch_bounds__(192, 2)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
-  pdl_trigger();  // after the TMEM allocation (see attention_tc_kernel)
+  // Dependents may launch only once this CTA HOLDS its TMEM: a CTA that triggered before allocating
+  // could find its columns taken by a co-resident dependent CTA that then waits (griddepcontrol.wait)
+  // on this grid -- a cycle.
+  pdl_trigger();
+  pdl_wait();  // the work list, lengths and Q / K / V are written by earlier kernels of the forward
+  const int items = (int)__ldg(work) * hk;
   const uint32_t tO = tmem_base + 2 * BN;
 
   // the CTA's k-th item: heaviest-first list dealt out boustrophedon (round k even: slot bid, odd:
@@ -461,11 +159,11 @@ __global__ void __launch_bounds__(192, 2)
   // 45.2 -> 41.3 us of item cost vs plain round-robin)
   auto item_at = [&](int k) { return k * (int)gridDim.x + ((k & 1) ? (int)gridDim.x - 1 - (int)blockIdx.x : (int)blockIdx.x); };
   auto decode = [&](int w, int& b, int& head, int& q0, int& nkv, int& len) {
-    const uint32_t pr = work.pair[w / hk];
+    const uint32_t pr = __ldg(work + 1 + w / hk);
     head = w % hk;
     b = (int)(pr >> 16);
     q0 = (int)(pr & 0xFFFFu) * BM;
-    len = lp.lens[b];
+    len = __ldg(lens + b);
     const int kv_end = causal ? min(len, q0 + BM) : len;
     nkv = (kv_end + BN - 1) / BN;
   };
@@ -473,7 +171,6 @@ __global__ void __launch_bounds__(192, 2)
   if (warp == 0) {
     if (lane == 0) {
       // ---------------- TMA producer: per item Q once, then K_0, K_1, V_0, K_2, V_1, ... (t = CTA tile count)
-      pdl_wait();
       int t = 0, qi = 0;
       for (int w = item_at(0); w < items; w = item_at(++qi)) {
         int b, head, q0, nkv, len;
@@ -704,59 +401,47 @@ __global__ void __launch_bounds__(192, 2)
   }
 }
 
-template <int D, bool V2>
+template <int D>
 static bool launch_tc(const bf16* Q, const bf16* K, const bf16* V, bf16* Cp, const int* offsets, bf16* Opad,
-                      const LensParam& lp, int B, int hk, int S, int causal, cudaStream_t st) {
-  using C = AttnCfg<D>;
-  constexpr int SMEM = V2 ? Attn2Cfg<D>::SMEM : C::SMEM;
-  // heaviest-first work list of (sequence, query tile) pairs, built from the host copy of the lengths
-  AttnWork work;  // 8 KB kernel parameter (copied into the launch)
-  int n = 0;
-  auto cost = [&](int b, int qt) {
-    const int len = lp.lens[b];
-    const int kv_end = causal ? std::min(len, (qt + 1) * C::BM) : len;
-    return (kv_end + C::BN - 1) / C::BN;
-  };
-  for (int b = 0; b < B; ++b)
-    for (int qt = 0; qt * C::BM < lp.lens[b]; ++qt) {
-      if (n >= ATTN_MAX_PAIRS) return false;
-      work.pair[n++] = ((uint32_t)b << 16) | (uint32_t)qt;
-    }
-  work.npairs = n;
-  std::stable_sort(work.pair, work.pair + n, [&](uint32_t x, uint32_t y) {
-    return cost((int)(x >> 16), (int)(x & 0xFFFF)) > cost((int)(y >> 16), (int)(y & 0xFFFF));
-  });
+                      const int* lens_d, const uint32_t* work_d, int B, int hk, int S, int causal, cudaStream_t st,
+                      AttnMaps* maps) {
+  using C = Attn2Cfg<D>;
   const int rows = B * hk * S;
-  CUtensorMap mq, mk, mv;
-  if (!make_tmap_kmajor(&mq, Q, rows, D, C::BM) || !make_tmap_kmajor(&mk, K, rows, D, C::BN) ||
-      !make_tmap_kmajor(&mv, V, rows, D, C::BN))
-    return false;
+  AttnMaps local;
+  AttnMaps* m = maps ? maps : &local;
+  if (!m->valid || m->q != Q || m->k != K || m->v != V || m->rows != rows || m->d != D) {
+    // cached per context: the maps depend only on the buffers and on B * hk * S
+    if (!make_tmap_kmajor(&m->mq, Q, rows, D, C::BM) || !make_tmap_kmajor(&m->mk, K, rows, D, C::BN) ||
+        !make_tmap_kmajor(&m->mv, V, rows, D, C::BN)) {
+      m->valid = false;
+      return false;
+    }
+    m->q = Q;
+    m->k = K;
+    m->v = V;
+    m->rows = rows;
+    m->d = D;
+    m->valid = true;
+  }
   static std::atomic<uint64_t> attr{0};
-  if (V2) smem_attr_once(attention_tc2_kernel<D>, SMEM, attr);
-  else smem_attr_once(attention_tc_kernel<D>, SMEM, attr);
-  const int items = n * hk;
-  const int slots = 2 * num_sms();  // 2 CTAs per SM (shared memory and 256 TMEM columns each)
-  const int grid = items < slots ? items : slots;
+  smem_attr_once(attention_tc2_kernel<D>, C::SMEM, attr);
+  // persistent grid: 2 CTAs per SM (shared memory and 256 TMEM columns each), no more than the largest
+  // possible item count (B sequences x ceil(S / BM) query tiles x hk heads); CTAs without items exit
+  const int64_t max_items = (int64_t)B * ((S + C::BM - 1) / C::BM) * hk;
+  const int slots = 2 * num_sms();
+  const int grid = max_items < slots ? (int)max_items : slots;
   if (grid <= 0) return true;
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)D);
-  if (V2)
-    launch_k(attention_tc2_kernel<D>, dim3(grid), dim3(192), SMEM, st, mq, mk, mv, Cp, offsets, Opad, lp, hk, S, causal,
-             scale_log2, work);
-  else
-    launch_k(attention_tc_kernel<D>, dim3(grid), dim3(192), SMEM, st, mq, mk, mv, Cp, offsets, Opad, lp, hk, S, causal,
-             scale_log2, work);
+  launch_k(attention_tc2_kernel<D>, dim3(grid), dim3(192), C::SMEM, st, m->mq, m->mk, m->mv, Cp, offsets, Opad, lens_d,
+           work_d, hk, S, causal, scale_log2);
   return true;
 }
 
 bool launch_attention_tc(const bf16* Q, const bf16* K, const bf16* V, bf16* ctx_packed, const int* offsets,
-                         bf16* O_padded, const LensParam& lp, int B, int hk, int S, int d, int causal, cudaStream_t st,
-                         bool v2) {
-  if (d == 128)
-    return v2 ? launch_tc<128, true>(Q, K, V, ctx_packed, offsets, O_padded, lp, B, hk, S, causal, st)
-              : launch_tc<128, false>(Q, K, V, ctx_packed, offsets, O_padded, lp, B, hk, S, causal, st);
-  if (d == 64)
-    return v2 ? launch_tc<64, true>(Q, K, V, ctx_packed, offsets, O_padded, lp, B, hk, S, causal, st)
-              : launch_tc<64, false>(Q, K, V, ctx_packed, offsets, O_padded, lp, B, hk, S, causal, st);
+                         bf16* O_padded, const int* lens_d, const uint32_t* work_d, int B, int hk, int S, int d,
+                         int causal, cudaStream_t st, AttnMaps* maps) {
+  if (d == 128) return launch_tc<128>(Q, K, V, ctx_packed, offsets, O_padded, lens_d, work_d, B, hk, S, causal, st, maps);
+  if (d == 64) return launch_tc<64>(Q, K, V, ctx_packed, offsets, O_padded, lens_d, work_d, B, hk, S, causal, st, maps);
   return false;
 }
 

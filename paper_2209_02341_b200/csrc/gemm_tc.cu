@@ -47,6 +47,7 @@ __device__ __forceinline__ bf16* qkv_dst(const QkvScatter& qs, int row, int n0, 
   const int which = n0 / Hk, rem = n0 - which * Hk;
   const int head = rem / qs.d, j = rem - head * qs.d;
   const int cell = qs.pack_idx ? __ldg(qs.pack_idx + row) : row;
+  if (cell < 0) return nullptr;  // a bucket row past T: not scattered
   const int b = cell / qs.S, s = cell - b * qs.S;
   bf16* base = which == 0 ? qs.q : (which == 1 ? qs.k : qs.v);
   return base + (((int64_t)b * qs.hk + head) * qs.S + s) * qs.d + j;
@@ -191,7 +192,7 @@ __global__ void __launch_bounds__(256, 1)
           if (EPI == EPI_BIAS_QKV) dst = qkv_dst(qs, row, n0, N);
 #pragma unroll
           for (int j = 0; j < 32; j += 8) {
-            if (n0 + j < N) {
+            if (n0 + j < N && dst) {
               uint4 o;
               o.x = pack_bf16x2(v[j], v[j + 1]);
               o.y = pack_bf16x2(v[j + 2], v[j + 3]);
@@ -457,6 +458,7 @@ __device__ __forceinline__ void epi_store(float (&v)[32], int row, int n0, int M
     for (int j = 0; j < 32; ++j) v[j] = gelu_fast(v[j]);
   }
   bf16* dst = (EPI == EPI_BIAS_QKV) ? qkv_dst(qs, row, n0, N) : D + (int64_t)row * N + n0;
+  if (!dst) return;
 #pragma unroll
   for (int j = 0; j < 32; j += 8) {
     if (n0 + j < N) {

@@ -69,10 +69,27 @@ void launch_p2p_reduce_ln(const PeerSet& ps, int k, int me, int64_t off_X, int64
 void launch_p2p_push_rows(const PeerSet& ps, int k, int me, int64_t off, int row0, int rows, int64_t row_bytes,
                           uint64_t epoch, cudaStream_t st);
 
-// a1
-// tok != nullptr: range-check the ids of the valid cells, raise *err on a bad one
-void launch_index_maps(const LensParam& lp, int B, int S, int* offsets, int* pack_idx, int* pos, int* unpack_idx,
-                       const int* tok, int V, int* err, cudaStream_t st);
+// a1.  Every argument but the lengths, which travel by value (LensParam) so a replayed CUDA graph
+// updates exactly one kernel node per batch (index_maps_kernel_fn identifies it).
+struct IndexMapsArgs {
+  int B, S;
+  int rows;                    // packed rows the linears run on (>= T): pack_idx[t] = -1 for t in [T, rows)
+  int* offsets;                // [B + 1]
+  int* pack_idx;               // [rows]
+  int* pos;                    // [rows]
+  int* unpack_idx;             // [B * S]
+  const int* tok;              // [B, S] token ids to range-check (nullptr: none)
+  int V;
+  int* err_flag;               // set to 1 on a bad token id
+  int* lens_d;                 // [B] device copy of the lengths for later kernels (nullptr: none)
+  uint32_t* attn_work;         // attention work list (nullptr: none), see build_attn_work
+  int causal, attn_bm, attn_bn;
+};
+void launch_index_maps(const LensParam& lp, const IndexMapsArgs& a, cudaStream_t st);
+const void* index_maps_kernel_fn();
+// lengths -> lens_d and the attention work list only (kernel-level attention entry)
+void launch_attn_plan(const LensParam& lp, int B, int causal, int bm, int bn, int* lens_d, uint32_t* work,
+                      cudaStream_t st);
 // a2 + a3
 // rows [row0, row0 + rows) of the packed layout
 template <typename Act>
@@ -80,8 +97,8 @@ void launch_embed_ln(const int* tok, const int* pack_idx, const int* unpack_idx,
                      const Act* tok_emb, const Act* pos_emb, const float* g, const float* b, float eps, float* X, Act* A,
                      cudaStream_t st);
 template <typename Act>
-void launch_gather_ln(const float* x, const int* pack_idx, int row0, int rows, int H, const float* g, const float* b,
-                      float eps, float* X, Act* A, cudaStream_t st);
+void launch_gather_ln(const float* x, const int* pack_idx, const int* T_dev, int row0, int rows, int H, const float* g,
+                      const float* b, float eps, float* X, Act* A, cudaStream_t st);
 // a9 / a12
 template <typename Act>
 void launch_residual_ln(float* X, const Act* P, const float* bias, int rows, int H, const float* g, const float* b,
@@ -110,19 +127,31 @@ void launch_relayout(const Src* src, int64_t ld, int64_t row0, int64_t col0, int
 template <typename Src, typename Dst>
 void launch_convert_vec(const Src* src, int64_t off, int N, Dst* dst, cudaStream_t st);
 
-// a6: masked attention over the padded per-head layout [B, hk, S, d]
-// ctx_packed != nullptr fuses a7: O rows are written straight to the packed [T, hk*d] layout at
-// row offsets[b] + s (bf16 tensor-core path only; returns false if the fused form is unsupported).
+// a6: masked attention over the padded per-head layout [B, hk, S, d].  The lengths and the work list
+// live in device memory (written by the index-maps kernel / launch_attn_plan), so no attention launch
+// depends on the batch's lengths on the host.
+// Tensor maps of Q / K / V of the tcgen05 kernel (cached per context: they depend on the buffers and B*hk*S)
+struct AttnMaps {
+  CUtensorMap mq, mk, mv;
+  const void *q = nullptr, *k = nullptr, *v = nullptr;
+  int rows = 0, d = 0;
+  bool valid = false;
+};
+int attention_tile_bm();  // query rows of one work item of the tcgen05 kernel
+int attention_tile_bn();  // keys per tile (the work list's cost unit)
+// padded O [B, hk, S, d]; bf16 d = 64 / 128 runs the tcgen05 kernel (needs work_d), otherwise SIMT
 template <typename Act>
-void launch_attention(const Act* Q, const Act* K, const Act* V, Act* O, const LensParam& lp, int B, int hk, int S,
-                      int d, int causal, cudaStream_t st);
+void launch_attention(const Act* Q, const Act* K, const Act* V, Act* O, const int* lens_d, const uint32_t* work_d,
+                      int B, int hk, int S, int d, int causal, cudaStream_t st, AttnMaps* maps = nullptr);
+// a7 fused: O rows written straight to the packed [T, hk*d] layout at row offsets[b] + s (bf16, d = 64 /
+// 128 only; false if unsupported or the tensor maps cannot be built)
 bool launch_attention_packed(const bf16* Q, const bf16* K, const bf16* V, bf16* ctx_packed, const int* offsets,
-                             const LensParam& lp, int B, int hk, int S, int d, int causal, cudaStream_t st);
-// tcgen05 / TMEM attention (d = 64 or 128): packed output (ctx_packed + offsets) or padded O.
+                             const int* lens_d, const uint32_t* work_d, int B, int hk, int S, int d, int causal,
+                             cudaStream_t st, AttnMaps* maps = nullptr);
 bool launch_attention_tc(const bf16* Q, const bf16* K, const bf16* V, bf16* ctx_packed, const int* offsets,
-                         bf16* O_padded, const LensParam& lp, int B, int hk, int S, int d, int causal, cudaStream_t st,
-                         bool v2);
-int attention_impl();  // ENERGON_ATTN: 4 = tcgen05, P in TMEM (default), 3 = tcgen05 v1, 2 / 1 = mma.sync
+                         bf16* O_padded, const int* lens_d, const uint32_t* work_d, int B, int hk, int S, int d,
+                         int causal, cudaStream_t st, AttnMaps* maps);
+int attention_impl();  // ENERGON_ATTN (A/B): 4 = tcgen05 (default)
 
 // GEMM epilogues.  EPI_BIAS_QKV = bias, then a5 fused: the packed QKV row t / column block is
 // scattered straight into the padded per-head Q, K, V [B, hk, S, d] (needs d % 32 == 0).

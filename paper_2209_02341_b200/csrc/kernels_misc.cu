@@ -23,21 +23,54 @@ static inline int grid_for(int64_t work, int threads, int max_blocks) {
 // offsets = exclusive prefix sum of lens (warp-shuffle scan); for each padded cell (b, s):
 //   s < lens[b] : t = offsets[b] + s, unpack_idx[cell] = t, pack_idx[t] = cell, pos[t] = s
 //   otherwise   : unpack_idx[cell] = -1
+// and pack_idx[t] = -1 for the bucket rows t in [T, rows): the linears run on `rows` >= T packed rows
+// (T rounded up to a bucket, so that one recorded CUDA graph serves every batch of that bucket); rows
+// marked -1 are never scattered, gathered or unpacked.
 // Every CTA recomputes the (tiny, B <= 1024) scan in shared memory, so the whole step is one launch.
+// This is the only kernel of a forward that takes the lengths by value (LensParam): it publishes them
+// to lens_d for every later kernel and (CTA 0) builds the attention work list there (attn_work), so a
+// replayed graph needs exactly one kernel-node parameter update per batch.
 // tok != nullptr: the token id of every VALID cell is range-checked here (pad cells are ignored,
 // energon.h); an id outside [0, V) raises the device error flag.  Every rank of a TP group runs this
 // kernel over the whole batch, so every rank raises the same flag (the embedding gathers only its own
 // rows and never checks).
-__global__ void __launch_bounds__(256) index_maps_kernel(LensParam lp, int B, int S, int* __restrict__ offsets,
-                                                         int* __restrict__ pack_idx, int* __restrict__ pos,
-                                                         int* __restrict__ unpack_idx, const int* __restrict__ tok,
-                                                         int V, int* err_flag) {
-  pdl_trigger();
-  pdl_wait();
-  __shared__ int s_off[ENERGON_MAX_B + 1];
-  __shared__ int s_len[ENERGON_MAX_B];
-  for (int b = threadIdx.x; b < B; b += blockDim.x) s_len[b] = lp.lens[b];
+constexpr int ATTN_COST_BUCKETS = 256;
+
+// Attention work list: one item per (sequence b, query tile qt) with qt * bm < len_b, ordered heaviest
+// first by cost = key tiles of bn keys the query tile reads (causal: min(len, (qt + 1) bm)).
+// work[0] = number of items, work[1 + i] = (b << 16) | qt.  Counting sort with shared-memory atomics:
+// the order among items of equal cost is arbitrary, which cannot change any result (every item is
+// computed by one CTA on its own).  One CTA, all threads.
+__device__ void build_attn_work(const int* s_len, int B, int causal, int bm, int bn, uint32_t* __restrict__ work) {
+  __shared__ int hist[ATTN_COST_BUCKETS];
+  for (int i = threadIdx.x; i < ATTN_COST_BUCKETS; i += blockDim.x) hist[i] = 0;
   __syncthreads();
+  auto cost = [&](int b, int qt) {
+    const int len = s_len[b];
+    const int kv_end = causal ? min(len, (qt + 1) * bm) : len;
+    return min((kv_end + bn - 1) / bn, ATTN_COST_BUCKETS - 1);
+  };
+  for (int b = threadIdx.x; b < B; b += blockDim.x)
+    for (int qt = 0; qt * bm < s_len[b]; ++qt) atomicAdd(&hist[cost(b, qt)], 1);
+  __syncthreads();
+  if (threadIdx.x == 0) {  // bucket starts, heaviest bucket first (256 entries, one thread)
+    int run = 0;
+    for (int c = ATTN_COST_BUCKETS - 1; c >= 0; --c) {
+      const int n = hist[c];
+      hist[c] = run;
+      run += n;
+    }
+    work[0] = (uint32_t)run;
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < B; b += blockDim.x)
+    for (int qt = 0; qt * bm < s_len[b]; ++qt) {
+      const int pos = atomicAdd(&hist[cost(b, qt)], 1);
+      work[1 + pos] = ((uint32_t)b << 16) | (uint32_t)qt;
+    }
+}
+
+__device__ void lens_scan(const int* s_len, int B, int* s_off) {
   if (threadIdx.x < 32) {
     // each lane owns a contiguous chunk of ceil(B/32) sequences
     const int lane = threadIdx.x;
@@ -58,25 +91,56 @@ __global__ void __launch_bounds__(256) index_maps_kernel(LensParam lp, int B, in
     }
     if (lane == 31) s_off[B] = incl;
   }
+}
+
+__global__ void __launch_bounds__(256) index_maps_kernel(LensParam lp, IndexMapsArgs a) {
+  pdl_trigger();
+  pdl_wait();
+  __shared__ int s_off[ENERGON_MAX_B + 1];
+  __shared__ int s_len[ENERGON_MAX_B];
+  const int B = a.B, S = a.S;
+  for (int b = threadIdx.x; b < B; b += blockDim.x) s_len[b] = lp.lens[b];
   __syncthreads();
-  if (blockIdx.x == 0)
-    for (int b = threadIdx.x; b <= B; b += blockDim.x) offsets[b] = s_off[b];
+  lens_scan(s_len, B, s_off);
+  __syncthreads();
+  if (blockIdx.x == 0) {
+    for (int b = threadIdx.x; b <= B; b += blockDim.x) a.offsets[b] = s_off[b];
+    if (a.lens_d)
+      for (int b = threadIdx.x; b < B; b += blockDim.x) a.lens_d[b] = s_len[b];
+    if (a.attn_work) build_attn_work(s_len, B, a.causal, a.attn_bm, a.attn_bn, a.attn_work);
+  }
+  const int T = s_off[B];
+  for (int t = T + blockIdx.x * blockDim.x + threadIdx.x; t < a.rows; t += gridDim.x * blockDim.x) a.pack_idx[t] = -1;
   const int cells = B * S;
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < cells; c += gridDim.x * blockDim.x) {
     const int b = c / S, s = c - b * S;
     if (s < s_len[b]) {
       const int t = s_off[b] + s;
-      unpack_idx[c] = t;
-      pack_idx[t] = c;
-      pos[t] = s;
-      if (tok) {
-        const int id = tok[c];
-        if (id < 0 || id >= V) *err_flag = 1;
+      a.unpack_idx[c] = t;
+      a.pack_idx[t] = c;
+      a.pos[t] = s;
+      if (a.tok) {
+        const int id = a.tok[c];
+        if (id < 0 || id >= a.V) *a.err_flag = 1;
       }
     } else {
-      unpack_idx[c] = -1;
+      a.unpack_idx[c] = -1;
     }
   }
+}
+
+// Lengths + attention work list only (the kernel-level attention entry, energon_attention).
+__global__ void __launch_bounds__(256) attn_plan_kernel(LensParam lp, int B, int causal, int bm, int bn, int* lens_d,
+                                                        uint32_t* work) {
+  pdl_trigger();
+  pdl_wait();
+  __shared__ int s_len[ENERGON_MAX_B];
+  for (int b = threadIdx.x; b < B; b += blockDim.x) {
+    s_len[b] = lp.lens[b];
+    lens_d[b] = lp.lens[b];
+  }
+  __syncthreads();
+  build_attn_work(s_len, B, causal, bm, bn, work);
 }
 
 // ============================================================================ 4-wide row vectors
@@ -150,6 +214,13 @@ __global__ void __launch_bounds__(LN_THREADS) embed_ln_kernel(const int* __restr
   __shared__ float red[32];
   const int t = row0 + blockIdx.x;
   const int cell = pack_idx ? pack_idx[t] : t;
+  if (cell < 0) {  // a bucket row past T (index_maps_kernel): zero, never read by a valid row
+    for (int c = threadIdx.x; c < H / 4; c += LN_THREADS) {
+      Row4<float>::store(X + (int64_t)t * H + 4 * c, make_float4(0.f, 0.f, 0.f, 0.f));
+      Row4<Act>::store(A + (int64_t)t * H + 4 * c, make_float4(0.f, 0.f, 0.f, 0.f));
+    }
+    return;
+  }
   const int s = cell % S;
   int id = (pack_idx || unpack_idx[cell] >= 0) ? tok[cell] : 0;
   if (id < 0 || id >= V) id = 0;
@@ -177,17 +248,26 @@ __global__ void __launch_bounds__(LN_THREADS) embed_ln_kernel(const int* __restr
   }
 }
 
-// Hidden-state entry (energon_forward_hidden): X[t] = x[cell] (fp32), A[t] = LN1(X[t]).
+// Hidden-state entry (energon_forward_hidden / a later pipeline stage): X[t] = x[cell] (fp32),
+// A[t] = LN1(X[t]).  pack_idx == nullptr: x is already packed, [n_valid, H] with n_valid = *T_dev
+// (offsets[B]); bucket rows past T are zeroed.
 template <typename Act, int LN_MAXV>
 __global__ void __launch_bounds__(LN_THREADS) gather_ln_kernel(const float* __restrict__ x, const int* __restrict__ pack_idx,
-                                                               int row0, int H, const float* __restrict__ g,
-                                                               const float* __restrict__ b, float eps, float* __restrict__ X,
-                                                               Act* __restrict__ A) {
+                                                               const int* __restrict__ T_dev, int row0, int H,
+                                                               const float* __restrict__ g, const float* __restrict__ b,
+                                                               float eps, float* __restrict__ X, Act* __restrict__ A) {
   pdl_trigger();
   pdl_wait();
   __shared__ float red[32];
   const int t = row0 + blockIdx.x;
-  const int cell = pack_idx ? pack_idx[t] : t;
+  const int cell = pack_idx ? pack_idx[t] : (t < *T_dev ? t : -1);
+  if (cell < 0) {
+    for (int c = threadIdx.x; c < H / 4; c += LN_THREADS) {
+      Row4<float>::store(X + (int64_t)t * H + 4 * c, make_float4(0.f, 0.f, 0.f, 0.f));
+      Row4<Act>::store(A + (int64_t)t * H + 4 * c, make_float4(0.f, 0.f, 0.f, 0.f));
+    }
+    return;
+  }
   float4 v[LN_MAXV];
   int nv = 0;
 #pragma unroll
@@ -320,6 +400,7 @@ __global__ void unpack_qkv_kernel(const Act* __restrict__ QKV, const int* __rest
     const int rem = col - which * Hk;
     const int head = rem / d, j = rem - head * d;
     const int cell = pack_idx ? pack_idx[t] : t;
+    if (cell < 0) continue;  // bucket row past T
     const int b = cell / S, s = cell - b * S;
     Act* dst = (which == 0 ? Q : (which == 1 ? K : Vv)) + (((int64_t)b * hk + head) * S + s) * d + j;
     *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(QKV + (int64_t)t * 3 * Hk + col);
@@ -345,7 +426,7 @@ __global__ void repack_kernel(const Act* __restrict__ O, const int* __restrict__
     const int cell = pack_idx ? pack_idx[t] : t;
     const int b = cell / S, s = cell - b * S;
     uint4 v = make_uint4(0, 0, 0, 0);
-    if (pack_idx || unpack_idx[cell] >= 0)
+    if (pack_idx ? cell >= 0 : unpack_idx[cell] >= 0)
       v = *reinterpret_cast<const uint4*>(O + (((int64_t)b * hk + head) * S + s) * d + j);
     *reinterpret_cast<uint4*>(C + (int64_t)t * Hk + col) = v;
   }
@@ -480,11 +561,16 @@ __global__ void convert_vec_kernel(const Src* __restrict__ src, int64_t off, int
 
 // ============================================================================ host launchers
 
-void launch_index_maps(const LensParam& lp, int B, int S, int* offsets, int* pack_idx, int* pos, int* unpack_idx,
-                       const int* tok, int V, int* err, cudaStream_t st) {
-  const int cells = B * S;
-  launch_k(index_maps_kernel, dim3(grid_for(cells, 256, 148 * 4)), dim3(256), 0, st, lp, B, S, offsets, pack_idx, pos,
-           unpack_idx, tok, V, err);
+void launch_index_maps(const LensParam& lp, const IndexMapsArgs& a, cudaStream_t st) {
+  const int cells = a.B * a.S > a.rows ? a.B * a.S : a.rows;
+  launch_k(index_maps_kernel, dim3(grid_for(cells, 256, 148 * 4)), dim3(256), 0, st, lp, a);
+}
+
+const void* index_maps_kernel_fn() { return reinterpret_cast<const void*>(&index_maps_kernel); }
+
+void launch_attn_plan(const LensParam& lp, int B, int causal, int bm, int bn, int* lens_d, uint32_t* work,
+                      cudaStream_t st) {
+  launch_k(attn_plan_kernel, dim3(1), dim3(256), 0, st, lp, B, causal, bm, bn, lens_d, work);
 }
 
 #define NV_DISPATCH(H, KERNEL_CALL)                                         \
@@ -513,10 +599,11 @@ void launch_embed_ln(const int* tok, const int* pack_idx, const int* unpack_idx,
 }
 
 template <typename Act>
-void launch_gather_ln(const float* x, const int* pack_idx, int row0, int rows, int H, const float* g, const float* b,
-                      float eps, float* X, Act* A, cudaStream_t st) {
+void launch_gather_ln(const float* x, const int* pack_idx, const int* T_dev, int row0, int rows, int H, const float* g,
+                      const float* b, float eps, float* X, Act* A, cudaStream_t st) {
   if (rows > 0)
-    NV_DISPATCH(H, (launch_k(gather_ln_kernel<Act, NVX>, dim3(rows), dim3(LN_THREADS), 0, st, x, pack_idx, row0, H, g, b, eps, X, A)))
+    NV_DISPATCH(H, (launch_k(gather_ln_kernel<Act, NVX>, dim3(rows), dim3(LN_THREADS), 0, st, x, pack_idx, T_dev, row0, H,
+                             g, b, eps, X, A)))
 }
 
 #define NV_DISPATCH_T(H, TPRV, KERNEL_CALL)                                 \
@@ -788,8 +875,8 @@ template void launch_p2p_reduce_ln<bf16>(const PeerSet&, int, int, int64_t, int6
 #define INST_ACT(Act)                                                                                                   \
   template void launch_embed_ln<Act>(const int*, const int*, const int*, int, int, int, int, int, const Act*,           \
                                      const Act*, const float*, const float*, float, float*, Act*, cudaStream_t);        \
-  template void launch_gather_ln<Act>(const float*, const int*, int, int, int, const float*, const float*, float,        \
-                                      float*, Act*, cudaStream_t);                                                      \
+  template void launch_gather_ln<Act>(const float*, const int*, const int*, int, int, int, const float*, const float*,  \
+                                      float, float*, Act*, cudaStream_t);                                               \
   template void launch_local_reduce_scatter<Act>(const PtrList&, int, int64_t, int, cudaStream_t);                     \
   template void launch_residual_ln<Act>(float*, const Act*, const float*, int, int, const float*, const float*, float,   \
                                         Act*, cudaStream_t);                                                            \

@@ -95,7 +95,11 @@ struct energon_ctx {
   // CUDA-graph cache (ENERGON_OPT_GRAPH): whole forwards captured on cap_stream, replayed on the caller's
   struct GraphEntry {
     std::vector<int64_t> key;
+    cudaGraph_t graph = nullptr;       // kept: its index-maps nodes are updated in `exec` on every replay
     cudaGraphExec_t exec = nullptr;
+    std::vector<cudaGraphNode_t> imap_node;  // per context of the group: its index-maps kernel node
+    std::vector<cudaKernelNodeParams> imap_kp;
+    std::vector<IndexMapsArgs> imap_args;
     std::vector<energon_stats> delta;  // per context of the group: stats one forward adds
     uint64_t last_use = 0;
   };
@@ -111,6 +115,11 @@ struct energon_ctx {
   std::vector<LayerDev> layers;
   // workspace (sized from max_tokens padded rows)
   int *offsets = nullptr, *pack_idx = nullptr, *pos = nullptr, *unpack_idx = nullptr;
+  int* lens_d = nullptr;           // [ENERGON_MAX_BATCH] this forward's lengths (written by the index-maps kernel)
+  uint32_t* attn_work = nullptr;   // attention work list (build_attn_work)
+  AttnMaps amaps;                  // cached Q / K / V tensor maps of the attention kernel
+  IndexMapsArgs last_imap{};       // arguments of this context's last index-maps launch (graph parameter updates)
+  double work_rows = 0;            // rows of algorithmic work (T with DRCE) for the profile's GEMM flops
   float* X = nullptr;
   void *A = nullptr, *QKV = nullptr, *Q = nullptr, *K = nullptr, *Vb = nullptr, *O = nullptr, *Ctx = nullptr,
        *P = nullptr, *G = nullptr;
@@ -248,6 +257,8 @@ energon_status setup(energon_ctx* c) {
   if ((s = dalloc(c, &c->offsets, sizeof(int) * (ENERGON_MAX_BATCH + 1), ws)) ||
       (s = dalloc(c, &c->pack_idx, sizeof(int) * R, ws)) || (s = dalloc(c, &c->pos, sizeof(int) * R, ws)) ||
       (s = dalloc(c, &c->unpack_idx, sizeof(int) * R, ws)) || (s = dalloc(c, &c->QKV, a * R * 3 * c->Hk, ws)) ||
+      (s = dalloc(c, &c->lens_d, sizeof(int) * ENERGON_MAX_BATCH, ws)) ||
+      (s = dalloc(c, &c->attn_work, sizeof(uint32_t) * (2 + ENERGON_MAX_BATCH + R / 64), ws)) ||
       (s = dalloc(c, &c->Q, a * R * c->Hk, ws)) || (s = dalloc(c, &c->K, a * R * c->Hk, ws)) ||
       (s = dalloc(c, &c->Vb, a * R * c->Hk, ws)) || (s = dalloc(c, &c->O, a * R * c->Hk, ws)) ||
       (s = dalloc(c, &c->Ctx, a * R * c->Hk, ws)) || (s = dalloc(c, &c->G, a * R * c->Fk, ws)))
@@ -287,8 +298,10 @@ void release(energon_ctx* c) {
   if (c->pm.copy) cudaStreamDestroy(c->pm.copy);
   if (c->err_host) cudaFreeHost(c->err_host);
   if (c->load_stream) cudaStreamDestroy(c->load_stream);
-  for (auto& g : c->gcache)
+  for (auto& g : c->gcache) {
     if (g.exec) cudaGraphExecDestroy(g.exec);
+    if (g.graph) cudaGraphDestroy(g.graph);
+  }
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   for (cudaEvent_t e : c->pool) cudaEventDestroy(e);
   if (c->nccl) ncclCommDestroy(c->nccl);
@@ -563,7 +576,7 @@ template <typename Act>
 void gemm(energon_ctx* c, const CUtensorMap& tmA, const CUtensorMap* tmB, const void* A, const void* W,
           const float* bias, void* D, int M, int N, int K, int epi, cudaStream_t st, const QkvScatter* qs = nullptr,
           const CUtensorMap* tmD = nullptr, const ShardStore* shard = nullptr) {
-  Prof p(c, st, P_GEMM, 2.0 * M * N * K);
+  Prof p(c, st, P_GEMM, 2.0 * c->work_rows * N * K);  // algorithmic: the valid rows only
   if constexpr (sizeof(Act) == 2) {
     const int code = tc_pick_bn(M, N);
     if (!launch_gemm_tc(tmA, tmB[box_slot(tc_w_box(code))], code, bias, reinterpret_cast<bf16*>(D), M, N, K, epi, st,
@@ -592,13 +605,21 @@ void pmep_fetch(energon_ctx* c, int j, int layer) {
   c->stats.prefetch_bytes += (int64_t)pm.bytes;
 }
 
+int bucket_rows(const energon_ctx* c, int64_t T) {
+  const int64_t b = (T + 127) / 128 * 128;
+  return (int)std::min<int64_t>(b, std::max<int64_t>(T, c->cfg.max_tokens));
+}
+
 template <typename Act>
 energon_status forward_t(energon_ctx** cs, int n, const Call& a, int64_t T) {
   cudaStream_t st = a.st;
   energon_ctx* c0 = cs[0];
   const energon_config& g = c0->cfg;
   const bool drce = g.drce == 1;
-  const int rows = drce ? (int)T : a.B * a.S;
+  // DRCE: the linears run on T packed rows rounded up to a bucket of 128 (<= max_tokens), so that one
+  // recorded CUDA graph serves every batch of the bucket (the bucket rows past T are marked -1 in
+  // pack_idx and carry zeros / finite values nobody reads); a 256-row GEMM tile count never changes
+  const int rows = drce ? bucket_rows(c0, T) : a.B * a.S;
   const float eps = g.ln_eps;
   const double act = (double)sizeof(Act), H = c0->H, Hk = c0->Hk;
   // Fused forms of the paper's two layout kernels on the bf16 tensor-core path:
@@ -649,9 +670,13 @@ energon_status forward_t(energon_ctx** cs, int n, const Call& a, int64_t T) {
     energon_ctx* c = cs[i];
     c->stats.last_tokens = T;
     c->stats.last_rows = rows;
+    c->work_rows = drce ? (double)T : (double)rows;
     {
       Prof p(c, st, P_MEM, 4.0 * (a.B + 1) + 8.0 * T + 4.0 * a.B * a.S);
-      launch_index_maps(lp, a.B, a.S, c->offsets, c->pack_idx, c->pos, c->unpack_idx, a.tokens, c->V, c->err_dev, st);
+      IndexMapsArgs ia{a.B, a.S, drce ? rows : (int)T, c->offsets, c->pack_idx, c->pos, c->unpack_idx, a.tokens, c->V,
+                       c->err_dev, c->lens_d, c->attn_work, g.causal, attention_tile_bm(), attention_tile_bn()};
+      launch_index_maps(lp, ia, st);
+      c->last_imap = ia;
     }
     c->stats.kernel_launches++;
     if (sizeof(Act) == 2 && c->tm_rows != rows) {
@@ -675,7 +700,7 @@ energon_status forward_t(energon_ctx** cs, int n, const Call& a, int64_t T) {
                              reinterpret_cast<const Act*>(c->tok_emb), reinterpret_cast<const Act*>(c->pos_emb), g1, b1,
                              eps, c->X, reinterpret_cast<Act*>(c->A), st);
       else
-        launch_gather_ln<Act>(a.x_in, a.x_packed ? nullptr : pidx, r0, sn, c->H, g1, b1, eps, c->X,
+        launch_gather_ln<Act>(a.x_in, a.x_packed ? nullptr : pidx, c->offsets + a.B, r0, sn, c->H, g1, b1, eps, c->X,
                               reinterpret_cast<Act*>(c->A), st);
     }
     c->stats.kernel_launches++;
@@ -717,15 +742,15 @@ energon_status forward_t(energon_ctx** cs, int n, const Call& a, int64_t T) {
         Prof p(c, st, P_ATTN, 4.0 * c->d * allowed * c->hk);
         if (!launch_attention_packed(reinterpret_cast<const bf16*>(c->Q), reinterpret_cast<const bf16*>(c->K),
                                      reinterpret_cast<const bf16*>(c->Vb), reinterpret_cast<bf16*>(c->Ctx), c->offsets,
-                                     lp, a.B, c->hk, a.S, c->d, g.causal, st))
+                                     c->lens_d, c->attn_work, a.B, c->hk, a.S, c->d, g.causal, st, &c->amaps))
           c->launch_err = "attention launch refused: tensor maps could not be built";
         c->stats.kernel_launches++;
       } else {
         {
           Prof p(c, st, P_ATTN, 4.0 * c->d * allowed * c->hk);
           launch_attention<Act>(reinterpret_cast<const Act*>(c->Q), reinterpret_cast<const Act*>(c->K),
-                                reinterpret_cast<const Act*>(c->Vb), reinterpret_cast<Act*>(c->O), lp, a.B, c->hk, a.S,
-                                c->d, g.causal, st);
+                                reinterpret_cast<const Act*>(c->Vb), reinterpret_cast<Act*>(c->O), c->lens_d,
+                                c->attn_work, a.B, c->hk, a.S, c->d, g.causal, st, &c->amaps);
         }
         {
           Prof p(c, st, P_MEM, 2.0 * rows * Hk * act);
@@ -809,9 +834,11 @@ energon_status forward_t(energon_ctx** cs, int n, const Call& a, int64_t T) {
     }
   energon_ctx* c = cs[0];
   if (a.out_packed) {
-    // pipeline stage output: the residual stream rows go to the next stage as they are
-    Prof p(c, st, P_MEM, 8.0 * rows * H);
-    cudaError_t e = cudaMemcpyAsync(a.out, c->X, sizeof(float) * (size_t)rows * c->H, cudaMemcpyDeviceToDevice, st);
+    // pipeline stage output: the residual stream rows go to the next stage as they are (the T valid
+    // rows with DRCE; a graph of a stage is keyed on T, see run())
+    const int64_t out_rows = drce ? T : rows;
+    Prof p(c, st, P_MEM, 8.0 * out_rows * H);
+    cudaError_t e = cudaMemcpyAsync(a.out, c->X, sizeof(float) * (size_t)out_rows * c->H, cudaMemcpyDeviceToDevice, st);
     if (e != cudaSuccess) return cuda_fail(c0, e, "stage output copy");
     e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(c0, e, "kernel launch");
@@ -863,21 +890,35 @@ energon_status run(energon_ctx** cs, int n, const Call& a) {
   for (int i = 0; i < n; ++i) graph_ok = graph_ok && !cs[i]->prof && cs[i]->pm.layers.empty() && !cs[i]->p2p;
   if (!graph_ok) return run_eager(cs, n, a, T);
 
-  // ---- CUDA graph: key = everything the launch sequence depends on
+  // ---- CUDA graph: key = everything the launch sequence depends on.  Not the lengths: they reach the
+  // device through the index-maps kernel's by-value parameter only (updated in the instantiated graph
+  // before every replay), and every other launch depends on the batch only through the row bucket.
+  const int rows = c0->cfg.drce ? bucket_rows(c0, T) : a.B * a.S;
   std::vector<int64_t> key = {n, (int64_t)(uintptr_t)a.tokens, (int64_t)(uintptr_t)a.x_in, (int64_t)(uintptr_t)a.out,
                               a.B, a.S, a.l0, a.l1, a.final_ln, a.out_f32, c0->cfg.drce, c0->sp, c0->fuse, c0->ring,
-                              a.x_packed, a.out_packed};
+                              a.x_packed, a.out_packed, rows};
   for (int i = 0; i < n; ++i) key.push_back((int64_t)(uintptr_t)cs[i]);
-  for (int b = 0; b < a.B; ++b) key.push_back(a.lens[b]);
+  if (a.x_packed || a.out_packed) key.push_back(T);  // a pipeline stage copies exactly T rows in or out
+  LensParam lp;
+  for (int b = 0; b < a.B; ++b) lp.lens[b] = a.lens[b];
   for (auto& g : c0->gcache)
     if (g.key == key) {
       g.last_use = ++c0->gclock;
+      for (size_t i = 0; i < g.imap_node.size(); ++i) {
+        IndexMapsArgs ia = g.imap_args[i];
+        void* args[2] = {&lp, &ia};
+        cudaKernelNodeParams kp = g.imap_kp[i];
+        kp.kernelParams = args;
+        kp.extra = nullptr;
+        e = cudaGraphExecKernelNodeSetParams(g.exec, g.imap_node[i], &kp);
+        if (e != cudaSuccess) return cuda_fail(c0, e, "cudaGraphExecKernelNodeSetParams (index maps)");
+      }
       e = cudaGraphLaunch(g.exec, a.st);
       if (e != cudaSuccess) return cuda_fail(c0, e, "cudaGraphLaunch");
       for (int i = 0; i < n; ++i) {
         stats_add(cs[i]->stats, g.delta[i]);
         cs[i]->stats.last_tokens = T;
-        cs[i]->stats.last_rows = c0->cfg.drce ? T : (int64_t)a.B * a.S;
+        cs[i]->stats.last_rows = rows;
       }
       return ENERGON_OK;
     }
@@ -903,9 +944,43 @@ energon_status run(energon_ctx** cs, int n, const Call& a) {
   }
   energon_ctx::GraphEntry ent;
   ent.key = key;
+  // the index-maps kernel node of every context (matched by its offsets pointer): the one node whose
+  // parameters change from batch to batch
+  {
+    size_t nn = 0;
+    cudaGraphGetNodes(graph, nullptr, &nn);
+    std::vector<cudaGraphNode_t> nodes(nn);
+    if (nn) cudaGraphGetNodes(graph, nodes.data(), &nn);
+    ent.imap_node.assign(n, nullptr);
+    ent.imap_kp.resize(n);
+    ent.imap_args.resize(n);
+    for (cudaGraphNode_t nd : nodes) {
+      cudaGraphNodeType ty;
+      if (cudaGraphNodeGetType(nd, &ty) != cudaSuccess || ty != cudaGraphNodeTypeKernel) continue;
+      cudaKernelNodeParams kp;
+      if (cudaGraphKernelNodeGetParams(nd, &kp) != cudaSuccess || kp.func != index_maps_kernel_fn()) continue;
+      const IndexMapsArgs* ia = static_cast<const IndexMapsArgs*>(kp.kernelParams[1]);
+      for (int i = 0; i < n; ++i)
+        if (ia->offsets == cs[i]->offsets) {
+          ent.imap_node[i] = nd;
+          ent.imap_kp[i] = kp;
+          ent.imap_args[i] = *ia;
+        }
+    }
+    cudaGetLastError();
+    for (int i = 0; i < n; ++i)
+      if (!ent.imap_node[i]) {
+        cudaGraphDestroy(graph);
+        return fail(c0, ENERGON_ERR_CUDA, "CUDA graph: index-maps kernel node not found");
+      }
+  }
   e = cudaGraphInstantiate(&ent.exec, graph, 0);
-  cudaGraphDestroy(graph);
-  if (e != cudaSuccess) return cuda_fail(c0, e, "cudaGraphInstantiate");
+  if (e != cudaSuccess) {
+    cudaGraphDestroy(graph);
+    return cuda_fail(c0, e, "cudaGraphInstantiate");
+  }
+  ent.graph = graph;
+  c0->stats.graphs_recorded++;
   for (int i = 0; i < n; ++i) {
     energon_stats d = after[i];
     d.forwards -= before[i].forwards;
@@ -921,6 +996,7 @@ energon_status run(energon_ctx** cs, int n, const Call& a) {
     for (size_t i = 1; i < c0->gcache.size(); ++i)
       if (c0->gcache[i].last_use < c0->gcache[v].last_use) v = i;
     cudaGraphExecDestroy(c0->gcache[v].exec);
+    cudaGraphDestroy(c0->gcache[v].graph);
     c0->gcache.erase(c0->gcache.begin() + v);
   }
   c0->gcache.push_back(ent);
@@ -1491,7 +1567,10 @@ energon_status energon_index_maps(const int32_t* lens, int32_t B, int32_t S, int
     if (lens[b] < 1 || lens[b] > S) return fail(nullptr, ENERGON_ERR_LENGTH, "seq_lens not in [1, max_len]");
     lp.lens[b] = lens[b];
   }
-  launch_index_maps(lp, B, S, offsets, pack_idx, pos, unpack_idx, nullptr, 0, nullptr, (cudaStream_t)stream);
+  int64_t T = 0;
+  for (int b = 0; b < B; ++b) T += lens[b];
+  IndexMapsArgs ia{B, S, (int)T, offsets, pack_idx, pos, unpack_idx, nullptr, 0, nullptr, nullptr, nullptr, 1, 128, 64};
+  launch_index_maps(lp, ia, (cudaStream_t)stream);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(nullptr, e, "index_maps");
   return ENERGON_OK;
@@ -1508,17 +1587,26 @@ energon_status energon_attention(int32_t dtype, const void* Q, const void* K, co
     if (lens[b] < 1 || lens[b] > S) return fail(nullptr, ENERGON_ERR_LENGTH, "seq_lens not in [1, max_len]");
     lp.lens[b] = lens[b];
   }
+  if (dtype != ENERGON_DTYPE_F32 && dtype != ENERGON_DTYPE_BF16) return fail(nullptr, ENERGON_ERR_ARG, "dtype must be F32 or BF16");
+  // stream-ordered scratch for the device lengths + work list (the forward path keeps them in the context)
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t n_work = 2 + (size_t)B * ((S + 63) / 64);
+  void* scratch = nullptr;
+  cudaError_t e = cudaMallocAsync(&scratch, sizeof(int) * ENERGON_MAX_BATCH + sizeof(uint32_t) * n_work, st);
+  if (e != cudaSuccess) return cuda_fail(nullptr, e, "cudaMallocAsync");
+  int* lens_d = static_cast<int*>(scratch);
+  uint32_t* work_d = reinterpret_cast<uint32_t*>(lens_d + ENERGON_MAX_BATCH);
+  launch_attn_plan(lp, B, causal, attention_tile_bm(), attention_tile_bn(), lens_d, work_d, st);
   if (dtype == ENERGON_DTYPE_F32)
     launch_attention<float>(reinterpret_cast<const float*>(Q), reinterpret_cast<const float*>(K),
-                            reinterpret_cast<const float*>(V), reinterpret_cast<float*>(O), lp, B, hk, S, d, causal,
-                            (cudaStream_t)stream);
-  else if (dtype == ENERGON_DTYPE_BF16)
-    launch_attention<bf16>(reinterpret_cast<const bf16*>(Q), reinterpret_cast<const bf16*>(K),
-                           reinterpret_cast<const bf16*>(V), reinterpret_cast<bf16*>(O), lp, B, hk, S, d, causal,
-                           (cudaStream_t)stream);
+                            reinterpret_cast<const float*>(V), reinterpret_cast<float*>(O), lens_d, work_d, B, hk, S, d,
+                            causal, st);
   else
-    return fail(nullptr, ENERGON_ERR_ARG, "dtype must be F32 or BF16");
-  cudaError_t e = cudaGetLastError();
+    launch_attention<bf16>(reinterpret_cast<const bf16*>(Q), reinterpret_cast<const bf16*>(K),
+                           reinterpret_cast<const bf16*>(V), reinterpret_cast<bf16*>(O), lens_d, work_d, B, hk, S, d,
+                           causal, st);
+  e = cudaGetLastError();
+  cudaFreeAsync(scratch, st);
   if (e != cudaSuccess) return cuda_fail(nullptr, e, "attention");
   return ENERGON_OK;
 }

@@ -61,7 +61,7 @@ class Shard(ctypes.Structure):
 class Stats(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int64) for n in ("forwards", "allreduce_calls", "kernel_launches", "last_tokens",
                                               "last_rows", "weight_bytes", "workspace_bytes", "prefetch_bytes",
-                                              "fused_exchanges")]
+                                              "fused_exchanges", "graphs_recorded")]
 
 
 class Profile(ctypes.Structure):

@@ -580,20 +580,31 @@ def test_pmep_offload_bitexact(slots, pool, dtype):
 # ----------------------------------------------------------------------------- CUDA graphs
 @pytest.mark.parametrize("k", [1, 2])
 def test_cuda_graph_replay_bitexact(k):
-    """ENERGON_OPT_GRAPH: a replayed graph gives the eager bits, reads the current contents of the
-    token buffer, and a new length vector records a new graph."""
+    """ENERGON_OPT_GRAPH: a replayed graph gives the eager bits and reads the current contents of the
+    token buffer; a graph is keyed on the row bucket (T rounded up to 128), not on the lengths -- a new
+    length vector of the same bucket (here: the batch's lengths permuted, and a different mix with the
+    same T) replays the recorded graph with its lengths written into the index-maps node, a new bucket
+    records a new graph."""
     shape = dict(SHAPES["gpt2s"], L=2)
     B, S, seed = 8, 96, 6
     lens = synth.random_lengths(B, S, seed)
-    lens2 = synth.random_lengths(B, S, seed + 1)
-    tok1 = torch.from_numpy(synth.tokens(B, S, shape["V"], lens, seed)).cuda()
-    tok2 = torch.from_numpy(synth.tokens(B, S, shape["V"], lens, seed + 5)).cuda()
+    lens_perm = lens[::-1]
+    lens_mix = list(lens)
+    i_hi, i_lo = int(np.argmax(lens)), int(np.argmin(lens))
+    shift = min(lens[i_hi] - 1, S - lens[i_lo], 9)
+    lens_mix[i_hi] -= shift
+    lens_mix[i_lo] += shift  # same T, different mix
+    lens2 = [min(S, x + 40) for x in lens]  # another bucket
+    assert (sum(lens2) + 127) // 128 != (sum(lens) + 127) // 128
+    tok1 = torch.from_numpy(synth.tokens(B, S, shape["V"], lens2, seed)).cuda()
+    tok2 = torch.from_numpy(synth.tokens(B, S, shape["V"], lens2, seed + 5)).cuda()
     ctxs = make_engine(shape, seed, "bf16", B * S, k=k)
     tok = torch.empty_like(tok1)
     out = torch.empty(B, S, shape["H"], dtype=torch.bfloat16, device="cuda")
 
     def fwd(t, ln):
         tok.copy_(t)
+        out.fill_(float("nan"))
         if k == 1:
             E().energon_forward(ctxs[0], tok, ln, out)
         else:
@@ -602,14 +613,19 @@ def test_cuda_graph_replay_bitexact(k):
         return out.clone()
 
     try:
-        eager = [fwd(tok1, lens), fwd(tok2, lens), fwd(tok1, lens2)]
+        cases = [(tok1, lens), (tok2, lens), (tok1, lens_perm), (tok2, lens_mix), (tok1, lens2)]
+        eager = [fwd(t, ln) for t, ln in cases]
         for c in ctxs:
             E().energon_set_option(c, E().OPT_GRAPH, 1)
-        graphed = [fwd(tok1, lens), fwd(tok1, lens), fwd(tok2, lens), fwd(tok1, lens2), fwd(tok1, lens2)]
+        rec = []
+        graphed = []
+        for t, ln in cases + cases:
+            graphed.append(fwd(t, ln))
+            rec.append(E().energon_get_stats(ctxs[0])["graphs_recorded"])
         st = E().energon_get_stats(ctxs[0])
     finally:
         destroy(ctxs)
-    assert torch.equal(graphed[0], eager[0]) and torch.equal(graphed[1], eager[0])
-    assert torch.equal(graphed[2], eager[1])  # replay reads the new token contents
-    assert torch.equal(graphed[3], eager[2]) and torch.equal(graphed[4], eager[2])
-    assert st["forwards"] == 8
+    for i, g in enumerate(graphed):
+        assert torch.equal(g, eager[i % len(cases)]), i
+    assert rec == [1, 1, 1, 1, 2] + [2] * 5  # one graph per bucket, recorded on its first batch
+    assert st["forwards"] == 15
