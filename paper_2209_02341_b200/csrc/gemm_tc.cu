@@ -306,22 +306,30 @@ __device__ __forceinline__ void raster(int tile, int num_m, int num_n, int group
   n_blk = r / gsize;
 }
 
-// Work decomposition of the pair kernel.  Tiles [0, full) are whole-K units handed out round-robin
-// (data parallel).  When the last wave would leave clusters idle, the k-iterations of the `rem` tail
-// tiles are spread evenly over the clusters instead ("stream-K tail"): cluster c runs the contiguous
-// iteration range [c L, (c + 1) L) of the tail's rem * nkb iterations, which may cover the end of one
-// tile and the start of the next.  A piece that is not a whole tile writes its fp32 partial to
-// workspace slot (c + tail) -- unique, at most clusters + rem slots -- in a coalesced [col/4][row][4]
-// layout; the last piece of a tile to arrive (per tile and CTA, counted in `counters`, which self-reset)
-// sums the tile's pieces in cluster order (deterministic) and runs the epilogue.
+// Work decomposition of the pair kernel (data parallel + stream-K with accumulator preload).
+// Tiles [0, full) are whole-K units handed out round-robin (data parallel).  When the tile count does
+// not fill the clusters' last round evenly, the last R tiles (one full round plus the remainder) are
+// processed stream-K: cluster c runs the contiguous iteration range [c L, (c + 1) L) of the R * nkb
+// iterations (L = ceil(R nkb / clusters) >= nkb, so a tile spans at most two clusters), walking each
+// tile's k-blocks in REVERSE iteration order.  A tile split between clusters c and c + 1 then has
+//   an EARLY piece  -- cluster c+1's first stream-K unit, the tile's low k-blocks [0, k): its fp32
+//                      accumulator goes to workspace slot c + 1 and flag (c + 1, CTA) is raised;
+//   a FINISHER piece -- cluster c's last unit, the high k-blocks [k, nkb): before its first MMA the
+//                      epilogue warps copy slot c + 1 into the TMEM accumulator (tcgen05.st), the MMAs
+//                      accumulate on top of it, and the normal epilogue writes the tile.
+// The early piece runs first in time (its cluster's first stream-K unit vs the finisher's cluster's
+// last), so the finisher practically never waits, and the preload happens while the finisher's
+// previous unit is still in the tensor pipe: no fix-up pass.  The accumulation order of a split tile
+// (low k-blocks, then high ones, one fp32 accumulator) is that of the unsplit tile: the output is
+// bit-identical to the data-parallel schedule.  Flags self-reset (the finisher clears its slot's flag).
 struct TailPlan {
-  int full;       // whole tiles (all tiles when L == 0)
-  int L;          // tail k-iterations per cluster (0: no stream-K tail)
-  int rem;        // tail tiles
-  float* ws;      // [slots][2][BN / 4][128][4] fp32 partials
-  int* counters;  // [rem][2]
+  int full;     // data-parallel tiles
+  int L;        // stream-K iterations per cluster (0: no stream-K)
+  int R;        // stream-K tiles [full, full + R)
+  float* ws;    // [clusters][2][BN / 4][128][4] fp32 partial accumulators of the early pieces
+  int* flags;   // [clusters][2] 1 = slot published
 };
-
+enum { UNIT_WHOLE = 0, UNIT_EARLY = 1, UNIT_FINISH = 2 };
 // Diagnostics (ENERGON_GEMM_TRACE=<file>): per-unit timestamps of the pair kernel (leader CTA) -- MMA
 // issuer: accumulator acquired, first stage full, last MMA issued; epilogue: accumulator full, unit
 // done (stores / fix-up issued) -- in %globaltimer ns, appended to the file after every launch (the
@@ -338,28 +346,27 @@ struct WorkIter {
   __device__ __forceinline__ WorkIter(int cid, const TailPlan& tp, int nkb) : u(cid), it(0), it_end(0) {
     if (tp.L > 0) {
       it = cid * tp.L;
-      it_end = min(it + tp.L, tp.rem * nkb);
+      it_end = min(it + tp.L, tp.R * nkb);
     }
   }
-  // next unit of this cluster: tile, k-block range, split index within the tile (-1: whole tile), tail
-  __device__ __forceinline__ bool next(const TailPlan& tp, int nkb, int ncl, int& tile, int& kb0, int& kb1, int& split,
-                                       int& tail) {
+  // next unit of this cluster: tile, k-block range [kb0, kb1), kind (UNIT_*)
+  __device__ __forceinline__ bool next(const TailPlan& tp, int nkb, int ncl, int& tile, int& kb0, int& kb1, int& kind) {
     if (u < tp.full) {
       tile = u;
       kb0 = 0;
       kb1 = nkb;
-      split = -1;
-      tail = -1;
+      kind = UNIT_WHOLE;
       u += ncl;
       return true;
     }
     if (it >= it_end) return false;
-    tail = it / nkb;
-    kb0 = it - tail * nkb;
-    kb1 = min(nkb, kb0 + (it_end - it));
-    tile = tp.full + tail;
-    split = (kb0 == 0 && kb1 == nkb) ? -1 : (it / tp.L) - (tail * nkb) / tp.L;
-    it += kb1 - kb0;
+    const int tl = it / nkb, jk = it - tl * nkb;
+    const int jend = min(it_end - tl * nkb, nkb);  // exclusive, iteration index within the tile
+    tile = tp.full + tl;
+    kb0 = nkb - jend;  // reversed k order: iterations [jk, jend) <-> k-blocks [nkb - jend, nkb - jk)
+    kb1 = nkb - jk;
+    kind = (jk == 0 && jend == nkb) ? UNIT_WHOLE : (jk != 0 ? UNIT_EARLY : UNIT_FINISH);
+    it += jend - jk;
     return true;
   }
 };
@@ -491,8 +498,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
-  int* fix_flag = reinterpret_cast<int*>(tmem_holder + 1);
+  uint64_t* pre_full = tempty + 2;  // the finisher unit's accumulator holds the early piece's partial
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(pre_full + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
@@ -512,6 +519,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], 2 * C::EPI_WARPS);  // epilogue warps x 2 CTAs
     }
+    mbar_init(pre_full, 2 * C::EPI_WARPS);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
@@ -536,8 +544,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       int stage = 0;
       uint32_t phase = 0;
       WorkIter wi(cid, tp, nkb);
-      int tile, kb0, kb1, split, tail;
-      while (wi.next(tp, nkb, ncl, tile, kb0, kb1, split, tail)) {
+      int tile, kb0, kb1, kind;
+      while (wi.next(tp, nkb, ncl, tile, kb0, kb1, kind)) {
         int m_blk, n_blk;
         raster(tile, num_m, num_n, group_m, m_blk, n_blk);
         for (int kb = kb0; kb < kb1; ++kb) {
@@ -567,15 +575,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       int acc = 0;
       uint32_t acc_phase = 0;
       WorkIter wi(cid, tp, nkb);
-      int tile, kb0, kb1, split, tail;
+      int tile, kb0, kb1, kind;
       uint64_t* trace = g_gemm_trace;
       int nu = 0;
-      while (wi.next(tp, nkb, ncl, tile, kb0, kb1, split, tail)) {
+      while (wi.next(tp, nkb, ncl, tile, kb0, kb1, kind)) {
         mbar_wait(&tempty[acc], acc_phase ^ 1);
+        if (kind == UNIT_FINISH) mbar_wait(pre_full, 0);  // at most one finisher unit per cluster
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
         uint64_t* rec = (trace && nu < 30) ? trace + ((size_t)cid * 32 + nu) * 6 : nullptr;
         if (rec) rec[0] = gtimer();
+        const uint32_t acc0 = kind == UNIT_FINISH ? 1u : 0u;  // accumulate onto the preloaded partial
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           if (rec && kb == kb0) rec[1] = gtimer();
@@ -584,7 +594,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
           const uint64_t b0 = umma_desc_sw128(smem_u32(sB + stage * C::B_BYTES));
 #pragma unroll
           for (int k = 0; k < TC_BK / 16; ++k)
-            umma_bf16_2sm(d_tmem, a0 + 2 * k, b0 + 2 * k, C::IDESC, (kb > kb0 || k > 0) ? 1u : 0u);
+            umma_bf16_2sm(d_tmem, a0 + 2 * k, b0 + 2 * k, C::IDESC, (kb > kb0 || k > 0) ? 1u : acc0);
           umma_commit_2sm_mc(&empty[stage]);
           if (++stage == C::STAGES) {
             stage = 0;
@@ -594,7 +604,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         umma_commit_2sm_mc(&tfull[acc]);
         if (rec) {
           rec[2] = gtimer();
-          rec[3] = (uint64_t)tile | ((uint64_t)(kb1 - kb0) << 32);
+          rec[3] = (uint64_t)tile | ((uint64_t)(kb1 - kb0) << 32) | ((uint64_t)kind << 48);
         }
         ++nu;
         if (++acc == 2) {
@@ -611,15 +621,66 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     constexpr int CH = BN / 32 / 2;         // 32-column chunks per warpgroup
     const int c0 = eg * CH;
     const uint32_t tempty_leader = smem_u32(&tempty[0]) & PEER_MASK;
+    const uint32_t pre_full_leader = smem_u32(pre_full) & PEER_MASK;
     uint8_t* my_stg = sStg + (warp - 4) * 2 * 2048;
     uint32_t nst = 0;  // TMA stores issued by this warp (double-buffered staging)
+    // The finisher's preload: after the previous user of the accumulator buffer drained it, copy the early
+    // piece's partial (slot cid + 1, this CTA's 128 rows) into the buffer, then release the MMA warp.
+    auto preload = [&](int buf) {
+      const int slot = cid + 1;
+      const int* flag = tp.flags + slot * 2 + rank;
+      if (lane == 0) {
+        while (true) {
+          int v;
+          asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+          if (v) break;
+          __nanosleep(64);
+        }
+      }
+      __syncwarp();
+      const float* part = tp.ws + ((size_t)slot * 2 + rank) * 128 * BN + (size_t)etid * 4;
+      const uint32_t tb = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * BN);
+#pragma unroll 1
+      for (int c = c0; c < c0 + CH; ++c) {
+        uint32_t r[32];
+#pragma unroll
+        for (int j = 0; j < 32; j += 4) {
+          const float4 x = __ldcg(reinterpret_cast<const float4*>(part + (size_t)((c * 32 + j) >> 2) * 512));
+          r[j] = __float_as_uint(x.x);
+          r[j + 1] = __float_as_uint(x.y);
+          r[j + 2] = __float_as_uint(x.z);
+          r[j + 3] = __float_as_uint(x.w);
+        }
+        tmem_st32_nowait(tb + (uint32_t)(c * 32), r);
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      epi_bar();  // every epilogue thread of this CTA has read the slot
+      if (warp == 4 && lane == 0) *const_cast<int*>(flag) = 0;  // self-reset for the next launch
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(pre_full_leader);
+    };
     int acc = 0;
     uint32_t acc_phase = 0;
     WorkIter wi(cid, tp, nkb);
-    int tile, kb0, kb1, split, tail;
+    int tile, kb0, kb1, kind;
+    // this cluster's early piece (its first stream-K unit, if split) and finisher (its last, if split).
+    // The finisher's preload runs after the epilogue of unit f - 2 (its buffer's previous user) -- or of
+    // f - 1 when the early piece is f - 1: a cluster publishes its own early piece before it ever waits
+    // for another cluster's, so the waits cannot chain from cluster to cluster
+    int e_idx = -1, f_idx = -1;
+    {
+      WorkIter sc(cid, tp, nkb);
+      int t2, k20, k21, kind2;
+      for (int n = 0; sc.next(tp, nkb, ncl, t2, k20, k21, kind2); ++n) {
+        if (kind2 == UNIT_EARLY) e_idx = n;
+        if (kind2 == UNIT_FINISH) f_idx = n;
+      }
+    }
+    const int preload_after = f_idx < 0 ? -2 : (f_idx >= 2 && e_idx <= f_idx - 2) ? f_idx - 2 : f_idx - 1;
     uint64_t* etrace = (leader && warp == 4 && lane == 0) ? g_gemm_trace : nullptr;
     int enu = 0;
-    while (wi.next(tp, nkb, ncl, tile, kb0, kb1, split, tail)) {
+    while (wi.next(tp, nkb, ncl, tile, kb0, kb1, kind)) {
       int m_blk, n_blk;
       raster(tile, num_m, num_n, group_m, m_blk, n_blk);
       mbar_wait(&tfull[acc], acc_phase);
@@ -629,10 +690,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       __syncwarp();  // reconverge the spin loop before the .sync.aligned tcgen05.ld
       tc_fence_after();
       const int row = m_blk * 256 + (int)rank * 128 + etid;
-      // split piece: this CTA's 128 x BN partial goes to workspace slot (cid + tail), [col/4][row][4]
-      float* part = (split >= 0) ? tp.ws + ((size_t)(cid + tail) * 2 + rank) * 128 * BN + (size_t)etid * 4 : nullptr;
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
-      if (TMA_ST && split < 0) {
+      if (kind == UNIT_EARLY) {
+        // this CTA's 128 x BN partial accumulator -> workspace slot cid, [col/4][row][4] (coalesced)
+        float* part = tp.ws + ((size_t)cid * 2 + rank) * 128 * BN + (size_t)etid * 4;
+#pragma unroll 1
+        for (int c = c0; c < c0 + CH; c += 2) {
+          const bool two = c + 1 < c0 + CH;
+          uint32_t r0[32], r1[32];
+          tmem_ld32_nowait(tbase + (uint32_t)(c * 32), r0);
+          if (two) tmem_ld32_nowait(tbase + (uint32_t)((c + 1) * 32), r1);
+          tmem_wait_ld();
+#pragma unroll
+          for (int j = 0; j < 32; j += 4) {
+            __stcg(reinterpret_cast<float4*>(part + (size_t)((c * 32 + j) >> 2) * 512),
+                   make_float4(__uint_as_float(r0[j]), __uint_as_float(r0[j + 1]), __uint_as_float(r0[j + 2]),
+                               __uint_as_float(r0[j + 3])));
+            if (two)
+              __stcg(reinterpret_cast<float4*>(part + (size_t)(((c + 1) * 32 + j) >> 2) * 512),
+                     make_float4(__uint_as_float(r1[j]), __uint_as_float(r1[j + 1]), __uint_as_float(r1[j + 2]),
+                                 __uint_as_float(r1[j + 3])));
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(tempty_leader + (uint32_t)(acc * sizeof(uint64_t)));
+        __threadfence();
+        epi_bar();  // all 256 epilogue threads of this CTA wrote their rows
+        if (warp == 4 && lane == 0)
+          asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(tp.flags + cid * 2 + rank), "r"(1) : "memory");
+      } else if (TMA_ST) {
         // two 32-column chunks per step: both TMEM loads in flight, one proxy fence and one wait for the
         // staging buffers per pair; the accumulator is released right after the tile's last TMEM load
 #pragma unroll 1
@@ -688,68 +775,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         for (int c = c0; c < c0 + CH; ++c) {
           uint32_t r[32];
           tmem_ld32(tbase + (uint32_t)(c * 32), r);
-          if (split >= 0) {
+          float v[32];
 #pragma unroll
-            for (int j = 0; j < 32; j += 4)
-              __stcg(reinterpret_cast<float4*>(part + (size_t)((c * 32 + j) >> 2) * 512),
-                     make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]), __uint_as_float(r[j + 2]),
-                                 __uint_as_float(r[j + 3])));
-          } else {
-            float v[32];
-#pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-            epi_store<EPI>(v, row, n_blk * BN + c * 32, M, N, D, bias, qs);
-          }
+          for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+          epi_store<EPI>(v, row, n_blk * BN + c * 32, M, N, D, bias, qs);
         }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(tempty_leader + (uint32_t)(acc * sizeof(uint64_t)));
       }
+      if (enu - 1 == preload_after) preload(f_idx & 1);
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
-      }
-      if (split >= 0) {
-        // publish the partial; the last of the tile's pieces to arrive reduces (fixed order) + epilogue
-        const int cfirst = (tail * nkb) / tp.L, nsplit = ((tail + 1) * nkb - 1) / tp.L - cfirst + 1;
-        uint64_t* srec = erec ? etrace + ((size_t)cid * 32 + 31) * 6 : nullptr;  // last split piece's phases
-        if (srec) srec[0] = gtimer();
-        __threadfence();
-        epi_bar();
-        if (warp == 4 && lane == 0) {
-          const int old = atomicAdd(tp.counters + tail * 2 + rank, 1);
-          *fix_flag = (old == nsplit - 1);
-          if (old == nsplit - 1) tp.counters[tail * 2 + rank] = 0;  // self-reset for the next launch
-        }
-        epi_bar();
-        if (srec) srec[1] = gtimer();
-        if (*fix_flag) {
-          __threadfence();
-#pragma unroll 1
-          for (int c = c0; c < c0 + CH; ++c) {
-            float v[32];
-#pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = 0.f;
-            for (int sp = 0; sp < nsplit; ++sp) {  // pieces in cluster order: deterministic
-              const float* ps = tp.ws + ((size_t)(cfirst + sp + tail) * 2 + rank) * 128 * BN + (size_t)etid * 4;
-#pragma unroll
-              for (int j = 0; j < 32; j += 4) {
-                const float4 x = __ldcg(reinterpret_cast<const float4*>(ps + (size_t)((c * 32 + j) >> 2) * 512));
-                v[j] += x.x;
-                v[j + 1] += x.y;
-                v[j + 2] += x.z;
-                v[j + 3] += x.w;
-              }
-            }
-            epi_store<EPI>(v, row, n_blk * BN + c * 32, M, N, D, bias, qs);
-          }
-        }
-        if (srec) srec[2] = gtimer();
-        epi_bar();  // fix_flag is reused by the next split unit
-        if (srec) {
-          srec[3] = gtimer();
-          srec[4] = (uint64_t)nsplit | ((uint64_t)(*fix_flag) << 32);
-        }
       }
       if (erec) erec[5] = gtimer();
     }
@@ -830,12 +868,12 @@ int tc_pick_bn(int M, int N) {
   return N <= 128 ? 128 : 256;
 }
 
-// fp32 partial-tile workspace + self-resetting arrival counters of the stream-K tail: <= 2 * pairs slots
-// of [2][128][256] fp32 and rem < pairs counter pairs.  Contexts own one each (runtime.cu); launches without one
+// fp32 partial-accumulator workspace + self-resetting flags of the stream-K early pieces: one slot of
+// [2][128][256] fp32 and one flag pair per cluster.  Contexts own one each (runtime.cu); launches without one
 // (the kernel-level ABI entry) share a per-device default.
 bool tail_ws_alloc(TailWs* w) {
-  const size_t units = (size_t)(num_sms() / 2);  // slots <= clusters + tail tiles <= 2 * pairs
-  if (cudaMalloc(&w->ws, 2 * units * 2 * 128 * 256 * sizeof(float)) != cudaSuccess ||
+  const size_t units = (size_t)(num_sms() / 2);
+  if (cudaMalloc(&w->ws, units * 2 * 128 * 256 * sizeof(float)) != cudaSuccess ||
       cudaMalloc(&w->counters, units * 2 * sizeof(int)) != cudaSuccess) {
     cudaGetLastError();
     tail_ws_free(w);
@@ -875,27 +913,19 @@ static bool launch_pair_epi(const CUtensorMap& tmA, const CUtensorMap& tmB, cons
   const int tiles = num_m * num_n;
   const int pairs = num_sms() / 2;
   const int nkb = (K + TC_BK - 1) / TC_BK;
-  // Stream-K tail (see TailPlan) when the last wave would leave >= 15% of the clusters idle and a tile
-  // is long (K >= 10240): splitting a tile costs ~7-12 us of partial-tile traffic and fix-up
-  // (measured: TP=4 out-proj 40 -> 48 us with 2 pieces per tail tile, qkv TP=8 60 -> 65 us), which
-  // only the long MLP-down tiles amortise.  ENERGON_NO_STREAMK=1 disables it (A/B, tests).
+  // Stream-K (see TailPlan) when whole-tile rounds would leave clusters idle in the last round: the last
+  // round plus the remainder (R tiles) are spread evenly, the rounds before stay data parallel.
+  // ENERGON_NO_STREAMK=1 disables it (A/B, tests).
   TailPlan tp{tiles, 0, 0, nullptr, nullptr};
-  const int rem = tiles % pairs;
   int grid_cl = tiles < pairs ? tiles : pairs;
-  static int min_nkb = -1;
-  if (min_nkb < 0) {  // ENERGON_SK_MIN_NKB: experiment hook for the K threshold (k-blocks of 64)
-    const char* e = getenv("ENERGON_SK_MIN_NKB");
-    min_nkb = e ? atoi(e) : 160;
-  }
-  if (!(shard && EPI == EPI_NONE) && rem > 0 && (pairs - rem) * 100 >= 15 * pairs && nkb >= min_nkb && !getenv("ENERGON_NO_STREAMK")) {
+  if (!getenv("ENERGON_NO_STREAMK") && tiles > pairs && tiles % pairs != 0) {
     const TailWs* w = tw ? tw : default_tail_ws();
     if (w->ws) {
-      const int Lmin = (rem * nkb + pairs - 1) / pairs;  // every tail cluster index < pairs
-      int L = Lmin < 8 ? 8 : Lmin;
-      if (const char* f = getenv("ENERGON_SK_L")) L = atoi(f) > Lmin ? atoi(f) : L;  // experiment hook
-      tp = TailPlan{tiles - rem, L, rem, w->ws, w->counters};
-      const int used = (rem * nkb + L - 1) / L;  // clusters with tail work
-      if (grid_cl < used) grid_cl = used;
+      const int full = (tiles / pairs - 1) * pairs;
+      const int R = tiles - full;  // in (pairs, 2 pairs): L >= nkb, a tile spans at most two clusters
+      const int L = (int)(((int64_t)R * nkb + pairs - 1) / pairs);
+      tp = TailPlan{full, L, R, w->ws, w->counters};
+      grid_cl = pairs;
     }
   }
   const int grid = 2 * grid_cl;
@@ -949,18 +979,13 @@ static bool launch_pair_epi(const CUtensorMap& tmA, const CUtensorMap& tmB, cons
     cudaMemcpy(h.data(), trace_buf, trace_n * sizeof(uint64_t), cudaMemcpyDeviceToHost);
     if (FILE* f = fopen(trace_file, "a")) {
       fprintf(f, "launch M=%d N=%d K=%d clusters=%d\n", M, N, K, grid / 2);
-      for (int c = 0; c < grid / 2; ++c) {
-        const uint64_t* q = &h[((size_t)c * 32 + 31) * 6];
-        if (q[0])
-          fprintf(f, "split %d %llu %llu %llu %llu %llu\n", c, (unsigned long long)q[0], (unsigned long long)q[1],
-                  (unsigned long long)q[2], (unsigned long long)q[3], (unsigned long long)q[4]);
-      }
       for (int c = 0; c < grid / 2; ++c)
         for (int u = 0; u < 30; ++u) {
           const uint64_t* r = &h[((size_t)c * 32 + u) * 6];
-          if (r[0]) fprintf(f, "%d %d %llu %llu %llu %llu %llu %llu %llu\n", c, u, (unsigned long long)(r[3] & 0xffffffffu),
-                            (unsigned long long)(r[3] >> 32), (unsigned long long)r[0], (unsigned long long)r[1],
-                            (unsigned long long)r[2], (unsigned long long)r[4], (unsigned long long)r[5]);
+          if (r[0]) fprintf(f, "%d %d %llu %llu %llu %llu %llu %llu %llu %llu\n", c, u, (unsigned long long)(r[3] & 0xffffffffu),
+                            (unsigned long long)((r[3] >> 32) & 0xffffu), (unsigned long long)r[0], (unsigned long long)r[1],
+                            (unsigned long long)r[2], (unsigned long long)r[4], (unsigned long long)r[5],
+                            (unsigned long long)(r[3] >> 48));
         }
       fclose(f);
     }

@@ -249,8 +249,9 @@ __global__ void __launch_bounds__(LN_THREADS) embed_ln_kernel(const int* __restr
 }
 
 // Hidden-state entry (energon_forward_hidden / a later pipeline stage): X[t] = x[cell] (fp32),
-// A[t] = LN1(X[t]).  pack_idx == nullptr: x is already packed, [n_valid, H] with n_valid = *T_dev
-// (offsets[B]); bucket rows past T are zeroed.
+// A[t] = LN1(X[t]).  pack_idx == nullptr: x is already in row order -- packed [n_valid, H] with
+// n_valid = *T_dev (offsets[B]; bucket rows past it are zeroed), or every row valid (T_dev == nullptr,
+// the padded A/B mode).
 template <typename Act, int LN_MAXV>
 __global__ void __launch_bounds__(LN_THREADS) gather_ln_kernel(const float* __restrict__ x, const int* __restrict__ pack_idx,
                                                                const int* __restrict__ T_dev, int row0, int H,
@@ -260,7 +261,7 @@ __global__ void __launch_bounds__(LN_THREADS) gather_ln_kernel(const float* __re
   pdl_wait();
   __shared__ float red[32];
   const int t = row0 + blockIdx.x;
-  const int cell = pack_idx ? pack_idx[t] : (t < *T_dev ? t : -1);
+  const int cell = pack_idx ? pack_idx[t] : ((!T_dev || t < *T_dev) ? t : -1);
   if (cell < 0) {
     for (int c = threadIdx.x; c < H / 4; c += LN_THREADS) {
       Row4<float>::store(X + (int64_t)t * H + 4 * c, make_float4(0.f, 0.f, 0.f, 0.f));

@@ -700,7 +700,8 @@ energon_status forward_t(energon_ctx** cs, int n, const Call& a, int64_t T) {
                              reinterpret_cast<const Act*>(c->tok_emb), reinterpret_cast<const Act*>(c->pos_emb), g1, b1,
                              eps, c->X, reinterpret_cast<Act*>(c->A), st);
       else
-        launch_gather_ln<Act>(a.x_in, a.x_packed ? nullptr : pidx, c->offsets + a.B, r0, sn, c->H, g1, b1, eps, c->X,
+        launch_gather_ln<Act>(a.x_in, a.x_packed ? nullptr : pidx, drce ? c->offsets + a.B : nullptr, r0, sn, c->H, g1,
+                              b1, eps, c->X,
                               reinterpret_cast<Act*>(c->A), st);
     }
     c->stats.kernel_launches++;
