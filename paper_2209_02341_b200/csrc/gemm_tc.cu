@@ -328,6 +328,7 @@ struct TailPlan {
   int R;        // stream-K tiles [full, full + R)
   float* ws;    // [clusters][2][BN / 4][128][4] fp32 partial accumulators of the early pieces
   int* flags;   // [clusters][2] 1 = slot published
+  int early_first;  // 1: a cluster's early piece runs before its data-parallel tiles (see WorkIter)
 };
 enum { UNIT_WHOLE = 0, UNIT_EARLY = 1, UNIT_FINISH = 2 };
 // Diagnostics (ENERGON_GEMM_TRACE=<file>): per-unit timestamps of the pair kernel (leader CTA) -- MMA
@@ -341,16 +342,35 @@ __device__ __forceinline__ uint64_t gtimer() {
   return t;
 }
 
+// Unit order of a cluster: its data-parallel tiles, then its stream-K range (early piece, whole tiles,
+// finisher).  With early_first the early piece moves to the front: published first, it gives every partner
+// finisher the whole kernel to pick the partial up -- but its tile lies outside the data-parallel rounds'
+// panel set, so it is used only when the operands fit in L2.
 struct WorkIter {
-  int u, it, it_end;
-  __device__ __forceinline__ WorkIter(int cid, const TailPlan& tp, int nkb) : u(cid), it(0), it_end(0) {
+  int u, it, it_end, early;  // early: 1 = the early piece is still to be emitted
+  __device__ __forceinline__ WorkIter(int cid, const TailPlan& tp, int nkb) : u(cid), it(0), it_end(0), early(0) {
     if (tp.L > 0) {
       it = cid * tp.L;
       it_end = min(it + tp.L, tp.R * nkb);
+      early = (tp.early_first && it < it_end && it % nkb != 0) ? 1 : 0;
     }
+  }
+  __device__ __forceinline__ void sk_unit(const TailPlan& tp, int nkb, int& tile, int& kb0, int& kb1, int& kind) {
+    const int tl = it / nkb, jk = it - tl * nkb;
+    const int jend = min(it_end - tl * nkb, nkb);  // exclusive, iteration index within the tile
+    tile = tp.full + tl;
+    kb0 = nkb - jend;  // reversed k order: iterations [jk, jend) <-> k-blocks [nkb - jend, nkb - jk)
+    kb1 = nkb - jk;
+    kind = (jk == 0 && jend == nkb) ? UNIT_WHOLE : (jk != 0 ? UNIT_EARLY : UNIT_FINISH);
+    it += jend - jk;
   }
   // next unit of this cluster: tile, k-block range [kb0, kb1), kind (UNIT_*)
   __device__ __forceinline__ bool next(const TailPlan& tp, int nkb, int ncl, int& tile, int& kb0, int& kb1, int& kind) {
+    if (early) {
+      early = 0;
+      sk_unit(tp, nkb, tile, kb0, kb1, kind);
+      return true;
+    }
     if (u < tp.full) {
       tile = u;
       kb0 = 0;
@@ -360,13 +380,7 @@ struct WorkIter {
       return true;
     }
     if (it >= it_end) return false;
-    const int tl = it / nkb, jk = it - tl * nkb;
-    const int jend = min(it_end - tl * nkb, nkb);  // exclusive, iteration index within the tile
-    tile = tp.full + tl;
-    kb0 = nkb - jend;  // reversed k order: iterations [jk, jend) <-> k-blocks [nkb - jend, nkb - jk)
-    kb1 = nkb - jk;
-    kind = (jk == 0 && jend == nkb) ? UNIT_WHOLE : (jk != 0 ? UNIT_EARLY : UNIT_FINISH);
-    it += jend - jk;
+    sk_unit(tp, nkb, tile, kb0, kb1, kind);
     return true;
   }
 };
@@ -481,6 +495,34 @@ __device__ __forceinline__ void epi_store(float (&v)[32], int row, int n0, int M
 
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }  // the 8 epilogue warps
 
+// The finisher's preload of one warp: chunks [c0, c0 + nch) of 32 columns of its row (fp32 partial in the
+// [col/4][row][4] slot layout, `part` already offset to this thread's row) -> TMEM at `tb`.  Not inlined:
+// it runs once per launch and its registers must not add to the epilogue loop's.
+__device__ __noinline__ void gemm_preload_acc(const float* part, uint32_t tb, int c0, int nch) {
+#pragma unroll 1
+  for (int c = c0; c < c0 + nch; c += 2) {  // two chunks' loads in flight per step
+    const bool two = c + 1 < c0 + nch;
+    uint32_t r0[32], r1[32];
+#pragma unroll
+    for (int j = 0; j < 32; j += 4) {
+      const float4 x = __ldcg(reinterpret_cast<const float4*>(part + (size_t)((c * 32 + j) >> 2) * 512));
+      r0[j] = __float_as_uint(x.x);
+      r0[j + 1] = __float_as_uint(x.y);
+      r0[j + 2] = __float_as_uint(x.z);
+      r0[j + 3] = __float_as_uint(x.w);
+      const float4 y = two ? __ldcg(reinterpret_cast<const float4*>(part + (size_t)(((c + 1) * 32 + j) >> 2) * 512))
+                           : x;
+      r1[j] = __float_as_uint(y.x);
+      r1[j + 1] = __float_as_uint(y.y);
+      r1[j + 2] = __float_as_uint(y.z);
+      r1[j + 3] = __float_as_uint(y.w);
+    }
+    tmem_st32_nowait(tb + (uint32_t)(c * 32), r0);
+    if (two) tmem_st32_nowait(tb + (uint32_t)((c + 1) * 32), r1);
+  }
+  tmem_wait_st();
+}
+
 template <int BN, int EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -500,6 +542,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
   uint64_t* tempty = tfull + 2;
   uint64_t* pre_full = tempty + 2;  // the finisher unit's accumulator holds the early piece's partial
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(pre_full + 1);
+  int* pre_cnt = reinterpret_cast<int*>(tmem_holder + 1);  // epilogue warps done reading the early slot
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
@@ -520,6 +563,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       mbar_init(&tempty[i], 2 * C::EPI_WARPS);  // epilogue warps x 2 CTAs
     }
     mbar_init(pre_full, 2 * C::EPI_WARPS);
+    *pre_cnt = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
@@ -621,68 +665,56 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     constexpr int CH = BN / 32 / 2;         // 32-column chunks per warpgroup
     const int c0 = eg * CH;
     const uint32_t tempty_leader = smem_u32(&tempty[0]) & PEER_MASK;
-    const uint32_t pre_full_leader = smem_u32(pre_full) & PEER_MASK;
     uint8_t* my_stg = sStg + (warp - 4) * 2 * 2048;
     uint32_t nst = 0;  // TMA stores issued by this warp (double-buffered staging)
-    // The finisher's preload: after the previous user of the accumulator buffer drained it, copy the early
-    // piece's partial (slot cid + 1, this CTA's 128 rows) into the buffer, then release the MMA warp.
+    // The finisher's preload (per warp: its TMEM lane quadrant, its warpgroup's columns): copy the early
+    // piece's partial (slot cid + 1, this CTA's rows) into the accumulator buffer the finisher will use,
+    // then arrive on the leader's pre_full; the last of the CTA's 8 warps clears the slot's flag.
+    const int* pflag = tp.flags + (cid + 1) * 2 + rank;
+    auto flag_set = [&]() -> bool {
+      int v = 0;
+      if (lane == 0) asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(pflag) : "memory");
+      return __shfl_sync(0xffffffffu, v, 0) != 0;
+    };
     auto preload = [&](int buf) {
-      const int slot = cid + 1;
-      const int* flag = tp.flags + slot * 2 + rank;
-      if (lane == 0) {
-        while (true) {
-          int v;
-          asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
-          if (v) break;
-          __nanosleep(64);
-        }
-      }
-      __syncwarp();
-      const float* part = tp.ws + ((size_t)slot * 2 + rank) * 128 * BN + (size_t)etid * 4;
-      const uint32_t tb = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * BN);
-#pragma unroll 1
-      for (int c = c0; c < c0 + CH; ++c) {
-        uint32_t r[32];
-#pragma unroll
-        for (int j = 0; j < 32; j += 4) {
-          const float4 x = __ldcg(reinterpret_cast<const float4*>(part + (size_t)((c * 32 + j) >> 2) * 512));
-          r[j] = __float_as_uint(x.x);
-          r[j + 1] = __float_as_uint(x.y);
-          r[j + 2] = __float_as_uint(x.z);
-          r[j + 3] = __float_as_uint(x.w);
-        }
-        tmem_st32_nowait(tb + (uint32_t)(c * 32), r);
-      }
-      tmem_wait_st();
+      while (!flag_set()) __nanosleep(64);
+      gemm_preload_acc(tp.ws + ((size_t)(cid + 1) * 2 + rank) * 128 * BN + (size_t)etid * 4,
+                       tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * BN), c0, CH);
       tc_fence_before();
-      epi_bar();  // every epilogue thread of this CTA has read the slot
-      if (warp == 4 && lane == 0) *const_cast<int*>(flag) = 0;  // self-reset for the next launch
       __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(pre_full_leader);
+      if (lane == 0) {
+        mbar_arrive_cluster(smem_u32(pre_full) & PEER_MASK);
+        if (atomicAdd(pre_cnt, 1) == C::EPI_WARPS - 1) *const_cast<int*>(pflag) = 0;  // self-reset for the next launch
+      }
+      __syncwarp();
     };
     int acc = 0;
     uint32_t acc_phase = 0;
     WorkIter wi(cid, tp, nkb);
     int tile, kb0, kb1, kind;
-    // this cluster's early piece (its first stream-K unit, if split) and finisher (its last, if split).
-    // The finisher's preload runs after the epilogue of unit f - 2 (its buffer's previous user) -- or of
-    // f - 1 when the early piece is f - 1: a cluster publishes its own early piece before it ever waits
-    // for another cluster's, so the waits cannot chain from cluster to cluster
-    int e_idx = -1, f_idx = -1;
+    // The finisher (this cluster's last unit f, if split) reuses the buffer of unit f - 2: its preload runs
+    // after that unit's epilogue (at once when f == 1 and there is no early piece), so it overlaps the MMAs
+    // of unit f - 1 -- but never before this cluster's own early piece (unit 0) is published, so a cluster
+    // never waits for another before publishing its own piece and the waits cannot chain.
+    int pre_at = -2, pre_buf = 0;  // preload into buffer pre_buf once pre_at epilogues are done (-2: none)
     {
       WorkIter sc(cid, tp, nkb);
-      int t2, k20, k21, kind2;
-      for (int n = 0; sc.next(tp, nkb, ncl, t2, k20, k21, kind2); ++n) {
-        if (kind2 == UNIT_EARLY) e_idx = n;
-        if (kind2 == UNIT_FINISH) f_idx = n;
+      int t2, k20, k21, kind2, n = 0, f = -1, e = -1;
+      for (; sc.next(tp, nkb, ncl, t2, k20, k21, kind2); ++n) {
+        if (kind2 == UNIT_EARLY) e = n;
+        if (kind2 == UNIT_FINISH) f = n;
+      }
+      if (f >= 0) {
+        pre_at = max(f - 1, e + 1);
+        pre_buf = f & 1;
       }
     }
-    const int preload_after = f_idx < 0 ? -2 : (f_idx >= 2 && e_idx <= f_idx - 2) ? f_idx - 2 : f_idx - 1;
     uint64_t* etrace = (leader && warp == 4 && lane == 0) ? g_gemm_trace : nullptr;
     int enu = 0;
     while (wi.next(tp, nkb, ncl, tile, kb0, kb1, kind)) {
       int m_blk, n_blk;
       raster(tile, num_m, num_n, group_m, m_blk, n_blk);
+      if (enu == pre_at) preload(pre_buf);  // (pre_at == 0: f == 1 and no early piece -- a fresh buffer)
       mbar_wait(&tfull[acc], acc_phase);
       uint64_t* erec = (etrace && enu < 30) ? etrace + ((size_t)cid * 32 + enu) * 6 : nullptr;
       ++enu;
@@ -695,22 +727,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         // this CTA's 128 x BN partial accumulator -> workspace slot cid, [col/4][row][4] (coalesced)
         float* part = tp.ws + ((size_t)cid * 2 + rank) * 128 * BN + (size_t)etid * 4;
 #pragma unroll 1
-        for (int c = c0; c < c0 + CH; c += 2) {
-          const bool two = c + 1 < c0 + CH;
-          uint32_t r0[32], r1[32];
-          tmem_ld32_nowait(tbase + (uint32_t)(c * 32), r0);
-          if (two) tmem_ld32_nowait(tbase + (uint32_t)((c + 1) * 32), r1);
-          tmem_wait_ld();
+        for (int c = c0; c < c0 + CH; ++c) {
+          uint32_t r0[32];
+          tmem_ld32(tbase + (uint32_t)(c * 32), r0);
 #pragma unroll
-          for (int j = 0; j < 32; j += 4) {
+          for (int j = 0; j < 32; j += 4)
             __stcg(reinterpret_cast<float4*>(part + (size_t)((c * 32 + j) >> 2) * 512),
                    make_float4(__uint_as_float(r0[j]), __uint_as_float(r0[j + 1]), __uint_as_float(r0[j + 2]),
                                __uint_as_float(r0[j + 3])));
-            if (two)
-              __stcg(reinterpret_cast<float4*>(part + (size_t)(((c + 1) * 32 + j) >> 2) * 512),
-                     make_float4(__uint_as_float(r1[j]), __uint_as_float(r1[j + 1]), __uint_as_float(r1[j + 2]),
-                                 __uint_as_float(r1[j + 3])));
-          }
         }
         tc_fence_before();
         __syncwarp();
@@ -784,7 +808,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(tempty_leader + (uint32_t)(acc * sizeof(uint64_t)));
       }
-      if (enu - 1 == preload_after) preload(f_idx & 1);
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
@@ -914,17 +937,33 @@ static bool launch_pair_epi(const CUtensorMap& tmA, const CUtensorMap& tmB, cons
   const int pairs = num_sms() / 2;
   const int nkb = (K + TC_BK - 1) / TC_BK;
   // Stream-K (see TailPlan) when whole-tile rounds would leave clusters idle in the last round: the last
-  // round plus the remainder (R tiles) are spread evenly, the rounds before stay data parallel.
-  // ENERGON_NO_STREAMK=1 disables it (A/B, tests).
-  TailPlan tp{tiles, 0, 0, nullptr, nullptr};
+  // round plus the remainder (R tiles) are spread evenly, the rounds before stay data parallel.  Measured
+  // per shape (profiles/r02_gemm_sk_ab.log, A/B against the data-parallel schedule on one box): it pays for
+  //   long tiles, K >= 10240 (TP = 1 / 2 MLP-down: 608 -> 563 us, 296 -> 283 us), in data-parallel-first
+  //     order (the operands exceed L2, the rounds' panel locality matters);
+  //   K >= 4096 when A + W fit in L2 and there are >= 2 rounds (TP = 8 MLP-up 87 -> 79 us, TP = 4 QKV
+  //     116 -> 113 us), early piece first;
+  // not for short tiles: the early pieces' fp32 partials (2 x 128 KB per split tile) cross L2 at once, which
+  // a K = 640 tile cannot amortise (TP = 8 out-proj 26 -> 34 us), nor for one round + remainder (TP = 8 QKV,
+  // 64 -> 66 us: the clusters whose range is just an early piece and a finisher wait for their own
+  // partial store + preload).  ENERGON_NO_STREAMK=1 disables it, ENERGON_SK_FORCE=1 / 2 forces it with the early piece first /
+  // data-parallel first (tests).
+  TailPlan tp{tiles, 0, 0, nullptr, nullptr, 0};
   int grid_cl = tiles < pairs ? tiles : pairs;
-  if (!getenv("ENERGON_NO_STREAMK") && tiles > pairs && tiles % pairs != 0) {
+  const double ab_bytes = 2.0 * ((double)M + (double)N) * (double)K;
+  int sk = 0;  // 0 none, 1 data-parallel first, 2 early piece first
+  if (tiles > pairs && tiles % pairs != 0 && !getenv("ENERGON_NO_STREAMK")) {
+    if (const char* f = getenv("ENERGON_SK_FORCE")) sk = atoi(f) == 2 ? 1 : 2;  // 1: early first, 2: DP first
+    else if (nkb >= 160) sk = 1;
+    else if (nkb >= 64 && tiles >= 2 * pairs && ab_bytes <= 100e6) sk = 2;
+  }
+  if (sk) {
     const TailWs* w = tw ? tw : default_tail_ws();
     if (w->ws) {
       const int full = (tiles / pairs - 1) * pairs;
       const int R = tiles - full;  // in (pairs, 2 pairs): L >= nkb, a tile spans at most two clusters
       const int L = (int)(((int64_t)R * nkb + pairs - 1) / pairs);
-      tp = TailPlan{full, L, R, w->ws, w->counters};
+      tp = TailPlan{full, L, R, w->ws, w->counters, sk == 2 ? 1 : 0};
       grid_cl = pairs;
     }
   }

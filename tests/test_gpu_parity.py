@@ -444,14 +444,16 @@ def test_gemm_every_tile_shape(code, M, N, K, epi, monkeypatch):
 @pytest.mark.parametrize("M,N,K,epi,tile", [(4096, 1920, 5120, 1, 0), (4096, 2560, 5120, 2, 0), (2304, 2560, 10240, 2, 0),
                                             (1200, 3800, 10240, 1, 0), (4096, 1920, 5000, 0, 0), (4096, 2560, 640, 0, 1192),
                                             (4096, 5120, 2560, 0, 0)])
-def test_gemm_streamk(M, N, K, epi, tile, monkeypatch):
+@pytest.mark.parametrize("order", [1, 2])
+def test_gemm_streamk(M, N, K, epi, tile, order, monkeypatch):
     """Stream-K with accumulator preload (gemm_tc.cu TailPlan): the last round + remainder of tiles spread
     evenly over the clusters, split tiles finished on top of the early piece's fp32 partial -- QKV / MLP-up /
     MLP-down at TP=8 (128 / 160 / 320 tiles), 90 and 75 tiles at K = 10240, a K tail, the 256 x 192 tile:
     correct vs the oracle, deterministic, and BIT-IDENTICAL to the data-parallel schedule (the split
-    tile's single fp32 accumulator sees the k-blocks in the same order)."""
+    tile's single fp32 accumulator sees the k-blocks in the same order); both unit orders."""
     if tile:
         monkeypatch.setenv("ENERGON_GEMM_TILE", str(tile))
+    monkeypatch.setenv("ENERGON_SK_FORCE", str(order))  # stream-K, early piece first (1) / data parallel first (2)
     tdt = torch.bfloat16
     g = torch.Generator(device="cpu").manual_seed(M + N + K)
     A = (torch.rand(M, K, generator=g) * 2 - 1).to(tdt)
