@@ -82,7 +82,7 @@ int attention_impl() {
   if (v < 0) {
     const char* e = getenv("ENERGON_ATTN");
     v = e ? atoi(e) : 4;
-    if (v != 4) v = 4;
+    if (v != 4 && v != 5) v = 4;
   }
   return v;
 }

@@ -17,6 +17,8 @@
 // Rows t >= len of the last V tile are zeroed in shared memory before P.V, so pad rows of V that a5
 // never wrote (possibly NaN) cannot reach the output even as 0 * NaN.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -25,8 +27,9 @@
 namespace energon {
 
 constexpr int ATTN_BM = 128, ATTN_BN = 64;  // query rows per item, keys per tile (the work list's costs)
-int attention_tile_bm() { return ATTN_BM; }
-int attention_tile_bn() { return ATTN_BN; }
+// the work list's item height / cost unit follow the selected kernel (v3: 256-row items, 128-key tiles)
+int attention_tile_bm() { return attention_impl() == 5 ? 256 : ATTN_BM; }
+int attention_tile_bn() { return attention_impl() == 5 ? 128 : ATTN_BN; }
 
 __device__ __forceinline__ float ex2f(float x) {
   float y;
@@ -389,18 +392,426 @@ __global__ void __launch_bounds__(192, 2)
   }
 }
 
+// ============================================================================ v3: one CTA per SM, two Q tiles
+// The FA4-style layout (ENERGON_ATTN=5, default).  One work item = 256 query rows of one (sequence, head):
+// two 128-row Q tiles that share every K / V tile of 128 keys, so each K / V byte staged in shared memory
+// feeds two S MMAs and two P.V MMAs.  TMEM holds both tiles' state at once (512 columns):
+//   S0/P0 [0,128) | S1/P1 [128,256) | O0 [256, 256+D) | O1 [256+D, 256+2D)
+// 12 warps: warps 0-3 softmax of Q tile 0 (warp w owns TMEM lanes 32(w&3).. = query rows), warps 4-7
+// softmax of Q tile 1, warp 8 TMA producer, warp 9 MMA issuer (+ TMEM owner), warps 10-11 idle.  Each SM
+// sub-partition holds 3 warps (one per warpgroup) in its 16K registers: the producer warpgroup gives
+// registers up (setmaxnreg 168 -> 88) so the softmax warps can hold a whole 128-key score row (168 -> 208);
+// 2 x 208 + 88 = 3 x 168, so the released registers exactly cover the increase (a larger increase than
+// the pool holds blocks setmaxnreg.inc forever).  The MMA thread issues, per
+// key tile j of an item:  P0_j V_j, S0_{j+1}, P1_j V_j, S1_{j+1}  -- so while softmax warpgroup 0 works on
+// S0_{j+1}, the tensor pipe runs P1_j V_j and S1_{j+1}, and vice versa: each warpgroup's softmax is hidden
+// behind the other tile's MMAs.  S_{j+1} overwrites P_j's TMEM columns without waiting for P_j V_j to
+// complete: tcgen05.mma operations issued by one thread execute in issue order (blackwell guide, "implicit
+// pipeline"), so the P_j V_j that reads them runs first.
+// Softmax per row as in v2 (fp32, exp2, lazy O rescale when the row max grows by > 2^8, P as packed bf16 over
+// its S columns), plus: 32-key chunks that no row of the warp may see (causal diagonal, key tail) skip
+// their exponentials, and warps whose 32 query rows all lie at or past the sequence end compute nothing.
+// The epilogue of a tile (O / l -> packed context rows) runs in its softmax warpgroup; the next item's
+// S MMAs and TMA loads proceed meanwhile, only its first P V waits for it (o_empty).
+// Diagnostics (ENERGON_ATTN_TRACE=<file>): clock64 timestamps of CTA 0's first 64 tiles per slot --
+// [slot][tile][4]: softmax S seen, softmax P handed over, MMA P seen, MMA P V + next S issued.  The launch is
+// then synchronous and the records are appended to the file.  Null in normal runs.
+__device__ long long* g_attn_trace = nullptr;
+__device__ __forceinline__ long long clk64() {
+  long long t;
+  asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));
+  return t;
+}
+
 template <int D>
-static bool launch_tc(const bf16* Q, const bf16* K, const bf16* V, bf16* Cp, const int* offsets, bf16* Opad,
-                      const int* lens_d, const uint32_t* work_d, int B, int hk, int S, int causal, cudaStream_t st,
-                      AttnMaps* maps) {
-  using C = Attn2Cfg<D>;
-  const int rows = B * hk * S;
-  AttnMaps local;
-  AttnMaps* m = maps ? maps : &local;
-  if (!m->valid || m->q != Q || m->k != K || m->v != V || m->rows != rows || m->d != D) {
-    // cached per context: the maps depend only on the buffers and on B * hk * S
-    if (!make_tmap_kmajor(&m->mq, Q, rows, D, C::BM) || !make_tmap_kmajor(&m->mk, K, rows, D, C::BN) ||
-        !make_tmap_kmajor(&m->mv, V, rows, D, C::BN)) {
+struct Attn3Cfg {
+  static constexpr int BM = 128, BN = 128, DH = D / 64;
+  static constexpr int Q_BYTES = BM * D * 2;
+  static constexpr int K_BYTES = BN * D * 2;
+  static constexpr int V_BYTES = BN * D * 2;
+  static constexpr int SMEM = 2 * Q_BYTES + 2 * K_BYTES + 2 * V_BYTES + 1024 + 256;
+  static constexpr int THREADS = 384;  // 12 warps: 3 per SM sub-partition (168 registers each at launch)
+  static constexpr uint32_t IDESC_S = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                                      ((uint32_t)(BM >> 4) << 24);
+  static constexpr uint32_t IDESC_O = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | ((uint32_t)(D >> 3) << 17) |
+                                      ((uint32_t)(BM >> 4) << 24);
+};
+
+// per-item geometry shared by the three roles (they must agree exactly): Q tile 0 reads key tiles
+// [0, kv0), Q tile 1 (if any of its rows is valid) [0, kv1), kv1 >= kv0
+struct Item3 {
+  int b, head, q0, len, kv0, kv1;
+  bool q1;
+};
+
+template <int D>
+__global__ void __launch_bounds__(384, 1)
+    attention_tc3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                         const __grid_constant__ CUtensorMap tmV, bf16* __restrict__ Cp, const int* __restrict__ offsets,
+                         bf16* __restrict__ Opad, const int* __restrict__ lens, const uint32_t* __restrict__ work,
+                         int hk, int S, int causal, float scale_log2) {
+  using C = Attn3Cfg<D>;
+  constexpr int BM = C::BM, BN = C::BN, DH = C::DH;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;                       // [2] Q tiles
+  uint8_t* sK = sQ + 2 * C::Q_BYTES;        // [2] stages
+  uint8_t* sV = sK + 2 * C::K_BYTES;        // [2] stages
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + 2 * C::V_BYTES);
+  uint64_t* q_full = bars + 0;    // [2] per Q slot
+  uint64_t* q_empty = bars + 2;   // [2]
+  uint64_t* o_empty = bars + 4;   // [2] the slot's epilogue has read O (4 warps)
+  uint64_t* s_full = bars + 6;    // [2] S_k of the slot's current tile computed
+  uint64_t* p_full = bars + 8;    // [2] P_k written (4 warps)
+  uint64_t* pv_done = bars + 10;  // [2 slots][2]: P V of the slot's tile n done, barrier n & 1
+  uint64_t* k_full = bars + 14;   // [2] stages
+  uint64_t* k_empty = bars + 16;
+  uint64_t* v_full = bars + 18;
+  uint64_t* v_empty = bars + 20;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 22);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 8 && lane == 0) {
+    tma_prefetch_desc(&tmQ);
+    tma_prefetch_desc(&tmK);
+    tma_prefetch_desc(&tmV);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&q_full[i], 1);
+      mbar_init(&q_empty[i], 1);
+      mbar_init(&o_empty[i], 4);
+      mbar_init(&s_full[i], 1);
+      mbar_init(&p_full[i], 4);
+      mbar_init(&pv_done[2 * i], 1);
+      mbar_init(&pv_done[2 * i + 1], 1);
+      mbar_init(&k_full[i], 1);
+      mbar_init(&k_empty[i], 1);
+      mbar_init(&v_full[i], 1);
+      mbar_init(&v_empty[i], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 9) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                 "n"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+  pdl_trigger();  // (after the TMEM allocation, see v2)
+  pdl_wait();
+  const int items = (int)__ldg(work) * hk;
+
+  auto item_at = [&](int k) { return k * (int)gridDim.x + ((k & 1) ? (int)gridDim.x - 1 - (int)blockIdx.x : (int)blockIdx.x); };
+  auto decode = [&](int w) {
+    Item3 it;
+    const uint32_t pr = __ldg(work + 1 + w / hk);
+    it.head = w % hk;
+    it.b = (int)(pr >> 16);
+    it.q0 = (int)(pr & 0xFFFFu) * (2 * BM);
+    it.len = __ldg(lens + it.b);
+    const int e0 = causal ? min(it.len, it.q0 + BM) : it.len;
+    const int e1 = causal ? min(it.len, it.q0 + 2 * BM) : it.len;
+    it.kv0 = (e0 + BN - 1) / BN;
+    it.q1 = it.q0 + BM < it.len;
+    it.kv1 = it.q1 ? (e1 + BN - 1) / BN : it.kv0;
+    return it;
+  };
+
+  if (warp >= 8) {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 88;");
+  if (warp == 8) {
+    if (lane == 0) {
+      // ---------------- TMA producer: per item Q0 (and Q1), then K_0, K_1, V_0, K_2, V_1, ...
+      int t = 0, c0 = 0, c1 = 0;
+      for (int qi = 0, w = item_at(0); w < items; w = item_at(++qi)) {
+        const Item3 it = decode(w);
+        const int row_base = (it.b * hk + it.head) * S;
+        mbar_wait(&q_empty[0], (c0 & 1) ^ 1);
+        mbar_expect_tx(&q_full[0], C::Q_BYTES);
+#pragma unroll
+        for (int h = 0; h < DH; ++h) tma_load_2d(&tmQ, smem_u32(sQ + h * BM * 128), &q_full[0], h * 64, row_base + it.q0);
+        ++c0;
+        if (it.q1) {
+          mbar_wait(&q_empty[1], (c1 & 1) ^ 1);
+          mbar_expect_tx(&q_full[1], C::Q_BYTES);
+#pragma unroll
+          for (int h = 0; h < DH; ++h)
+            tma_load_2d(&tmQ, smem_u32(sQ + C::Q_BYTES + h * BM * 128), &q_full[1], h * 64, row_base + it.q0 + BM);
+          ++c1;
+        }
+        const int nkv = it.kv1;
+        auto load_k = [&](int tt, int j) {
+          const int s2 = tt & 1;
+          mbar_wait(&k_empty[s2], ((tt >> 1) & 1) ^ 1);
+          mbar_expect_tx(&k_full[s2], C::K_BYTES);
+#pragma unroll
+          for (int h = 0; h < DH; ++h)
+            tma_load_2d(&tmK, smem_u32(sK + s2 * C::K_BYTES + h * BN * 128), &k_full[s2], h * 64, row_base + j * BN);
+        };
+        load_k(t, 0);
+        for (int j = 0; j < nkv; ++j) {
+          if (j + 1 < nkv) load_k(t + j + 1, j + 1);
+          const int tt = t + j, s2 = tt & 1;
+          mbar_wait(&v_empty[s2], ((tt >> 1) & 1) ^ 1);
+          mbar_expect_tx(&v_full[s2], C::V_BYTES);
+#pragma unroll
+          for (int h = 0; h < DH; ++h)
+            tma_load_2d(&tmV, smem_u32(sV + s2 * C::V_BYTES + h * BN * 128), &v_full[s2], h * 64, row_base + j * BN);
+        }
+        t += nkv;
+      }
+    }
+  } else if (warp == 9) {
+    if (lane == 0) {
+      // ---------------- MMA issuer
+      int t = 0, c0 = 0, c1 = 0;
+      int n0 = 0, n1 = 0;  // P V count per slot (pv_done barrier n & 1)
+      auto issue_s = [&](int k, int tt) {  // S_k = Q_k K_tt^T
+        const int s2 = tt & 1;
+        const uint32_t tS = tmem_base + (uint32_t)(k * BN);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t off = (kk & 3) * 32;
+          const uint64_t a = umma_desc_sw128(smem_u32(sQ + k * C::Q_BYTES + (kk >> 2) * BM * 128 + off));
+          const uint64_t bb = umma_desc_sw128(smem_u32(sK + s2 * C::K_BYTES + (kk >> 2) * BN * 128 + off));
+          umma_bf16(tS, a, bb, C::IDESC_S, kk > 0 ? 1u : 0u);
+        }
+        umma_commit(&s_full[k]);
+      };
+      long long* trace = blockIdx.x == 0 ? g_attn_trace : nullptr;
+      auto issue_pv = [&](int k, int tt, bool first) {  // O_k (+)= P_k V_tt
+        const int s2 = tt & 1;
+        int& n = k ? n1 : n0;
+        mbar_wait(&p_full[k], n & 1);
+        if (trace && n < 64) trace[(k * 64 + n) * 4 + 2] = clk64();
+        tc_fence_after();
+        const uint32_t tP = tmem_base + (uint32_t)(k * BN);
+        const uint32_t tO = tmem_base + (uint32_t)(2 * BN + k * D);
+#pragma unroll
+        for (int kk = 0; kk < BN / 16; ++kk) {
+          const uint64_t bb = umma_desc_sw128_mn(smem_u32(sV + s2 * C::V_BYTES + kk * 16 * 128), BN * 128);
+          umma_bf16_ts(tO, tP + (uint32_t)(kk * 8), bb, C::IDESC_O, (!first || kk > 0) ? 1u : 0u);
+        }
+        umma_commit(&pv_done[2 * k + (n & 1)]);
+        ++n;
+      };
+      for (int qi = 0, w = item_at(0); w < items; w = item_at(++qi)) {
+        const Item3 it = decode(w);
+        const int nkv = it.kv1;
+        // prologue: S0_0 (and S1_0) on K_0
+        mbar_wait(&k_full[t & 1], (t >> 1) & 1);
+        mbar_wait(&q_full[0], c0 & 1);
+        tc_fence_after();
+        issue_s(0, t);
+        if (it.kv0 == 1) umma_commit(&q_empty[0]);
+        if (it.q1) {
+          mbar_wait(&q_full[1], c1 & 1);
+          tc_fence_after();
+          issue_s(1, t);
+          if (it.kv1 == 1) umma_commit(&q_empty[1]);
+        }
+        umma_commit(&k_empty[t & 1]);
+        for (int j = 0; j < nkv; ++j) {
+          const int tt = t + j;
+          const bool next = j + 1 < nkv;
+          if (next) mbar_wait(&k_full[(tt + 1) & 1], ((tt + 1) >> 1) & 1);
+          mbar_wait(&v_full[tt & 1], (tt >> 1) & 1);
+          if (j < it.kv0) {
+            if (j == 0) mbar_wait(&o_empty[0], (c0 & 1) ^ 1);
+            issue_pv(0, tt, j == 0);
+            if (j + 1 < it.kv0) {
+              issue_s(0, tt + 1);
+              if (j + 2 == it.kv0) umma_commit(&q_empty[0]);
+            }
+            if (trace && n0 - 1 < 64) trace[(n0 - 1) * 4 + 3] = clk64();
+          }
+          if (it.q1) {
+            if (j == 0) mbar_wait(&o_empty[1], (c1 & 1) ^ 1);
+            issue_pv(1, tt, j == 0);
+            if (next) {
+              issue_s(1, tt + 1);
+              if (j + 2 == it.kv1) umma_commit(&q_empty[1]);
+            }
+            if (trace && n1 - 1 < 64) trace[(64 + n1 - 1) * 4 + 3] = clk64();
+          }
+          umma_commit(&v_empty[tt & 1]);
+          if (next) umma_commit(&k_empty[(tt + 1) & 1]);
+        }
+        t += nkv;
+        ++c0;
+        if (it.q1) ++c1;
+      }
+    }
+  }
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 208;");
+    // ---------------- softmax warpgroup k = warp / 4: thread owns query row r of Q tile k (TMEM lane r)
+    const int k = warp >> 2, qd = warp & 3;
+    const int r = qd * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(qd * 32) << 16;
+    const uint32_t tS = tmem_base + lane_off + (uint32_t)(k * BN);
+    const uint32_t tO = tmem_base + lane_off + (uint32_t)(2 * BN + k * D);
+    int t = 0, n = 0, c = 0;  // global K/V tile, this slot's P V count, this slot's item count
+    long long* trace = (blockIdx.x == 0 && qd == 0 && lane == 0) ? g_attn_trace : nullptr;
+    for (int qi = 0, w = item_at(0); w < items; w = item_at(++qi)) {
+      const Item3 it = decode(w);
+      const int nkv = it.kv1;
+      if (k == 1 && !it.q1) {
+        t += nkv;
+        continue;
+      }
+      const int kv = k == 0 ? it.kv0 : it.kv1;
+      const int len = it.len;
+      const int qrow0 = it.q0 + k * BM + qd * 32;  // this warp's first query row
+      const int srow = qrow0 + lane;
+      const bool dead = qrow0 >= len;  // warp-uniform: none of the warp's rows is a query
+      // keys a row may see: [0, lim_row); the warp's union: [0, lim_warp)
+      const int lim_row = causal ? min(len, srow + 1) : len;
+      const int lim_warp = causal ? min(len, qrow0 + 32) : len;
+      float m_ref = -INFINITY, l = 0.f;
+      for (int j = 0; j < kv; ++j, ++n) {
+        const int tt = t + j, s2 = tt & 1;
+        const int k0 = j * BN;
+        mbar_wait(&s_full[k], n & 1);
+        if (trace && n < 64) trace[(k * 64 + n) * 4 + 0] = clk64();
+        __syncwarp();
+        tc_fence_after();
+        bool seen_prev = j == 0;
+        if (!dead) {
+          uint32_t sr[4][32];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) tmem_ld32_nowait(tS + q * 32, sr[q]);
+          tmem_wait_ld();
+          const int lim = lim_row - k0;   // this row: keys c < lim allowed
+          const int wl = lim_warp - k0;   // chunks q with 32 q >= wl are empty for the whole warp
+          float mx[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) mx[e] = -INFINITY;
+          if (__any_sync(0xffffffffu, lim < BN)) {
+#pragma unroll
+            for (int cc = 0; cc < BN; ++cc) {
+              float v = __uint_as_float(sr[cc >> 5][cc & 31]);
+              if (cc >= lim) v = -INFINITY;
+              sr[cc >> 5][cc & 31] = __float_as_uint(v);
+              mx[cc & 7] = fmaxf(mx[cc & 7], v);
+            }
+          } else {
+#pragma unroll
+            for (int cc = 0; cc < BN; ++cc) mx[cc & 7] = fmaxf(mx[cc & 7], __uint_as_float(sr[cc >> 5][cc & 31]));
+          }
+          float mt = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])), fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+          mt *= scale_log2;
+          const bool grow = mt > m_ref + 8.f;
+          const float alpha = !grow ? 1.f : (m_ref == -INFINITY) ? 0.f : ex2f(m_ref - mt);
+          if (j > 0 && __any_sync(0xffffffffu, grow)) {
+            // O_k must hold P_{j-1} V_{j-1} before it is rescaled
+            mbar_wait(&pv_done[2 * k + ((n - 1) & 1)], ((n - 1) >> 1) & 1);
+            seen_prev = true;
+            __syncwarp();
+            tc_fence_after();
+#pragma unroll 1
+            for (int cd = 0; cd < D; cd += 32) {
+              uint32_t o[32];
+              tmem_ld32(tO + cd, o);
+#pragma unroll
+              for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+              tmem_st32(tO + cd, o);
+            }
+          }
+          if (grow) {
+            l *= alpha;
+            m_ref = mt;
+          }
+          const float base = (m_ref == -INFINITY) ? 0.f : m_ref;
+          float ls[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {  // 32 keys -> 16 packed bf16x2, in place -> one 16-column TMEM store
+            if (32 * q < wl) {
+#pragma unroll
+              for (int e = 0; e < 32; e += 2) {
+                const float p0 = ex2f(fmaf(__uint_as_float(sr[q][e]), scale_log2, -base));
+                const float p1 = ex2f(fmaf(__uint_as_float(sr[q][e + 1]), scale_log2, -base));
+                ls[(e >> 1) & 3] += p0 + p1;
+                sr[q][e >> 1] = pack_bf16x2(p0, p1);
+              }
+            } else {
+#pragma unroll
+              for (int e = 0; e < 16; ++e) sr[q][e] = 0u;
+            }
+            tmem_st16_nowait(tS + q * 16, sr[q]);
+          }
+          tmem_wait_st();
+          l += (ls[0] + ls[1]) + (ls[2] + ls[3]);
+        }
+        if (k0 + BN > len) {  // zero V rows of keys >= len (pad rows a5 never wrote may hold NaN)
+          mbar_wait(&v_full[s2], (tt >> 1) & 1);
+          if (k0 + r >= len) {
+#pragma unroll
+            for (int h = 0; h < DH; ++h) {
+              uint4* vr = reinterpret_cast<uint4*>(sV + s2 * C::V_BYTES + h * BN * 128 + r * 128);
+#pragma unroll
+              for (int c8 = 0; c8 < 8; ++c8) vr[c8] = make_uint4(0, 0, 0, 0);
+            }
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[k]);
+        if (trace && n < 64) trace[(k * 64 + n) * 4 + 1] = clk64();
+        if (!dead && !seen_prev) mbar_wait(&pv_done[2 * k + ((n - 1) & 1)], ((n - 1) >> 1) & 1);
+      }
+      // ---------------- epilogue of this Q tile: O / l -> packed context rows (or padded O rows)
+      if (!dead) {
+        mbar_wait(&pv_done[2 * k + ((n - 1) & 1)], ((n - 1) >> 1) & 1);
+        __syncwarp();
+        tc_fence_after();
+        const float inv = 1.f / l;
+        const bool valid = srow < len;
+        bf16* dst = Cp ? Cp + ((int64_t)__ldg(offsets + it.b) + srow) * (int64_t)(hk * D) + it.head * D
+                       : Opad + ((int64_t)(it.b * hk + it.head) * S + srow) * D;
+#pragma unroll 1
+        for (int cd = 0; cd < D; cd += 64) {
+          uint32_t o[2][32];
+          tmem_ld32_nowait(tO + cd, o[0]);
+          tmem_ld32_nowait(tO + cd + 32, o[1]);
+          tmem_wait_ld();
+          if (valid) {
+#pragma unroll
+            for (int e = 0; e < 64; e += 8) {
+              const uint32_t* oe = &o[e >> 5][e & 31];
+              uint4 pq;
+              pq.x = pack_bf16x2(__uint_as_float(oe[0]) * inv, __uint_as_float(oe[1]) * inv);
+              pq.y = pack_bf16x2(__uint_as_float(oe[2]) * inv, __uint_as_float(oe[3]) * inv);
+              pq.z = pack_bf16x2(__uint_as_float(oe[4]) * inv, __uint_as_float(oe[5]) * inv);
+              pq.w = pack_bf16x2(__uint_as_float(oe[6]) * inv, __uint_as_float(oe[7]) * inv);
+              *reinterpret_cast<uint4*>(dst + cd + e) = pq;
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&o_empty[k]);
+      t += nkv;
+      ++c;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 9) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(512));
+  }
+}
+
+static bool attn_maps(AttnMaps* m, const bf16* Q, const bf16* K, const bf16* V, int rows, int D, int bm, int bn) {
+  if (!m->valid || m->q != Q || m->k != K || m->v != V || m->rows != rows || m->d != D || m->bn != bn) {
+    // cached per context: the maps depend only on the buffers, B * hk * S and the key-tile box
+    if (!make_tmap_kmajor(&m->mq, Q, rows, D, bm) || !make_tmap_kmajor(&m->mk, K, rows, D, bn) ||
+        !make_tmap_kmajor(&m->mv, V, rows, D, bn)) {
       m->valid = false;
       return false;
     }
@@ -409,8 +820,53 @@ static bool launch_tc(const bf16* Q, const bf16* K, const bf16* V, bf16* Cp, con
     m->v = V;
     m->rows = rows;
     m->d = D;
+    m->bn = bn;
     m->valid = true;
   }
+  return true;
+}
+
+template <int D>
+static bool launch_tc(const bf16* Q, const bf16* K, const bf16* V, bf16* Cp, const int* offsets, bf16* Opad,
+                      const int* lens_d, const uint32_t* work_d, int B, int hk, int S, int causal, cudaStream_t st,
+                      AttnMaps* maps) {
+  const int rows = B * hk * S;
+  AttnMaps local;
+  AttnMaps* m = maps ? maps : &local;
+  const float scale_log2 = 1.4426950408889634f / sqrtf((float)D);
+  if (attention_impl() == 5) {
+    using C = Attn3Cfg<D>;
+    if (!attn_maps(m, Q, K, V, rows, D, C::BM, C::BN)) return false;
+    static std::atomic<uint64_t> attr{0};
+    smem_attr_once(attention_tc3_kernel<D>, C::SMEM, attr);
+    // persistent grid: one CTA per SM (512 TMEM columns, ~197 KB of shared memory), no more than the
+    // largest possible item count (B sequences x ceil(S / 256) query-tile pairs x hk heads)
+    const int64_t max_items = (int64_t)B * ((S + 2 * C::BM - 1) / (2 * C::BM)) * hk;
+    const int grid = max_items < num_sms() ? (int)max_items : num_sms();
+    if (grid <= 0) return true;
+    static const char* trace_file = getenv("ENERGON_ATTN_TRACE");
+    static long long* trace_buf = nullptr;
+    if (trace_file && !trace_buf) {
+      cudaMalloc(&trace_buf, 2 * 64 * 4 * sizeof(long long));
+      cudaMemcpyToSymbol(g_attn_trace, &trace_buf, sizeof(trace_buf));
+    }
+    if (trace_buf) cudaMemsetAsync(trace_buf, 0, 2 * 64 * 4 * sizeof(long long), st);
+    launch_k(attention_tc3_kernel<D>, dim3(grid), dim3(C::THREADS), C::SMEM, st, m->mq, m->mk, m->mv, Cp, offsets,
+             Opad, lens_d, work_d, hk, S, causal, scale_log2);
+    if (trace_buf) {  // diagnostics only: synchronous dump
+      long long h[2 * 64 * 4];
+      cudaMemcpy(h, trace_buf, sizeof(h), cudaMemcpyDeviceToHost);
+      if (FILE* f = fopen(trace_file, "a")) {
+        fprintf(f, "launch B=%d hk=%d S=%d\n", B, hk, S);
+        for (int i = 0; i < 2 * 64; ++i)
+          if (h[i * 4]) fprintf(f, "%d %d %lld %lld %lld %lld\n", i / 64, i % 64, h[i * 4], h[i * 4 + 1], h[i * 4 + 2], h[i * 4 + 3]);
+        fclose(f);
+      }
+    }
+    return true;
+  }
+  using C = Attn2Cfg<D>;
+  if (!attn_maps(m, Q, K, V, rows, D, C::BM, C::BN)) return false;
   static std::atomic<uint64_t> attr{0};
   smem_attr_once(attention_tc2_kernel<D>, C::SMEM, attr);
   // persistent grid: 2 CTAs per SM (shared memory and 256 TMEM columns each), no more than the largest
@@ -419,7 +875,6 @@ static bool launch_tc(const bf16* Q, const bf16* K, const bf16* V, bf16* Cp, con
   const int slots = 2 * num_sms();
   const int grid = max_items < slots ? (int)max_items : slots;
   if (grid <= 0) return true;
-  const float scale_log2 = 1.4426950408889634f / sqrtf((float)D);
   launch_k(attention_tc2_kernel<D>, dim3(grid), dim3(192), C::SMEM, st, m->mq, m->mk, m->mv, Cp, offsets, Opad, lens_d,
            work_d, hk, S, causal, scale_log2);
   return true;

@@ -134,7 +134,7 @@ void launch_convert_vec(const Src* src, int64_t off, int N, Dst* dst, cudaStream
 struct AttnMaps {
   CUtensorMap mq, mk, mv;
   const void *q = nullptr, *k = nullptr, *v = nullptr;
-  int rows = 0, d = 0;
+  int rows = 0, d = 0, bn = 0;
   bool valid = false;
 };
 int attention_tile_bm();  // query rows of one work item of the tcgen05 kernel
@@ -151,7 +151,7 @@ bool launch_attention_packed(const bf16* Q, const bf16* K, const bf16* V, bf16* 
 bool launch_attention_tc(const bf16* Q, const bf16* K, const bf16* V, bf16* ctx_packed, const int* offsets,
                          bf16* O_padded, const int* lens_d, const uint32_t* work_d, int B, int hk, int S, int d,
                          int causal, cudaStream_t st, AttnMaps* maps);
-int attention_impl();  // ENERGON_ATTN (A/B): 4 = tcgen05 (default)
+int attention_impl();  // ENERGON_ATTN (A/B): 4 = tcgen05 v2 (default), 5 = tcgen05 v3 (one CTA per SM, two Q tiles)
 
 // GEMM epilogues.  EPI_BIAS_QKV = bias, then a5 fused: the packed QKV row t / column block is
 // scattered straight into the padded per-head Q, K, V [B, hk, S, d] (needs d % 32 == 0).

@@ -1,0 +1,17 @@
+# Round 2, call i: evidence at HEAD (stream-K GEMM): full GPU suite, smoke, default bench, launch list,
+# ncu --set full of two layers, attention microbench, local TP=8 step.
+mkdir -p gpurun_out
+timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider --durations=10 > gpurun_out/pytest_gpu_r2i.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/pytest_gpu_r2i.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2
+timeout 900 python bench.py > gpurun_out/bench_r2i.json 2>gpurun_out/bench_r2i.err; python -c "
+import json; d=json.load(open('gpurun_out/bench_r2i.json')); print(d['value'], d['ms_per_step'], d['e2e']['value'], d['roofline'], d['clocks'])"
+export ENERGON_PROFILE_RANGE=1
+timeout 900 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_r2i.csv python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-ab --graph 0 > gpurun_out/ncu_launch_run.log 2>&1
+timeout 900 ncu --profile-from-start off --set full --clock-control none --import-source on -c 9 -o gpurun_out/prof_full_r2i -f python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-ab --layers 2 --graph 0 > gpurun_out/ncu_full_run.log 2>&1
+python scripts/ncu_summary.py launches gpurun_out/launches_r2i.csv > gpurun_out/launches_summary_r2i.md
+python scripts/ncu_summary.py full gpurun_out/prof_full_r2i.ncu-rep > gpurun_out/full_summary_r2i.md
+cat gpurun_out/launches_summary_r2i.md | head -30
+unset ENERGON_PROFILE_RANGE
+timeout 300 python scripts/bench_attn.py 2>&1 | tail -6 > gpurun_out/attn_bench_r2i.txt; cat gpurun_out/attn_bench_r2i.txt
+timeout 900 python bench.py --local-tp 8 --no-cpu-baseline --no-ab --no-e2e --steps 5 > gpurun_out/bench_ltp8_r2i.json 2>/dev/null; python -c "
+import json; d=json.load(open('gpurun_out/bench_ltp8_r2i.json')); print('ltp8', d['ms_per_step'], json.dumps(d['phases']), d['clocks'])"

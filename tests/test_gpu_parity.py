@@ -292,12 +292,24 @@ def test_not_loaded():
 
 
 # ----------------------------------------------------------------------------- a6 attention kernel
+ATTN_LEN_CASES = {
+    # straddle the 64-key tiles of v2
+    "t64": (150, [1, 63, 64, 65, 130, 150], 3),
+    # straddle v3's 128-key tiles and 256-row items (Q tile 1 empty / one row / full, dead warps)
+    "t128": (520, [1, 31, 32, 127, 128, 129, 160, 255, 256, 257, 385, 520], 2),
+}
+
+
 @pytest.mark.parametrize("dtype,d", [("bf16", 128), ("bf16", 64), ("f32", 64), ("bf16", 16)])
 @pytest.mark.parametrize("causal", [1, 0])
-def test_attention_kernel_vs_oracle(dtype, d, causal):
-    """Lengths straddling the 64-row tiles (1, 63, 64, 65, 130, S) incl. NaN in every pad row of K/V."""
-    B, hk, S = 6, 3, 150
-    lens = [1, 63, 64, 65, 130, 150]
+@pytest.mark.parametrize("lcase", ["t64", "t128"])
+def test_attention_kernel_vs_oracle(dtype, d, causal, lcase):
+    """Lengths straddling the key tiles and query items of both tcgen05 kernels, incl. NaN in every pad row
+    of Q/K/V."""
+    if lcase == "t128" and dtype == "f32":
+        pytest.skip("the SIMT fp32 kernel has no tiles; t64 covers it")
+    S, lens, hk = ATTN_LEN_CASES[lcase]
+    B = len(lens)
     g = torch.Generator(device="cpu").manual_seed(d + causal)
     tdt = torch_dtype(dtype)
     Qh, Kh, Vh = ((torch.randn(B, hk, S, d, generator=g) * s).to(tdt) for s in (1.0, 1.0, 1.0))
