@@ -484,9 +484,9 @@ __global__ void __launch_bounds__(384, 1)
       mbar_init(&pv_done[2 * i], 1);
       mbar_init(&pv_done[2 * i + 1], 1);
       mbar_init(&k_full[i], 1);
-      mbar_init(&k_empty[i], 1);
+      mbar_init(&k_empty[i], 2);  // both slots' MMA threads release every K / V tile
       mbar_init(&v_full[i], 1);
-      mbar_init(&v_empty[i], 1);
+      mbar_init(&v_empty[i], 2);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -523,24 +523,32 @@ __global__ void __launch_bounds__(384, 1)
   asm volatile("setmaxnreg.dec.sync.aligned.u32 88;");
   if (warp == 8) {
     if (lane == 0) {
-      // ---------------- TMA producer: per item Q0 (and Q1), then K_0, K_1, V_0, K_2, V_1, ...
+      // ---------------- TMA producer: K_0, K_1, V_0, K_2, V_1, ... per item; the NEXT item's Q0 is loaded
+      // right after this item's V_{n-2} (Q0 is free once slot 0's last S is done, which needs nothing loaded
+      // later) and its Q1 right after V_{n-1}, so a slot's next item never waits for a Q load after its epilogue.
       int t = 0, c0 = 0, c1 = 0;
-      for (int qi = 0, w = item_at(0); w < items; w = item_at(++qi)) {
-        const Item3 it = decode(w);
+      auto load_q = [&](const Item3& it, int k) {
+        int& c = k ? c1 : c0;
+        mbar_wait(&q_empty[k], (c & 1) ^ 1);
+        mbar_expect_tx(&q_full[k], C::Q_BYTES);
+        const int row = (it.b * hk + it.head) * S + it.q0 + k * BM;
+#pragma unroll
+        for (int h = 0; h < DH; ++h)
+          tma_load_2d(&tmQ, smem_u32(sQ + k * C::Q_BYTES + h * BM * 128), &q_full[k], h * 64, row);
+        ++c;
+      };
+      int qi = 0, w = item_at(0);
+      Item3 it;
+      if (w < items) {
+        it = decode(w);
+        load_q(it, 0);
+        if (it.q1) load_q(it, 1);
+      }
+      while (w < items) {
+        const int wn = item_at(qi + 1);
+        Item3 nx;
+        if (wn < items) nx = decode(wn);
         const int row_base = (it.b * hk + it.head) * S;
-        mbar_wait(&q_empty[0], (c0 & 1) ^ 1);
-        mbar_expect_tx(&q_full[0], C::Q_BYTES);
-#pragma unroll
-        for (int h = 0; h < DH; ++h) tma_load_2d(&tmQ, smem_u32(sQ + h * BM * 128), &q_full[0], h * 64, row_base + it.q0);
-        ++c0;
-        if (it.q1) {
-          mbar_wait(&q_empty[1], (c1 & 1) ^ 1);
-          mbar_expect_tx(&q_full[1], C::Q_BYTES);
-#pragma unroll
-          for (int h = 0; h < DH; ++h)
-            tma_load_2d(&tmQ, smem_u32(sQ + C::Q_BYTES + h * BM * 128), &q_full[1], h * 64, row_base + it.q0 + BM);
-          ++c1;
-        }
         const int nkv = it.kv1;
         auto load_k = [&](int tt, int j) {
           const int s2 = tt & 1;
@@ -559,18 +567,31 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
           for (int h = 0; h < DH; ++h)
             tma_load_2d(&tmV, smem_u32(sV + s2 * C::V_BYTES + h * BN * 128), &v_full[s2], h * 64, row_base + j * BN);
+          if (wn < items) {
+            if (j == max(nkv - 2, 0)) load_q(nx, 0);
+            if (j == nkv - 1 && nx.q1) load_q(nx, 1);
+          }
         }
         t += nkv;
+        ++qi;
+        w = wn;
+        it = nx;
       }
     }
-  } else if (warp == 9) {
+  } else if (warp == 9 || warp == 10) {
     if (lane == 0) {
-      // ---------------- MMA issuer
-      int t = 0, c0 = 0, c1 = 0;
-      int n0 = 0, n1 = 0;  // P V count per slot (pv_done barrier n & 1)
-      auto issue_s = [&](int k, int tt) {  // S_k = Q_k K_tt^T
+      // ---------------- MMA issuer of slot k (one thread per Q tile, so neither slot's chain
+      // softmax -> P V -> next S waits for the other's).  Per item it issues S_0, then per key tile j:
+      // P_j V_j, S_{j+1}; K / V stages are released (count 2) by both slots for every tile -- by the
+      // commit of the MMAs that read it, or by a plain arrival (after the stage's full barrier, so the
+      // arrival falls in the right phase) for a tile the slot does not use.
+      const int k = warp - 9;
+      int t = 0, c = 0, n = 0;  // K/V tile, this slot's item count, this slot's P V count
+      const uint32_t tS = tmem_base + (uint32_t)(k * BN);
+      const uint32_t tO = tmem_base + (uint32_t)(2 * BN + k * D);
+      long long* trace = blockIdx.x == 0 ? g_attn_trace : nullptr;
+      auto issue_s = [&](int tt) {  // S_k = Q_k K_tt^T
         const int s2 = tt & 1;
-        const uint32_t tS = tmem_base + (uint32_t)(k * BN);
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
           const uint32_t off = (kk & 3) * 32;
@@ -579,69 +600,54 @@ __global__ void __launch_bounds__(384, 1)
           umma_bf16(tS, a, bb, C::IDESC_S, kk > 0 ? 1u : 0u);
         }
         umma_commit(&s_full[k]);
-      };
-      long long* trace = blockIdx.x == 0 ? g_attn_trace : nullptr;
-      auto issue_pv = [&](int k, int tt, bool first) {  // O_k (+)= P_k V_tt
-        const int s2 = tt & 1;
-        int& n = k ? n1 : n0;
-        mbar_wait(&p_full[k], n & 1);
-        if (trace && n < 64) trace[(k * 64 + n) * 4 + 2] = clk64();
-        tc_fence_after();
-        const uint32_t tP = tmem_base + (uint32_t)(k * BN);
-        const uint32_t tO = tmem_base + (uint32_t)(2 * BN + k * D);
-#pragma unroll
-        for (int kk = 0; kk < BN / 16; ++kk) {
-          const uint64_t bb = umma_desc_sw128_mn(smem_u32(sV + s2 * C::V_BYTES + kk * 16 * 128), BN * 128);
-          umma_bf16_ts(tO, tP + (uint32_t)(kk * 8), bb, C::IDESC_O, (!first || kk > 0) ? 1u : 0u);
-        }
-        umma_commit(&pv_done[2 * k + (n & 1)]);
-        ++n;
+        umma_commit(&k_empty[s2]);
       };
       for (int qi = 0, w = item_at(0); w < items; w = item_at(++qi)) {
         const Item3 it = decode(w);
         const int nkv = it.kv1;
-        // prologue: S0_0 (and S1_0) on K_0
-        mbar_wait(&k_full[t & 1], (t >> 1) & 1);
-        mbar_wait(&q_full[0], c0 & 1);
-        tc_fence_after();
-        issue_s(0, t);
-        if (it.kv0 == 1) umma_commit(&q_empty[0]);
-        if (it.q1) {
-          mbar_wait(&q_full[1], c1 & 1);
+        const bool act = k == 0 || it.q1;
+        const int kv = act ? (k == 0 ? it.kv0 : it.kv1) : 0;
+        if (kv > 0) {
+          mbar_wait(&k_full[t & 1], (t >> 1) & 1);
+          mbar_wait(&q_full[k], c & 1);
           tc_fence_after();
-          issue_s(1, t);
-          if (it.kv1 == 1) umma_commit(&q_empty[1]);
+          issue_s(t);
+          if (kv == 1) umma_commit(&q_empty[k]);
         }
-        umma_commit(&k_empty[t & 1]);
         for (int j = 0; j < nkv; ++j) {
-          const int tt = t + j;
-          const bool next = j + 1 < nkv;
-          if (next) mbar_wait(&k_full[(tt + 1) & 1], ((tt + 1) >> 1) & 1);
-          mbar_wait(&v_full[tt & 1], (tt >> 1) & 1);
-          if (j < it.kv0) {
-            if (j == 0) mbar_wait(&o_empty[0], (c0 & 1) ^ 1);
-            issue_pv(0, tt, j == 0);
-            if (j + 1 < it.kv0) {
-              issue_s(0, tt + 1);
-              if (j + 2 == it.kv0) umma_commit(&q_empty[0]);
+          const int tt = t + j, s2 = tt & 1;
+          if (j < kv) {
+            mbar_wait(&v_full[s2], (tt >> 1) & 1);
+            if (j == 0) mbar_wait(&o_empty[k], (c & 1) ^ 1);
+            mbar_wait(&p_full[k], n & 1);
+            if (trace && n < 64) trace[(k * 64 + n) * 4 + 2] = clk64();
+            tc_fence_after();
+#pragma unroll
+            for (int kk = 0; kk < BN / 16; ++kk) {
+              const uint64_t bb = umma_desc_sw128_mn(smem_u32(sV + s2 * C::V_BYTES + kk * 16 * 128), BN * 128);
+              umma_bf16_ts(tO, tS + (uint32_t)(kk * 8), bb, C::IDESC_O, (j > 0 || kk > 0) ? 1u : 0u);
             }
-            if (trace && n0 - 1 < 64) trace[(n0 - 1) * 4 + 3] = clk64();
-          }
-          if (it.q1) {
-            if (j == 0) mbar_wait(&o_empty[1], (c1 & 1) ^ 1);
-            issue_pv(1, tt, j == 0);
-            if (next) {
-              issue_s(1, tt + 1);
-              if (j + 2 == it.kv1) umma_commit(&q_empty[1]);
+            umma_commit(&pv_done[2 * k + (n & 1)]);
+            umma_commit(&v_empty[s2]);
+            ++n;
+            if (j + 1 < kv) {
+              mbar_wait(&k_full[(tt + 1) & 1], ((tt + 1) >> 1) & 1);
+              tc_fence_after();
+              issue_s(tt + 1);
+              if (j + 2 == kv) umma_commit(&q_empty[k]);
             }
-            if (trace && n1 - 1 < 64) trace[(64 + n1 - 1) * 4 + 3] = clk64();
+            if (trace && n - 1 < 64) trace[(k * 64 + n - 1) * 4 + 3] = clk64();
+          } else {
+            // a tile this slot does not read: release its stages in phase (its K arrival for j == kv was not
+            // made by an S, since S_{kv} is never issued; j = 0 of an inactive slot likewise)
+            mbar_wait(&k_full[s2], (tt >> 1) & 1);
+            mbar_arrive(&k_empty[s2]);
+            mbar_wait(&v_full[s2], (tt >> 1) & 1);
+            mbar_arrive(&v_empty[s2]);
           }
-          umma_commit(&v_empty[tt & 1]);
-          if (next) umma_commit(&k_empty[(tt + 1) & 1]);
         }
         t += nkv;
-        ++c0;
-        if (it.q1) ++c1;
+        if (act) ++c;
       }
     }
   }
