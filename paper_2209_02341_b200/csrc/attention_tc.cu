@@ -469,8 +469,11 @@ __global__ void __launch_bounds__(384, 1)
   uint64_t* v_full = bars + 18;
   uint64_t* v_empty = bars + 20;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 22);
+  // softmax ping-pong: prog[q] = exponential passes finished by warp q of warpgroup 0 (SM sub-partition q)
+  volatile int* prog = reinterpret_cast<volatile int*>(bars + 23);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x < 4) prog[threadIdx.x] = 0;
   if (warp == 8 && lane == 0) {
     tma_prefetch_desc(&tmQ);
     tma_prefetch_desc(&tmK);
@@ -620,7 +623,7 @@ __global__ void __launch_bounds__(384, 1)
             mbar_wait(&v_full[s2], (tt >> 1) & 1);
             if (j == 0) mbar_wait(&o_empty[k], (c & 1) ^ 1);
             mbar_wait(&p_full[k], n & 1);
-            if (trace && n < 64) trace[(k * 64 + n) * 4 + 2] = clk64();
+            if (trace && n < 64) trace[(k * 64 + n) * 8 + 2] = clk64();
             tc_fence_after();
 #pragma unroll
             for (int kk = 0; kk < BN / 16; ++kk) {
@@ -636,7 +639,7 @@ __global__ void __launch_bounds__(384, 1)
               issue_s(tt + 1);
               if (j + 2 == kv) umma_commit(&q_empty[k]);
             }
-            if (trace && n - 1 < 64) trace[(k * 64 + n - 1) * 4 + 3] = clk64();
+            if (trace && n - 1 < 64) trace[(k * 64 + n - 1) * 8 + 3] = clk64();
           } else {
             // a tile this slot does not read: release its stages in phase (its K arrival for j == kv was not
             // made by an S, since S_{kv} is never issued; j = 0 of an inactive slot likewise)
@@ -660,8 +663,9 @@ __global__ void __launch_bounds__(384, 1)
     const uint32_t tS = tmem_base + lane_off + (uint32_t)(k * BN);
     const uint32_t tO = tmem_base + lane_off + (uint32_t)(2 * BN + k * D);
     int t = 0, n = 0, c = 0;  // global K/V tile, this slot's P V count, this slot's item count
+    int n0_base = 0;          // (warpgroup 1) warpgroup 0's tile count before this item
     long long* trace = (blockIdx.x == 0 && qd == 0 && lane == 0) ? g_attn_trace : nullptr;
-    for (int qi = 0, w = item_at(0); w < items; w = item_at(++qi)) {
+    for (int qi = 0, w = item_at(0); w < items; w = item_at(++qi), n0_base += decode(item_at(qi - 1)).kv0) {
       const Item3 it = decode(w);
       const int nkv = it.kv1;
       if (k == 1 && !it.q1) {
@@ -681,7 +685,7 @@ __global__ void __launch_bounds__(384, 1)
         const int tt = t + j, s2 = tt & 1;
         const int k0 = j * BN;
         mbar_wait(&s_full[k], n & 1);
-        if (trace && n < 64) trace[(k * 64 + n) * 4 + 0] = clk64();
+        if (trace && n < 64) trace[(k * 64 + n) * 8 + 0] = clk64();
         __syncwarp();
         tc_fence_after();
         bool seen_prev = j == 0;
@@ -690,6 +694,7 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
           for (int q = 0; q < 4; ++q) tmem_ld32_nowait(tS + q * 32, sr[q]);
           tmem_wait_ld();
+          if (trace && n < 64) trace[(k * 64 + n) * 8 + 4] = clk64();
           const int lim = lim_row - k0;   // this row: keys c < lim allowed
           const int wl = lim_warp - k0;   // chunks q with 32 q >= wl are empty for the whole warp
           float mx[8];
@@ -731,6 +736,15 @@ __global__ void __launch_bounds__(384, 1)
             m_ref = mt;
           }
           const float base = (m_ref == -INFINITY) ? 0.f : m_ref;
+          if (k == 1) {
+            // ping-pong: this warp's exponentials start only after the warpgroup-0 warp on the same SM
+            // sub-partition finished those of its tile j (its last one if it has fewer), so the two share
+            // the MUFU in turn and each slot's MMAs run while the other slot computes its exponentials.
+            // Warpgroup 0 never waits for warpgroup 1, so this cannot deadlock.
+            const int target = n0_base + min(j, it.kv0 - 1);
+            while (prog[qd] <= target) __nanosleep(20);
+          }
+          if (trace && n < 64) trace[(k * 64 + n) * 8 + 5] = clk64();
           float ls[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
           for (int q = 0; q < 4; ++q) {  // 32 keys -> 16 packed bf16x2, in place -> one 16-column TMEM store
@@ -748,9 +762,16 @@ __global__ void __launch_bounds__(384, 1)
             }
             tmem_st16_nowait(tS + q * 16, sr[q]);
           }
+          if (trace && n < 64) trace[(k * 64 + n) * 8 + 6] = clk64();
+          if (k == 0) {
+            __syncwarp();
+            if (lane == 0) prog[qd] = n + 1;
+          }
           tmem_wait_st();
+          if (trace && n < 64) trace[(k * 64 + n) * 8 + 7] = clk64();
           l += (ls[0] + ls[1]) + (ls[2] + ls[3]);
         }
+        if (dead && k == 0 && lane == 0) prog[qd] = n + 1;
         if (k0 + BN > len) {  // zero V rows of keys >= len (pad rows a5 never wrote may hold NaN)
           mbar_wait(&v_full[s2], (tt >> 1) & 1);
           if (k0 + r >= len) {
@@ -766,7 +787,7 @@ __global__ void __launch_bounds__(384, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[k]);
-        if (trace && n < 64) trace[(k * 64 + n) * 4 + 1] = clk64();
+        if (trace && n < 64) trace[(k * 64 + n) * 8 + 1] = clk64();
         if (!dead && !seen_prev) mbar_wait(&pv_done[2 * k + ((n - 1) & 1)], ((n - 1) >> 1) & 1);
       }
       // ---------------- epilogue of this Q tile: O / l -> packed context rows (or padded O rows)
@@ -853,19 +874,21 @@ static bool launch_tc(const bf16* Q, const bf16* K, const bf16* V, bf16* Cp, con
     static const char* trace_file = getenv("ENERGON_ATTN_TRACE");
     static long long* trace_buf = nullptr;
     if (trace_file && !trace_buf) {
-      cudaMalloc(&trace_buf, 2 * 64 * 4 * sizeof(long long));
+      cudaMalloc(&trace_buf, 2 * 64 * 8 * sizeof(long long));
       cudaMemcpyToSymbol(g_attn_trace, &trace_buf, sizeof(trace_buf));
     }
-    if (trace_buf) cudaMemsetAsync(trace_buf, 0, 2 * 64 * 4 * sizeof(long long), st);
+    if (trace_buf) cudaMemsetAsync(trace_buf, 0, 2 * 64 * 8 * sizeof(long long), st);
     launch_k(attention_tc3_kernel<D>, dim3(grid), dim3(C::THREADS), C::SMEM, st, m->mq, m->mk, m->mv, Cp, offsets,
              Opad, lens_d, work_d, hk, S, causal, scale_log2);
     if (trace_buf) {  // diagnostics only: synchronous dump
-      long long h[2 * 64 * 4];
+      long long h[2 * 64 * 8];
       cudaMemcpy(h, trace_buf, sizeof(h), cudaMemcpyDeviceToHost);
       if (FILE* f = fopen(trace_file, "a")) {
         fprintf(f, "launch B=%d hk=%d S=%d\n", B, hk, S);
         for (int i = 0; i < 2 * 64; ++i)
-          if (h[i * 4]) fprintf(f, "%d %d %lld %lld %lld %lld\n", i / 64, i % 64, h[i * 4], h[i * 4 + 1], h[i * 4 + 2], h[i * 4 + 3]);
+          if (h[i * 8])
+            fprintf(f, "%d %d %lld %lld %lld %lld %lld %lld %lld %lld\n", i / 64, i % 64, h[i * 8], h[i * 8 + 1], h[i * 8 + 2],
+                    h[i * 8 + 3], h[i * 8 + 4], h[i * 8 + 5], h[i * 8 + 6], h[i * 8 + 7]);
         fclose(f);
       }
     }
