@@ -4,6 +4,9 @@ Bars (BASELINE.json north_star): index maps bit-exact; max-abs-rel (SURVEY.md C1
 the fp32 mode and <= 2e-2 in the bf16 mode.  Inputs are seeded synthetic batches with the
 shapes of the paper's workloads.
 """
+import os
+import sys
+
 import numpy as np
 import pytest
 
@@ -331,6 +334,19 @@ def test_attention_kernel_vs_oracle(dtype, d, causal, lcase):
         assert np.isfinite(got[b, :, :n]).all()
         assert np.abs(got[b, :, :n] - ref[b, :, :n]).max() <= tol * max(1.0, np.abs(ref[b, :, :n]).max())
         assert (got[b, :, n:] == 7.0).all()  # pad query rows untouched
+
+
+@pytest.mark.skipif(os.environ.get("ENERGON_ATTN") == "5", reason="already the v3 run")
+def test_attention_v3_kernel_vs_oracle():
+    """The same attention cases through the v3 kernel (ENERGON_ATTN=5: one CTA per SM, two Q tiles sharing
+    K/V tiles), which a process selects once at load: run them in a child process."""
+    import subprocess
+    env = dict(os.environ, ENERGON_ATTN="5")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider", "-x", "-m", "gpu",
+                        os.path.abspath(__file__), "-k", "test_attention_kernel_vs_oracle"],
+                       env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert " passed" in r.stdout
 
 
 # ----------------------------------------------------------------------------- a5 / a7 / a13 vs the oracle's maps
