@@ -37,6 +37,19 @@ __device__ __forceinline__ float ex2f(float x) {
   return y;
 }
 
+// 2^x on the FMA pipe (FA4's MUFU offload): x = j + f with j = round(x), |f| <= 1/2; 2^f by a degree-3
+// polynomial (max relative error ~1e-4, below the bf16 rounding of P, 2^-9); 2^j added to the exponent
+// bits.  x is clamped at -127 (a result of ~1e-38 instead of 0), so only unmasked keys may use it.
+__device__ __forceinline__ float ex2_poly(float x) {
+  x = fmaxf(x, -127.f);
+  const float t = x + 12582912.f;  // 1.5 * 2^23: round to nearest integer in the low mantissa bits
+  const float xr = t - 12582912.f;
+  const float f = x - xr;
+  const int j = __float_as_int(t) - 0x4B400000;
+  const float p = fmaf(fmaf(fmaf(0.0555041f, f, 0.2402265f), f, 0.6931472f), f, 1.0f);
+  return __int_as_float(__float_as_int(p) + (j << 23));
+}
+
 // MN-major (N contiguous) 128B-swizzled operand: 64-element rows of 128 B; SBO = 1024 B between
 // 8-row groups along K, LBO = distance between 64-wide blocks along N.
 __device__ __forceinline__ uint64_t umma_desc_sw128_mn(uint32_t saddr, uint32_t lbo_bytes) {
@@ -423,6 +436,10 @@ __device__ __forceinline__ long long clk64() {
   return t;
 }
 
+#ifndef ATTN3_EMU
+#define ATTN3_EMU 0  // keys of every 32 whose exponential runs on the FMA pipe in unmasked tiles (v3)
+#endif
+
 template <int D>
 struct Attn3Cfg {
   static constexpr int BM = 128, BN = 128, DH = D / 64;
@@ -700,7 +717,8 @@ __global__ void __launch_bounds__(384, 1)
           float mx[8];
 #pragma unroll
           for (int e = 0; e < 8; ++e) mx[e] = -INFINITY;
-          if (__any_sync(0xffffffffu, lim < BN)) {
+          const bool masked = __any_sync(0xffffffffu, lim < BN);
+          if (masked) {
 #pragma unroll
             for (int cc = 0; cc < BN; ++cc) {
               float v = __uint_as_float(sr[cc >> 5][cc & 31]);
@@ -749,12 +767,25 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
           for (int q = 0; q < 4; ++q) {  // 32 keys -> 16 packed bf16x2, in place -> one 16-column TMEM store
             if (32 * q < wl) {
+              if (!masked && ATTN3_EMU > 0) {
+                // unmasked tile: the last ATTN3_EMU keys of each 32 take 2^x on the FMA pipe, the rest on MUFU
 #pragma unroll
-              for (int e = 0; e < 32; e += 2) {
-                const float p0 = ex2f(fmaf(__uint_as_float(sr[q][e]), scale_log2, -base));
-                const float p1 = ex2f(fmaf(__uint_as_float(sr[q][e + 1]), scale_log2, -base));
-                ls[(e >> 1) & 3] += p0 + p1;
-                sr[q][e >> 1] = pack_bf16x2(p0, p1);
+                for (int e = 0; e < 32; e += 2) {
+                  const float x0 = fmaf(__uint_as_float(sr[q][e]), scale_log2, -base);
+                  const float x1 = fmaf(__uint_as_float(sr[q][e + 1]), scale_log2, -base);
+                  const float p0 = e >= 32 - ATTN3_EMU ? ex2_poly(x0) : ex2f(x0);
+                  const float p1 = e + 1 >= 32 - ATTN3_EMU ? ex2_poly(x1) : ex2f(x1);
+                  ls[(e >> 1) & 3] += p0 + p1;
+                  sr[q][e >> 1] = pack_bf16x2(p0, p1);
+                }
+              } else {
+#pragma unroll
+                for (int e = 0; e < 32; e += 2) {
+                  const float p0 = ex2f(fmaf(__uint_as_float(sr[q][e]), scale_log2, -base));
+                  const float p1 = ex2f(fmaf(__uint_as_float(sr[q][e + 1]), scale_log2, -base));
+                  ls[(e >> 1) & 3] += p0 + p1;
+                  sr[q][e >> 1] = pack_bf16x2(p0, p1);
+                }
               }
             } else {
 #pragma unroll
