@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--drce", type=int, default=1)
     ap.add_argument("--layers", type=int, default=None, help="override the layer count (debug only)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-tp-check", action="store_true",
+                    help="skip the post-timing TP = k checks (replicas bit-identical, TP = k vs TP = 1 on rank 0)")
     ap.add_argument("--no-ab", action="store_true", help="skip the DRCE-off (padded) A/B")
     ap.add_argument("--graph", type=int, default=None,
                     help="replay each forward as a CUDA graph (ENERGON_OPT_GRAPH); default on for one GPU, off "
@@ -261,6 +263,64 @@ class Engine:
     def destroy(self):
         for c in self.ctxs:
             self.e.energon_destroy(c)
+
+
+def tp_check(args, energon, eng, fwd, out, bt, shape, B, S, world, rank, dist, barrier, plumb):
+    """After the timed region of a TP = k run (k ranks, or a --local-tp group): (1) every rank's output of the
+    first batch is bit-identical (replicas: each packed row is reduced once, by its owner, and
+    every rank receives the same LayerNorm rows); (2) rank 0 runs the same batch through a TP = 1 context of
+    the same weights on its own GPU and reports max-abs-rel of the TP = k output against it
+    over the valid positions -- the north star's "TP = k equals TP = 1" property, measured over the real
+    exchange.  Not timed."""
+    import hashlib
+    import torch
+    import synth
+    fwd(0)
+    eng.sync()
+    torch.cuda.synchronize()
+    lens = bt["lens"]
+    digest = hashlib.sha256(out.view(torch.int16).cpu().numpy().tobytes()).hexdigest()
+    res = {"batch_seed": bt["seed"], "bar": 2e-2}
+    if dist is not None:
+        digs = [None] * world
+        dist.all_gather_object(digs, digest)
+        res["replicas_bit_identical"] = len(set(digs)) == 1
+    H, L = shape["H"], shape["L"]
+    full_bytes = 2 * (12 * H * H + 13 * H) * L + 2 * (shape["V"] + shape["max_seq"]) * H
+    if full_bytes > 100e9:
+        res["vs_tp1"] = f"skipped: a TP=1 copy ({full_bytes / 1e9:.0f} GB) does not fit next to the shard"
+        barrier()
+        return res
+    if rank == 0:
+        cfg1 = energon.make_config(L, H, shape["h"], shape["F"], shape["V"], shape["max_seq"], B * S, dtype="bf16",
+                                   drce=args.drce, tp_size=1, tp_rank=0, device=torch.cuda.current_device())
+        c1 = energon.energon_init(cfg1, None)
+        try:
+            emb = {n: synth.emb_tensor_device(n, H, shape["V"], shape["max_seq"], args.seed, True, torch.bfloat16)
+                   for n in synth.EMB_TENSORS}
+            energon.energon_load_embeddings(c1, emb["tok_emb"], emb["pos_emb"], emb["lnf_g"], emb["lnf_b"])
+            del emb
+            for l in range(L):
+                w = {n: synth.layer_tensor_device(n, l, H, shape["F"], args.seed, True, torch.bfloat16)
+                     for n in synth.LAYER_TENSORS}
+                energon.energon_load_layer_weights(c1, l, w)
+                del w
+            out1 = torch.empty_like(out)
+            energon.energon_forward(c1, bt["tok_d"], lens, out1, torch.cuda.current_stream())
+            energon.energon_sync(c1)
+            torch.cuda.synchronize()
+            num = den = 0.0
+            for b, n in enumerate(lens):
+                y, y1 = out[b, :n].float(), out1[b, :n].float()
+                num = max(num, (y - y1).abs().max().item())
+                den = max(den, y1.abs().max().item())
+            res["max_abs_rel_vs_tp1"] = num / den
+            res["pass"] = res["max_abs_rel_vs_tp1"] <= res["bar"] and res.get("replicas_bit_identical", True)
+        finally:
+            energon.energon_destroy(c1)
+            torch.cuda.empty_cache()
+    barrier()
+    return res
 
 
 def energon_arm(args, world, rank, local):
@@ -566,6 +626,9 @@ def energon_arm(args, world, rank, local):
         v, note = describe(run())
         result["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
                                   "sample": note, "cpu_model": cpu_model()}
+    if k_tp > 1 and not args.no_tp_check:
+        result["tp_check"] = tp_check(args, energon, eng, fwd, out, batches[0], shape, B, S, world, rank, dist, barrier,
+                                      plumb)
     if args.local_tp > 1:
         result["local_tp_emulation"] = (f"TP={args.local_tp} ranks run serially on ONE GPU (in-device reductions): "
                                         "per-rank kernel shapes of TP=k, not a TP=k latency")
