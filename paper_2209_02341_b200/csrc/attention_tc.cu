@@ -487,7 +487,8 @@ __global__ void __launch_bounds__(384, 1)
   uint64_t* v_empty = bars + 20;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 22);
   // softmax ping-pong: prog[q] = exponential passes finished by warp q of warpgroup 0 (SM sub-partition q)
-  volatile int* prog = reinterpret_cast<volatile int*>(bars + 23);
+  // (shared-memory atomics: a monotonic progress flag read by a spinning warp of another warpgroup)
+  int* prog = reinterpret_cast<int*>(bars + 23);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x < 4) prog[threadIdx.x] = 0;
@@ -760,7 +761,7 @@ __global__ void __launch_bounds__(384, 1)
             // the MUFU in turn and each slot's MMAs run while the other slot computes its exponentials.
             // Warpgroup 0 never waits for warpgroup 1, so this cannot deadlock.
             const int target = n0_base + min(j, it.kv0 - 1);
-            while (prog[qd] <= target) __nanosleep(20);
+            while (atomicAdd(&prog[qd], 0) <= target) __nanosleep(20);
           }
           if (trace && n < 64) trace[(k * 64 + n) * 8 + 5] = clk64();
           float ls[4] = {0.f, 0.f, 0.f, 0.f};
@@ -796,13 +797,13 @@ __global__ void __launch_bounds__(384, 1)
           if (trace && n < 64) trace[(k * 64 + n) * 8 + 6] = clk64();
           if (k == 0) {
             __syncwarp();
-            if (lane == 0) prog[qd] = n + 1;
+            if (lane == 0) atomicExch(&prog[qd], n + 1);
           }
           tmem_wait_st();
           if (trace && n < 64) trace[(k * 64 + n) * 8 + 7] = clk64();
           l += (ls[0] + ls[1]) + (ls[2] + ls[3]);
         }
-        if (dead && k == 0 && lane == 0) prog[qd] = n + 1;
+        if (dead && k == 0 && lane == 0) atomicExch(&prog[qd], n + 1);
         if (k0 + BN > len) {  // zero V rows of keys >= len (pad rows a5 never wrote may hold NaN)
           mbar_wait(&v_full[s2], (tt >> 1) & 1);
           if (k0 + r >= len) {
