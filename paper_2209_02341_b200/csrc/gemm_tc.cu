@@ -697,6 +697,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     // of unit f - 1 -- but never before this cluster's own early piece (unit 0) is published, so a cluster
     // never waits for another before publishing its own piece and the waits cannot chain.
     int pre_at = -2, pre_buf = 0;  // preload into buffer pre_buf once pre_at epilogues are done (-2: none)
+    int pre_first = 0;             // the target buffer is free once this many epilogues are done (f - 1)
     {
       WorkIter sc(cid, tp, nkb);
       int t2, k20, k21, kind2, n = 0, f = -1, e = -1;
@@ -707,6 +708,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       if (f >= 0) {
         pre_at = max(f - 1, e + 1);
         pre_buf = f & 1;
+        pre_first = max(f - 1, 0);
       }
     }
     uint64_t* etrace = (leader && warp == 4 && lane == 0) ? g_gemm_trace : nullptr;
@@ -714,6 +716,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     while (wi.next(tp, nkb, ncl, tile, kb0, kb1, kind)) {
       int m_blk, n_blk;
       raster(tile, num_m, num_n, group_m, m_blk, n_blk);
+      if (pre_at >= 0 && enu >= pre_first && enu < pre_at) {
+        // Opportunistic preload: while this unit's accumulator is still being computed, copy the partner's
+        // partial in as soon as it is published (a non-blocking check, so no cluster ever waits for another
+        // here and the waits cannot chain) -- the finisher's MMAs then start right after this unit's instead
+        // of after this unit's epilogue plus the ~4 us preload (traced on the TP = 8 QKV shape).
+        const uint32_t ta = smem_u32(&tfull[acc]);
+        for (;;) {
+          const int ready = __shfl_sync(0xffffffffu, mbar_try_wait(ta, acc_phase) ? 1 : 0, 0);
+          if (ready) break;
+          if (flag_set()) {
+            preload(pre_buf);
+            pre_at = -2;
+            break;
+          }
+        }
+      }
       if (enu == pre_at) preload(pre_buf);  // (pre_at == 0: f == 1 and no early piece -- a fresh buffer)
       mbar_wait(&tfull[acc], acc_phase);
       uint64_t* erec = (etrace && enu < 30) ? etrace + ((size_t)cid * 32 + enu) * 6 : nullptr;
