@@ -51,6 +51,8 @@ def parse():
                     help="SURVEY.md 8(d): the timed steps rotate over the batches of seeds seed..seed+seeds-1 "
                          "(new lengths and tokens every step); per-seed medians are reported")
     ap.add_argument("--drce", type=int, default=1)
+    ap.add_argument("--ln-fuse", type=int, default=0,
+                    help="N3 (TP = 1, bf16): LN1 / LN2 applied in the QKV / MLP-up GEMM prologues (ENERGON_OPT_LN_FUSE)")
     ap.add_argument("--layers", type=int, default=None, help="override the layer count (debug only)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-tp-check", action="store_true",
@@ -399,6 +401,8 @@ def energon_arm(args, world, rank, local):
     if args.graph is None:
         args.graph = 1 if world == 1 else 0
     eng.set_option(energon.OPT_GRAPH, args.graph)
+    if args.ln_fuse:
+        eng.set_option(energon.OPT_LN_FUSE, 1)
 
     stream = torch.cuda.current_stream()
     for bt in batches:
@@ -605,6 +609,8 @@ def energon_arm(args, world, rank, local):
     gpus_active = world if not share else 1
     config = workload_config(args, shape, bcfg, lens0, k_tp)
     config["seeds"] = seeds
+    if args.ln_fuse:
+        config["ln_fuse"] = True
     config["valid_tokens_per_step"] = tokens_timed / args.steps
     result = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
               "warmup": args.warmup, "warmup_steps_run": warm, "ms_per_step": total_ms / args.steps,

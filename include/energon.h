@@ -290,8 +290,14 @@ ENERGON_API energon_status energon_get_stats(const energon_ctx* ctx, energon_sta
  *                      payload -- each chunk's running sum travels rank s+1 -> ... -> s and is rounded to
  *                      the activation type after every hop -- instead of the fp32 rank-order sum (0,
  *                      default).  Lets one GPU check the parity of the NCCL exchange.
+ *   ENERGON_OPT_LN_FUSE  bf16, TP = 1, hidden % 64 == 0: 1 = FasterTransformer-style fusion (PAPER.md:572-576,
+ *                      SURVEY.md 8(f) N3): the residual kernels write only X and each row's (mean, rstd), and
+ *                      the QKV / MLP-up GEMMs build LN(X) in their prologue (bit-identical A, so identical
+ *                      output); 0 (default) = the residual kernel writes the bf16 LN output A.
+ *                      ENERGON_ERR_CONFIG outside that domain.
  */
-enum { ENERGON_OPT_DRCE = 1, ENERGON_OPT_TP_SP = 2, ENERGON_OPT_GRAPH = 3, ENERGON_OPT_RING_NUMERICS = 4 };
+enum { ENERGON_OPT_DRCE = 1, ENERGON_OPT_TP_SP = 2, ENERGON_OPT_GRAPH = 3, ENERGON_OPT_RING_NUMERICS = 4,
+       ENERGON_OPT_LN_FUSE = 5 };
 ENERGON_API energon_status energon_set_option(energon_ctx* ctx, int32_t option, int32_t value);
 
 /* Enable (1) / disable (0) per-launch CUDA-event timing; enabling resets the accumulators. */

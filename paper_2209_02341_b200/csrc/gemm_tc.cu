@@ -493,6 +493,208 @@ __device__ __forceinline__ void epi_store(float (&v)[32], int row, int n0, int M
   }
 }
 
+// ----------------------------------------------------------------------------- LN-prologue GEMM (N3)
+// FT-style fusion ("which we can also adopt"): the QKV / MLP-up GEMM
+// builds its A operand, LN(X), on the fly instead of reading the bf16 A the residual kernel would write.
+// The residual kernel then writes only X (fp32) and the row statistics (mean, rstd); four producer warps
+// (warps 8-11, 32 A-tile rows each) load the rows' 64 fp32 columns of each k-block, apply
+// (x - mean) * rstd * g + b with exactly the residual kernel's fp32 expression (so A is bit-identical),
+// round to bf16 and store into the stage in the 128B-swizzled K-major layout the TMA would have produced
+// (16-byte chunk c of row r at chunk c ^ (r & 7)); loads are coalesced (two rows' 256-byte k-block slices
+// per warp instruction) and the next k-block's loads are in flight while the current one is converted.  W still comes by TMA (warp 0).  1-CTA 128 x 256 tiles
+// (M = 128, N = 256), warps 1 (MMA), 2 (TMEM), 4-7 (epilogue) as in gemm_tc_kernel.
+struct LnA {
+  const float* X;       // [M, K] fp32 residual stream
+  const float2* stats;  // [M] (mean, rstd)
+  const float* g;       // [K] LayerNorm weight
+  const float* b;       // [K] LayerNorm bias
+};
+
+template <int EPI>
+__global__ void __launch_bounds__(384, 1)
+    gemm_ln_kernel(const __grid_constant__ CUtensorMap tmB, const LnA ln, bf16* __restrict__ D,
+                   const float* __restrict__ bias, int M, int N, int K, const QkvScatter qs) {
+  constexpr int BN = 256;
+  using C = TcCfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + C::STAGES * C::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + C::STAGES * C::B_BYTES);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tfull = empty + C::STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int num_m = (M + TC_BM - 1) / TC_BM, num_n = (N + BN - 1) / BN;
+  const int num_tiles = num_m * num_n;
+  const int nkb = (K + TC_BK - 1) / TC_BK;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmB);
+    for (int i = 0; i < C::STAGES; ++i) {
+      mbar_init(&full[i], 1 + 4);  // the W TMA (expect_tx) + the 4 A-producer warps
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                 "n"(C::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+  pdl_trigger();  // (after the TMEM allocation, see gemm_tc_kernel)
+
+  if (warp == 0) {
+    if (lane == 0) {
+      pdl_wait();
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int n_blk = tile / num_m;
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], C::B_BYTES);
+          tma_load_2d(&tmB, smem_u32(sB + stage * C::B_BYTES), &full[stage], kb * TC_BK, n_blk * BN);
+          if (++stage == C::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp >= 8) {
+    // ---------------- A producers: warp w builds rows [32 w, 32 w + 32) of every A stage, two rows per
+    // instruction (lanes 0-15: row 2i, lanes 16-31: row 2i+1, 16 B of the row's 256 B k-block slice each), so
+    // every load is a fully coalesced 2 x 256 B access; lane l owns columns [4 (l & 15), 4 (l & 15) + 4)
+    pdl_wait();  // X and the statistics are written by the previous kernel
+    const int w = warp - 8, hl = lane & 15, half = lane >> 4;
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      const int m_blk = tile % num_m;
+      const int rbase = m_blk * TC_BM + w * 32 + half;  // rows rbase + 2 i, i = 0..15
+      float2 st[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int row = rbase + 2 * i;
+        st[i] = row < M ? __ldg(ln.stats + row) : make_float2(0.f, 0.f);
+      }
+      auto load = [&](float4 (&x)[16], int kb) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int row = rbase + 2 * i;
+          x[i] = row < M ? __ldcg(reinterpret_cast<const float4*>(ln.X + (int64_t)row * K + kb * TC_BK) + hl)
+                         : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      };
+      float4 xc[16], xn[16];
+      load(xc, 0);
+      for (int kb = 0; kb < nkb; ++kb) {
+        if (kb + 1 < nkb) load(xn, kb + 1);
+        const int k0 = kb * TC_BK + 4 * hl;
+        const float4 gg = __ldg(reinterpret_cast<const float4*>(ln.g + k0));
+        const float4 bb = __ldg(reinterpret_cast<const float4*>(ln.b + k0));
+        mbar_wait(&empty[stage], phase ^ 1);
+        uint8_t* sa = sA + stage * C::A_BYTES;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int r = w * 32 + 2 * i + half;  // row within the tile
+          const float mean = st[i].x, rstd = st[i].y;
+          const float4 x = xc[i];
+          uint2 o;
+          o.x = pack_bf16x2((x.x - mean) * rstd * gg.x + bb.x, (x.y - mean) * rstd * gg.y + bb.y);
+          o.y = pack_bf16x2((x.z - mean) * rstd * gg.z + bb.z, (x.w - mean) * rstd * gg.w + bb.w);
+          // 128B swizzle: 16-byte chunk c of row r at chunk c ^ (r & 7); this lane's 8 bytes are half (hl & 1) of chunk hl / 2
+          *reinterpret_cast<uint2*>(sa + r * 128 + ((((hl >> 1) ^ (r & 7))) << 4) + ((hl & 1) << 3)) = o;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic-proxy stores -> the MMA's reads
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&full[stage]);
+        if (++stage == C::STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+#pragma unroll
+        for (int i = 0; i < 16; ++i) xc[i] = xn[i];
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint64_t a0 = umma_desc_sw128(smem_u32(sA + stage * C::A_BYTES));
+          const uint64_t b0 = umma_desc_sw128(smem_u32(sB + stage * C::B_BYTES));
+#pragma unroll
+          for (int k = 0; k < TC_BK / 16; ++k) umma_bf16(d_tmem, a0 + 2 * k, b0 + 2 * k, C::IDESC, (kb | k) != 0);
+          umma_commit(&empty[stage]);
+          if (++stage == C::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit(&tfull[acc]);
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    pdl_wait();
+    const int q = warp - 4;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      const int m_blk = tile % num_m, n_blk = tile / num_m;
+      mbar_wait(&tfull[acc], acc_phase);
+      __syncwarp();
+      tc_fence_after();
+      const int row = m_blk * TC_BM + q * 32 + lane;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t rr[32];
+        tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c * 32), rr);
+        float v[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(rr[j]);
+        epi_store<EPI>(v, row, n_blk * BN + c * 32, M, N, D, bias, qs);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(C::TMEM_COLS));
+  }
+}
+
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }  // the 8 epilogue warps
 
 // The finisher's preload of one warp: chunks [c0, c0 + nch) of 32 columns of its row (fp32 partial in the
@@ -1073,6 +1275,28 @@ static bool launch_bn_epi(const CUtensorMap& tmA, const CUtensorMap& tmB, const 
 #define BN256 256,
 #define BN192 192,
 #define BN128 128,
+
+bool launch_gemm_ln(const CUtensorMap& tmB, const float* X, const float2* stats, const float* g, const float* b,
+                    const float* bias, bf16* D, int M, int N, int K, int epi, cudaStream_t st, const QkvScatter* qkv) {
+  if (M <= 0 || N <= 0) return true;
+  if (K % TC_BK != 0) return false;  // the producers build whole 64-column k-blocks
+  QkvScatter qs{};
+  if (qkv) qs = *qkv;
+  const LnA ln{X, stats, g, b};
+  using C = TcCfg<256>;
+  const int tiles = ((M + TC_BM - 1) / TC_BM) * ((N + 255) / 256);
+  const int grid = tiles < num_sms() ? tiles : num_sms();
+  static std::atomic<uint64_t> attr[4];  // per epilogue: the four kernels share one function-pointer type
+  auto go = [&](auto kern) {
+    smem_attr_once(kern, C::SMEM, attr[epi & 3]);
+    launch_k(kern, dim3(grid), dim3(384), C::SMEM, st, tmB, ln, D, bias, M, N, K, qs);
+  };
+  if (epi == EPI_BIAS_QKV) go(gemm_ln_kernel<EPI_BIAS_QKV>);
+  else if (epi == EPI_BIAS_GELU) go(gemm_ln_kernel<EPI_BIAS_GELU>);
+  else if (epi == EPI_BIAS) go(gemm_ln_kernel<EPI_BIAS>);
+  else go(gemm_ln_kernel<EPI_NONE>);
+  return true;
+}
 
 bool launch_gemm_tc(const CUtensorMap& tmA, const CUtensorMap& tmB, int bn, const float* bias, bf16* D, int M, int N,
                     int K, int epi, cudaStream_t st, const QkvScatter* qkv, const CUtensorMap* tmD, const TailWs* tw,

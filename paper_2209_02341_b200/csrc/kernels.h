@@ -95,14 +95,16 @@ void launch_attn_plan(const LensParam& lp, int B, int causal, int bm, int bn, in
 template <typename Act>
 void launch_embed_ln(const int* tok, const int* pack_idx, const int* unpack_idx, int row0, int rows, int S, int V, int H,
                      const Act* tok_emb, const Act* pos_emb, const float* g, const float* b, float eps, float* X, Act* A,
-                     cudaStream_t st);
+                     cudaStream_t st, float2* stats = nullptr);
 template <typename Act>
 void launch_gather_ln(const float* x, const int* pack_idx, const int* T_dev, int row0, int rows, int H, const float* g,
-                      const float* b, float eps, float* X, Act* A, cudaStream_t st);
+                      const float* b, float eps, float* X, Act* A, cudaStream_t st, float2* stats = nullptr);
 // a9 / a12
 template <typename Act>
 void launch_residual_ln(float* X, const Act* P, const float* bias, int rows, int H, const float* g, const float* b,
-                        float eps, Act* A, cudaStream_t st);
+                        float eps, Act* A, cudaStream_t st, float2* stats = nullptr);
+// stats != nullptr (the N3 LN-prologue mode): the row's (mean, rstd) are written to stats[t] for the GEMM
+// prologue to apply, and A (may be nullptr) is not needed
 // a13
 template <typename Out>
 void launch_final_ln_unpack(const float* X, const int* unpack_idx, int rows_are_cells, int cells, int H, const float* g,
@@ -195,6 +197,11 @@ struct ShardStore {
 bool launch_gemm_tc(const CUtensorMap& tmA, const CUtensorMap& tmB, int bn, const float* bias, bf16* D, int M, int N,
                     int K, int epi, cudaStream_t st, const QkvScatter* qkv = nullptr, const CUtensorMap* tmD = nullptr,
                     const TailWs* tw = nullptr, const ShardStore* shard = nullptr);
+// N3: bf16 GEMM whose A operand is LN(X) built in the prologue from fp32 X [M, K], the row statistics
+// (mean, rstd) and the LN weight / bias (1-CTA 128 x 256 tiles, W from the box-256 map); K % 64 == 0.
+// Same epilogues as launch_gemm_tc; false if unsupported.
+bool launch_gemm_ln(const CUtensorMap& tmB, const float* X, const float2* stats, const float* g, const float* b,
+                    const float* bias, bf16* D, int M, int N, int K, int epi, cudaStream_t st, const QkvScatter* qkv);
 int num_sms();  // SM count of the current device
 
 }  // namespace energon

@@ -208,7 +208,7 @@ __global__ void __launch_bounds__(LN_THREADS) embed_ln_kernel(const int* __restr
                                                               int H, const Act* __restrict__ tok_emb,
                                                               const Act* __restrict__ pos_emb, const float* __restrict__ g,
                                                               const float* __restrict__ b, float eps, float* __restrict__ X,
-                                                              Act* __restrict__ A) {
+                                                              Act* __restrict__ A, float2* __restrict__ stats) {
   pdl_trigger();
   pdl_wait();
   __shared__ float red[32];
@@ -217,8 +217,9 @@ __global__ void __launch_bounds__(LN_THREADS) embed_ln_kernel(const int* __restr
   if (cell < 0) {  // a bucket row past T (index_maps_kernel): zero, never read by a valid row
     for (int c = threadIdx.x; c < H / 4; c += LN_THREADS) {
       Row4<float>::store(X + (int64_t)t * H + 4 * c, make_float4(0.f, 0.f, 0.f, 0.f));
-      Row4<Act>::store(A + (int64_t)t * H + 4 * c, make_float4(0.f, 0.f, 0.f, 0.f));
+      if (A) Row4<Act>::store(A + (int64_t)t * H + 4 * c, make_float4(0.f, 0.f, 0.f, 0.f));
     }
+    if (stats && threadIdx.x == 0) stats[t] = make_float2(0.f, 0.f);
     return;
   }
   const int s = cell % S;
@@ -241,6 +242,8 @@ __global__ void __launch_bounds__(LN_THREADS) embed_ln_kernel(const int* __restr
   }
   float mean, rstd;
   row_stats(v, nv, H, eps, red, mean, rstd);
+  if (stats && threadIdx.x == 0) stats[t] = make_float2(mean, rstd);  // LN applied in the GEMM prologue (N3)
+  if (!A) return;
 #pragma unroll
   for (int i = 0; i < LN_MAXV; ++i) {
     const int c = (threadIdx.x + i * LN_THREADS);
@@ -256,7 +259,8 @@ template <typename Act, int LN_MAXV>
 __global__ void __launch_bounds__(LN_THREADS) gather_ln_kernel(const float* __restrict__ x, const int* __restrict__ pack_idx,
                                                                const int* __restrict__ T_dev, int row0, int H,
                                                                const float* __restrict__ g, const float* __restrict__ b,
-                                                               float eps, float* __restrict__ X, Act* __restrict__ A) {
+                                                               float eps, float* __restrict__ X, Act* __restrict__ A,
+                                                               float2* __restrict__ stats) {
   pdl_trigger();
   pdl_wait();
   __shared__ float red[32];
@@ -265,8 +269,9 @@ __global__ void __launch_bounds__(LN_THREADS) gather_ln_kernel(const float* __re
   if (cell < 0) {
     for (int c = threadIdx.x; c < H / 4; c += LN_THREADS) {
       Row4<float>::store(X + (int64_t)t * H + 4 * c, make_float4(0.f, 0.f, 0.f, 0.f));
-      Row4<Act>::store(A + (int64_t)t * H + 4 * c, make_float4(0.f, 0.f, 0.f, 0.f));
+      if (A) Row4<Act>::store(A + (int64_t)t * H + 4 * c, make_float4(0.f, 0.f, 0.f, 0.f));
     }
+    if (stats && threadIdx.x == 0) stats[t] = make_float2(0.f, 0.f);
     return;
   }
   float4 v[LN_MAXV];
@@ -282,6 +287,8 @@ __global__ void __launch_bounds__(LN_THREADS) gather_ln_kernel(const float* __re
   }
   float mean, rstd;
   row_stats(v, nv, H, eps, red, mean, rstd);
+  if (stats && threadIdx.x == 0) stats[t] = make_float2(mean, rstd);
+  if (!A) return;
 #pragma unroll
   for (int i = 0; i < LN_MAXV; ++i)
     if (i < nv) Row4<Act>::store(A + (int64_t)t * H + 4 * (threadIdx.x + i * LN_THREADS),
@@ -296,7 +303,7 @@ template <typename Act, int LN_MAXV, int TPR>
 __global__ void __launch_bounds__(TPR) residual_ln_kernel(float* __restrict__ X, const Act* __restrict__ P,
                                                           const float* __restrict__ bias, int H,
                                                           const float* __restrict__ g, const float* __restrict__ b,
-                                                          float eps, Act* __restrict__ A) {
+                                                          float eps, Act* __restrict__ A, float2* __restrict__ stats) {
   pdl_trigger();
   pdl_wait();
   __shared__ float red[32];
@@ -328,9 +335,11 @@ __global__ void __launch_bounds__(TPR) residual_ln_kernel(float* __restrict__ X,
       Row4<float>::store(xrow + 4 * c, v[i]);
     }
   }
-  if (A == nullptr) return;
+  if (A == nullptr && stats == nullptr) return;
   float mean, rstd;
   row_stats(v, nv, H, eps, red, mean, rstd);
+  if (stats && threadIdx.x == 0) stats[t] = make_float2(mean, rstd);  // LN applied in the GEMM prologue (N3)
+  if (A == nullptr) return;
 #pragma unroll
   for (int i = 0; i < LN_MAXV; ++i)
     if (i < nv) Row4<Act>::store(A + (int64_t)t * H + 4 * (threadIdx.x + i * TPR),
@@ -593,18 +602,18 @@ void launch_attn_plan(const LensParam& lp, int B, int causal, int bm, int bn, in
 template <typename Act>
 void launch_embed_ln(const int* tok, const int* pack_idx, const int* unpack_idx, int row0, int rows, int S, int V, int H,
                      const Act* tok_emb, const Act* pos_emb, const float* g, const float* b, float eps, float* X, Act* A,
-                     cudaStream_t st) {
+                     cudaStream_t st, float2* stats) {
   if (rows > 0)
     NV_DISPATCH(H, (launch_k(embed_ln_kernel<Act, NVX>, dim3(rows), dim3(LN_THREADS), 0, st, tok, pack_idx, unpack_idx,
-                             row0, S, V, H, tok_emb, pos_emb, g, b, eps, X, A)))
+                             row0, S, V, H, tok_emb, pos_emb, g, b, eps, X, A, stats)))
 }
 
 template <typename Act>
 void launch_gather_ln(const float* x, const int* pack_idx, const int* T_dev, int row0, int rows, int H, const float* g,
-                      const float* b, float eps, float* X, Act* A, cudaStream_t st) {
+                      const float* b, float eps, float* X, Act* A, cudaStream_t st, float2* stats) {
   if (rows > 0)
     NV_DISPATCH(H, (launch_k(gather_ln_kernel<Act, NVX>, dim3(rows), dim3(LN_THREADS), 0, st, x, pack_idx, T_dev, row0, H,
-                             g, b, eps, X, A)))
+                             g, b, eps, X, A, stats)))
 }
 
 #define NV_DISPATCH_T(H, TPRV, KERNEL_CALL)                                 \
@@ -642,15 +651,15 @@ static int ln_tpr(int H, int rows) {
 
 template <typename Act>
 void launch_residual_ln(float* X, const Act* P, const float* bias, int rows, int H, const float* g, const float* b,
-                        float eps, Act* A, cudaStream_t st) {
+                        float eps, Act* A, cudaStream_t st, float2* stats) {
   if (rows <= 0) return;
   const int tpr = ln_tpr(H, rows);
   if (tpr == 128)
-    NV_DISPATCH_T(H, 128, (launch_k(residual_ln_kernel<Act, NVX, 128>, dim3(rows), dim3(128), 0, st, X, P, bias, H, g, b, eps, A)))
+    NV_DISPATCH_T(H, 128, (launch_k(residual_ln_kernel<Act, NVX, 128>, dim3(rows), dim3(128), 0, st, X, P, bias, H, g, b, eps, A, stats)))
   else if (tpr == 512)
-    NV_DISPATCH_T(H, 512, (launch_k(residual_ln_kernel<Act, NVX, 512>, dim3(rows), dim3(512), 0, st, X, P, bias, H, g, b, eps, A)))
+    NV_DISPATCH_T(H, 512, (launch_k(residual_ln_kernel<Act, NVX, 512>, dim3(rows), dim3(512), 0, st, X, P, bias, H, g, b, eps, A, stats)))
   else
-    NV_DISPATCH_T(H, 256, (launch_k(residual_ln_kernel<Act, NVX, 256>, dim3(rows), dim3(256), 0, st, X, P, bias, H, g, b, eps, A)))
+    NV_DISPATCH_T(H, 256, (launch_k(residual_ln_kernel<Act, NVX, 256>, dim3(rows), dim3(256), 0, st, X, P, bias, H, g, b, eps, A, stats)))
 }
 
 template <typename Out>
@@ -875,12 +884,13 @@ template void launch_p2p_reduce_ln<bf16>(const PeerSet&, int, int, int64_t, int6
 
 #define INST_ACT(Act)                                                                                                   \
   template void launch_embed_ln<Act>(const int*, const int*, const int*, int, int, int, int, int, const Act*,           \
-                                     const Act*, const float*, const float*, float, float*, Act*, cudaStream_t);        \
+                                     const Act*, const float*, const float*, float, float*, Act*, cudaStream_t,         \
+                                     float2*);                                                                          \
   template void launch_gather_ln<Act>(const float*, const int*, const int*, int, int, int, const float*, const float*,  \
-                                      float, float*, Act*, cudaStream_t);                                               \
+                                      float, float*, Act*, cudaStream_t, float2*);                                      \
   template void launch_local_reduce_scatter<Act>(const PtrList&, int, int64_t, int, cudaStream_t);                     \
   template void launch_residual_ln<Act>(float*, const Act*, const float*, int, int, const float*, const float*, float,   \
-                                        Act*, cudaStream_t);                                                            \
+                                        Act*, cudaStream_t, float2*);                                                   \
   template void launch_final_ln_unpack<Act>(const float*, const int*, int, int, int, const float*, const float*, float,  \
                                             int, Act*, cudaStream_t);                                                   \
   template void launch_unpack_qkv<Act>(const Act*, const int*, int, int, int, int, Act*, Act*, Act*, cudaStream_t);    \

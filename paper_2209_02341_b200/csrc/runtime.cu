@@ -90,6 +90,8 @@ struct energon_ctx {
   ShardStore shard{};
   ShardStore shard_rpr{};  // `shard` with this forward's rows per rank
   bool fuse = true;  // fused a5 / a7 (ENERGON_NO_FUSE=1 disables, for A/B and tests)
+  bool ln_fuse = false;  // N3 (ENERGON_OPT_LN_FUSE): LN1 / LN2 applied in the QKV / MLP-up GEMM prologues
+  float2* ln_stats = nullptr;  // [R] row (mean, rstd) of the last LayerNorm input, for the fused prologue
   bool sp = true;    // k > 1: sequence-parallel schedule (reduce-scatter / LN on own rows / all-gather)
   bool ring = false; // local group: NCCL ring numerics in the in-device reductions (ENERGON_OPT_RING_NUMERICS)
   // CUDA-graph cache (ENERGON_OPT_GRAPH): whole forwards captured on cap_stream, replayed on the caller's
@@ -259,6 +261,7 @@ energon_status setup(energon_ctx* c) {
       (s = dalloc(c, &c->unpack_idx, sizeof(int) * R, ws)) || (s = dalloc(c, &c->QKV, a * R * 3 * c->Hk, ws)) ||
       (s = dalloc(c, &c->lens_d, sizeof(int) * ENERGON_MAX_BATCH, ws)) ||
       (s = dalloc(c, &c->attn_work, sizeof(uint32_t) * (2 + ENERGON_MAX_BATCH + R / 64), ws)) ||
+      (s = dalloc(c, &c->ln_stats, sizeof(float2) * R, ws)) ||
       (s = dalloc(c, &c->Q, a * R * c->Hk, ws)) || (s = dalloc(c, &c->K, a * R * c->Hk, ws)) ||
       (s = dalloc(c, &c->Vb, a * R * c->Hk, ws)) || (s = dalloc(c, &c->O, a * R * c->Hk, ws)) ||
       (s = dalloc(c, &c->Ctx, a * R * c->Hk, ws)) || (s = dalloc(c, &c->G, a * R * c->Fk, ws)))
@@ -589,6 +592,16 @@ void gemm(energon_ctx* c, const CUtensorMap& tmA, const CUtensorMap* tmB, const 
   c->stats.kernel_launches++;
 }
 
+// N3: LN(X) built in the GEMM prologue (QKV with LN1, MLP-up with LN2); bf16, TP = 1 only
+void gemm_ln(energon_ctx* c, const CUtensorMap* tmB, const float* g, const float* b, const float* bias, void* D, int M,
+             int N, int epi, cudaStream_t st, const QkvScatter* qs = nullptr) {
+  Prof p(c, st, P_GEMM, 2.0 * c->work_rows * N * c->H);
+  if (!launch_gemm_ln(tmB[box_slot(256)], c->X, c->ln_stats, g, b, bias, reinterpret_cast<bf16*>(D), M, N, c->H, epi, st,
+                      qs))
+    c->launch_err = "LN-prologue GEMM refused: hidden % 64 != 0";
+  c->stats.kernel_launches++;
+}
+
 // ----------------------------------------------------------------------------- PMEP prefetch
 // Copy off-device layer `layer` (the j-th off-device layer of this forward) into staging slot
 // j % slots on the copy stream, after the slot's previous occupant finished computing.
@@ -695,14 +708,15 @@ energon_status forward_t(energon_ctx** cs, int n, const Call& a, int64_t T) {
       // reads: ids + 2 embedding rows (or one fp32 row); writes: X (fp32) + A -- this rank's rows
       const int r0 = shard0(c), sn = shardn(c);
       Prof p(c, st, P_MEM, a.tokens ? sn * (4.0 + H * (2 * act + 4 + act)) : sn * H * (4 + 4 + act));
+      Act* A0 = c->ln_fuse ? nullptr : reinterpret_cast<Act*>(c->A);  // N3: statistics only, LN in the QKV prologue
+      float2* st0 = c->ln_fuse ? c->ln_stats : nullptr;
       if (a.tokens)
         launch_embed_ln<Act>(a.tokens, pidx, c->unpack_idx, r0, sn, a.S, c->V, c->H,
                              reinterpret_cast<const Act*>(c->tok_emb), reinterpret_cast<const Act*>(c->pos_emb), g1, b1,
-                             eps, c->X, reinterpret_cast<Act*>(c->A), st);
+                             eps, c->X, A0, st, st0);
       else
         launch_gather_ln<Act>(a.x_in, a.x_packed ? nullptr : pidx, drce ? c->offsets + a.B : nullptr, r0, sn, c->H, g1,
-                              b1, eps, c->X,
-                              reinterpret_cast<Act*>(c->A), st);
+                              b1, eps, c->X, A0, st, st0);
     }
     c->stats.kernel_launches++;
   }
@@ -729,9 +743,15 @@ energon_status forward_t(energon_ctx** cs, int n, const Call& a, int64_t T) {
         // a4 + a5: the QKV epilogue scatters straight into the padded per-head Q, K, V
         QkvScatter qs{pidx, reinterpret_cast<bf16*>(c->Q), reinterpret_cast<bf16*>(c->K),
                       reinterpret_cast<bf16*>(c->Vb), a.S, c->hk, c->d};
-        gemm<Act>(c, c->tmA_A, W.tm_qkv, c->A, W.wqkv, L.bqkv, nullptr, rows, 3 * c->Hk, c->H, EPI_BIAS_QKV, st, &qs);
+        if (c->ln_fuse)
+          gemm_ln(c, W.tm_qkv, L.ln1g, L.ln1b, L.bqkv, nullptr, rows, 3 * c->Hk, EPI_BIAS_QKV, st, &qs);
+        else
+          gemm<Act>(c, c->tmA_A, W.tm_qkv, c->A, W.wqkv, L.bqkv, nullptr, rows, 3 * c->Hk, c->H, EPI_BIAS_QKV, st, &qs);
       } else {
-        gemm<Act>(c, c->tmA_A, W.tm_qkv, c->A, W.wqkv, L.bqkv, c->QKV, rows, 3 * c->Hk, c->H, EPI_BIAS, st);
+        if (c->ln_fuse)
+          gemm_ln(c, W.tm_qkv, L.ln1g, L.ln1b, L.bqkv, c->QKV, rows, 3 * c->Hk, EPI_BIAS, st);
+        else
+          gemm<Act>(c, c->tmA_A, W.tm_qkv, c->A, W.wqkv, L.bqkv, c->QKV, rows, 3 * c->Hk, c->H, EPI_BIAS, st);
         Prof p(c, st, P_MEM, 2.0 * rows * 3 * Hk * act);
         launch_unpack_qkv<Act>(reinterpret_cast<const Act*>(c->QKV), pidx, rows, a.S, c->hk, c->d,
                                reinterpret_cast<Act*>(c->Q), reinterpret_cast<Act*>(c->K), reinterpret_cast<Act*>(c->Vb),
@@ -777,7 +797,8 @@ energon_status forward_t(energon_ctx** cs, int n, const Call& a, int64_t T) {
       const int sn = shardn(c);
       Prof p(c, st, P_MEM, sn * H * (8.0 + 2 * act));
       launch_residual_ln<Act>(c->X + o, reinterpret_cast<const Act*>(c->P) + o, L.bo, sn, c->H, L.ln2g, L.ln2b, eps,
-                              reinterpret_cast<Act*>(c->A) + o, st);
+                              c->ln_fuse ? nullptr : reinterpret_cast<Act*>(c->A) + o, st,
+                              c->ln_fuse ? c->ln_stats + shard0(c) : nullptr);
       c->stats.kernel_launches++;
     }
     if (sp && !p2p && (s = tp_gather<Act>(cs, n, rpr, false, st))) return s;
@@ -786,7 +807,10 @@ energon_status forward_t(energon_ctx** cs, int n, const Call& a, int64_t T) {
       energon_ctx* c = cs[i];
       const LayerDev& W = weights(i, l);
       const LayerDev& L = c->layers[l];
-      gemm<Act>(c, c->tmA_A, W.tm_1, c->A, W.w1, L.b1, c->G, rows, c->Fk, c->H, EPI_BIAS_GELU, st, nullptr, &c->tmD_G);
+      if (c->ln_fuse)
+        gemm_ln(c, W.tm_1, L.ln2g, L.ln2b, L.b1, c->G, rows, c->Fk, EPI_BIAS_GELU, st);
+      else
+        gemm<Act>(c, c->tmA_A, W.tm_1, c->A, W.w1, L.b1, c->G, rows, c->Fk, c->H, EPI_BIAS_GELU, st, nullptr, &c->tmD_G);
       gemm<Act>(c, c->tmA_G, W.tm_2, c->G, W.w2, nullptr, c->P, rows, c->H, c->Fk, EPI_NONE, st, nullptr, &c->tmD_P,
                 fused_rs ? &c->shard_rpr : nullptr);
       if (!c->pm.layers.empty() && c->pm.index[l] >= 0) {
@@ -813,7 +837,8 @@ energon_status forward_t(energon_ctx** cs, int n, const Call& a, int64_t T) {
       const int sn = shardn(c);
       Prof p(c, st, P_MEM, sn * H * (8.0 + (last ? 1 : 2) * act));
       launch_residual_ln<Act>(c->X + o, reinterpret_cast<const Act*>(c->P) + o, L.b2, sn, c->H, Ln.ln1g, Ln.ln1b, eps,
-                              last ? nullptr : reinterpret_cast<Act*>(c->A) + o, st);
+                              (last || c->ln_fuse) ? nullptr : reinterpret_cast<Act*>(c->A) + o, st,
+                              (!last && c->ln_fuse) ? c->ln_stats + shard0(c) : nullptr);
       c->stats.kernel_launches++;
     }
     if (sp && !p2p && !last && (s = tp_gather<Act>(cs, n, rpr, false, st))) return s;
@@ -896,7 +921,7 @@ energon_status run(energon_ctx** cs, int n, const Call& a) {
   // before every replay), and every other launch depends on the batch only through the row bucket.
   const int rows = c0->cfg.drce ? bucket_rows(c0, T) : a.B * a.S;
   std::vector<int64_t> key = {n, (int64_t)(uintptr_t)a.tokens, (int64_t)(uintptr_t)a.x_in, (int64_t)(uintptr_t)a.out,
-                              a.B, a.S, a.l0, a.l1, a.final_ln, a.out_f32, c0->cfg.drce, c0->sp, c0->fuse, c0->ring,
+                              a.B, a.S, a.l0, a.l1, a.final_ln, a.out_f32, c0->cfg.drce, c0->sp, c0->fuse, c0->ring, c0->ln_fuse,
                               a.x_packed, a.out_packed, rows};
   for (int i = 0; i < n; ++i) key.push_back((int64_t)(uintptr_t)cs[i]);
   if (a.x_packed || a.out_packed) key.push_back(T);  // a pipeline stage copies exactly T rows in or out
@@ -1515,6 +1540,13 @@ energon_status energon_set_option(energon_ctx* c, int32_t option, int32_t value)
     if (value != 0 && value != 1) return fail(c, ENERGON_ERR_ARG, "ENERGON_OPT_RING_NUMERICS takes 0 or 1");
     if (!c->local_group && value) return fail(c, ENERGON_ERR_CONFIG, "ENERGON_OPT_RING_NUMERICS needs a local group");
     c->ring = value != 0;
+    return ENERGON_OK;
+  }
+  if (option == ENERGON_OPT_LN_FUSE) {
+    if (value != 0 && value != 1) return fail(c, ENERGON_ERR_ARG, "ENERGON_OPT_LN_FUSE takes 0 or 1");
+    if (value && (c->act != 2 || c->k != 1 || c->local_group || c->H % 64 != 0))
+      return fail(c, ENERGON_ERR_CONFIG, "ENERGON_OPT_LN_FUSE needs bf16, TP = 1 and hidden % 64 == 0");
+    c->ln_fuse = value != 0;
     return ENERGON_OK;
   }
   if (option == ENERGON_OPT_TP_SP) {

@@ -23,6 +23,7 @@ OPT_DRCE = 1
 OPT_TP_SP = 2
 OPT_GRAPH = 3
 OPT_RING_NUMERICS = 4
+OPT_LN_FUSE = 5
 STAGE_PACKED, STAGE_FINAL = 0, 1
 COMM_NCCL, COMM_P2P = 0, 1
 LAYER_TENSORS = ("wq", "wk", "wv", "wo", "bq", "bk", "bv", "bo",

@@ -664,3 +664,49 @@ def test_cuda_graph_replay_bitexact(k):
         assert torch.equal(g, eager[i % len(cases)]), i
     assert rec == [1, 1, 1, 1, 2] + [2] * 5  # one graph per bucket, recorded on its first batch
     assert st["forwards"] == 15
+
+
+# ----------------------------------------------------------------------------- N3: LN in the GEMM prologue
+@pytest.mark.parametrize("name,B,S,fuse_layout", [("gpt2s", 9, 100, True), ("ln_d128", 5, 140, True),
+                                                  ("ln_d128", 5, 140, False)])
+def test_ln_prologue_fusion(name, B, S, fuse_layout, monkeypatch):
+    """ENERGON_OPT_LN_FUSE: the residual kernels write only X and the
+    row statistics, and the QKV / MLP-up GEMMs apply LN1 / LN2 in their prologue with the residual kernel's
+    fp32 expression, so the forward must be bit-identical to the unfused one (which runs the same
+    products through the 2-CTA GEMM) and within the bf16 bar of the fp64 oracle; also with the standalone
+    a5 / a7 layout kernels (ENERGON_NO_FUSE=1) and graph replay."""
+    if not fuse_layout:
+        monkeypatch.setenv("ENERGON_NO_FUSE", "1")
+    shape = dict(SHAPES["gpt2s"], L=2) if name == "gpt2s" else dict(L=2, H=256, h=2, F=1024, V=600, max_seq=160)
+    seed = 13
+    lens = synth.random_lengths(B, S, seed)
+    tok = synth.tokens(B, S, shape["V"], lens, seed)
+    ctxs = make_engine(shape, seed, "bf16", B * S)
+    try:
+        y0 = run_forward(ctxs, tok, lens, "bf16", shape["H"])
+        E().energon_set_option(ctxs[0], E().OPT_LN_FUSE, 1)
+        y1 = run_forward(ctxs, tok, lens, "bf16", shape["H"])
+        E().energon_set_option(ctxs[0], E().OPT_GRAPH, 1)
+        y2 = run_forward(ctxs, tok, lens, "bf16", shape["H"])
+        y3 = run_forward(ctxs, tok, lens, "bf16", shape["H"])
+    finally:
+        destroy(ctxs)
+    assert np.array_equal(y0, y1), f"LN-prologue forward differs: max |d| {np.nanmax(np.abs(y0 - y1))}"
+    assert np.array_equal(y1, y2) and np.array_equal(y2, y3)
+    layers, emb = oracle_model(shape, seed, "bf16")
+    cfg = oracle.make_cfg(shape["L"], shape["H"], shape["h"], shape["F"])
+    ref = oracle.forward_padded(cfg, layers, emb, tok, lens)
+    assert max_abs_rel(y1, ref, lens) <= TOL["bf16"]
+
+
+def test_ln_prologue_fusion_refused_outside_domain():
+    """ENERGON_OPT_LN_FUSE is bf16 / TP = 1 only: fp32 contexts and local TP groups get ENERGON_ERR_CONFIG."""
+    shape = dict(SHAPES["tiny"])
+    for dtype, k in (("f32", 1), ("bf16", 2)):
+        ctxs = make_engine(shape, 0, dtype, 64, k=k)
+        try:
+            with pytest.raises(E().EnergonError) as ei:
+                E().energon_set_option(ctxs[0], E().OPT_LN_FUSE, 1)
+            assert ei.value.status == -2
+        finally:
+            destroy(ctxs)
