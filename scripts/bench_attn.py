@@ -20,7 +20,7 @@ cases = {
 if os.environ.get("ATTN_CASES"):  # a subset by name prefix, e.g. "gpt3" or "full S2048" (under ncu)
     cases = {k: v for k, v in cases.items() if k.startswith(os.environ["ATTN_CASES"])}
 hk, d = int(os.environ.get("ATTN_HK", "40")), 128  # ATTN_HK: heads per rank (TP=8: 5)
-impl = os.environ.get("ENERGON_ATTN", "5")
+impl = os.environ.get("ENERGON_ATTN", "4")
 REPS = 20
 for name, (B, S, lens) in cases.items():
     g = torch.Generator(device="cuda").manual_seed(0)
