@@ -378,10 +378,30 @@ def energon_arm(args, world, rank, local):
         ctxs = energon.energon_init_local_group(cfg, args.local_tp)
     else:
         ctxs = [energon.energon_init(cfg, uid)]
+    p2p_fallback = None
     if comm == energon.COMM_P2P and world > 1:  # map every rank's exchange region (CUDA IPC handles, all-gathered)
-        handles = [None] * world
-        dist.all_gather_object(handles, energon.energon_p2p_handle(ctxs[0]))
-        energon.energon_p2p_connect(ctxs[0], handles)
+        err = ""
+        try:
+            handles = [None] * world
+            dist.all_gather_object(handles, energon.energon_p2p_handle(ctxs[0]))
+            energon.energon_p2p_connect(ctxs[0], handles)
+        except energon.EnergonError as e:  # peer mapping refused on this box: every rank falls back to NCCL
+            err = str(e)
+        errs = [None] * world
+        dist.all_gather_object(errs, err)
+        bad = [e for e in errs if e]
+        if bad and not share:
+            energon.energon_destroy(ctxs[0])
+            comm = energon.COMM_NCCL
+            args.comm = "nccl"
+            cfg = energon.make_config(shape["L"], H, shape["h"], shape["F"], shape["V"], shape["max_seq"], B * S,
+                                      dtype="bf16", drce=args.drce, tp_size=world, tp_rank=rank, device=local,
+                                      comm=comm)
+            uid = edist.broadcast_bytes(energon.energon_get_unique_id() if rank == 0 else None, 128, device=plumb)
+            ctxs = [energon.energon_init(cfg, uid)]
+            p2p_fallback = f"p2p connect failed ({bad[0][:160]}); NCCL exchange used"
+        elif bad:
+            raise RuntimeError(bad[0])
     eng = Engine(energon, ctxs)
 
     # weights: generated on the device by the seeded counter-based generator, loaded unsharded
@@ -611,6 +631,8 @@ def energon_arm(args, world, rank, local):
     config["seeds"] = seeds
     if args.ln_fuse:
         config["ln_fuse"] = True
+    if p2p_fallback:
+        config["p2p_fallback"] = p2p_fallback
     config["valid_tokens_per_step"] = tokens_timed / args.steps
     result = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
               "warmup": args.warmup, "warmup_steps_run": warm, "ms_per_step": total_ms / args.steps,
