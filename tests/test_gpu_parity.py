@@ -667,21 +667,21 @@ def test_cuda_graph_replay_bitexact(k):
 
 
 # ----------------------------------------------------------------------------- N3: LN in the GEMM prologue
-@pytest.mark.parametrize("name,B,S,fuse_layout", [("gpt2s", 9, 100, True), ("ln_d128", 5, 140, True),
-                                                  ("ln_d128", 5, 140, False)])
-def test_ln_prologue_fusion(name, B, S, fuse_layout, monkeypatch):
+@pytest.mark.parametrize("name,B,S,fuse_layout,drce", [("gpt2s", 9, 100, True, 1), ("ln_d128", 5, 140, True, 1),
+                                                       ("ln_d128", 5, 140, False, 1), ("ln_d128", 4, 70, True, 0)])
+def test_ln_prologue_fusion(name, B, S, fuse_layout, drce, monkeypatch):
     """ENERGON_OPT_LN_FUSE: the residual kernels write only X and the
     row statistics, and the QKV / MLP-up GEMMs apply LN1 / LN2 in their prologue with the residual kernel's
     fp32 expression, so the forward must be bit-identical to the unfused one (which runs the same
     products through the 2-CTA GEMM) and within the bf16 bar of the fp64 oracle; also with the standalone
-    a5 / a7 layout kernels (ENERGON_NO_FUSE=1) and graph replay."""
+    a5 / a7 layout kernels (ENERGON_NO_FUSE=1), in the padded A/B mode (drce=0) and with graph replay."""
     if not fuse_layout:
         monkeypatch.setenv("ENERGON_NO_FUSE", "1")
     shape = dict(SHAPES["gpt2s"], L=2) if name == "gpt2s" else dict(L=2, H=256, h=2, F=1024, V=600, max_seq=160)
     seed = 13
     lens = synth.random_lengths(B, S, seed)
     tok = synth.tokens(B, S, shape["V"], lens, seed)
-    ctxs = make_engine(shape, seed, "bf16", B * S)
+    ctxs = make_engine(shape, seed, "bf16", B * S, drce=drce)
     try:
         y0 = run_forward(ctxs, tok, lens, "bf16", shape["H"])
         E().energon_set_option(ctxs[0], E().OPT_LN_FUSE, 1)
