@@ -734,7 +734,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   using C = Tc2Cfg<BN>;
-  constexpr bool TMA_ST = (EPI != EPI_BIAS_QKV);  // QKV scatters (a5); everything else leaves by TMA store
+  // QKV's a5 scatter leaves by TMA too when the host built the Q / K / V store maps (shard.qkv_tma)
+  const bool TMA_ST = (EPI != EPI_BIAS_QKV) || shard.qkv_tma;
   uint8_t* sA = smem;
   uint8_t* sB = smem + C::STAGES * C::A_BYTES;
   uint8_t* sStg = sB + C::STAGES * C::B_BYTES;
@@ -995,7 +996,57 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
           if (two) epi_stage(v1, my_stg + 2048, lane);
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
-          if (lane == 0) {
+          if (EPI == EPI_BIAS_QKV) {
+            // a5 by TMA: the box's first run of rows (the sequence b its row 0 belongs to) is stored with one 3-D
+            // box store per 32-column chunk into the padded plane [b * hk + head] at rows s_0 .. s_0 + 31 -- rows
+            // of later sequences in the box land at s >= len_b (pad rows, never read) or past S (clipped).  A
+            // sequence that starts inside the box (run start r > 0) would need a negative box row, which the TMA
+            // store rejects (illegal instruction, measured), so those rows are scattered by their own lanes from
+            // the registers they still hold (typically < 6% of the rows).
+            const int t = rowt + lane;
+            const int cell = t < M ? (qs.pack_idx ? __ldg(qs.pack_idx + t) : t) : -1;
+            const int b = cell >= 0 ? cell / qs.S : -1;
+            const int bprev = __shfl_up_sync(0xffffffffu, b, 1);
+            const unsigned starts = __ballot_sync(0xffffffffu, cell >= 0 && (lane == 0 || bprev != b));
+            const int my_run = 31 - __clz(starts & (0xffffffffu >> (31 - lane)));  // start lane of this row's run
+            if (lane == 0) {
+              if (starts & 1u) {
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                  if (u == 1 && !two) break;
+                  const int n0 = n_blk * BN + (c + u) * 32;
+                  if (n0 >= N) break;
+                  const int Hk = N / 3, which = n0 / Hk, rem = n0 - which * Hk;
+                  const int head = rem / qs.d, j = rem - head * qs.d;
+                  asm volatile(
+                      "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                          reinterpret_cast<uint64_t>(&shard.maps[which])),
+                      "r"(smem_u32(my_stg + u * 2048)), "r"(j), "r"(cell - b * qs.S), "r"(b * qs.hk + head)
+                      : "memory");
+                }
+              }
+              bulk_commit();
+            }
+            if (cell >= 0 && my_run > 0) {  // rows of a sequence that starts inside the box: per-thread stores
+#pragma unroll
+              for (int u = 0; u < 2; ++u) {
+                if (u == 1 && !two) break;
+                const int n0 = n_blk * BN + (c + u) * 32;
+                if (n0 >= N) break;
+                bf16* dst = qkv_dst(qs, t, n0, N);
+                const float* vv = u ? v1 : v0;
+#pragma unroll
+                for (int jj = 0; jj < 32; jj += 8) {
+                  uint4 o;
+                  o.x = pack_bf16x2(vv[jj], vv[jj + 1]);
+                  o.y = pack_bf16x2(vv[jj + 2], vv[jj + 3]);
+                  o.z = pack_bf16x2(vv[jj + 4], vv[jj + 5]);
+                  o.w = pack_bf16x2(vv[jj + 6], vv[jj + 7]);
+                  *reinterpret_cast<uint4*>(dst + jj) = o;
+                }
+              }
+            }
+          } else if (lane == 0) {
             const CUtensorMap* dm = &tmD;
             if (shard.k > 0) {  // GEMM -> reduce-scatter: these 32 rows go straight to their owner's slot
               const int s = min(rowt / shard.rpr, shard.k - 1);
@@ -1082,6 +1133,25 @@ bool make_tmap_store(CUtensorMap* map, const void* ptr, int rows, int N) {
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
+}
+
+bool make_qkv_store_maps(CUtensorMap (&maps)[3], const bf16* q, const bf16* k, const bf16* v, int B, int hk, int S,
+                         int d) {
+  auto enc = encode_fn();
+  if (!enc || B <= 0 || hk <= 0 || S <= 0 || d % 32 != 0) return false;
+  const bf16* p[3] = {q, k, v};
+  for (int i = 0; i < 3; ++i) {
+    if (reinterpret_cast<uintptr_t>(p[i]) & 15) return false;
+    cuuint64_t dims[3] = {(cuuint64_t)d, (cuuint64_t)S, (cuuint64_t)B * hk};
+    cuuint64_t strides[2] = {(cuuint64_t)d * 2, (cuuint64_t)S * d * 2};
+    cuuint32_t box[3] = {32, 32, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    if (enc(&maps[i], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<bf16*>(p[i]), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return false;
+  }
+  return true;
 }
 
 int num_sms() {
@@ -1230,6 +1300,10 @@ static bool launch_pair_epi(const CUtensorMap& tmA, const CUtensorMap& tmB, cons
     sh = *shard;
   } else {
     memset(&sh, 0, sizeof(sh));  // k = 0: the output map tmD
+    if (EPI == EPI_BIAS_QKV && qs.maps) {  // a5 by TMA
+      for (int i = 0; i < 3; ++i) sh.maps[i] = qs.maps[i];
+      sh.qkv_tma = 1;
+    }
   }
   launch_k(gemm_tc2_kernel<BN, EPI>, dim3(grid), dim3(128 + 32 * C::EPI_WARPS), C::SMEM, st, tmA, tmB, D, bias, M, N, K,
            group_m, qs, tp, md, hints, sh);

@@ -162,6 +162,7 @@ struct QkvScatter {
   const int* pack_idx;  // packed row -> padded cell (nullptr: identity, padded A/B mode)
   bf16 *q, *k, *v;
   int S, hk, d;
+  const CUtensorMap* maps = nullptr;  // host: make_qkv_store_maps output (2-CTA kernel: TMA-store a5)
 };
 
 // fp32 SIMT GEMM (parity mode): D[M,N] = A[M,K] W[N,K]^T (+bias) (gelu)
@@ -191,7 +192,12 @@ struct ShardStore {
   CUtensorMap maps[8];
   int rpr;
   int k;
+  // QKV GEMM (EPI_BIAS_QKV) instead: maps[0..2] are 3-D store maps of Q, K, V [B*hk, S, d] (32 x 32 x 1 box,
+  // 64-byte swizzle) and the a5 scatter leaves by TMA bulk-tensor stores (qkv_tma = 1)
+  int qkv_tma;
 };
+// the three Q / K / V store maps of the TMA a5 scatter (false if they cannot be encoded)
+bool make_qkv_store_maps(CUtensorMap (&maps)[3], const bf16* q, const bf16* k, const bf16* v, int B, int hk, int S, int d);
 // tmD: the output map (make_tmap_store) or nullptr to build it per call.
 // returns false (nothing launched) if the output tensor map cannot be built (D not 16-byte aligned)
 bool launch_gemm_tc(const CUtensorMap& tmA, const CUtensorMap& tmB, int bn, const float* bias, bf16* D, int M, int N,

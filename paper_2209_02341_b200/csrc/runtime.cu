@@ -92,6 +92,10 @@ struct energon_ctx {
   bool fuse = true;  // fused a5 / a7 (ENERGON_NO_FUSE=1 disables, for A/B and tests)
   bool ln_fuse = false;  // N3 (ENERGON_OPT_LN_FUSE): LN1 / LN2 applied in the QKV / MLP-up GEMM prologues
   float2* ln_stats = nullptr;  // [R] row (mean, rstd) of the last LayerNorm input, for the fused prologue
+  // a5 by TMA: 3-D store maps of Q / K / V for the current (B, S) (make_qkv_store_maps), rebuilt when they change
+  CUtensorMap qkv_maps[3];
+  int qkv_maps_B = 0, qkv_maps_S = 0;
+  bool qkv_maps_ok = false;
   bool sp = true;    // k > 1: sequence-parallel schedule (reduce-scatter / LN on own rows / all-gather)
   bool ring = false; // local group: NCCL ring numerics in the in-device reductions (ENERGON_OPT_RING_NUMERICS)
   // CUDA-graph cache (ENERGON_OPT_GRAPH): whole forwards captured on cap_stream, replayed on the caller's
@@ -741,8 +745,16 @@ energon_status forward_t(energon_ctx** cs, int n, const Call& a, int64_t T) {
       const int* pidx = drce ? c->pack_idx : nullptr;
       if (fuse_a5) {
         // a4 + a5: the QKV epilogue scatters straight into the padded per-head Q, K, V
+        if (c->qkv_maps_B != a.B || c->qkv_maps_S != a.S) {
+          c->qkv_maps_ok = !getenv("ENERGON_NO_QKV_TMA") &&
+                           make_qkv_store_maps(c->qkv_maps, reinterpret_cast<const bf16*>(c->Q),
+                                               reinterpret_cast<const bf16*>(c->K), reinterpret_cast<const bf16*>(c->Vb),
+                                               a.B, c->hk, a.S, c->d);
+          c->qkv_maps_B = a.B;
+          c->qkv_maps_S = a.S;
+        }
         QkvScatter qs{pidx, reinterpret_cast<bf16*>(c->Q), reinterpret_cast<bf16*>(c->K),
-                      reinterpret_cast<bf16*>(c->Vb), a.S, c->hk, c->d};
+                      reinterpret_cast<bf16*>(c->Vb), a.S, c->hk, c->d, c->qkv_maps_ok ? c->qkv_maps : nullptr};
         if (c->ln_fuse)
           gemm_ln(c, W.tm_qkv, L.ln1g, L.ln1b, L.bqkv, nullptr, rows, 3 * c->Hk, EPI_BIAS_QKV, st, &qs);
         else

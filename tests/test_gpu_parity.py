@@ -422,22 +422,29 @@ def test_layout_kernels_bitexact_vs_oracle_maps(dtype, lens, S, hk, d):
 
 # ----------------------------------------------------------------------------- fused a5 / a7
 @pytest.mark.parametrize("drce", [1, 0])
-def test_fused_layout_kernels_bitexact(drce, monkeypatch):
-    """a5 fused into the QKV epilogue and a7 fused into attention produce the same bits as the
-    standalone paper kernels."""
+@pytest.mark.parametrize("B,S,seed", [(8, 96, 2), (40, 40, 3)])
+def test_fused_layout_kernels_bitexact(drce, B, S, seed, monkeypatch):
+    """a5 fused into the QKV epilogue -- as TMA bulk-tensor stores into the padded Q / K / V planes (one
+    3-D box store per sequence a 32-row box touches; the default) and as per-thread scatter stores
+    (ENERGON_NO_QKV_TMA=1) -- and a7 fused into attention produce the same bits as the standalone paper
+    kernels; (40, 40, 3) has many sequences shorter than a 32-row box."""
     shape = dict(SHAPES["gpt2s"], L=2)
-    B, S, seed = 8, 96, 2
     lens = synth.random_lengths(B, S, seed)
     tok = synth.tokens(B, S, shape["V"], lens, seed)
     outs = []
-    for nofuse in ("0", "1"):
+    for nofuse, notma in (("0", "0"), ("0", "1"), ("1", "0")):
         monkeypatch.setenv("ENERGON_NO_FUSE", nofuse)
+        if notma == "1":
+            monkeypatch.setenv("ENERGON_NO_QKV_TMA", "1")
+        else:
+            monkeypatch.delenv("ENERGON_NO_QKV_TMA", raising=False)
         ctxs = make_engine(shape, seed, "bf16", B * S, drce=drce)
         try:
             outs.append(run_forward(ctxs, tok, lens, "bf16", shape["H"]))
         finally:
             destroy(ctxs)
     assert np.array_equal(outs[0], outs[1])
+    assert np.array_equal(outs[0], outs[2])
 
 
 @pytest.mark.parametrize("k", [2, 4])
