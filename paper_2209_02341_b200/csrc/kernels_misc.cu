@@ -639,13 +639,16 @@ static int ln_tpr(int H, int rows) {
   if (v < 0) {
     const char* e = getenv("ENERGON_LN_TPR");
     v = e ? atoi(e) : 0;  // 0: by hidden size and row count
-    if (v != 0 && v != 128 && v != 256 && v != 512) v = 0;
+    if (v != 0 && v != 128 && v != 256 && v != 512 && v != 640) v = 0;
   }
   // measured (H = 5120): 512 threads per row is ~4% faster for the 4096 rows of TP = 1 (40.3 vs 42.0 us),
   // 256 is 21% faster for the 512 rows a rank normalises at TP = 8 (8.6 vs 10.9 us): few rows want
   // more, smaller CTAs per SM
-  if (v == 0) return (H >= 4096 && rows > 8 * 148) ? 512 : 256;
+  // and 640 threads (exactly H / 2560 float4 each, no idle third slot at H = 5120) beat 512 by 7.6% per
+  // launch at TP = 1 (ncu: 43.0 vs 46.5 us)
+  if (v == 0) return (H >= 4096 && rows > 8 * 148) ? ((H / 4) % 640 == 0 ? 640 : 512) : 256;
   if (v == 128 && H / 4 > 128 * 12) return 256;
+  if (v == 640 && (H / 4) % 640 != 0) return 512;  // 640: exactly H / 2560 float4 per thread (no idle slot)
   return v;
 }
 
@@ -658,6 +661,8 @@ void launch_residual_ln(float* X, const Act* P, const float* bias, int rows, int
     NV_DISPATCH_T(H, 128, (launch_k(residual_ln_kernel<Act, NVX, 128>, dim3(rows), dim3(128), 0, st, X, P, bias, H, g, b, eps, A, stats)))
   else if (tpr == 512)
     NV_DISPATCH_T(H, 512, (launch_k(residual_ln_kernel<Act, NVX, 512>, dim3(rows), dim3(512), 0, st, X, P, bias, H, g, b, eps, A, stats)))
+  else if (tpr == 640)
+    NV_DISPATCH_T(H, 640, (launch_k(residual_ln_kernel<Act, NVX, 640>, dim3(rows), dim3(640), 0, st, X, P, bias, H, g, b, eps, A, stats)))
   else
     NV_DISPATCH_T(H, 256, (launch_k(residual_ln_kernel<Act, NVX, 256>, dim3(rows), dim3(256), 0, st, X, P, bias, H, g, b, eps, A, stats)))
 }
