@@ -94,6 +94,50 @@ __device__ __forceinline__ void umma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, u
       "r"(tmem_a), "l"(b), "r"(idesc), "r"(acc));
 }
 
+// Batched MMA issue.  The MMA thread is a single lane, so every tcgen05.mma it issues from C++ is wrapped by
+// the compiler in an elect / R2UR.BROADCAST loop (~14 instructions, 40-90 clocks per MMA measured in the
+// traces), which is longer than a 128 x 64 x 16 S MMA takes to execute (32 clocks).  These helpers issue a
+// tile's whole group of MMAs from one asm block, advancing the descriptors with PTX adds, so the loop wraps
+// the group once (ATTN_MMA_BATCH=0 restores the per-MMA issue for A/B).
+#ifndef ATTN_MMA_BATCH
+#define ATTN_MMA_BATCH 1
+#endif
+// S = Q K^T over K = d: 4 MMAs (d = 64) from (a0, b0) advancing 32 B each; 8 (d = 128) with the second 64-wide
+// half at (a1, b1).  The first MMA overwrites the accumulator, the rest accumulate.
+__device__ __forceinline__ void umma_s4(uint32_t d, uint64_t a0, uint64_t b0, uint32_t idesc) {
+  asm volatile(
+      "{\n.reg .pred p;\n.reg .b64 x, y;\nsetp.ne.b32 p, 0, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\nsetp.eq.b32 p, 0, 0;\n"
+      "add.s64 x, %1, 2;\nadd.s64 y, %2, 2;\ntcgen05.mma.cta_group::1.kind::f16 [%0], x, y, %3, p;\n"
+      "add.s64 x, %1, 4;\nadd.s64 y, %2, 4;\ntcgen05.mma.cta_group::1.kind::f16 [%0], x, y, %3, p;\n"
+      "add.s64 x, %1, 6;\nadd.s64 y, %2, 6;\ntcgen05.mma.cta_group::1.kind::f16 [%0], x, y, %3, p;\n}\n" ::"r"(d),
+      "l"(a0), "l"(b0), "r"(idesc));
+}
+__device__ __forceinline__ void umma_s8(uint32_t d, uint64_t a0, uint64_t b0, uint64_t a1, uint64_t b1, uint32_t idesc) {
+  asm volatile(
+      "{\n.reg .pred p;\n.reg .b64 x, y;\nsetp.ne.b32 p, 0, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\nsetp.eq.b32 p, 0, 0;\n"
+      "add.s64 x, %1, 2;\nadd.s64 y, %2, 2;\ntcgen05.mma.cta_group::1.kind::f16 [%0], x, y, %3, p;\n"
+      "add.s64 x, %1, 4;\nadd.s64 y, %2, 4;\ntcgen05.mma.cta_group::1.kind::f16 [%0], x, y, %3, p;\n"
+      "add.s64 x, %1, 6;\nadd.s64 y, %2, 6;\ntcgen05.mma.cta_group::1.kind::f16 [%0], x, y, %3, p;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %4, %5, %3, p;\n"
+      "add.s64 x, %4, 2;\nadd.s64 y, %5, 2;\ntcgen05.mma.cta_group::1.kind::f16 [%0], x, y, %3, p;\n"
+      "add.s64 x, %4, 4;\nadd.s64 y, %5, 4;\ntcgen05.mma.cta_group::1.kind::f16 [%0], x, y, %3, p;\n"
+      "add.s64 x, %4, 6;\nadd.s64 y, %5, 6;\ntcgen05.mma.cta_group::1.kind::f16 [%0], x, y, %3, p;\n}\n" ::"r"(d),
+      "l"(a0), "l"(b0), "r"(idesc), "l"(a1), "l"(b1));
+}
+// O (+)= P V over 64 keys (4 MMAs): A = P from TMEM columns ta + 8 kk, B = V (MN-major) descriptor + 128 kk;
+// acc = 0 makes the first MMA overwrite O.
+__device__ __forceinline__ void umma_pv4(uint32_t d, uint32_t ta, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\n.reg .b32 t;\n.reg .b64 y;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\nsetp.eq.b32 p, 0, 0;\n"
+      "add.u32 t, %1, 8;\nadd.s64 y, %2, 128;\ntcgen05.mma.cta_group::1.kind::f16 [%0], [t], y, %3, p;\n"
+      "add.u32 t, %1, 16;\nadd.s64 y, %2, 256;\ntcgen05.mma.cta_group::1.kind::f16 [%0], [t], y, %3, p;\n"
+      "add.u32 t, %1, 24;\nadd.s64 y, %2, 384;\ntcgen05.mma.cta_group::1.kind::f16 [%0], [t], y, %3, p;\n}\n" ::"r"(d),
+      "r"(ta), "l"(b), "r"(idesc), "r"(acc));
+}
+
 template <int D>
 __global__ void __launch_bounds__(192, 2)
     attention_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
@@ -222,10 +266,14 @@ __global__ void __launch_bounds__(192, 2)
         if (jj == 0) mbar_wait(o_empty, (qq & 1) ^ 1);  // the previous item's epilogue has read O
         tc_fence_after();
         const uint32_t tP = tmem_base + (uint32_t)(b2 * BN);
+        if (ATTN_MMA_BATCH) {
+          umma_pv4(tO, tP, umma_desc_sw128_mn(smem_u32(sV + b2 * C::V_BYTES), BN * 128), C::IDESC_O, jj > 0 ? 1u : 0u);
+        } else {
 #pragma unroll
-        for (int kk = 0; kk < BN / 16; ++kk) {
-          const uint64_t bb = umma_desc_sw128_mn(smem_u32(sV + b2 * C::V_BYTES + kk * 16 * 128), BN * 128);
-          umma_bf16_ts(tO, tP + (uint32_t)(kk * 8), bb, C::IDESC_O, (jj > 0 || kk > 0) ? 1u : 0u);
+          for (int kk = 0; kk < BN / 16; ++kk) {
+            const uint64_t bb = umma_desc_sw128_mn(smem_u32(sV + b2 * C::V_BYTES + kk * 16 * 128), BN * 128);
+            umma_bf16_ts(tO, tP + (uint32_t)(kk * 8), bb, C::IDESC_O, (jj > 0 || kk > 0) ? 1u : 0u);
+          }
         }
         umma_commit(&v_empty[b2]);
         umma_commit(&p_free[b2]);
@@ -243,12 +291,22 @@ __global__ void __launch_bounds__(192, 2)
         mbar_wait(&p_free[b2], ((t >> 1) & 1) ^ 1);  // P_{t-2} V done: buffer b2 is free
         tc_fence_after();
         const uint32_t tS = tmem_base + (uint32_t)(b2 * BN);
+        if (ATTN_MMA_BATCH) {
+          const uint64_t a0 = umma_desc_sw128(smem_u32(sQ));
+          const uint64_t b0 = umma_desc_sw128(smem_u32(sK + b2 * C::K_BYTES));
+          if (D == 128)
+            umma_s8(tS, a0, b0, umma_desc_sw128(smem_u32(sQ + BM * 128)),
+                    umma_desc_sw128(smem_u32(sK + b2 * C::K_BYTES + BN * 128)), C::IDESC_S);
+          else
+            umma_s4(tS, a0, b0, C::IDESC_S);
+        } else {
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t off = (kk & 3) * 32;
-          const uint64_t a = umma_desc_sw128(smem_u32(sQ + (kk >> 2) * BM * 128 + off));
-          const uint64_t bb = umma_desc_sw128(smem_u32(sK + b2 * C::K_BYTES + (kk >> 2) * BN * 128 + off));
-          umma_bf16(tS, a, bb, C::IDESC_S, kk > 0 ? 1u : 0u);
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint32_t off = (kk & 3) * 32;
+            const uint64_t a = umma_desc_sw128(smem_u32(sQ + (kk >> 2) * BM * 128 + off));
+            const uint64_t bb = umma_desc_sw128(smem_u32(sK + b2 * C::K_BYTES + (kk >> 2) * BN * 128 + off));
+            umma_bf16(tS, a, bb, C::IDESC_S, kk > 0 ? 1u : 0u);
+          }
         }
         umma_commit(&k_empty[b2]);
         if (j + 1 == nkv) umma_commit(q_empty);
