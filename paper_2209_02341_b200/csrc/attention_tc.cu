@@ -138,6 +138,54 @@ __device__ __forceinline__ void umma_pv4(uint32_t d, uint32_t ta, uint64_t b, ui
       "r"(ta), "l"(b), "r"(idesc), "r"(acc));
 }
 
+__device__ __forceinline__ void umma_s4e(uint32_t d, uint64_t a0, uint64_t b0, uint32_t idesc) {
+  asm volatile(
+      "{\n.reg .pred p, e;\nelect.sync _|e, 0xffffffff;\n.reg .b64 x, y;\nsetp.ne.b32 p, 0, 0;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\nsetp.eq.b32 p, 0, 0;\n"
+      "add.s64 x, %1, 2;\nadd.s64 y, %2, 2;\n@e tcgen05.mma.cta_group::1.kind::f16 [%0], x, y, %3, p;\n"
+      "add.s64 x, %1, 4;\nadd.s64 y, %2, 4;\n@e tcgen05.mma.cta_group::1.kind::f16 [%0], x, y, %3, p;\n"
+      "add.s64 x, %1, 6;\nadd.s64 y, %2, 6;\n@e tcgen05.mma.cta_group::1.kind::f16 [%0], x, y, %3, p;\n}\n" ::"r"(d),
+      "l"(a0), "l"(b0), "r"(idesc));
+}
+__device__ __forceinline__ void umma_s8e(uint32_t d, uint64_t a0, uint64_t b0, uint64_t a1, uint64_t b1, uint32_t idesc) {
+  asm volatile(
+      "{\n.reg .pred p, e;\nelect.sync _|e, 0xffffffff;\n.reg .b64 x, y;\nsetp.ne.b32 p, 0, 0;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\nsetp.eq.b32 p, 0, 0;\n"
+      "add.s64 x, %1, 2;\nadd.s64 y, %2, 2;\n@e tcgen05.mma.cta_group::1.kind::f16 [%0], x, y, %3, p;\n"
+      "add.s64 x, %1, 4;\nadd.s64 y, %2, 4;\n@e tcgen05.mma.cta_group::1.kind::f16 [%0], x, y, %3, p;\n"
+      "add.s64 x, %1, 6;\nadd.s64 y, %2, 6;\n@e tcgen05.mma.cta_group::1.kind::f16 [%0], x, y, %3, p;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %4, %5, %3, p;\n"
+      "add.s64 x, %4, 2;\nadd.s64 y, %5, 2;\n@e tcgen05.mma.cta_group::1.kind::f16 [%0], x, y, %3, p;\n"
+      "add.s64 x, %4, 4;\nadd.s64 y, %5, 4;\n@e tcgen05.mma.cta_group::1.kind::f16 [%0], x, y, %3, p;\n"
+      "add.s64 x, %4, 6;\nadd.s64 y, %5, 6;\n@e tcgen05.mma.cta_group::1.kind::f16 [%0], x, y, %3, p;\n}\n" ::"r"(d),
+      "l"(a0), "l"(b0), "r"(idesc), "l"(a1), "l"(b1));
+}
+// O (+)= P V over 64 keys (4 MMAs): A = P from TMEM columns ta + 8 kk, B = V (MN-major) descriptor + 128 kk;
+// acc = 0 makes the first MMA overwrite O.
+__device__ __forceinline__ void umma_pv4e(uint32_t d, uint32_t ta, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p, e;\nelect.sync _|e, 0xffffffff;\n.reg .b32 t;\n.reg .b64 y;\nsetp.ne.b32 p, %4, 0;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\nsetp.eq.b32 p, 0, 0;\n"
+      "add.u32 t, %1, 8;\nadd.s64 y, %2, 128;\n@e tcgen05.mma.cta_group::1.kind::f16 [%0], [t], y, %3, p;\n"
+      "add.u32 t, %1, 16;\nadd.s64 y, %2, 256;\n@e tcgen05.mma.cta_group::1.kind::f16 [%0], [t], y, %3, p;\n"
+      "add.u32 t, %1, 24;\nadd.s64 y, %2, 384;\n@e tcgen05.mma.cta_group::1.kind::f16 [%0], [t], y, %3, p;\n}\n" ::"r"(d),
+      "r"(ta), "l"(b), "r"(idesc), "r"(acc));
+}
+
+// commit by one elected lane of a converged warp
+__device__ __forceinline__ void umma_commit_e(uint64_t* bar) {
+  asm volatile(
+      "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(smem_u32(bar))
+      : "memory");
+}
+// ATTN_WARP_ISSUE (default): the MMA role runs on its whole warp, converged, and each asm block elects one lane to
+// issue -- ptxas then predicates UTCHMMA on a uniform predicate (@UP) with plain R2UR operands, instead of
+// wrapping every MMA of a single-lane branch in an ELECT / R2UR.BROADCAST / BRA.U.ANY loop.
+#ifndef ATTN_WARP_ISSUE
+#define ATTN_WARP_ISSUE 1
+#endif
+
 template <int D>
 __global__ void __launch_bounds__(192, 2)
     attention_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
@@ -250,7 +298,7 @@ __global__ void __launch_bounds__(192, 2)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    if (ATTN_WARP_ISSUE || lane == 0) {  // (ATTN_WARP_ISSUE: the whole warp, converged; one lane issues)
       // ---------------- MMA issuer: S_t, then P_{t-1} V_{t-1}, over the CTA's whole tile sequence
       int w = item_at(0), qi = 0, j = 0, nkv = 0;
       {
@@ -266,6 +314,14 @@ __global__ void __launch_bounds__(192, 2)
         if (jj == 0) mbar_wait(o_empty, (qq & 1) ^ 1);  // the previous item's epilogue has read O
         tc_fence_after();
         const uint32_t tP = tmem_base + (uint32_t)(b2 * BN);
+        if (ATTN_WARP_ISSUE) {
+          __syncwarp();
+          umma_pv4e(tO, tP, umma_desc_sw128_mn(smem_u32(sV + b2 * C::V_BYTES), BN * 128), C::IDESC_O, jj > 0 ? 1u : 0u);
+          umma_commit_e(&v_empty[b2]);
+          umma_commit_e(&p_free[b2]);
+          umma_commit_e(&o_full[b2]);
+          return;
+        }
         if (ATTN_MMA_BATCH) {
           umma_pv4(tO, tP, umma_desc_sw128_mn(smem_u32(sV + b2 * C::V_BYTES), BN * 128), C::IDESC_O, jj > 0 ? 1u : 0u);
         } else {
@@ -291,7 +347,19 @@ __global__ void __launch_bounds__(192, 2)
         mbar_wait(&p_free[b2], ((t >> 1) & 1) ^ 1);  // P_{t-2} V done: buffer b2 is free
         tc_fence_after();
         const uint32_t tS = tmem_base + (uint32_t)(b2 * BN);
-        if (ATTN_MMA_BATCH) {
+        if (ATTN_WARP_ISSUE) {
+          __syncwarp();
+          const uint64_t a0 = umma_desc_sw128(smem_u32(sQ));
+          const uint64_t b0 = umma_desc_sw128(smem_u32(sK + b2 * C::K_BYTES));
+          if (D == 128)
+            umma_s8e(tS, a0, b0, umma_desc_sw128(smem_u32(sQ + BM * 128)),
+                     umma_desc_sw128(smem_u32(sK + b2 * C::K_BYTES + BN * 128)), C::IDESC_S);
+          else
+            umma_s4e(tS, a0, b0, C::IDESC_S);
+          umma_commit_e(&k_empty[b2]);
+          if (j + 1 == nkv) umma_commit_e(q_empty);
+          umma_commit_e(&s_full[b2]);
+        } else if (ATTN_MMA_BATCH) {
           const uint64_t a0 = umma_desc_sw128(smem_u32(sQ));
           const uint64_t b0 = umma_desc_sw128(smem_u32(sK + b2 * C::K_BYTES));
           if (D == 128)
@@ -308,9 +376,11 @@ __global__ void __launch_bounds__(192, 2)
             umma_bf16(tS, a, bb, C::IDESC_S, kk > 0 ? 1u : 0u);
           }
         }
-        umma_commit(&k_empty[b2]);
-        if (j + 1 == nkv) umma_commit(q_empty);
-        umma_commit(&s_full[b2]);
+        if (!ATTN_WARP_ISSUE) {
+          umma_commit(&k_empty[b2]);
+          if (j + 1 == nkv) umma_commit(q_empty);
+          umma_commit(&s_full[b2]);
+        }
         if (pv_j >= 0) issue_pv(t - 1, pv_j, pv_qi);
         pv_j = j;
         pv_qi = qi;
