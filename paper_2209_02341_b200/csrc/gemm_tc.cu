@@ -292,6 +292,32 @@ __device__ __forceinline__ void umma_commit_2sm_mc(uint64_t* bar) {
       "h"((uint16_t)3)
       : "memory");
 }
+// GEMM_WARP_ISSUE (default): the pair's MMA role runs on its whole (converged) warp and one elected lane issues a
+// k-block's four MMAs and the stage commit from one asm block -- UTCHMMA on a uniform predicate, no per-MMA
+// ELECT / R2UR.BROADCAST / BRA.U.ANY loop (as in the attention kernel).
+#ifndef GEMM_WARP_ISSUE
+#define GEMM_WARP_ISSUE 1
+#endif
+__device__ __forceinline__ void umma_2sm_kblock_e(uint32_t d, uint64_t a0, uint64_t b0, uint32_t idesc, uint32_t acc,
+                                                  uint64_t* bar) {
+  asm volatile(
+      "{\n.reg .pred p, e;\n.reg .b64 x, y;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\nsetp.eq.b32 p, 0, 0;\n"
+      "add.s64 x, %1, 2;\nadd.s64 y, %2, 2;\n@e tcgen05.mma.cta_group::2.kind::f16 [%0], x, y, %3, p;\n"
+      "add.s64 x, %1, 4;\nadd.s64 y, %2, 4;\n@e tcgen05.mma.cta_group::2.kind::f16 [%0], x, y, %3, p;\n"
+      "add.s64 x, %1, 6;\nadd.s64 y, %2, 6;\n@e tcgen05.mma.cta_group::2.kind::f16 [%0], x, y, %3, p;\n"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%5], %6;\n}\n" ::"r"(d),
+      "l"(a0), "l"(b0), "r"(idesc), "r"(acc), "r"(smem_u32(bar)), "h"((uint16_t)3)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit_2sm_mc_e(uint64_t* bar) {
+  asm volatile(
+      "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n}\n" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t addr) {
   asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(addr) : "memory");
 }
@@ -816,14 +842,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       }
     }
   } else if (warp == 1) {
-    if (leader && lane == 0) {
+    if (leader && (GEMM_WARP_ISSUE || lane == 0)) {
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
       WorkIter wi(cid, tp, nkb);
       int tile, kb0, kb1, kind;
-      uint64_t* trace = g_gemm_trace;
+      uint64_t* trace = lane == 0 ? g_gemm_trace : nullptr;
       int nu = 0;
       while (wi.next(tp, nkb, ncl, tile, kb0, kb1, kind)) {
         mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -839,16 +865,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
           tc_fence_after();
           const uint64_t a0 = umma_desc_sw128(smem_u32(sA + stage * C::A_BYTES));
           const uint64_t b0 = umma_desc_sw128(smem_u32(sB + stage * C::B_BYTES));
+          if (GEMM_WARP_ISSUE) {
+            __syncwarp();
+            umma_2sm_kblock_e(d_tmem, a0, b0, C::IDESC, kb > kb0 ? 1u : acc0, &empty[stage]);
+          } else {
 #pragma unroll
-          for (int k = 0; k < TC_BK / 16; ++k)
-            umma_bf16_2sm(d_tmem, a0 + 2 * k, b0 + 2 * k, C::IDESC, (kb > kb0 || k > 0) ? 1u : acc0);
-          umma_commit_2sm_mc(&empty[stage]);
+            for (int k = 0; k < TC_BK / 16; ++k)
+              umma_bf16_2sm(d_tmem, a0 + 2 * k, b0 + 2 * k, C::IDESC, (kb > kb0 || k > 0) ? 1u : acc0);
+            umma_commit_2sm_mc(&empty[stage]);
+          }
           if (++stage == C::STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        umma_commit_2sm_mc(&tfull[acc]);
+        if (GEMM_WARP_ISSUE) {
+          __syncwarp();
+          umma_commit_2sm_mc_e(&tfull[acc]);
+        } else {
+          umma_commit_2sm_mc(&tfull[acc]);
+        }
         if (rec) {
           rec[2] = gtimer();
           rec[3] = (uint64_t)tile | ((uint64_t)(kb1 - kb0) << 32) | ((uint64_t)kind << 48);
