@@ -298,6 +298,9 @@ __device__ __forceinline__ void umma_commit_2sm_mc(uint64_t* bar) {
 #ifndef GEMM_WARP_ISSUE
 #define GEMM_WARP_ISSUE 1
 #endif
+#ifndef GEMM_WARP_TMA  // the TMA producer likewise (k-block loads + expect_tx from one asm block)
+#define GEMM_WARP_TMA 1
+#endif
 __device__ __forceinline__ void umma_2sm_kblock_e(uint32_t d, uint64_t a0, uint64_t b0, uint32_t idesc, uint32_t acc,
                                                   uint64_t* bar) {
   asm volatile(
@@ -308,6 +311,20 @@ __device__ __forceinline__ void umma_2sm_kblock_e(uint32_t d, uint64_t a0, uint6
       "add.s64 x, %1, 6;\nadd.s64 y, %2, 6;\n@e tcgen05.mma.cta_group::2.kind::f16 [%0], x, y, %3, p;\n"
       "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%5], %6;\n}\n" ::"r"(d),
       "l"(a0), "l"(b0), "r"(idesc), "r"(acc), "r"(smem_u32(bar)), "h"((uint16_t)3)
+      : "memory");
+}
+// the producer's k-block (converged warp, one elected lane): the leader CTA arms the full barrier with the pair's
+// bytes (leader != 0), then the A and W half-tiles of this CTA are loaded onto the leader's barrier
+__device__ __forceinline__ void tma_kblock_2sm_e(const CUtensorMap* ma, const CUtensorMap* mb, uint32_t da, uint32_t db,
+                                                 uint32_t full_local, uint32_t full_leader, uint32_t bytes, int leader,
+                                                 int xk, int ya, int yb) {
+  asm volatile(
+      "{\n.reg .pred e, l;\nelect.sync _|e, 0xffffffff;\nsetp.ne.and.b32 l, %8, 0, e;\n"
+      "@l mbarrier.arrive.expect_tx.shared::cta.b64 _, [%4], %6;\n"
+      "@e cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%2, {%7, %9}], [%5];\n"
+      "@e cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%1], [%3, {%7, %10}], [%5];\n}\n"
+      ::"r"(da), "r"(db), "l"(reinterpret_cast<uint64_t>(ma)), "l"(reinterpret_cast<uint64_t>(mb)), "r"(full_local),
+      "r"(full_leader), "r"(bytes), "r"(xk), "r"(leader), "r"(ya), "r"(yb)
       : "memory");
 }
 __device__ __forceinline__ void umma_commit_2sm_mc_e(uint64_t* bar) {
@@ -811,7 +828,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
   pdl_trigger();
 
   if (warp == 0) {
-    if (lane == 0) {
+    const bool warp_issue = GEMM_WARP_TMA && !(l2_hints & 1);  // (the L2-hint loads keep the one-lane path)
+    if (warp_issue || lane == 0) {
       pdl_wait();  // inputs of this GEMM are written by the previous kernel
       const uint64_t pol_a = policy_evict_last(), pol_b = policy_evict_first();
       int stage = 0;
@@ -824,8 +842,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           const uint32_t fb = smem_u32(&full[stage]) & PEER_MASK;
-          if (leader) mbar_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
-          if (l2_hints & 1) {
+          if (warp_issue) {
+            __syncwarp();
+            tma_kblock_2sm_e(&tmA, &tmB, smem_u32(sA + stage * C::A_BYTES), smem_u32(sB + stage * C::B_BYTES),
+                             smem_u32(&full[stage]), fb, 2 * C::STAGE_BYTES, leader ? 1 : 0, kb * TC_BK,
+                             m_blk * 256 + (int)rank * 128, n_blk * BN + (int)rank * (BN / 2));
+          } else if (leader) {
+            mbar_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
+          }
+          if (warp_issue) {
+          } else if (l2_hints & 1) {
             tma_load_2d_2sm_hint(&tmA, smem_u32(sA + stage * C::A_BYTES), fb, kb * TC_BK, m_blk * 256 + (int)rank * 128,
                                  pol_a);
             tma_load_2d_2sm_hint(&tmB, smem_u32(sB + stage * C::B_BYTES), fb, kb * TC_BK,
