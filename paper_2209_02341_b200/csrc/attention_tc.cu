@@ -172,6 +172,18 @@ __device__ __forceinline__ void umma_pv4e(uint32_t d, uint32_t ta, uint64_t b, u
       "r"(ta), "l"(b), "r"(idesc), "r"(acc));
 }
 
+// expect_tx + the 64-column halves of one tile (DH = 1 or 2 loads) by one elected lane of a converged warp
+__device__ __forceinline__ void tma_tile_e(const CUtensorMap* m, uint32_t dst, uint32_t half_bytes, uint64_t* bar,
+                                           uint32_t bytes, int y, int dh) {
+  asm volatile(
+      "{\n.reg .pred e, two;\n.reg .b32 d1;\nelect.sync _|e, 0xffffffff;\nsetp.ne.and.b32 two, %5, 1, e;\n"
+      "@e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%2], %3;\n"
+      "@e cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {0, %4}], [%2];\n"
+      "add.u32 d1, %0, %6;\n"
+      "@two cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [d1], [%1, {64, %4}], [%2];\n}\n"
+      ::"r"(dst), "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(bytes), "r"(y), "r"(dh), "r"(half_bytes)
+      : "memory");
+}
 // commit by one elected lane of a converged warp
 __device__ __forceinline__ void umma_commit_e(uint64_t* bar) {
   asm volatile(
@@ -265,34 +277,36 @@ __global__ void __launch_bounds__(192, 2)
   };
 
   if (warp == 0) {
-    if (lane == 0) {
+    if (ATTN_WARP_ISSUE || lane == 0) {  // (ATTN_WARP_ISSUE: converged warp, one elected lane issues)
       // ---------------- TMA producer: per item Q once, then K_0, K_1, V_0, K_2, V_1, ... (t = CTA tile count)
       int t = 0, qi = 0;
+      auto load = [&](const CUtensorMap* m, uint8_t* dst, uint32_t half_bytes, uint64_t* bar, uint32_t bytes, int y) {
+        if (ATTN_WARP_ISSUE) {
+          __syncwarp();
+          tma_tile_e(m, smem_u32(dst), half_bytes, bar, bytes, y, DH);
+        } else {
+          mbar_expect_tx(bar, bytes);
+#pragma unroll
+          for (int h = 0; h < DH; ++h) tma_load_2d(m, smem_u32(dst + h * half_bytes), bar, h * 64, y);
+        }
+      };
       for (int w = item_at(0); w < items; w = item_at(++qi)) {
         int b, head, q0, nkv, len;
         decode(w, b, head, q0, nkv, len);
         const int row_base = (b * hk + head) * S;
         mbar_wait(q_empty, (qi & 1) ^ 1);  // the previous item's last S has consumed Q
-        mbar_expect_tx(q_full, C::Q_BYTES);
-#pragma unroll
-        for (int h = 0; h < DH; ++h) tma_load_2d(&tmQ, smem_u32(sQ + h * BM * 128), q_full, h * 64, row_base + q0);
+        load(&tmQ, sQ, BM * 128, q_full, C::Q_BYTES, row_base + q0);
         auto load_k = [&](int tt, int j) {
           const int s2 = tt & 1;
           mbar_wait(&k_empty[s2], ((tt >> 1) & 1) ^ 1);
-          mbar_expect_tx(&k_full[s2], C::K_BYTES);
-#pragma unroll
-          for (int h = 0; h < DH; ++h)
-            tma_load_2d(&tmK, smem_u32(sK + s2 * C::K_BYTES + h * BN * 128), &k_full[s2], h * 64, row_base + j * BN);
+          load(&tmK, sK + s2 * C::K_BYTES, BN * 128, &k_full[s2], C::K_BYTES, row_base + j * BN);
         };
         load_k(t, 0);
         for (int j = 0; j < nkv; ++j) {
           if (j + 1 < nkv) load_k(t + j + 1, j + 1);
           const int tt = t + j, s2 = tt & 1;
           mbar_wait(&v_empty[s2], ((tt >> 1) & 1) ^ 1);
-          mbar_expect_tx(&v_full[s2], C::V_BYTES);
-#pragma unroll
-          for (int h = 0; h < DH; ++h)
-            tma_load_2d(&tmV, smem_u32(sV + s2 * C::V_BYTES + h * BN * 128), &v_full[s2], h * 64, row_base + j * BN);
+          load(&tmV, sV + s2 * C::V_BYTES, BN * 128, &v_full[s2], C::V_BYTES, row_base + j * BN);
         }
         t += nkv;
       }
