@@ -172,6 +172,20 @@ __device__ __forceinline__ void umma_pv4e(uint32_t d, uint32_t ta, uint64_t b, u
       "r"(ta), "l"(b), "r"(idesc), "r"(acc));
 }
 
+// O (+)= P V over 128 keys (v3): 8 MMAs, A = P at TMEM columns ta + 8 kk, B = V descriptor + 128 kk; one elected lane
+__device__ __forceinline__ void umma_pv8e(uint32_t d, uint32_t ta, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p, e;\nelect.sync _|e, 0xffffffff;\n.reg .b32 t;\n.reg .b64 y;\nsetp.ne.b32 p, %4, 0;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\nsetp.eq.b32 p, 0, 0;\n"
+      "add.u32 t, %1, 8;\nadd.s64 y, %2, 128;\n@e tcgen05.mma.cta_group::1.kind::f16 [%0], [t], y, %3, p;\n"
+      "add.u32 t, %1, 16;\nadd.s64 y, %2, 256;\n@e tcgen05.mma.cta_group::1.kind::f16 [%0], [t], y, %3, p;\n"
+      "add.u32 t, %1, 24;\nadd.s64 y, %2, 384;\n@e tcgen05.mma.cta_group::1.kind::f16 [%0], [t], y, %3, p;\n"
+      "add.u32 t, %1, 32;\nadd.s64 y, %2, 512;\n@e tcgen05.mma.cta_group::1.kind::f16 [%0], [t], y, %3, p;\n"
+      "add.u32 t, %1, 40;\nadd.s64 y, %2, 640;\n@e tcgen05.mma.cta_group::1.kind::f16 [%0], [t], y, %3, p;\n"
+      "add.u32 t, %1, 48;\nadd.s64 y, %2, 768;\n@e tcgen05.mma.cta_group::1.kind::f16 [%0], [t], y, %3, p;\n"
+      "add.u32 t, %1, 56;\nadd.s64 y, %2, 896;\n@e tcgen05.mma.cta_group::1.kind::f16 [%0], [t], y, %3, p;\n}\n" ::"r"(d),
+      "r"(ta), "l"(b), "r"(idesc), "r"(acc));
+}
 // expect_tx + the 64-column halves of one tile (DH = 1 or 2 loads) by one elected lane of a converged warp
 __device__ __forceinline__ void tma_tile_e(const CUtensorMap* m, uint32_t dst, uint32_t half_bytes, uint64_t* bar,
                                            uint32_t bytes, int y, int dh) {
@@ -578,6 +592,9 @@ __device__ __forceinline__ long long clk64() {
   return t;
 }
 
+#ifndef ATTN3_PINGPONG  // v3's asymmetric softmax ping-pong (measured slower: alternation without gain, §12)
+#define ATTN3_PINGPONG 0
+#endif
 #ifndef ATTN3_EMU
 #define ATTN3_EMU 0  // keys of every 32 whose exponential runs on the FMA pipe in unmasked tiles (v3)
 #endif
@@ -742,7 +759,7 @@ __global__ void __launch_bounds__(384, 1)
       }
     }
   } else if (warp == 9 || warp == 10) {
-    if (lane == 0) {
+    if (ATTN_WARP_ISSUE || lane == 0) {  // (ATTN_WARP_ISSUE: converged warp, one elected lane issues)
       // ---------------- MMA issuer of slot k (one thread per Q tile, so neither slot's chain
       // softmax -> P V -> next S waits for the other's).  Per item it issues S_0, then per key tile j:
       // P_j V_j, S_{j+1}; K / V stages are released (count 2) by both slots for every tile -- by the
@@ -752,9 +769,22 @@ __global__ void __launch_bounds__(384, 1)
       int t = 0, c = 0, n = 0;  // K/V tile, this slot's item count, this slot's P V count
       const uint32_t tS = tmem_base + (uint32_t)(k * BN);
       const uint32_t tO = tmem_base + (uint32_t)(2 * BN + k * D);
-      long long* trace = blockIdx.x == 0 ? g_attn_trace : nullptr;
+      long long* trace = (blockIdx.x == 0 && lane == 0) ? g_attn_trace : nullptr;
       auto issue_s = [&](int tt) {  // S_k = Q_k K_tt^T
         const int s2 = tt & 1;
+        if (ATTN_WARP_ISSUE) {
+          __syncwarp();
+          const uint64_t a0 = umma_desc_sw128(smem_u32(sQ + k * C::Q_BYTES));
+          const uint64_t b0 = umma_desc_sw128(smem_u32(sK + s2 * C::K_BYTES));
+          if (D == 128)
+            umma_s8e(tS, a0, b0, umma_desc_sw128(smem_u32(sQ + k * C::Q_BYTES + BM * 128)),
+                     umma_desc_sw128(smem_u32(sK + s2 * C::K_BYTES + BN * 128)), C::IDESC_S);
+          else
+            umma_s4e(tS, a0, b0, C::IDESC_S);
+          umma_commit_e(&s_full[k]);
+          umma_commit_e(&k_empty[s2]);
+          return;
+        }
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
           const uint32_t off = (kk & 3) * 32;
@@ -775,7 +805,10 @@ __global__ void __launch_bounds__(384, 1)
           mbar_wait(&q_full[k], c & 1);
           tc_fence_after();
           issue_s(t);
-          if (kv == 1) umma_commit(&q_empty[k]);
+          if (kv == 1) {
+            if (ATTN_WARP_ISSUE) umma_commit_e(&q_empty[k]);
+            else umma_commit(&q_empty[k]);
+          }
         }
         for (int j = 0; j < nkv; ++j) {
           const int tt = t + j, s2 = tt & 1;
@@ -785,28 +818,38 @@ __global__ void __launch_bounds__(384, 1)
             mbar_wait(&p_full[k], n & 1);
             if (trace && n < 64) trace[(k * 64 + n) * 8 + 2] = clk64();
             tc_fence_after();
+            if (ATTN_WARP_ISSUE) {
+              __syncwarp();
+              umma_pv8e(tO, tS, umma_desc_sw128_mn(smem_u32(sV + s2 * C::V_BYTES), BN * 128), C::IDESC_O, j > 0 ? 1u : 0u);
+              umma_commit_e(&pv_done[2 * k + (n & 1)]);
+              umma_commit_e(&v_empty[s2]);
+            } else {
 #pragma unroll
-            for (int kk = 0; kk < BN / 16; ++kk) {
-              const uint64_t bb = umma_desc_sw128_mn(smem_u32(sV + s2 * C::V_BYTES + kk * 16 * 128), BN * 128);
-              umma_bf16_ts(tO, tS + (uint32_t)(kk * 8), bb, C::IDESC_O, (j > 0 || kk > 0) ? 1u : 0u);
+              for (int kk = 0; kk < BN / 16; ++kk) {
+                const uint64_t bb = umma_desc_sw128_mn(smem_u32(sV + s2 * C::V_BYTES + kk * 16 * 128), BN * 128);
+                umma_bf16_ts(tO, tS + (uint32_t)(kk * 8), bb, C::IDESC_O, (j > 0 || kk > 0) ? 1u : 0u);
+              }
+              umma_commit(&pv_done[2 * k + (n & 1)]);
+              umma_commit(&v_empty[s2]);
             }
-            umma_commit(&pv_done[2 * k + (n & 1)]);
-            umma_commit(&v_empty[s2]);
             ++n;
             if (j + 1 < kv) {
               mbar_wait(&k_full[(tt + 1) & 1], ((tt + 1) >> 1) & 1);
               tc_fence_after();
               issue_s(tt + 1);
-              if (j + 2 == kv) umma_commit(&q_empty[k]);
+              if (j + 2 == kv) {
+                if (ATTN_WARP_ISSUE) umma_commit_e(&q_empty[k]);
+                else umma_commit(&q_empty[k]);
+              }
             }
             if (trace && n - 1 < 64) trace[(k * 64 + n - 1) * 8 + 3] = clk64();
           } else {
             // a tile this slot does not read: release its stages in phase (its K arrival for j == kv was not
             // made by an S, since S_{kv} is never issued; j = 0 of an inactive slot likewise)
             mbar_wait(&k_full[s2], (tt >> 1) & 1);
-            mbar_arrive(&k_empty[s2]);
+            if (lane == 0) mbar_arrive(&k_empty[s2]);
             mbar_wait(&v_full[s2], (tt >> 1) & 1);
-            mbar_arrive(&v_empty[s2]);
+            if (lane == 0) mbar_arrive(&v_empty[s2]);
           }
         }
         t += nkv;
@@ -897,13 +940,20 @@ __global__ void __launch_bounds__(384, 1)
             m_ref = mt;
           }
           const float base = (m_ref == -INFINITY) ? 0.f : m_ref;
-          if (k == 1) {
+          if (ATTN3_PINGPONG && k == 1) {
             // ping-pong: this warp's exponentials start only after the warpgroup-0 warp on the same SM
             // sub-partition finished those of its tile j (its last one if it has fewer), so the two share
             // the MUFU in turn and each slot's MMAs run while the other slot computes its exponentials.
             // Warpgroup 0 never waits for warpgroup 1, so this cannot deadlock.
             const int target = n0_base + min(j, it.kv0 - 1);
-            while (atomicAdd(&prog[qd], 0) <= target) __nanosleep(20);
+            // relaxed (strong) shared-memory loads: a memory-model-clean poll that does not occupy the atomics
+            // unit (polling with atomicAdd(…, 0) measured 15% slower)
+            for (;;) {
+              int v;
+              asm volatile("ld.relaxed.cta.shared.b32 %0, [%1];" : "=r"(v) : "r"(smem_u32(&prog[qd])) : "memory");
+              if (v > target) break;
+              __nanosleep(20);
+            }
           }
           if (trace && n < 64) trace[(k * 64 + n) * 8 + 5] = clk64();
           float ls[4] = {0.f, 0.f, 0.f, 0.f};
@@ -937,15 +987,16 @@ __global__ void __launch_bounds__(384, 1)
             tmem_st16_nowait(tS + q * 16, sr[q]);
           }
           if (trace && n < 64) trace[(k * 64 + n) * 8 + 6] = clk64();
-          if (k == 0) {
+          if (ATTN3_PINGPONG && k == 0) {
             __syncwarp();
-            if (lane == 0) atomicExch(&prog[qd], n + 1);
+            if (lane == 0) asm volatile("st.relaxed.cta.shared.b32 [%0], %1;" ::"r"(smem_u32(&prog[qd])), "r"(n + 1) : "memory");
           }
           tmem_wait_st();
           if (trace && n < 64) trace[(k * 64 + n) * 8 + 7] = clk64();
           l += (ls[0] + ls[1]) + (ls[2] + ls[3]);
         }
-        if (dead && k == 0 && lane == 0) atomicExch(&prog[qd], n + 1);
+        if (ATTN3_PINGPONG && dead && k == 0 && lane == 0)
+          asm volatile("st.relaxed.cta.shared.b32 [%0], %1;" ::"r"(smem_u32(&prog[qd])), "r"(n + 1) : "memory");
         if (k0 + BN > len) {  // zero V rows of keys >= len (pad rows a5 never wrote may hold NaN)
           mbar_wait(&v_full[s2], (tt >> 1) & 1);
           if (k0 + r >= len) {
