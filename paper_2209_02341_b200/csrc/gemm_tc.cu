@@ -925,10 +925,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
   } else if (warp >= 4) {
     pdl_wait();  // outputs: the previous kernel must be done with them
     const int q = warp & 3;                 // TMEM lane quadrant this warp may access
-    const int eg = (warp - 4) >> 2;         // epilogue warpgroup: columns [eg * BN/2, (eg+1) * BN/2)
+    const int eg = (warp - 4) >> 2;         // epilogue warpgroup: 32-column chunks [c0, c0 + CH) of the tile
     const int etid = q * 32 + lane;         // this thread's TMEM lane / tile row
-    constexpr int CH = BN / 32 / 2;         // 32-column chunks per warpgroup
-    const int c0 = eg * CH;
+    constexpr int NCH = BN / 32, H0 = (NCH + 1) / 2;  // chunks per tile; warpgroup 0 takes the first H0 (BN = 224: 4 + 3)
+    const int c0 = eg ? H0 : 0;
+    const int CH = eg ? NCH - H0 : H0;
     const uint32_t tempty_leader = smem_u32(&tempty[0]) & PEER_MASK;
     uint8_t* my_stg = sStg + (warp - 4) * 2 * 2048;
     uint32_t nst = 0;  // TMA stores issued by this warp (double-buffered staging)
@@ -1229,18 +1230,32 @@ int num_sms() {
   return n;
 }
 
-// Tile choice.  Codes: 1256 / 1192 / 1128 = 2-CTA pair with a 256 x {256, 192, 128} tile (the W
-// tensor map then has a BN/2-row box), 256 / 128 = 1-CTA 128 x {256, 128} tile.  Measured on B200
-// (profiles/r01_tile_sweep.log) the 256 x 256 pair tile is the fastest on every DRCE GEMM shape at
-// TP 1..8 even where a narrower tile would quantise into fewer waves, so it is used whenever both
-// dimensions can fill it; the 1-CTA kernel covers M <= 128 or N < 256.
-int tc_pick_bn(int M, int N) {
+// Tile choice.  Codes: 1256 / 1224 / 1192 / 1128 = 2-CTA pair with a 256 x {256, 224, 192, 128} tile (the W
+// tensor map then has a BN/2-row box), 256 / 128 = 1-CTA 128 x {256, 128} tile.  The 256 x 256 pair tile is the
+// most efficient per FLOP: per SM and 64-deep k-block it moves 32 KB through shared memory (TMA writes) for a
+// 512-clock MMA, and the MMA reads the same 32 KB -- 128 B / clock, the shared-memory bandwidth.  A narrower
+// tile keeps A's 16 KB for less MMA time, so it runs at ~(BN/256) / (shared-memory bytes ratio) of the
+// 256-wide time per round (224: 0.875 / 0.955 = 0.916; 192: 0.75 / 0.875 -> measured 20% below its width
+// share, profiles/r02_gemm_tiles_sk_tp8.log).  224 is chosen when its whole rounds beat the 256-wide rounds
+// (with the stream-K tail where the launcher would use it): N = 1920 (TP = 8 QKV: 9 n-blocks, 144 tiles in
+// 2 rounds of 74 pairs, instead of 2 full-width rounds for 7.5 n-blocks) and N = 5120 at short K (23
+// n-blocks, 368 tiles in 5 rounds instead of 320 tiles in 5 rounds); the 1-CTA kernel covers M <= 128 or
+// N < 256.  K = 0: unknown (no stream-K assumed).
+static bool streamk_would_run(int tiles, int pairs, int nkb, double ab_bytes);
+int tc_pick_bn(int M, int N, int K) {
   if (const char* f = getenv("ENERGON_GEMM_TILE")) {  // test hook: force a tile code
     const int code = atoi(f);
-    if (code == 1256 || code == 1192 || code == 1128 || code == 256 || code == 128) return code;
+    if (code == 1256 || code == 1224 || code == 1192 || code == 1128 || code == 256 || code == 128) return code;
   }
-  if (M > 128 && N >= 256) return 1256;
-  return N <= 128 ? 128 : 256;
+  if (!(M > 128 && N >= 256)) return N <= 128 ? 128 : 256;
+  static const int no224 = getenv("ENERGON_NO_TILE224") ? 1 : 0;
+  if (no224 || K <= 0) return 1256;
+  const int pairs = num_sms() / 2, num_m = (M + 255) / 256, nkb = (K + TC_BK - 1) / TC_BK;
+  const int t256 = num_m * ((N + 255) / 256), t224 = num_m * ((N + 223) / 224);
+  const double ab = 2.0 * ((double)M + (double)N) * (double)K;
+  const double r256 = streamk_would_run(t256, pairs, nkb, ab) ? 1.03 * t256 / pairs : (double)((t256 + pairs - 1) / pairs);
+  const double r224 = (double)((t224 + pairs - 1) / pairs) * (0.875 / 0.955);
+  return r224 < 0.97 * r256 ? 1224 : 1256;
 }
 
 // fp32 partial-accumulator workspace + self-resetting flags of the stream-K early pieces: one slot of
@@ -1277,6 +1292,12 @@ static const TailWs* default_tail_ws() {
 
 int tc_w_box(int code) { return code > 1000 ? (code - 1000) / 2 : code; }
 
+// the launcher's stream-K policy (measured per shape, see launch_pair_epi), shared with the tile choice
+static bool streamk_would_run(int tiles, int pairs, int nkb, double ab_bytes) {
+  if (!(tiles > pairs && tiles % pairs != 0) || getenv("ENERGON_NO_STREAMK")) return false;
+  return nkb >= 160 || (nkb >= 64 && tiles >= 2 * pairs && ab_bytes <= 100e6);
+}
+
 template <int BN, int EPI>
 static bool launch_pair_epi(const CUtensorMap& tmA, const CUtensorMap& tmB, const float* bias, bf16* D, int M, int N,
                             int K, cudaStream_t st, const QkvScatter& qs, const CUtensorMap* tmD, const TailWs* tw,
@@ -1306,8 +1327,7 @@ static bool launch_pair_epi(const CUtensorMap& tmA, const CUtensorMap& tmB, cons
   int sk = 0;  // 0 none, 1 data-parallel first, 2 early piece first
   if (tiles > pairs && tiles % pairs != 0 && !getenv("ENERGON_NO_STREAMK")) {
     if (const char* f = getenv("ENERGON_SK_FORCE")) sk = atoi(f) == 2 ? 1 : 2;  // 1: early first, 2: DP first
-    else if (nkb >= 160) sk = 1;
-    else if (nkb >= 64 && tiles >= 2 * pairs && ab_bytes <= 100e6) sk = 2;
+    else if (streamk_would_run(tiles, pairs, nkb, ab_bytes)) sk = nkb >= 160 ? 1 : 2;
   }
   if (sk) {
     const TailWs* w = tw ? tw : default_tail_ws();
@@ -1409,6 +1429,7 @@ static bool launch_bn_epi(const CUtensorMap& tmA, const CUtensorMap& tmB, const 
     default: return F<BNARGS EPI_BIAS_QKV>(tmA, tmB, bias, D, M, N, K, st, qs, tmD, tw, shard);   \
   }
 #define BN256 256,
+#define BN224 224,
 #define BN192 192,
 #define BN128 128,
 
@@ -1442,6 +1463,8 @@ bool launch_gemm_tc(const CUtensorMap& tmA, const CUtensorMap& tmB, int bn, cons
   if (qkv) qs = *qkv;
   if (bn == 1256) {
     DISPATCH_EPI(launch_pair_epi, BN256)
+  } else if (bn == 1224) {
+    DISPATCH_EPI(launch_pair_epi, BN224)
   } else if (bn == 1192) {
     DISPATCH_EPI(launch_pair_epi, BN192)
   } else if (bn == 1128) {

@@ -171,10 +171,10 @@ void launch_gemm_f32(const float* A, const float* W, const float* bias, float* D
 
 // bf16 tcgen05 GEMM.  Operands are K-major bf16 described by TMA maps with a 64-element (128 B)
 // inner box and 128-byte swizzle: A [M,K] with a 128-row box, W [N,K] with a bn-row box (bn = the
-// tile N, 256 or 128, chosen per call by tc_pick_bn).
+// tile N, or half of it for the 2-CTA pair tiles, chosen per call by tc_pick_bn).
 bool make_tmap_kmajor(CUtensorMap* map, const void* ptr, int rows, int K, int box_rows);  // inner box 64, SW128
-int tc_pick_bn(int M, int N);  // tile code (see gemm_tc.cu)
-int tc_w_box(int code);        // row box of the W tensor map the code needs (256, 128, 96 or 64)
+int tc_pick_bn(int M, int N, int K = 0);  // tile code (see gemm_tc.cu); K = 0: unknown
+int tc_w_box(int code);        // row box of the W tensor map the code needs (256, 128, 112, 96 or 64)
 bool make_tmap_store(CUtensorMap* map, const void* ptr, int rows, int N);  // D map of the TMA-store epilogue
 // Scratch of the stream-K tail split: fp32 partial tiles + self-resetting arrival counters.  GEMMs that
 // share one are stream-ordered, so each context (one forward stream at a time) owns its own;

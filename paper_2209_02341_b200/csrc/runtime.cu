@@ -44,14 +44,15 @@ namespace {
 
 thread_local std::string g_last_error;
 
-const int kBoxes[4] = {256, 128, 96, 64};
-int box_slot(int box) { return box == 256 ? 0 : box == 128 ? 1 : box == 96 ? 2 : 3; }
+constexpr int kNumBoxes = 5;
+const int kBoxes[kNumBoxes] = {256, 128, 96, 64, 112};
+int box_slot(int box) { return box == 256 ? 0 : box == 128 ? 1 : box == 96 ? 2 : box == 112 ? 4 : 3; }
 
 struct LayerDev {
   void *wqkv = nullptr, *wo = nullptr, *w1 = nullptr, *w2 = nullptr;  // [N, K] row-major (K-major operands)
   float *bqkv = nullptr, *bo = nullptr, *b1 = nullptr, *b2 = nullptr;
   float *ln1g = nullptr, *ln1b = nullptr, *ln2g = nullptr, *ln2b = nullptr;
-  CUtensorMap tm_qkv[4], tm_o[4], tm_1[4], tm_2[4];  // W row box 256 / 128 / 96 / 64 (box_slot())
+  CUtensorMap tm_qkv[kNumBoxes], tm_o[kNumBoxes], tm_1[kNumBoxes], tm_2[kNumBoxes];  // W row box 256 / 128 / 96 / 64 / 112 (box_slot())
   bool loaded = false;
 };
 
@@ -585,7 +586,7 @@ void gemm(energon_ctx* c, const CUtensorMap& tmA, const CUtensorMap* tmB, const 
           const CUtensorMap* tmD = nullptr, const ShardStore* shard = nullptr) {
   Prof p(c, st, P_GEMM, 2.0 * c->work_rows * N * K);  // algorithmic: the valid rows only
   if constexpr (sizeof(Act) == 2) {
-    const int code = tc_pick_bn(M, N);
+    const int code = tc_pick_bn(M, N, K);
     if (!launch_gemm_tc(tmA, tmB[box_slot(tc_w_box(code))], code, bias, reinterpret_cast<bf16*>(D), M, N, K, epi, st,
                         qs, tmD, &c->tail, shard))
       c->launch_err = "GEMM launch refused: output tensor map could not be built";
@@ -1166,7 +1167,7 @@ energon_status energon_offload_layers(energon_ctx* c, const int32_t* layers, int
     S.w1 = (char*)buf + sz[0] + sz[1];
     S.w2 = (char*)buf + sz[0] + sz[1] + sz[2];
     if (c->bf16)
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < kNumBoxes; ++i)
         if (!make_tmap_kmajor(&S.tm_qkv[i], S.wqkv, 3 * c->Hk, c->H, kBoxes[i]) ||
             !make_tmap_kmajor(&S.tm_o[i], S.wo, c->H, c->Hk, kBoxes[i]) ||
             !make_tmap_kmajor(&S.tm_1[i], S.w1, c->Fk, c->H, kBoxes[i]) ||
@@ -1428,7 +1429,7 @@ energon_status energon_load_layer_weights(energon_ctx* c, int32_t layer, const e
     return s;
   CU(c, cudaStreamSynchronize(c->load_stream));
   if (c->bf16) {
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < kNumBoxes; ++i) {
       if (!make_tmap_kmajor(&L.tm_qkv[i], L.wqkv, 3 * Hk, H, kBoxes[i]) ||
           !make_tmap_kmajor(&L.tm_o[i], L.wo, H, Hk, kBoxes[i]) || !make_tmap_kmajor(&L.tm_1[i], L.w1, Fk, H, kBoxes[i]) ||
           !make_tmap_kmajor(&L.tm_2[i], L.w2, H, Fk, kBoxes[i]))
@@ -1668,7 +1669,7 @@ energon_status energon_gemm(int32_t dtype, const void* A, const void* W, const f
     if (K % 8 || N % 8) return fail(nullptr, ENERGON_ERR_SHAPE, "bf16 GEMM needs K and N multiples of 8");
     if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(W) | reinterpret_cast<uintptr_t>(D)) & 15)
       return fail(nullptr, ENERGON_ERR_SHAPE, "bf16 GEMM needs 16-byte aligned A, W and D");
-    const int code = tc_pick_bn(M, N);
+    const int code = tc_pick_bn(M, N, K);
     CUtensorMap ta, tb;
     if (!make_tmap_kmajor(&ta, A, M, K, 128) || !make_tmap_kmajor(&tb, W, N, K, tc_w_box(code)))
       return fail(nullptr, ENERGON_ERR_CUDA, "cuTensorMapEncodeTiled failed");
