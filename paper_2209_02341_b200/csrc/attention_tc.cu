@@ -14,11 +14,15 @@
 //             (bf16) back over its scores in TMEM; O stays in TMEM and is rescaled only when the row
 //             maximum grew by more than 2^8 (exact: P values are bounded by 256).
 // Key tiles stop at min(len, q0 + 128) (causal) or len; query tiles with q0 >= len are not items.
+// Item epilogue: O / l leaves through shared memory by TMA bulk-tensor stores (32 x 32 boxes, one staging
+// buffer per softmax warp) whenever all 32 rows of the warp are queries; O's TMEM is released to the next
+// item right after its last tcgen05.ld.  Warps holding the sequence's last, partial rows store per thread.
 // Rows t >= len of the last V tile are zeroed in shared memory before P.V, so pad rows of V that a5
 // never wrote (possibly NaN) cannot reach the output even as 0 * NaN.
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -67,7 +71,7 @@ __device__ __forceinline__ uint64_t umma_desc_sw128_mn(uint32_t saddr, uint32_t 
 // operand straight from TMEM (tcgen05.mma ... [d], [a_tmem], b_desc), V is double-buffered in shared
 // memory, and the MMA thread issues S_{t+1} before P_t V_t across the CTA's whole tile sequence
 // (items included), so the tensor pipe works on the next scores while the softmax warps run.
-//   TMEM: S0 | S1 | O  (BN + BN + D <= 256 columns)      smem: Q | K[2] | V[2]
+//   TMEM: S0 | S1 | O  (BN + BN + D <= 256 columns)      smem: Q | K[2] | V[2] | epilogue staging [4 warps]
 // Ordering: S_t overwrites buffer t&1 only after P_{t-2} V (the last reader of that buffer) completed
 // (p_free); the O rescale waits for P_{t-1} V (o_full); P_t V is issued after p_full of tile t.
 template <int D>
@@ -76,7 +80,8 @@ struct Attn2Cfg {
   static constexpr int Q_BYTES = BM * D * 2;
   static constexpr int K_BYTES = BN * D * 2;
   static constexpr int V_BYTES = BN * D * 2;
-  static constexpr int SMEM = Q_BYTES + 2 * K_BYTES + 2 * V_BYTES + 1024 + 256;
+  static constexpr int STG_BYTES = 4 * 32 * 64;  // epilogue staging: per softmax warp 32 rows x 32 columns (bf16)
+  static constexpr int SMEM = Q_BYTES + 2 * K_BYTES + 2 * V_BYTES + STG_BYTES + 1024 + 256;
   static constexpr int TMEM_COLS = 256;  // 2 * BN + D <= 256 for D <= 128
   // S = Q K^T: M=128, N=BN, both K-major
   static constexpr uint32_t IDESC_S = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
@@ -198,6 +203,47 @@ __device__ __forceinline__ void tma_tile_e(const CUtensorMap* m, uint32_t dst, u
       ::"r"(dst), "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(bytes), "r"(y), "r"(dh), "r"(half_bytes)
       : "memory");
 }
+// Epilogue by TMA: one softmax warp's 32 rows x 32 columns of O / l, bf16, staged in shared memory with the
+// 64-byte swizzle of the output map (16-byte chunk j of row r at chunk j ^ ((r >> 1) & 3)) and stored with one
+// bulk-tensor store.  The per-thread row stores it replaces touched 32 rows per instruction (half-used 32-byte
+// sectors) and blocked the softmax warps: dropping them altogether (a probe with wrong output) sped the
+// config-3 mix up from 50.9 to 38.3 us; this epilogue gets 47.2 us.  One 2 KB buffer per warp: 32 x 16 boxes
+// double-buffered in the same space measured slower (48.9 us), and two 2 KB buffers per warp exceed the
+// shared memory two CTAs per SM leave by 256 bytes.
+__device__ __forceinline__ void attn_stage32(const uint32_t* o, float inv, uint32_t stg, int lane) {
+  const uint32_t base = stg + lane * 64;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const uint32_t a = base + ((j ^ ((lane >> 1) & 3)) << 4);
+    const uint32_t* e = o + 8 * j;
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a),
+                 "r"(pack_bf16x2(__uint_as_float(e[0]) * inv, __uint_as_float(e[1]) * inv)),
+                 "r"(pack_bf16x2(__uint_as_float(e[2]) * inv, __uint_as_float(e[3]) * inv)),
+                 "r"(pack_bf16x2(__uint_as_float(e[4]) * inv, __uint_as_float(e[5]) * inv)),
+                 "r"(pack_bf16x2(__uint_as_float(e[6]) * inv, __uint_as_float(e[7]) * inv))
+                 : "memory");
+  }
+}
+// 16 columns of one row (32 bytes: a whole sector) with one 256-bit store (STG.E.256) -- the fallback for warps
+// holding a sequence's last, partial rows (half as many store instructions as 16-byte stores, full sectors)
+__device__ __forceinline__ void attn_st256(bf16* dst, const uint32_t* e, float inv) {
+  asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst),
+               "r"(pack_bf16x2(__uint_as_float(e[0]) * inv, __uint_as_float(e[1]) * inv)),
+               "r"(pack_bf16x2(__uint_as_float(e[2]) * inv, __uint_as_float(e[3]) * inv)),
+               "r"(pack_bf16x2(__uint_as_float(e[4]) * inv, __uint_as_float(e[5]) * inv)),
+               "r"(pack_bf16x2(__uint_as_float(e[6]) * inv, __uint_as_float(e[7]) * inv)),
+               "r"(pack_bf16x2(__uint_as_float(e[8]) * inv, __uint_as_float(e[9]) * inv)),
+               "r"(pack_bf16x2(__uint_as_float(e[10]) * inv, __uint_as_float(e[11]) * inv)),
+               "r"(pack_bf16x2(__uint_as_float(e[12]) * inv, __uint_as_float(e[13]) * inv)),
+               "r"(pack_bf16x2(__uint_as_float(e[14]) * inv, __uint_as_float(e[15]) * inv))
+               : "memory");
+}
+__device__ __forceinline__ void attn_tma_store(const CUtensorMap* map, uint32_t src, int x, int y) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];\n"
+               "cp.async.bulk.commit_group;" ::"l"(reinterpret_cast<uint64_t>(map)),
+               "r"(src), "r"(x), "r"(y)
+               : "memory");
+}
 // commit by one elected lane of a converged warp
 __device__ __forceinline__ void umma_commit_e(uint64_t* bar) {
   asm volatile(
@@ -217,7 +263,8 @@ __global__ void __launch_bounds__(192, 2)
     attention_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                          const __grid_constant__ CUtensorMap tmV, bf16* __restrict__ Cp, const int* __restrict__ offsets,
                          bf16* __restrict__ Opad, const int* __restrict__ lens, const uint32_t* __restrict__ work,
-                         int hk, int S, int causal, float scale_log2) {
+                         int hk, int S, int causal, float scale_log2, const __grid_constant__ CUtensorMap tmO,
+                         int o_tma) {
   using C = Attn2Cfg<D>;
   constexpr int BM = C::BM, BN = C::BN, DH = C::DH;
   extern __shared__ uint8_t smem_raw[];
@@ -225,7 +272,8 @@ __global__ void __launch_bounds__(192, 2)
   uint8_t* sQ = smem;
   uint8_t* sK = sQ + C::Q_BYTES;
   uint8_t* sV = sK + 2 * C::K_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + 2 * C::V_BYTES);
+  uint8_t* sStg = sV + 2 * C::V_BYTES;  // [4 softmax warps][32 rows][64 B]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sStg + C::STG_BYTES);
   uint64_t* q_full = bars + 0;
   uint64_t* q_empty = bars + 1;
   uint64_t* o_empty = bars + 2;
@@ -244,6 +292,7 @@ __global__ void __launch_bounds__(192, 2)
     tma_prefetch_desc(&tmQ);
     tma_prefetch_desc(&tmK);
     tma_prefetch_desc(&tmV);
+    if (o_tma) tma_prefetch_desc(&tmO);
     mbar_init(q_full, 1);
     mbar_init(q_empty, 1);
     mbar_init(o_empty, 4);
@@ -430,7 +479,8 @@ __global__ void __launch_bounds__(192, 2)
     const int qd = warp & 3;
     const int r = qd * 32 + lane;
     const uint32_t lane_off = (uint32_t)(qd * 32) << 16;
-    int t = 0;
+    const uint32_t stg = smem_u32(sStg + qd * 32 * 64);
+    int t = 0, nst = 0;  // nst: bulk stores this warp issued (the staging buffer is reused after their reads)
     for (int k = 0, w = item_at(0); w < items; w = item_at(++k)) {
       int b, head, q0, nkv, len;
       decode(w, b, head, q0, nkv, len);
@@ -527,6 +577,12 @@ __global__ void __launch_bounds__(192, 2)
       tc_fence_after();
       const float inv = 1.f / l;
       const bool valid = srow < len;
+      const int qrow0 = q0 + qd * 32;
+      // warp-uniform: all 32 rows of the warp are queries -> TMA box stores (rows past the sequence end would
+      // land on the next sequence's packed rows, so partial warps keep the per-thread stores)
+      const bool box = o_tma && qrow0 + 32 <= len;
+      const int ox = Cp ? head * D : 0;
+      const int oy = Cp ? __ldg(offsets + b) + qrow0 : (b * hk + head) * S + qrow0;
       bf16* dst = Cp ? Cp + ((int64_t)__ldg(offsets + b) + srow) * (int64_t)(hk * D) + head * D
                      : Opad + ((int64_t)(b * hk + head) * S + srow) * D;
 #pragma unroll 1
@@ -535,23 +591,31 @@ __global__ void __launch_bounds__(192, 2)
         tmem_ld32_nowait(tO + lane_off + c, o[0]);
         tmem_ld32_nowait(tO + lane_off + c + 32, o[1]);
         tmem_wait_ld();
-        if (valid) {
+        if (c + 64 >= D) {  // O has been read: the next item's first P V may overwrite it
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(o_empty);
+        }
+        if (box) {
 #pragma unroll
-          for (int e = 0; e < 64; e += 8) {
-            const uint32_t* oe = &o[e >> 5][e & 31];
-            uint4 pq;
-            pq.x = pack_bf16x2(__uint_as_float(oe[0]) * inv, __uint_as_float(oe[1]) * inv);
-            pq.y = pack_bf16x2(__uint_as_float(oe[2]) * inv, __uint_as_float(oe[3]) * inv);
-            pq.z = pack_bf16x2(__uint_as_float(oe[4]) * inv, __uint_as_float(oe[5]) * inv);
-            pq.w = pack_bf16x2(__uint_as_float(oe[6]) * inv, __uint_as_float(oe[7]) * inv);
-            *reinterpret_cast<uint4*>(dst + c + e) = pq;
+          for (int u = 0; u < 2; ++u) {  // 32-column chunks
+            if (nst > 0) {  // the previous store has finished reading the staging buffer
+              if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+              __syncwarp();
+            }
+            attn_stage32(o[u], inv, stg, lane);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) attn_tma_store(&tmO, stg, ox + c + 32 * u, oy);
+            ++nst;
           }
+        } else if (valid) {
+#pragma unroll
+          for (int e = 0; e < 64; e += 16) attn_st256(dst + c + e, &o[e >> 5][e & 31], inv);
         }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(o_empty);
     }
+    if (nst > 0 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // before smem goes away
   }
   tc_fence_before();
   __syncthreads();
@@ -605,7 +669,8 @@ struct Attn3Cfg {
   static constexpr int Q_BYTES = BM * D * 2;
   static constexpr int K_BYTES = BN * D * 2;
   static constexpr int V_BYTES = BN * D * 2;
-  static constexpr int SMEM = 2 * Q_BYTES + 2 * K_BYTES + 2 * V_BYTES + 1024 + 256;
+  static constexpr int STG_BYTES = 8 * 32 * 64;  // epilogue staging: per softmax warp 32 rows x 32 columns (bf16)
+  static constexpr int SMEM = 2 * Q_BYTES + 2 * K_BYTES + 2 * V_BYTES + STG_BYTES + 1024 + 256;
   static constexpr int THREADS = 384;  // 12 warps: 3 per SM sub-partition (168 registers each at launch)
   static constexpr uint32_t IDESC_S = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
                                       ((uint32_t)(BM >> 4) << 24);
@@ -625,7 +690,8 @@ __global__ void __launch_bounds__(384, 1)
     attention_tc3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                          const __grid_constant__ CUtensorMap tmV, bf16* __restrict__ Cp, const int* __restrict__ offsets,
                          bf16* __restrict__ Opad, const int* __restrict__ lens, const uint32_t* __restrict__ work,
-                         int hk, int S, int causal, float scale_log2) {
+                         int hk, int S, int causal, float scale_log2, const __grid_constant__ CUtensorMap tmO,
+                         int o_tma) {
   using C = Attn3Cfg<D>;
   constexpr int BM = C::BM, BN = C::BN, DH = C::DH;
   extern __shared__ uint8_t smem_raw[];
@@ -633,7 +699,8 @@ __global__ void __launch_bounds__(384, 1)
   uint8_t* sQ = smem;                       // [2] Q tiles
   uint8_t* sK = sQ + 2 * C::Q_BYTES;        // [2] stages
   uint8_t* sV = sK + 2 * C::K_BYTES;        // [2] stages
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + 2 * C::V_BYTES);
+  uint8_t* sStg = sV + 2 * C::V_BYTES;     // [8 softmax warps][2][32 rows][32 B]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sStg + C::STG_BYTES);
   uint64_t* q_full = bars + 0;    // [2] per Q slot
   uint64_t* q_empty = bars + 2;   // [2]
   uint64_t* o_empty = bars + 4;   // [2] the slot's epilogue has read O (4 warps)
@@ -655,6 +722,7 @@ __global__ void __launch_bounds__(384, 1)
     tma_prefetch_desc(&tmQ);
     tma_prefetch_desc(&tmK);
     tma_prefetch_desc(&tmV);
+    if (o_tma) tma_prefetch_desc(&tmO);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&q_full[i], 1);
       mbar_init(&q_empty[i], 1);
@@ -866,6 +934,8 @@ __global__ void __launch_bounds__(384, 1)
     const uint32_t tS = tmem_base + lane_off + (uint32_t)(k * BN);
     const uint32_t tO = tmem_base + lane_off + (uint32_t)(2 * BN + k * D);
     int t = 0, n = 0, c = 0;  // global K/V tile, this slot's P V count, this slot's item count
+    const uint32_t stg = smem_u32(sStg + (k * 4 + qd) * 32 * 64);
+    int nst = 0;  // bulk stores issued by this warp (the staging buffer is reused after their reads)
     int n0_base = 0;          // (warpgroup 1) warpgroup 0's tile count before this item
     long long* trace = (blockIdx.x == 0 && qd == 0 && lane == 0) ? g_attn_trace : nullptr;
     for (int qi = 0, w = item_at(0); w < items; w = item_at(++qi), n0_base += decode(item_at(qi - 1)).kv0) {
@@ -1015,13 +1085,18 @@ __global__ void __launch_bounds__(384, 1)
         if (trace && n < 64) trace[(k * 64 + n) * 8 + 1] = clk64();
         if (!dead && !seen_prev) mbar_wait(&pv_done[2 * k + ((n - 1) & 1)], ((n - 1) >> 1) & 1);
       }
-      // ---------------- epilogue of this Q tile: O / l -> packed context rows (or padded O rows)
+      // ---------------- epilogue of this Q tile: O / l -> packed context rows (or padded O rows), by TMA box
+      // stores when all 32 rows of the warp are queries (as in v2), O released right after its last TMEM read
+      bool released = false;
       if (!dead) {
         mbar_wait(&pv_done[2 * k + ((n - 1) & 1)], ((n - 1) >> 1) & 1);
         __syncwarp();
         tc_fence_after();
         const float inv = 1.f / l;
         const bool valid = srow < len;
+        const bool box = o_tma && qrow0 + 32 <= len;
+        const int ox = Cp ? it.head * D : 0;
+        const int oy = Cp ? __ldg(offsets + it.b) + qrow0 : (it.b * hk + it.head) * S + qrow0;
         bf16* dst = Cp ? Cp + ((int64_t)__ldg(offsets + it.b) + srow) * (int64_t)(hk * D) + it.head * D
                        : Opad + ((int64_t)(it.b * hk + it.head) * S + srow) * D;
 #pragma unroll 1
@@ -1030,26 +1105,40 @@ __global__ void __launch_bounds__(384, 1)
           tmem_ld32_nowait(tO + cd, o[0]);
           tmem_ld32_nowait(tO + cd + 32, o[1]);
           tmem_wait_ld();
-          if (valid) {
+          if (cd + 64 >= D) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&o_empty[k]);
+            released = true;
+          }
+          if (box) {
 #pragma unroll
-            for (int e = 0; e < 64; e += 8) {
-              const uint32_t* oe = &o[e >> 5][e & 31];
-              uint4 pq;
-              pq.x = pack_bf16x2(__uint_as_float(oe[0]) * inv, __uint_as_float(oe[1]) * inv);
-              pq.y = pack_bf16x2(__uint_as_float(oe[2]) * inv, __uint_as_float(oe[3]) * inv);
-              pq.z = pack_bf16x2(__uint_as_float(oe[4]) * inv, __uint_as_float(oe[5]) * inv);
-              pq.w = pack_bf16x2(__uint_as_float(oe[6]) * inv, __uint_as_float(oe[7]) * inv);
-              *reinterpret_cast<uint4*>(dst + cd + e) = pq;
+            for (int u = 0; u < 2; ++u) {
+              if (nst > 0) {
+                if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                __syncwarp();
+              }
+              attn_stage32(o[u], inv, stg, lane);
+              asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+              __syncwarp();
+              if (lane == 0) attn_tma_store(&tmO, stg, ox + cd + 32 * u, oy);
+              ++nst;
             }
+          } else if (valid) {
+#pragma unroll
+            for (int e = 0; e < 64; e += 16) attn_st256(dst + cd + e, &o[e >> 5][e & 31], inv);
           }
         }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&o_empty[k]);
+      if (!released) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&o_empty[k]);
+      }
       t += nkv;
       ++c;
     }
+    if (nst > 0 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // before smem goes away
   }
   tc_fence_before();
   __syncthreads();
@@ -1086,6 +1175,19 @@ static bool launch_tc(const bf16* Q, const bf16* K, const bf16* V, bf16* Cp, con
   AttnMaps local;
   AttnMaps* m = maps ? maps : &local;
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)D);
+  // output map of the TMA-store epilogue, cached like the input maps: packed rows [<= B S, hk d] (a7 fused) or
+  // padded O [B hk S, d]; boxes are stored only for warps whose 32 rows are all queries (rows < T)
+  static const int no_otma = getenv("ENERGON_NO_ATTN_TMA") ? 1 : 0;
+  const void* optr = Cp ? (const void*)Cp : (const void*)Opad;
+  const int o_rows = Cp ? B * S : rows, o_n = Cp ? hk * D : D;
+  if (!no_otma && (!m->o_valid || m->o != optr || m->o_rows != o_rows || m->o_n != o_n)) {
+    m->o_valid = make_tmap_store_box(&m->mo, optr, o_rows, o_n, 32);
+    m->o = optr;
+    m->o_rows = o_rows;
+    m->o_n = o_n;
+  }
+  const int o_tma = (!no_otma && m->o_valid) ? 1 : 0;
+  if (!o_tma) memset(&m->mo, 0, sizeof(m->mo));
   if (attention_impl() == 5) {
     using C = Attn3Cfg<D>;
     if (!attn_maps(m, Q, K, V, rows, D, C::BM, C::BN)) return false;
@@ -1104,7 +1206,7 @@ static bool launch_tc(const bf16* Q, const bf16* K, const bf16* V, bf16* Cp, con
     }
     if (trace_buf) cudaMemsetAsync(trace_buf, 0, 2 * 64 * 8 * sizeof(long long), st);
     launch_k(attention_tc3_kernel<D>, dim3(grid), dim3(C::THREADS), C::SMEM, st, m->mq, m->mk, m->mv, Cp, offsets,
-             Opad, lens_d, work_d, hk, S, causal, scale_log2);
+             Opad, lens_d, work_d, hk, S, causal, scale_log2, m->mo, o_tma);
     if (trace_buf) {  // diagnostics only: synchronous dump
       long long h[2 * 64 * 8];
       cudaMemcpy(h, trace_buf, sizeof(h), cudaMemcpyDeviceToHost);
@@ -1130,7 +1232,7 @@ static bool launch_tc(const bf16* Q, const bf16* K, const bf16* V, bf16* Cp, con
   const int grid = max_items < slots ? (int)max_items : slots;
   if (grid <= 0) return true;
   launch_k(attention_tc2_kernel<D>, dim3(grid), dim3(192), C::SMEM, st, m->mq, m->mk, m->mv, Cp, offsets, Opad, lens_d,
-           work_d, hk, S, causal, scale_log2);
+           work_d, hk, S, causal, scale_log2, m->mo, o_tma);
   return true;
 }
 

@@ -1185,16 +1185,20 @@ bool make_tmap_kmajor(CUtensorMap* map, const void* ptr, int rows, int K, int bo
 }
 
 // Output map for the TMA-store epilogue: D [rows, N] bf16 row-major, 32 x 32 box, 64-byte swizzle.
-bool make_tmap_store(CUtensorMap* map, const void* ptr, int rows, int N) {
+bool make_tmap_store(CUtensorMap* map, const void* ptr, int rows, int N) { return make_tmap_store_box(map, ptr, rows, N, 32); }
+
+// the same with a box of 32 rows x box_cols (32: 64-byte swizzle, 16: 32-byte swizzle)
+bool make_tmap_store_box(CUtensorMap* map, const void* ptr, int rows, int N, int box_cols) {
   auto enc = encode_fn();
   if (!enc || rows <= 0 || N <= 0 || (N % 8) != 0 || (reinterpret_cast<uintptr_t>(ptr) & 15)) return false;
+  if (box_cols != 32 && box_cols != 16) return false;
   cuuint64_t dims[2] = {(cuuint64_t)N, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)N * 2};
-  cuuint32_t box[2] = {32, 32};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, 32};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, box_cols == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B,
+                   CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
 

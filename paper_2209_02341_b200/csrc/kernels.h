@@ -138,6 +138,10 @@ struct AttnMaps {
   const void *q = nullptr, *k = nullptr, *v = nullptr;
   int rows = 0, d = 0, bn = 0;
   bool valid = false;
+  CUtensorMap mo;  // output map of the TMA-store epilogue (packed context rows or padded O)
+  const void* o = nullptr;
+  int o_rows = 0, o_n = 0;
+  bool o_valid = false;
 };
 int attention_tile_bm();  // query rows of one work item of the tcgen05 kernel
 int attention_tile_bn();  // keys per tile (the work list's cost unit)
@@ -176,6 +180,7 @@ bool make_tmap_kmajor(CUtensorMap* map, const void* ptr, int rows, int K, int bo
 int tc_pick_bn(int M, int N, int K = 0);  // tile code (see gemm_tc.cu); K = 0: unknown
 int tc_w_box(int code);        // row box of the W tensor map the code needs (256, 128, 112, 96 or 64)
 bool make_tmap_store(CUtensorMap* map, const void* ptr, int rows, int N);  // D map of the TMA-store epilogue
+bool make_tmap_store_box(CUtensorMap* map, const void* ptr, int rows, int N, int box_cols);  // 32 rows x 32 / 16 cols
 // Scratch of the stream-K tail split: fp32 partial tiles + self-resetting arrival counters.  GEMMs that
 // share one are stream-ordered, so each context (one forward stream at a time) owns its own;
 // tail_ws_alloc sizes it for this device, nullptr in launch_gemm_tc = a per-device default.
