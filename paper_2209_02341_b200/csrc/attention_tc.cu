@@ -257,6 +257,9 @@ __device__ __forceinline__ void umma_commit_e(uint64_t* bar) {
 #ifndef ATTN_WARP_ISSUE
 #define ATTN_WARP_ISSUE 1
 #endif
+#ifndef ATTN2_OBSERVE_ALL  // A/B: 1 = the softmax warps wait for every tile's P V after handing P over (old behaviour)
+#define ATTN2_OBSERVE_ALL 0
+#endif
 
 template <int D>
 __global__ void __launch_bounds__(192, 2)
@@ -518,15 +521,18 @@ __global__ void __launch_bounds__(192, 2)
         float mt = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])), fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
         mt *= scale_log2;
         // lazy rescale, warp-wide (tcgen05.ld / st are .sync.aligned), alpha = 1 for rows keeping their max.
-        // Every tile's P V completion (o_full[t & 1], one phase per two tiles) is observed exactly once,
-        // in order: here when the rescale needs O, else right after this tile's P is handed over -- a
-        // parity wait must never fall two phases behind its barrier.
+        // o_full[b] completes once per P V on buffer b (tiles b, b + 2, ...), and a parity wait is exact only
+        // while the barrier is no more than one phase ahead of or behind the waited one.  The two waits on it
+        // (P_{t-1} V here, the item's last P V in the epilogue) are exact without observing every phase:
+        // this warp holds S_t, which the MMA thread issued only after P_{t-2} V completed (p_free), so
+        // P_{t-3} V -- the previous phase of P_{t-1} V's barrier -- is complete (one thread's tcgen05 ops
+        // complete in order), and P_{t+1} V -- the next one -- needs P_{t+1} from this warp.  (Observing
+        // P_{t-1} V after every hand-over cost a ~200-clock try_wait round trip per tile, trace in
+        // profiles/r02_attn_v2_trace_report.txt.)
         const bool grow = mt > m_ref + 8.f;
         const float alpha = !grow ? 1.f : (m_ref == -INFINITY) ? 0.f : ex2f(m_ref - mt);
-        bool seen_prev = j == 0;  // the previous item's last P V was observed by its epilogue
         if (j > 0 && __any_sync(0xffffffffu, grow)) {
           mbar_wait(&o_full[(t - 1) & 1], ((t - 1) >> 1) & 1);  // P_{t-1} V_{t-1}: the last writer of O
-          seen_prev = true;
           __syncwarp();
           tc_fence_after();
 #pragma unroll 1
@@ -569,7 +575,7 @@ __global__ void __launch_bounds__(192, 2)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[b2]);
-        if (!seen_prev) mbar_wait(&o_full[(t - 1) & 1], ((t - 1) >> 1) & 1);
+        if (ATTN2_OBSERVE_ALL && j > 0) mbar_wait(&o_full[(t - 1) & 1], ((t - 1) >> 1) & 1);
       }
       // ---------------- item epilogue: O / l -> packed context row (or padded O row)
       mbar_wait(&o_full[(t - 1) & 1], ((t - 1) >> 1) & 1);
