@@ -1,4 +1,5 @@
-"""v2 attention timeline (diagnostics build -DATTN2_TRACE=1 via AB_LIB, ENERGON_ATTN_TRACE=<file>): calls the kernel
+"""v2 attention timeline (a diagnostics build with clock64 stamps, -DATTN2_TRACE=1, loaded via AB_LIB; the
+instrumentation itself is not kept in the tree -- profiles/r02_attn_v2_trace_report.txt lists the stamp points; ENERGON_ATTN_TRACE=<file>): calls the kernel
 eagerly on one length mix and prints CTA 0's per-tile clock64 stamps relative to its first record."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
