@@ -1,3 +1,6 @@
+"""Item-change Q-load latency of attention v2 (CTA 0): needs a diagnostics build with clock64 stamps at the producer's Q
+load and the MMA thread's q_full / k_full waits (not kept in the tree; profiles/r02_attn_v2_trace_report.txt lists them),
+loaded via AB_LIB, with ENERGON_ATTN_TRACE=<file>."""
 import os, sys
 sys.path.insert(0, os.getcwd())
 import torch, synth
